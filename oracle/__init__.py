@@ -1,0 +1,52 @@
+"""CPU oracle for the CountSketch / TensorSketch ID hot path -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package, and only as the checker or
+the timed CPU baseline.  The product package (``paper_1901_10559_b200``) never
+imports it and has no CPU fallback.
+
+Contents
+--------
+* ``hash_oracle.c`` (built to ``oracle/_build/libidsketch_oracle.so`` by
+  ``oracle/Makefile``): plain-C restatement of the PCG64 / Lemire /
+  Fisher-Yates draw sequence behind ``CountSketchOp.__init__``
+  (reference ``pkg/src/idsketch/sketch.py:77-84``).
+* ``port.py``: numpy/scipy restatement of the reference's sketch + ID path
+  (``sketch.py:116-186``, ``linalg.py:76-147``, ``matrix_id.py:56-182``,
+  ``cp_tensor.py:215-276``), calling the same third-party kernels the
+  reference calls (scipy sparse products, pocketfft, LAPACK dgeqp3/dtrtrs).
+
+Parity pin: the oracle is checked against golden vectors produced by the
+real reference package (``tests/golden/make_golden.py``) in
+``tests/test_oracle_golden.py``.
+"""
+
+from .cs_hash import countsketch_hash, pcg64_stream32, seed_state
+from .port import (
+    OracleCountSketch,
+    OracleTensorSketch,
+    coeffs_from_pivoted,
+    countsketch_id,
+    cpqr,
+    cs_apply,
+    matrix_id,
+    tensorsketch_apply,
+    tensorsketch_id,
+    ts_new_weights,
+)
+
+__all__ = [
+    "OracleCountSketch",
+    "OracleTensorSketch",
+    "coeffs_from_pivoted",
+    "countsketch_hash",
+    "countsketch_id",
+    "cpqr",
+    "cs_apply",
+    "matrix_id",
+    "pcg64_stream32",
+    "seed_state",
+    "tensorsketch_apply",
+    "tensorsketch_id",
+    "ts_new_weights",
+]
