@@ -1,0 +1,381 @@
+"""Benchmark of the CountSketch matrix-ID hot path on B200.
+
+Workload (BASELINE.json configs[1], the largest single-GPU config): dense
+fp64 A of 1,000,000 x 2,000 with a rank-20 part and geometric tail
+0.9^(i-20) plus N(0, 1e-8) noise; K = 20, CountSketch rows L = 100,
+surjective hash.  One step = one countsketch_id of A: device hash draw
+(bit-exact numpy PCG64), bucket index, sketch, all-reduce (N > 1), k-step
+pivoted QR, triangular solve, and the j / P device->host copy.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun (N > 1) the rows are split into N contiguous blocks (strong
+scaling: total work fixed) and the L x R sketch is summed with one NCCL
+all-reduce.  A (16 GB) is larger than L2 (126 MB), so no flush is needed.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: rows, cols, k, L, low rank, tail ratio, noise std
+    "C2": dict(rows=1_000_000, cols=2_000, k=20, L=100, lowrank=20, ratio=0.9, noise=1e-4),
+    "C1": dict(rows=10_000, cols=1_000, k=10, L=40, lowrank=10, ratio=10 ** -0.1, noise=0.0),
+}
+METRIC = "sketch HBM GB/s (fraction of B200 peak); matrix ID seconds"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    p.add_argument("--rows", type=int, default=0, help="override rows (debug only)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-rows", type=int, default=200_000)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            m = json.load(fh)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def sigma_of(w):
+    i = np.arange(1, w["cols"] + 1, dtype=np.float64)
+    return np.where(i <= w["lowrank"], 1.0, w["ratio"] ** (i - w["lowrank"]))
+
+
+# ----------------------------------------------------------------- inputs --
+CHUNK = 125_000  # global rows per generator chunk (so A is identical for any N | 8)
+
+
+def make_rows_device(w, r0, r1, torch, dev):
+    """Rows [r0, r1) of A = U diag(sigma) V^T + noise, generated on the GPU.
+
+    U's rows are N(0, 1/rows) (columns orthonormal up to O(1/sqrt(rows))),
+    V is the Q factor of a seeded 2000 x 2000 Gaussian, both seeded per fixed
+    global chunk so every rank builds the same global matrix."""
+    cols = w["cols"]
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)
+    v = torch.linalg.qr(torch.randn(cols, cols, generator=g, device=dev, dtype=torch.float64))[0]
+    vs = (v * torch.from_numpy(sigma_of(w)).to(dev)).t().contiguous()  # diag(s) V^T
+    out = torch.empty((r1 - r0, cols), dtype=torch.float64, device=dev)
+    c = (r0 // CHUNK) * CHUNK
+    while c < r1:
+        c1 = min(c + CHUNK, w["rows"])
+        g.manual_seed(10_000 + c // CHUNK)
+        u = torch.randn(c1 - c, cols, generator=g, device=dev, dtype=torch.float64)
+        u /= float(np.sqrt(w["rows"]))
+        blk = u @ vs
+        if w["noise"] > 0:
+            blk += w["noise"] * torch.randn(c1 - c, cols, generator=g, device=dev,
+                                            dtype=torch.float64)
+        a, b = max(c, r0), min(c1, r1)
+        out[a - r0:b - r0] = blk[a - c:b - c]
+        del u, blk
+        c = c1
+    return out
+
+
+# ----------------------------------------------------------------- clocks --
+class Clocks:
+    def __init__(self, enabled):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        if not enabled:
+            return
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self, gpu_index):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) != gpu_index:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU -----
+def cpu_sample_gbs(w, rows, seed=0):
+    """The oracle port (reference algorithm on numpy/scipy/LAPACK) on a
+    bounded row sample of the workload; returns (GB/s, seconds, rows)."""
+    import oracle
+
+    rng = np.random.default_rng(7)
+    cols = w["cols"]
+    v = np.linalg.qr(rng.standard_normal((cols, cols)))[0]
+    u = rng.standard_normal((rows, cols)) / np.sqrt(w["rows"])
+    a = (u * sigma_of(w)) @ v.T
+    if w["noise"] > 0:
+        a += w["noise"] * rng.standard_normal(a.shape)
+    del u
+    t0 = time.perf_counter()
+    oracle.countsketch_id(a, w["k"], w["L"], seed=seed)
+    dt = time.perf_counter() - t0
+    return a.nbytes / dt / 1e9, dt, rows
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    rows = min(args.cpu_rows, w["rows"])
+    vals = []
+    for step in range(args.warmup + args.steps):
+        gbs, dt, _ = cpu_sample_gbs(w, rows, seed=step)
+        if step >= args.warmup:
+            vals.append((gbs, dt))
+    gb = float(np.median([v[0] for v in vals]))
+    sec = float(np.median([v[1] for v in vals]))
+    sample = (f"{rows} x {w['cols']} row sample of {args.workload} "
+              f"({rows * w['cols'] * 8 / 1e9:.2f} GB), full countsketch_id")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gb, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, w, world),
+        "cpu_baseline": {"value": gb, "unit": "GB/s", "cores": cores(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": gb, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_of(args, w, world):
+    rows = args.rows or w["rows"]
+    return {"workload": f"{args.workload}: dense fp64 {rows}x{w['cols']} countsketch_id "
+                        f"K={w['k']} L={w['L']} surjective",
+            "rows": rows, "cols": w["cols"], "rank": w["k"], "sketch_dim": w["L"],
+            "parallelism": f"rows{world}", "l2": "A (>126 MB) larger than L2, no flush"}
+
+
+# ----------------------------------------------------------------- GPU -----
+def main():
+    args = parse()
+    w = dict(WORKLOADS[args.workload])
+    if args.rows:
+        w["rows"] = args.rows
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, w, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_1901_10559_b200 as ids
+    from paper_1901_10559_b200 import _native
+    from paper_1901_10559_b200._inputs import dense_operand
+    from paper_1901_10559_b200.distributed import countsketch_id_sharded, row_block
+    from paper_1901_10559_b200.matrix_id import device_matrix_id
+
+    lib = _native.load()
+    r0, r1 = row_block(w["rows"], world, rank)
+    a_dev = make_rows_device(w, r0, r1, torch, dev)
+    torch.cuda.synchronize()
+    operand = dense_operand(a_dev)
+    bytes_local = a_dev.numel() * 8
+    bytes_total = w["rows"] * w["cols"] * 8
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(seed):
+        return countsketch_id_sharded(operand, r0, w["rows"], w["k"], w["L"], seed=seed)
+
+    # ---- device-resident steps (value) ----
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = Clocks(rank == 0)
+    n0 = lib.ids_launch_count()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    start.record()
+    for s in range(args.steps):
+        d = step(1000 + s)
+    stop.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = (lib.ids_launch_count() - n0) // max(args.steps, 1)
+    ms = start.elapsed_time(stop) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    clk = clocks.stop(local)
+
+    # ---- dominant kernel alone: the sketch (roofline) ----
+    op = ids.CountSketchOp(w["rows"], w["L"], seed=5, surjective=True)
+    y = torch.empty((w["cols"], w["L"]), dtype=torch.float64, device=dev)
+    op.bucket_index()
+    for _ in range(2):
+        op.sketch_into(operand, y, row0=r0, flags=1)
+    torch.cuda.synchronize()
+    reps = max(3, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        op.sketch_into(operand, y, row0=r0, flags=1)
+    e1.record()
+    torch.cuda.synchronize()
+    sk_ms = e0.elapsed_time(e1) / reps
+    # CPQR + coefficients alone (ID seconds without the sketch)
+    e0.record()
+    for _ in range(reps):
+        device_matrix_id(y, w["L"], w["cols"], w["k"])
+    e1.record()
+    torch.cuda.synchronize()
+    id_ms = e0.elapsed_time(e1) / reps
+    # hash draw alone
+    e0.record()
+    for s in range(reps):
+        ids.CountSketchOp(w["rows"], w["L"], seed=s, surjective=True).bucket_index()
+    e1.record()
+    torch.cuda.synchronize()
+    hash_ms = e0.elapsed_time(e1) / reps
+
+    peak, peak_kind = peaks()
+    achieved = bytes_local / (sk_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.workload)
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        try:
+            host = torch.empty((r1 - r0, w["cols"]), dtype=torch.float64, pin_memory=True)
+            host.copy_(a_dev, non_blocking=False)
+            del_dev = True
+        except RuntimeError:
+            host, del_dev = None, False
+        if host is not None:
+            def api(seed):
+                if world == 1:  # the call a user makes
+                    return ids.countsketch_id(host, w["k"], w["L"], seed=seed)
+                return countsketch_id_sharded(host, r0, w["rows"], w["k"], w["L"], seed=seed)
+
+            d = api(1)
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            e0.record()
+            nsteps = max(1, min(args.steps, 3))
+            for s in range(nsteps):
+                d = api(2000 + s)
+            e1.record()
+            torch.cuda.synchronize()
+            e2e_ms = e0.elapsed_time(e1) / nsteps
+            if world > 1:
+                t = torch.tensor([e2e_ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                e2e_ms = float(t.item())
+            e2e = {"value": bytes_total / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+                   "h2d_bytes_per_step": bytes_total,
+                   "d2h_bytes_per_step": int(d.coeffs.nbytes + d.cols.nbytes) * world,
+                   "ms_per_step": e2e_ms, "wall_s": time.perf_counter() - t0}
+            del host
+            _ = del_dev
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gbs, dt, rows = cpu_sample_gbs(w, min(args.cpu_rows, w["rows"]))
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores(), "kind": "port",
+               "sample": f"{rows} x {w['cols']} row sample of {args.workload}, full "
+                         f"countsketch_id in {dt:.2f} s (scipy S@A single-threaded, "
+                         f"LAPACK dgeqp3 multithreaded)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": bytes_total / (ms * 1e-3) / 1e9,
+            "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_of(args, w, world),
+            "id_seconds": ms * 1e-3,
+            "phases_ms": {"hash_and_index": hash_ms, "sketch": sk_ms, "cpqr_and_coeffs": id_ms},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "cs_rowmajor_kernel", "peak_kind": peak_kind,
+                         "bytes_per_launch": bytes_local},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/*
+ * idsketch_b200.h -- C ABI of the B200 CountSketch / TensorSketch ID hot path.
+ *
+ * The reference (arXiv 1901.10559's `idsketch` package, /root/reference/pkg)
+ * is pure Python and has no FFI of its own; each entry point below replaces
+ * the in-process native call the reference makes at the cited line (paths
+ * relative to /root/reference/pkg/src/idsketch).  INTEGRATION.md shows the
+ * ctypes binding that sits behind the reference's Python surface.
+ *
+ * Conventions
+ *   - All pointers except the explicitly host-side ones are DEVICE pointers.
+ *   - Every function takes the CUDA stream as `void* stream` (cudaStream_t),
+ *     enqueues asynchronously and never synchronizes, unless it says so.
+ *   - Temporary memory comes from a caller-owned workspace whose size the
+ *     matching *_workspace_bytes() query returns.  No hidden global state.
+ *   - Return value: IDS_OK or an error code; no exceptions cross the ABI.
+ *     ids_last_error() returns a thread-local message for the last failure.
+ *   - Matrices: "col-major" = Fortran order with leading dimension ld;
+ *     sketches Y are written col-major L x R (ld = L), the layout the
+ *     pivoted QR consumes (reference linalg.py:29 keeps F order).
+ *   - Reentrant: distinct workspaces / outputs may be used concurrently.
+ */
+#ifndef IDSKETCH_B200_H
+#define IDSKETCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    IDS_OK = 0,
+    IDS_EINVAL = 1,      /* -> ValueError (shapes, bounds)                     */
+    IDS_ENONFINITE = 2,  /* -> ValueError ("contains non-finite entries")      */
+    IDS_ESINGULAR = 3,   /* -> SingularTriangleError (linalg.py:141-144)       */
+    IDS_ECUDA = 4,       /* -> RuntimeError (CUDA launch / runtime failure)    */
+    IDS_EWORKSPACE = 5,  /* -> RuntimeError (workspace too small)              */
+    IDS_ERETRY = 6       /* internal: draw buffer exhausted, caller grows it   */
+};
+
+enum { IDS_ROW_MAJOR = 0, IDS_COL_MAJOR = 1 };
+
+/* flags for the CountSketch kernels */
+enum { IDS_FLAG_ORDERED = 1 /* force scipy's summation order (bit-exact Y) */ };
+
+const char* ids_last_error(void);
+int ids_version(void);
+/* Diagnostic: number of kernels this library has launched so far (process-wide). */
+int64_t ids_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Hash generation.  Replaces sketch.py:77-84 (CountSketchOp.__init__):
+ * numpy default_rng(seed) -> [integers(0,L,I-L); permutation(arange(L)++tail)]
+ * or integers(0,L,I); then integers(0,2,I)*2-1.  (state, inc) are the 128-bit
+ * PCG64 state numpy's SeedSequence produced, split into 64-bit halves.
+ * Outputs: bucket int32[in_dim] in [0, out_dim), sign int8[in_dim] in {-1,+1};
+ * draws_out (device int64[4], may be NULL): 32-bit draws consumed by phase A,
+ * phase B (permutation), signs, and a status word (0 ok).
+ * Bit-exact with numpy 2.3.5 for in_dim < 2^32.
+ * ------------------------------------------------------------------------- */
+size_t ids_hash_workspace_bytes(int64_t in_dim, int64_t out_dim, int surjective);
+int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                         uint64_t inc_lo, int64_t in_dim, int64_t out_dim,
+                         int surjective, int32_t* bucket, int8_t* sign,
+                         int64_t* draws_out, void* workspace, size_t ws_bytes,
+                         void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Bucket index: the rows of each bucket in increasing row order, i.e. the CSR
+ * structure of the L x I operator S that sketch.py:108-114 (`_matrix`) builds.
+ * order_signed[k] = row (sign +1) or ~row (sign -1); bstart int64[L+1].
+ * ------------------------------------------------------------------------- */
+size_t ids_bucket_index_workspace_bytes(int64_t in_dim, int64_t out_dim);
+int ids_bucket_index(const int32_t* bucket, const int8_t* sign, int64_t in_dim,
+                     int64_t out_dim, int32_t* order_signed, int64_t* bstart,
+                     void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Dense CountSketch Y (+)= S[:, row0:row0+rows] @ A.  Replaces sketch.py:119
+ * (`self._matrix @ a` -> scipy csr_matvecs) for dense A.
+ *   A: rows x cols, layout IDS_ROW_MAJOR (A[i*ld + c]) or IDS_COL_MAJOR
+ *      (A[c*ld + i]); local row i is global row row0 + i.
+ *   bucket/sign: the FULL hash (global rows); order_signed/bstart: the full
+ *      bucket index (used by the row-major path).
+ *   Y: col-major out_dim x cols.  accumulate = 0 overwrites, 1 adds.
+ *   nonfinite: device int32 flag, set to 1 when a sketch entry comes out
+ *      NaN/Inf (which an input NaN/Inf always causes; linalg.py:34 rejects
+ *      those); the host confirms with ids_dense_has_nonfinite before raising.
+ *   flags: IDS_FLAG_ORDERED forces one pass per bucket in scipy's order
+ *      (increasing row), making Y bit-identical to the reference.  Without
+ *      it the kernel may split long buckets into segments whose partial sums
+ *      are combined in a fixed order: still deterministic run to run.
+ * ------------------------------------------------------------------------- */
+size_t ids_countsketch_dense_workspace_bytes(int64_t rows, int64_t cols, int64_t out_dim,
+                                             int layout);
+int ids_countsketch_dense_f64(const double* A, int64_t rows, int64_t cols, int64_t ld,
+                              int layout, int64_t row0, int64_t in_dim,
+                              const int32_t* bucket, const int8_t* sign,
+                              const int32_t* order_signed, const int64_t* bstart,
+                              int64_t out_dim, double* Y, int accumulate, int flags,
+                              int32_t* nonfinite, void* workspace, size_t ws_bytes,
+                              void* stream);
+
+/* Exact isfinite scan of a dense matrix (host-confirmation path). */
+int ids_dense_has_nonfinite(const double* A, int64_t rows, int64_t cols, int64_t ld,
+                            int layout, int32_t* flag, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * CSC CountSketch Y (+)= S[:, row0:row0+rows] @ A for A in CSC form -- the
+ * reference's canonical sparse container (linalg.py:39-53).  colptr int64 or
+ * int32 [cols+1], rowidx int32[nnz] (local rows), data double[nnz].  With
+ * sorted row indices and no duplicates (canonical), Y is bit-identical to the
+ * reference's SpGEMM order.  nonfinite: as for the dense kernel (confirm with
+ * ids_values_has_nonfinite).
+ * ------------------------------------------------------------------------- */
+size_t ids_countsketch_csc_workspace_bytes(int64_t cols, int64_t out_dim);
+int ids_countsketch_csc_f64(const void* colptr, int colptr64, const int32_t* rowidx,
+                            const double* data, int64_t rows, int64_t cols, int64_t nnz,
+                            int64_t row0, int64_t in_dim, const int32_t* bucket,
+                            const int8_t* sign, int64_t out_dim, double* Y, int accumulate,
+                            int32_t* nonfinite, void* workspace, size_t ws_bytes, void* stream);
+
+/* Exact isfinite scan of a value array (sparse host-confirmation path). */
+int ids_values_has_nonfinite(const double* v, int64_t n, int32_t* flag, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * CSR CountSketch Y (+)= S[:, row0:row0+rows] @ A.  Replaces sketch.py:119 with
+ * CSC/CSR A (scipy csr_matmat after as_csc, linalg.py:39-53).
+ *   indptr: int64[rows+1] (indptr64 = 1) or int32[rows+1] (indptr64 = 0),
+ *   indices int32[nnz] (column ids < cols), data double[nnz].  Duplicate
+ *   entries are summed in storage order, explicit zeros are harmless.
+ * ------------------------------------------------------------------------- */
+size_t ids_countsketch_csr_workspace_bytes(int64_t rows, int64_t cols, int64_t nnz,
+                                           int64_t out_dim);
+int ids_countsketch_csr_f64(const void* indptr, int indptr64, const int32_t* indices,
+                            const double* data, int64_t rows, int64_t cols, int64_t nnz,
+                            int64_t row0, int64_t in_dim, const int32_t* bucket,
+                            const int8_t* sign, const int32_t* order_signed,
+                            const int64_t* bstart, int64_t out_dim, double* Y,
+                            int accumulate, int flags, int32_t* nonfinite, void* workspace,
+                            size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * TensorSketch of a Khatri-Rao product, scaled columnwise.  Replaces
+ * sketch.py:156-186 (per-mode csr_matvecs, rfft, spectrum product, irfft,
+ * x weights).  Never forms Khatri-Rao columns.
+ *   n_modes, and HOST arrays of per-mode DEVICE pointers:
+ *   factors[n]: col-major dims[n] x ncols with leading dimension lds[n];
+ *   order_signed[n], bstart[n]: bucket index of mode n (out_dim buckets).
+ *   weights: device double[ncols] or NULL.  Y: col-major out_dim x ncols.
+ *   colnorm2 (may be NULL): ||Y[:,r]||^2 per column.
+ * ------------------------------------------------------------------------- */
+size_t ids_tensorsketch_workspace_bytes(int n_modes, const int64_t* dims, int64_t ncols,
+                                        int64_t out_dim);
+int ids_tensorsketch_f64(int n_modes, const double* const* factors, const int64_t* dims,
+                         const int64_t* lds, int64_t ncols,
+                         const int32_t* const* order_signed, const int64_t* const* bstart,
+                         int64_t out_dim, const double* weights, double* Y,
+                         double* colnorm2, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Truncated column-pivoted Householder QR (k steps).  Replaces linalg.py:97-102
+ * (scipy.linalg.qr(pivoting=True) -> LAPACK dgeqp3 + dorgqr, truncation,
+ * numerical_rank).  Pivoting follows dgeqp3: largest partial column norm with
+ * LAPACK's norm downdating / tol3z recompute rule, ties to the lowest current
+ * position.
+ *   Y: col-major rows x cols (ld = ldy), not modified.
+ *   perm int32[cols]: the k pivots first, then the remaining columns.
+ *   Rtop: row-major k x cols (R[:k, :] in pivoted order).
+ *   Q: col-major rows x k or NULL.   numerical_rank: device int32[1].
+ * ------------------------------------------------------------------------- */
+size_t ids_cpqr_workspace_bytes(int64_t rows, int64_t cols, int64_t k);
+int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, int64_t ldy,
+                       int64_t k, double rank_tol, int32_t* perm, double* Rtop,
+                       double* Q, int32_t* numerical_rank, void* workspace,
+                       size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * ID coefficients from the truncated factorization.  Replaces
+ * matrix_id.py:56-84 (_coeffs_from_pivoted) + linalg.py:130-147: floor
+ * |R11[d,d]| < rank_tol*|R11[0,0]| to +-floor when numerical_rank < k,
+ * T = R11^{-1} R12, P[:, perm[:k]] = I exactly, P[:, perm[k:]] = T; zero input
+ * gives T = 0.   P: row-major k x cols.  deficient: device int32[1].
+ * ------------------------------------------------------------------------- */
+size_t ids_id_coeffs_workspace_bytes(int64_t k, int64_t cols);
+int ids_id_coeffs_f64(const double* Rtop, const int32_t* perm, int64_t k, int64_t cols,
+                      double rank_tol, const int32_t* numerical_rank, double* P,
+                      int32_t* deficient, void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Upper/lower triangular solve r @ x = b (linalg.py:130-147).  r row-major
+ * n x n, b/x row-major n x m.  Synchronizes the stream to report an exactly
+ * zero diagonal as IDS_ESINGULAR with *bad_index set (host int64).
+ * ------------------------------------------------------------------------- */
+int ids_triangular_solve_f64(const double* r, const double* b, int64_t n, int64_t m,
+                             int lower, double* x, int64_t* bad_index, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IDSKETCH_B200_H */

@@ -1,0 +1,50 @@
+"""B200-native CountSketch / TensorSketch interpolative decomposition.
+
+Drop-in for the hot path of the reference package ``idsketch`` (arXiv
+1901.10559): the public names below keep the reference's signatures,
+defaults, return layout and exceptions (reference ``pkg/src/idsketch/
+__init__.py:9-86``), restricted to the CountSketch matrix ID and TensorSketch
+tensor ID path.  All compute runs in hand-written sm_100a kernels reached
+through the C ABI of ``include/idsketch_b200.h`` (``libidsketch_b200.so``);
+there is no CPU fallback.
+"""
+
+from .cp_tensor import (
+    CpTensor,
+    TensorIdResult,
+    check_tensor_id_args,
+    tensor_id_from_sketch,
+    tensorsketch_id,
+)
+from .errors import SingularTriangleError
+from .linalg import DEFAULT_RANK_TOL, PivotedQr, cpqr, triangular_solve
+from .matrix_id import (
+    InterpolativeDecomposition,
+    check_matrix_id_args,
+    countsketch_id,
+    matrix_id,
+    matrix_sketch,
+)
+from .sketch import CountSketchOp, TensorSketchOp
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CountSketchOp",
+    "CpTensor",
+    "DEFAULT_RANK_TOL",
+    "InterpolativeDecomposition",
+    "PivotedQr",
+    "SingularTriangleError",
+    "TensorIdResult",
+    "TensorSketchOp",
+    "check_matrix_id_args",
+    "check_tensor_id_args",
+    "countsketch_id",
+    "cpqr",
+    "matrix_id",
+    "matrix_sketch",
+    "tensor_id_from_sketch",
+    "tensorsketch_id",
+    "triangular_solve",
+]

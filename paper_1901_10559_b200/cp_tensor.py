@@ -1,0 +1,223 @@
+"""CP tensors and TensorSketch rank reduction on B200.
+
+Drop-in for the hot-path part of reference ``pkg/src/idsketch/cp_tensor.py``:
+``CpTensor`` (:41-128, the input/output container), ``TensorIdResult``
+(:200-212), ``tensor_id_from_sketch`` (:235-239), ``check_tensor_id_args``
+(:242-263) and ``tensorsketch_id`` (:266-276).  The sketch and the ID run on
+the device; the recombined weights ``weights[cols] * coeffs.sum(axis=1)``
+(:216) are formed on the host from the returned coefficients so they equal
+numpy's own evaluation bit for bit (the reference test
+test_cp_tensor.py:193-203 demands array_equal).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from .linalg import DEFAULT_RANK_TOL
+from .matrix_id import DEFAULT_OVERSAMPLE, device_matrix_id, matrix_id
+from .sketch import TensorSketchOp
+
+TENSOR_METHODS = ("tensorsketch",)
+_MAX_DENSE_ENTRIES = 50_000_000
+
+
+def _canon_factor(f, n):
+    if sp.issparse(f):
+        out = sp.csc_array(f, dtype=np.float64)
+        out.sum_duplicates()
+        out.eliminate_zeros()
+        out.sort_indices()
+        if out.nnz and not np.isfinite(out.data).all():
+            raise ValueError("a contains non-finite entries")
+        return out
+    out = np.asfortranarray(f, dtype=np.float64)
+    if out.ndim != 2:
+        raise ValueError(f"factor {n} must be 2-D, got ndim={out.ndim}")
+    if out.size == 0:
+        raise ValueError(f"factor {n} must be nonempty")
+    if not np.isfinite(out).all():
+        raise ValueError(f"factor {n} contains non-finite entries")
+    return out
+
+
+def _col_norms(f):
+    if sp.issparse(f):
+        return np.sqrt(np.asarray(f.power(2).sum(axis=0)).ravel())
+    return np.linalg.norm(f, axis=0)
+
+
+def _scaled(f, scale):
+    if sp.issparse(f):
+        out = sp.csc_array(f @ sp.diags_array(scale), dtype=np.float64)
+        out.sum_duplicates()
+        out.eliminate_zeros()
+        out.sort_indices()
+        return out
+    return f * scale
+
+
+def _unit_columns(f, cols):
+    """Replace zero columns by e_0 (cp_tensor.py:131-141)."""
+    if sp.issparse(f):
+        lil = f.tolil()
+        for c in cols:
+            lil[:, c] = 0.0
+            lil[0, c] = 1.0
+        return _canon_factor(lil, 0)
+    f = f.copy()
+    f[:, cols] = 0.0
+    f[0, cols] = 1.0
+    return f
+
+
+class CpTensor:
+    """CP tensor: nonnegative `weights` (R) and one unit-column factor per mode
+    (cp_tensor.py:41-95).  Norms and the sign that keeps weights nonnegative
+    (applied to mode 0) are folded into the weights; zero columns get weight 0
+    and an arbitrary unit vector.  Columns already unit to 1e-12 are kept bit
+    for bit, so selecting terms is an exact column-subset operation."""
+
+    def __init__(self, weights, factors):
+        if len(factors) == 0:
+            raise ValueError("need at least one factor matrix")
+        factors = [_canon_factor(f, n) for n, f in enumerate(factors)]
+        rank = factors[0].shape[1]
+        for n, f in enumerate(factors):
+            if f.shape[1] != rank:
+                raise ValueError(f"factor {n} has {f.shape[1]} columns, expected {rank}")
+        weights = np.asarray(weights, dtype=np.float64).copy()
+        if weights.shape != (rank,):
+            raise ValueError(f"weights must have length {rank}")
+        if not np.isfinite(weights).all():
+            raise ValueError("weights must be finite")
+        zero_cols = np.zeros(rank, dtype=bool)
+        normalized = []
+        for f in factors:
+            norms = _col_norms(f)
+            zero = norms == 0.0
+            zero_cols |= zero
+            norms = np.where(np.abs(norms - 1.0) <= 1e-12, 1.0, norms)
+            if np.any(norms != 1.0):
+                f = _scaled(f, 1.0 / np.where(zero, 1.0, norms))
+            if zero.any():
+                f = _unit_columns(f, np.flatnonzero(zero))
+            weights *= np.where(zero, 0.0, norms)
+            normalized.append(f)
+        negative = weights < 0.0
+        if negative.any():
+            normalized[0] = _scaled(normalized[0], np.where(negative, -1.0, 1.0))
+            weights = np.abs(weights)
+        self.weights = weights
+        self.factors = normalized
+        self.zero_columns = np.flatnonzero(zero_cols)
+
+    @property
+    def rank(self):
+        return self.weights.size
+
+    @property
+    def ndim(self):
+        return len(self.factors)
+
+    @property
+    def mode_dims(self):
+        return tuple(f.shape[0] for f in self.factors)
+
+    @property
+    def total_entries(self):
+        return int(np.prod(self.mode_dims))
+
+    def select(self, cols, weights):
+        """CP tensor built from the given term indices and new weights."""
+        return CpTensor(weights, [f[:, cols] for f in self.factors])
+
+    def to_dense(self, max_entries=_MAX_DENSE_ENTRIES):
+        """Materialize the full tensor (testing and small problems only)."""
+        if self.total_entries > max_entries:
+            raise ValueError("tensor too large to densify")
+        out = np.zeros(self.mode_dims)
+        for r in range(self.rank):
+            term = np.array(self.weights[r])
+            for f in self.factors:
+                col = f[:, [r]].toarray().ravel() if sp.issparse(f) else f[:, r]
+                term = np.multiply.outer(term, col)
+            out += term
+        return out
+
+
+@dataclass(frozen=True)
+class TensorIdResult:
+    """Rank reduction output (cp_tensor.py:200-212): new_weights[k] =
+    weights[cols[k]] * coeffs[k, :].sum()."""
+
+    reduced: CpTensor
+    cols: np.ndarray
+    coeffs: np.ndarray
+    new_weights: np.ndarray
+    method: str
+    numerical_rank: int
+    rank_deficient: bool
+
+
+def _assemble(x, decomp, method):
+    """cp_tensor.py:215-232."""
+    new_weights = x.weights[decomp.cols] * decomp.coeffs.sum(axis=1)
+    reduced_weights = new_weights
+    if decomp.rank_deficient:
+        reduced_weights = new_weights.copy()
+        reduced_weights[decomp.numerical_rank:] = 0.0
+    reduced = x.select(decomp.cols, reduced_weights)
+    return TensorIdResult(
+        reduced=reduced, cols=decomp.cols, coeffs=decomp.coeffs, new_weights=new_weights,
+        method=method, numerical_rank=decomp.numerical_rank,
+        rank_deficient=decomp.rank_deficient,
+    )
+
+
+def tensor_id_from_sketch(x, sketch, rank, method, rank_tol=DEFAULT_RANK_TOL):
+    """ID of a (host or device) sketch, then recombined weights (cp_tensor.py:235-239)."""
+    decomp = matrix_id(sketch, rank, rank_tol=rank_tol)
+    return _assemble(x, decomp, method)
+
+
+def check_tensor_id_args(x, rank, sketch_dim, method):
+    """cp_tensor.py:242-263."""
+    if not 1 <= rank <= x.rank:
+        raise ValueError(f"rank must be in [1, {x.rank}], got {rank}")
+    if method == "gram":
+        return None
+    if sketch_dim is None:
+        sketch_dim = rank + DEFAULT_OVERSAMPLE
+    if sketch_dim < rank:
+        raise ValueError(f"sketch dimension {sketch_dim} is below the target rank {rank}")
+    if method == "tensorsketch" and sketch_dim >= x.total_entries:
+        raise ValueError(f"sketch dimension {sketch_dim} must be < {x.total_entries} tensor entries")
+    return sketch_dim
+
+
+def tensorsketch_device(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL):
+    """Device half of tensorsketch_id: (DeviceId, sketch (R, L))."""
+    sketch_dim = check_tensor_id_args(x, rank, sketch_dim, "tensorsketch")
+    op = TensorSketchOp(x.mode_dims, sketch_dim, seed=seed)
+    y = op.apply_device(x.factors, x.weights)
+    return device_matrix_id(y, sketch_dim, x.rank, rank, rank_tol), y
+
+
+def tensorsketch_id(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL):
+    """Rank reduction via a TensorSketch of the flattened rank-1 terms
+    (cp_tensor.py:266-276)."""
+    d, _ = tensorsketch_device(x, rank, sketch_dim, seed, rank_tol)
+    return _assemble(x, d.to_host("tensorsketch"), "tensorsketch")
+
+
+__all__ = [
+    "CpTensor",
+    "TENSOR_METHODS",
+    "TensorIdResult",
+    "check_tensor_id_args",
+    "tensor_id_from_sketch",
+    "tensorsketch_device",
+    "tensorsketch_id",
+]

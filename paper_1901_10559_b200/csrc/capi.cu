@@ -1,0 +1,23 @@
+// Error reporting and version of the C ABI (include/idsketch_b200.h).
+#include <string.h>
+
+#include <atomic>
+
+#include "common.cuh"
+
+static thread_local char g_last_error[512] = "";
+
+void ids_set_last_error(const char* msg) {
+    strncpy(g_last_error, msg ? msg : "", sizeof(g_last_error) - 1);
+    g_last_error[sizeof(g_last_error) - 1] = '\0';
+}
+
+extern "C" const char* ids_last_error(void) { return g_last_error; }
+
+extern "C" int ids_version(void) { return 1; }
+
+static std::atomic<long long> g_launches{0};
+
+void ids_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" int64_t ids_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }

@@ -1,0 +1,73 @@
+// Shared helpers for the idsketch-b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/idsketch_b200.h"
+
+#define IDS_CUDA_TRY(expr)                                   \
+    do {                                                     \
+        cudaError_t _e = (expr);                             \
+        if (_e != cudaSuccess) {                             \
+            ids_set_last_error(cudaGetErrorString(_e));      \
+            return IDS_ECUDA;                                \
+        }                                                    \
+    } while (0)
+
+#define IDS_LAUNCH_CHECK()                                   \
+    do {                                                     \
+        ids_count_launch();                                  \
+        cudaError_t _e = cudaGetLastError();                 \
+        if (_e != cudaSuccess) {                             \
+            ids_set_last_error(cudaGetErrorString(_e));      \
+            return IDS_ECUDA;                                \
+        }                                                    \
+    } while (0)
+
+void ids_set_last_error(const char* msg);
+void ids_count_launch();
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+template <class T>
+__host__ __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+template <class T>
+__host__ __device__ __forceinline__ T tmax(T a, T b) { return a < b ? b : a; }
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Simple bump allocator over a caller-owned workspace.
+struct WsCarve {
+    char* base;
+    size_t cap;
+    size_t off;
+    __host__ WsCarve(void* b, size_t c) : base(static_cast<char*>(b)), cap(c), off(0) {}
+    template <class T>
+    __host__ T* take(size_t n) {
+        off = align_up(off, 256);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += n * sizeof(T);
+        return p;
+    }
+    __host__ bool ok() const { return off <= cap; }
+};
+
+// Byte count the same carve sequence needs (workspace query helpers).
+struct WsCount {
+    size_t off = 0;
+    template <class T>
+    void take(size_t n) {
+        off = align_up(off, 256);
+        off += n * sizeof(T);
+    }
+};
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
+
+// Signed-row encoding used by the bucket index: row >= 0 with sign +1 is
+// stored as row, sign -1 as ~row (negative).
+__device__ __forceinline__ int32_t enc_row(int32_t row, int8_t s) { return s > 0 ? row : ~row; }
+__device__ __forceinline__ int32_t dec_row(int32_t e) { return e >= 0 ? e : ~e; }

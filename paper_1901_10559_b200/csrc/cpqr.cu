@@ -1,0 +1,581 @@
+// Truncated column-pivoted Householder QR + ID coefficients on B200.
+//
+// Replaces reference linalg.py:76-103 (cpqr: scipy.linalg.qr(pivoting=True)
+// -> LAPACK dgeqp3/dorgqr, then truncation to k rows and numerical_rank) and
+// matrix_id.py:56-84 (_coeffs_from_pivoted) + linalg.py:130-147
+// (triangular_solve -> dtrtrs).
+//
+// Only k pivots are ever needed (k = rank <= sketch_dim), so the factorization
+// runs k steps of LAPACK's pivoting rule and never touches the trailing
+// matrix: like dlaqps it keeps the Householder vectors V (m x k) and the
+// update factors F (n x k) so that the partially reduced matrix is
+// Y - V F^T, and each step needs ONE streaming pass over Y (the GEMV
+// Y^T v).  One persistent cooperative grid runs all k steps; column j is
+// owned by one CTA for the whole factorization, rows are split across CTAs
+// for the pivot-column work, and three grid-wide barriers separate the
+// phases of a step (argmax -> pivot column -> GEMV -> downdate).
+//
+// Pivot rule (dgeqp3 / dlaqps): pivot = largest partial norm vn1 over the
+// remaining columns, ties to the lowest current position (idamax); norms are
+// downdated with LAPACK's formula and recomputed exactly when the downdate
+// is untrustworthy (temp2 <= tol3z = sqrt(eps)).
+#include <cooperative_groups.h>
+
+#include <float.h>
+#include <math.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+struct ArgMax {
+    double val;
+    int64_t pos;
+    int64_t col;
+    int64_t col_at_next;  // column currently at position (step + 1), or -1
+};
+
+__device__ __forceinline__ bool better(double v, int64_t p, double bv, int64_t bp) {
+    // larger value wins; equal values -> lower position (first max, idamax)
+    return v > bv || (v == bv && p < bp);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// LAPACK dlapy2: sqrt(x^2 + y^2) avoiding overflow.
+__device__ __forceinline__ double dlapy2(double x, double y) {
+    const double xa = fabs(x), ya = fabs(y);
+    const double w = fmax(xa, ya), z = fmin(xa, ya);
+    if (z == 0.0 || w > DBL_MAX) return w;
+    const double r = z / w;
+    return w * sqrt(1.0 + r * r);
+}
+
+struct CpqrArgs {
+    const double* Y;
+    int64_t m, n, ldy, k;
+    double rank_tol;
+    int32_t* perm;
+    double* Rtop;
+    int32_t* numerical_rank;
+    // workspace
+    double *vn1, *vn2, *F, *Rcol, *W, *V, *tau, *beta, *a, *normpart, *zpart;
+    int64_t* pos;
+    ArgMax* amax;
+};
+
+// Block-wide sum of one double per thread; result valid in all threads.
+__device__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < kWarps; ++i) s += red[i];
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double vsm[];  // v of the current step (m), then z (k)
+    double* zsh = vsm + g.m;
+    __shared__ double red[kWarps];
+    __shared__ ArgMax warp_best[kWarps];
+    __shared__ int64_t s_piv[3];
+
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    const int64_t m = g.m, n = g.n, k = g.k, ldy = g.ldy;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c0 = n * b / G, c1 = n * (b + 1) / G;   // owned columns
+    const int64_t r0 = m * b / G, r1 = m * (b + 1) / G;   // owned rows
+    const double tol3z = sqrt(DBL_EPSILON);
+
+    // local argmax over owned columns with pos >= pmin; reports column at pnext
+    auto local_argmax = [&](int64_t pmin, int64_t pnext) {
+        ArgMax best{-1.0, INT64_MAX, -1, -1};
+        for (int64_t j = c0 + threadIdx.x; j < c1; j += kThreads) {
+            const int64_t pj = g.pos[j];
+            if (pj == pnext) best.col_at_next = j;
+            if (pj >= pmin) {
+                const double v = g.vn1[j];
+                if (better(v, pj, best.val, best.pos)) {
+                    best.val = v;
+                    best.pos = pj;
+                    best.col = j;
+                }
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            ArgMax ot;
+            ot.val = __shfl_xor_sync(0xffffffffu, best.val, o);
+            ot.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
+            ot.col = __shfl_xor_sync(0xffffffffu, best.col, o);
+            ot.col_at_next = __shfl_xor_sync(0xffffffffu, best.col_at_next, o);
+            if (better(ot.val, ot.pos, best.val, best.pos)) {
+                best.val = ot.val;
+                best.pos = ot.pos;
+                best.col = ot.col;
+            }
+            if (ot.col_at_next >= 0) best.col_at_next = ot.col_at_next;
+        }
+        if (lane == 0) warp_best[wid] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ArgMax r = warp_best[0];
+            for (int i = 1; i < kWarps; ++i) {
+                const ArgMax o = warp_best[i];
+                if (better(o.val, o.pos, r.val, r.pos)) {
+                    r.val = o.val;
+                    r.pos = o.pos;
+                    r.col = o.col;
+                }
+                if (o.col_at_next >= 0) r.col_at_next = o.col_at_next;
+            }
+            g.amax[b] = r;
+        }
+        __syncthreads();
+    };
+
+    // ---- prologue: column norms (dnrm2), positions ----
+    for (int64_t j = c0 + wid; j < c1; j += kWarps) {
+        const double* y = g.Y + j * ldy;
+        double s = 0.0;
+        for (int64_t r = lane; r < m; r += 32) s = fma(y[r], y[r], s);
+        s = warp_sum(s);
+        if (lane == 0) {
+            g.vn1[j] = sqrt(s);
+            g.vn2[j] = sqrt(s);
+            g.pos[j] = j;
+        }
+    }
+    __syncthreads();
+    local_argmax(0, 0);
+    grid.sync();
+
+    for (int64_t kk = 0; kk < k; ++kk) {
+        // ---- S1: global pivot, position swap, distributed pivot column ----
+        if (threadIdx.x == 0) {
+            ArgMax r = g.amax[0];
+            for (int64_t i = 1; i < G; ++i) {
+                const ArgMax o = g.amax[i];
+                if (better(o.val, o.pos, r.val, r.pos)) {
+                    r.val = o.val;
+                    r.pos = o.pos;
+                    r.col = o.col;
+                }
+                if (o.col_at_next >= 0) r.col_at_next = o.col_at_next;
+            }
+            s_piv[0] = r.col;          // pivot column c*
+            s_piv[1] = r.pos;          // its position p*
+            s_piv[2] = r.col_at_next;  // column at position kk
+        }
+        __syncthreads();
+        const int64_t cs = s_piv[0], ps = s_piv[1], ck = s_piv[2];
+        if (threadIdx.x == 0) {
+            if (ck >= c0 && ck < c1 && ck != cs) g.pos[ck] = ps;
+            if (cs >= c0 && cs < c1) g.pos[cs] = kk;
+        }
+        {
+            const double* ycol = g.Y + cs * ldy;
+            const double* fr = g.F + cs * k;
+            double ss = 0.0;
+            for (int64_t r = max(r0, kk) + threadIdx.x; r < r1; r += kThreads) {
+                double v = ycol[r];
+                for (int64_t q = 0; q < kk; ++q) v = fma(-g.V[q * m + r], fr[q], v);
+                g.a[r] = v;
+                if (r > kk) ss = fma(v, v, ss);
+            }
+            ss = block_sum(ss, red);
+            if (threadIdx.x == 0) g.normpart[b] = ss;
+        }
+        grid.sync();
+
+        // ---- S2: Householder vector (redundantly per CTA), z partials, GEMV ----
+        double xs = 0.0;
+        for (int64_t i = 0; i < G; ++i) xs += g.normpart[i];
+        const double xnorm = sqrt(xs);
+        const double alpha = g.a[kk];
+        double tau, beta, scal;
+        if (xnorm == 0.0) {
+            tau = 0.0;
+            beta = alpha;
+            scal = 0.0;
+        } else {
+            beta = -copysign(dlapy2(alpha, xnorm), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        for (int64_t r = kk + threadIdx.x; r < m; r += kThreads)
+            vsm[r] = (r == kk) ? 1.0 : g.a[r] * scal;
+        __syncthreads();
+        if (b == 0) {
+            for (int64_t r = threadIdx.x; r < m; r += kThreads)
+                g.V[kk * m + r] = r < kk ? 0.0 : vsm[r];
+            if (threadIdx.x == 0) {
+                g.tau[kk] = tau;
+                g.beta[kk] = beta;
+            }
+        }
+        if (threadIdx.x == 0 && cs >= c0 && cs < c1) g.Rcol[cs * k + kk] = beta;
+        // z partials: z_q = V[:, q]^T v over owned rows >= kk
+        for (int64_t q = wid; q < kk; q += kWarps) {
+            double s = 0.0;
+            for (int64_t r = max(r0, kk) + lane; r < r1; r += 32) s = fma(g.V[q * m + r], vsm[r], s);
+            s = warp_sum(s);
+            if (lane == 0) g.zpart[b * k + q] = s;
+        }
+        // GEMV over owned remaining columns: W_j = Y[kk:, j]^T v
+        for (int64_t j = c0 + wid; j < c1; j += kWarps) {
+            if (g.pos[j] <= kk) continue;
+            const double* y = g.Y + j * ldy;
+            double s = 0.0;
+            for (int64_t r = kk + lane; r < m; r += 32) s = fma(y[r], vsm[r], s);
+            s = warp_sum(s);
+            if (lane == 0) g.W[j] = s;
+        }
+        grid.sync();
+
+        // ---- S3: F column, row kk of R, norm downdate, next argmax ----
+        for (int64_t q = threadIdx.x; q < kk; q += kThreads) {
+            double s = 0.0;
+            for (int64_t i = 0; i < G; ++i) s += g.zpart[i * k + q];
+            zsh[q] = s;
+        }
+        __syncthreads();
+        for (int64_t j = c0 + wid; j < c1; j += kWarps) {
+            if (g.pos[j] <= kk) continue;
+            double* fr = g.F + j * k;
+            double rk = 0.0, vn1 = 0.0;
+            bool recompute = false;
+            if (lane == 0) {
+                double f = g.W[j];
+                for (int64_t q = 0; q < kk; ++q) f = fma(-fr[q], zsh[q], f);
+                f *= tau;
+                fr[kk] = f;
+                rk = g.Y[j * ldy + kk];
+                for (int64_t q = 0; q < kk; ++q) rk = fma(-g.V[q * m + kk], fr[q], rk);
+                rk -= f;  // V[kk, kk] = 1
+                g.Rcol[j * k + kk] = rk;
+                vn1 = g.vn1[j];
+                if (kk < m - 1 && vn1 != 0.0) {
+                    double temp = fabs(rk) / vn1;
+                    temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+                    const double ratio = vn1 / g.vn2[j];
+                    const double temp2 = temp * ratio * ratio;
+                    if (temp2 <= tol3z) recompute = true;
+                    else g.vn1[j] = vn1 * sqrt(temp);
+                }
+            }
+            recompute = __shfl_sync(0xffffffffu, recompute, 0);
+            __syncwarp();
+            if (recompute) {
+                const double* y = g.Y + j * ldy;
+                double s = 0.0;
+                for (int64_t r = kk + 1 + lane; r < m; r += 32) {
+                    double v = y[r];
+                    for (int64_t q = 0; q < kk; ++q) v = fma(-g.V[q * m + r], fr[q], v);
+                    v = fma(-vsm[r], fr[kk], v);
+                    s = fma(v, v, s);
+                }
+                s = warp_sum(s);
+                if (lane == 0) {
+                    g.vn1[j] = sqrt(s);
+                    g.vn2[j] = sqrt(s);
+                }
+            }
+        }
+        __syncthreads();
+        local_argmax(kk + 1, kk + 1);
+        grid.sync();
+    }
+
+    // ---- outputs: perm, Rtop, numerical rank ----
+    for (int64_t j = c0 + threadIdx.x; j < c1; j += kThreads) {
+        const int64_t p = g.pos[j];
+        g.perm[p] = (int32_t)j;
+        for (int64_t q = 0; q < k; ++q)
+            g.Rtop[q * n + p] = (p >= q) ? g.Rcol[j * k + q] : 0.0;
+    }
+    if (b == 0 && threadIdx.x == 0) {
+        const double lead = fabs(g.beta[0]);
+        int32_t nr = 0;
+        if (lead != 0.0)
+            for (int64_t q = 0; q < k; ++q) nr += fabs(g.beta[q]) > g.rank_tol * lead ? 1 : 0;
+        *g.numerical_rank = nr;
+    }
+}
+
+// Q[:, c] = H_0 H_1 ... H_c e_c  (dorgqr's explicit Q, first k columns)
+__global__ void __launch_bounds__(kThreads) form_q_kernel(const double* __restrict__ V,
+                                                          const double* __restrict__ tau,
+                                                          int64_t m, int64_t k, double* Q) {
+    __shared__ double red[kWarps];
+    const int64_t c = blockIdx.x;
+    double* q = Q + c * m;
+    for (int64_t r = threadIdx.x; r < m; r += kThreads) q[r] = (r == c) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int64_t h = c; h >= 0; --h) {
+        const double* v = V + h * m;
+        double s = 0.0;
+        for (int64_t r = h + threadIdx.x; r < m; r += kThreads) s = fma(v[r], q[r], s);
+        s = block_sum(s, red);
+        const double t = tau[h] * s;
+        for (int64_t r = h + threadIdx.x; r < m; r += kThreads) q[r] = fma(-t, v[r], q[r]);
+        __syncthreads();
+    }
+}
+
+// One thread per non-selected position p >= k: T[:, p-k] = R11^{-1} R12[:, p-k]
+// by back substitution in the order of reference BLAS dtrsm (column sweep
+// from the last row up), with LAPACK-side diagonal flooring
+// (matrix_id.py:68-79).  T: row-major k x (n - k) scratch.
+__global__ void id_solve_kernel(const double* __restrict__ Rtop, int64_t k, int64_t n,
+                                double rank_tol, const int32_t* __restrict__ numerical_rank,
+                                double* __restrict__ T) {
+    const int64_t nt = n - k;
+    const double lead = fabs(Rtop[0]);
+    const bool deficient = *numerical_rank < k;
+    const double floorv = rank_tol * lead;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nt;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        if (lead == 0.0) {
+            for (int64_t q = 0; q < k; ++q) T[q * nt + p] = 0.0;
+            continue;
+        }
+        for (int64_t q = 0; q < k; ++q) T[q * nt + p] = Rtop[q * n + k + p];
+        for (int64_t q = k - 1; q >= 0; --q) {
+            double d = Rtop[q * n + q];
+            if (deficient && fabs(d) < floorv) d = d < 0.0 ? -floorv : floorv;
+            double tq = T[q * nt + p];
+            if (tq != 0.0) {
+                tq = tq / d;
+                T[q * nt + p] = tq;
+                for (int64_t i = 0; i < q; ++i)
+                    T[i * nt + p] = fma(-tq, Rtop[i * n + q], T[i * nt + p]);
+            }
+        }
+    }
+}
+
+// P[q, perm[c]] = (c < k) ? (q == c) : T[q, c - k]   (row-major k x n)
+__global__ void id_scatter_kernel(const double* __restrict__ T, const int32_t* __restrict__ perm,
+                                  int64_t k, int64_t n, double* __restrict__ P) {
+    const int64_t nt = n - k;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < k * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = e / n, c = e % n;
+        const int64_t col = perm[c];
+        P[q * n + col] = (c < k) ? (q == c ? 1.0 : 0.0) : T[q * nt + (c - k)];
+    }
+}
+
+__global__ void deficient_kernel(const int32_t* nr, int64_t k, int32_t* deficient) {
+    *deficient = (*nr < k) ? 1 : 0;
+}
+
+// Generic triangular solve r x = b (reference dtrsm loop order), one thread
+// per right-hand-side column.  r row-major n x n, b/x row-major n x m.
+__global__ void trsm_kernel(const double* __restrict__ r, const double* __restrict__ b,
+                            int64_t n, int64_t m, int lower, double* __restrict__ x) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < m;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        for (int64_t i = 0; i < n; ++i) x[i * m + c] = b[i * m + c];
+        if (!lower) {
+            for (int64_t q = n - 1; q >= 0; --q) {
+                double t = x[q * m + c];
+                if (t != 0.0) {
+                    t /= r[q * n + q];
+                    x[q * m + c] = t;
+                    for (int64_t i = 0; i < q; ++i) x[i * m + c] = fma(-t, r[i * n + q], x[i * m + c]);
+                }
+            }
+        } else {
+            for (int64_t q = 0; q < n; ++q) {
+                double t = x[q * m + c];
+                if (t != 0.0) {
+                    t /= r[q * n + q];
+                    x[q * m + c] = t;
+                    for (int64_t i = q + 1; i < n; ++i)
+                        x[i * m + c] = fma(-t, r[i * n + q], x[i * m + c]);
+                }
+            }
+        }
+    }
+}
+
+template <class W>
+void carve_cpqr(W& ws, int64_t m, int64_t n, int64_t k, int64_t G, CpqrArgs& a) {
+    a.vn1 = ws.template take<double>(n);
+    a.vn2 = ws.template take<double>(n);
+    a.F = ws.template take<double>(n * k);
+    a.Rcol = ws.template take<double>(n * k);
+    a.W = ws.template take<double>(n);
+    a.V = ws.template take<double>(m * k);
+    a.tau = ws.template take<double>(k);
+    a.beta = ws.template take<double>(k);
+    a.a = ws.template take<double>(m);
+    a.normpart = ws.template take<double>(G);
+    a.zpart = ws.template take<double>(G * k);
+    a.pos = ws.template take<int64_t>(n);
+    a.amax = ws.template take<ArgMax>(G);
+}
+
+struct CountCarve {
+    size_t off = 0;
+    template <class T>
+    T* take(size_t cnt) {
+        off = align_up(off, 256) + cnt * sizeof(T);
+        return nullptr;
+    }
+};
+
+int grid_size(int64_t m, int64_t n, size_t smem) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_kernel, kThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    // ~ one warp per owned column at least; tiny problems use few CTAs
+    const int64_t want = tmax<int64_t>(1, tmin<int64_t>(ceil_div(n, 2 * kWarps), (int64_t)sms));
+    const int64_t by_rows = tmax<int64_t>(1, ceil_div(m * n, 16384));
+    return (int)tmin<int64_t>((int64_t)sms * per_sm, min(want, tmax<int64_t>(by_rows, 1)));
+}
+
+constexpr int64_t kMaxG = 148;
+
+}  // namespace
+
+extern "C" size_t ids_cpqr_workspace_bytes(int64_t rows, int64_t cols, int64_t k) {
+    CountCarve c;
+    CpqrArgs a{};
+    carve_cpqr(c, rows, cols, k, kMaxG, a);
+    return c.off + 256;
+}
+
+extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, int64_t ldy,
+                                  int64_t k, double rank_tol, int32_t* perm, double* Rtop,
+                                  double* Q, int32_t* numerical_rank, void* workspace,
+                                  size_t ws_bytes, void* stream) {
+    if (rows < 1 || cols < 1 || k < 1 || k > rows || k > cols || ldy < rows || k > 64 * 1024) {
+        ids_set_last_error("cpqr: bad arguments (need 1 <= k <= min(rows, cols))");
+        return IDS_EINVAL;
+    }
+    cudaStream_t st = as_stream(stream);
+    const size_t smem = (size_t)(rows + k) * sizeof(double);
+    if (smem > 200 * 1024) {
+        ids_set_last_error("cpqr: sketch too tall for the shared-memory Householder vector");
+        return IDS_EINVAL;
+    }
+    if (smem > 48 * 1024)
+        IDS_CUDA_TRY(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+    const int G = (int)tmin<int64_t>(grid_size(rows, cols, smem), kMaxG);
+    CpqrArgs a{};
+    a.Y = Y;
+    a.m = rows;
+    a.n = cols;
+    a.ldy = ldy;
+    a.k = k;
+    a.rank_tol = rank_tol;
+    a.perm = perm;
+    a.Rtop = Rtop;
+    a.numerical_rank = numerical_rank;
+    WsCarve ws(workspace, ws_bytes);
+    carve_cpqr(ws, rows, cols, k, kMaxG, a);
+    if (!ws.ok()) {
+        ids_set_last_error("cpqr: workspace too small");
+        return IDS_EWORKSPACE;
+    }
+    void* args[] = {&a};
+    IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cpqr_kernel, dim3(G), dim3(kThreads),
+                                             args, smem, st));
+    ids_count_launch();
+    if (Q) {
+        form_q_kernel<<<(unsigned)k, kThreads, 0, st>>>(a.V, a.tau, rows, k, Q);
+        IDS_LAUNCH_CHECK();
+    }
+    return IDS_OK;
+}
+
+extern "C" size_t ids_id_coeffs_workspace_bytes(int64_t k, int64_t cols) {
+    return (size_t)k * (size_t)(cols > k ? cols - k : 0) * sizeof(double) + 256;
+}
+
+extern "C" int ids_id_coeffs_f64(const double* Rtop, const int32_t* perm, int64_t k, int64_t cols,
+                                 double rank_tol, const int32_t* numerical_rank, double* P,
+                                 int32_t* deficient, void* workspace, size_t ws_bytes,
+                                 void* stream) {
+    if (k < 1 || cols < k) {
+        ids_set_last_error("id coeffs: bad arguments");
+        return IDS_EINVAL;
+    }
+    cudaStream_t st = as_stream(stream);
+    // T = R11^{-1} R12 in position order (k x (cols - k)), then scattered into P
+    WsCarve ws(workspace, ws_bytes);
+    const int64_t nt = cols - k;
+    double* T = nt > 0 ? ws.take<double>((size_t)k * nt) : nullptr;
+    if (!ws.ok()) {
+        ids_set_last_error("id coeffs: workspace too small");
+        return IDS_EWORKSPACE;
+    }
+    if (nt > 0) {
+        const unsigned g = (unsigned)tmin<int64_t>(ceil_div(nt, 128), 148 * 8);
+        id_solve_kernel<<<g, 128, 0, st>>>(Rtop, k, cols, rank_tol, numerical_rank, T);
+        IDS_LAUNCH_CHECK();
+    }
+    const unsigned g2 = (unsigned)tmin<int64_t>(ceil_div(k * cols, 256), 148 * 8);
+    id_scatter_kernel<<<g2, 256, 0, st>>>(T, perm, k, cols, P);
+    IDS_LAUNCH_CHECK();
+    if (deficient) {
+        deficient_kernel<<<1, 1, 0, st>>>(numerical_rank, k, deficient);
+        IDS_LAUNCH_CHECK();
+    }
+    return IDS_OK;
+}
+
+extern "C" int ids_triangular_solve_f64(const double* r, const double* b, int64_t n, int64_t m,
+                                        int lower, double* x, int64_t* bad_index, void* stream) {
+    if (n < 1 || m < 0) {
+        ids_set_last_error("triangular solve: bad shape");
+        return IDS_EINVAL;
+    }
+    cudaStream_t st = as_stream(stream);
+    // diagonal to the host (strided copy), checked there (linalg.py:141-144)
+    double* diag = static_cast<double*>(malloc(sizeof(double) * n));
+    if (!diag) return IDS_EINVAL;
+    cudaError_t e = cudaMemcpy2DAsync(diag, sizeof(double), r, sizeof(double) * (n + 1),
+                                      sizeof(double), n, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        free(diag);
+        ids_set_last_error(cudaGetErrorString(e));
+        return IDS_ECUDA;
+    }
+    int64_t h = -1;
+    for (int64_t i = 0; i < n; ++i)
+        if (diag[i] == 0.0) {
+            h = i;
+            break;
+        }
+    free(diag);
+    if (h != -1) {
+        if (bad_index) *bad_index = h;
+        ids_set_last_error("zero diagonal entry");
+        return IDS_ESINGULAR;
+    }
+    if (m == 0) return IDS_OK;
+    const unsigned g = (unsigned)tmin<int64_t>(ceil_div(m, 128), 148 * 8);
+    trsm_kernel<<<g, 128, 0, st>>>(r, b, n, m, lower, x);
+    IDS_LAUNCH_CHECK();
+    return IDS_OK;
+}

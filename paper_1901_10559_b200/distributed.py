@@ -1,0 +1,152 @@
+"""Multi-GPU CountSketch / TensorSketch ID (one process per GPU).
+
+The reference is single-process (SPEC.md:490 makes distribution a non-goal);
+this module adds the two partitionings SURVEY.md section 8(e) derives:
+
+* matrices: A is split into contiguous row blocks; every rank draws the SAME
+  global hash (it is a deterministic function of the seed), sketches its
+  block with the global bucket/sign slice (row0 offset), then ONE
+  all-reduce(SUM) of the small L x R sketch (1.6 MB for configs[1]) over
+  NCCL/NVLink; the k-step pivoted QR + solve then run redundantly on every
+  rank, so no broadcast of j / P is needed;
+* CP tensors: the R rank-1 terms are split into column blocks; column r of
+  the TensorSketch depends only on column r of each factor, so each rank
+  sketches its block independently and one all-gather assembles Y.
+
+The arithmetic goes through a backend object so the partitioning and the
+collectives can be exercised on CPU with gloo (tests/test_distributed_gloo.py,
+whose backend is the CPU oracle); the product backend is ``DeviceBackend``.
+"""
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def row_block(n, world, rank):
+    """Contiguous block [r0, r1) of n rows owned by `rank` of `world`."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+class DeviceBackend:
+    """sm_100a kernels through the C ABI (the product path)."""
+
+    def matrix_sketch(self, a_local, row0, in_dim, sketch_dim, seed, surjective):
+        from . import _device
+        from ._inputs import DenseOperand, SparseOperand, matrix_operand
+        from ._native import IDS_FLAG_ORDERED
+        from .sketch import CountSketchOp
+
+        if isinstance(a_local, (DenseOperand, SparseOperand)):
+            operand = a_local
+        else:
+            operand = matrix_operand(a_local)
+        op = CountSketchOp(in_dim, sketch_dim, seed=seed, surjective=surjective)
+        y = _device.empty((operand.cols, sketch_dim), torch.float64)
+        flag = _device.zeros(1, torch.int32)
+        op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,
+                       nonfinite=flag)
+        return y, flag, operand
+
+    def confirm_nonfinite(self, operand):
+        from . import _device
+        from ._native import call
+
+        conf = _device.zeros(1, torch.int32)
+        if operand.kind == "dense":
+            call("ids_dense_has_nonfinite", _device.ptr(operand.t), operand.rows, operand.cols,
+                 operand.ld, operand.layout, _device.ptr(conf), _device.stream_ptr())
+        else:
+            call("ids_values_has_nonfinite", _device.ptr(operand.data), operand.nnz,
+                 _device.ptr(conf), _device.stream_ptr())
+        return conf
+
+    def tensor_sketch(self, factors_local, weights_local, mode_dims, sketch_dim, seed):
+        from .sketch import TensorSketchOp
+
+        op = TensorSketchOp(mode_dims, sketch_dim, seed=seed)
+        return op.apply_device(factors_local, weights_local)
+
+    def matrix_id(self, y, rows, cols, rank, rank_tol, method):
+        from .matrix_id import device_matrix_id
+
+        return device_matrix_id(y, rows, cols, rank, rank_tol).to_host(method)
+
+
+def _world(group):
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def countsketch_id_sharded(a_local, row0, in_dim, rank, sketch_dim=None, seed=None,
+                           rank_tol=1e-12, surjective=True, group=None, backend=None):
+    """countsketch_id of the global matrix whose rows [row0, row0 + rows) are
+    `a_local` on this rank.  Every rank returns the same decomposition."""
+    from .matrix_id import check_matrix_id_args
+
+    backend = backend or DeviceBackend()
+    world, _ = _world(group)
+    cols = a_local.shape[1]
+
+    class _Shape:
+        shape = (in_dim, cols)
+
+    sketch_dim = check_matrix_id_args(_Shape, rank, sketch_dim, "countsketch")
+    if seed is None:
+        # every rank must draw the same hash: agree on fresh entropy first
+        ent = torch.tensor([np.random.SeedSequence().entropy % (2**63)], dtype=torch.int64)
+        if world > 1:
+            dist.broadcast(ent, src=0, group=group)
+        seed = int(ent.item())
+    y, flag, operand = backend.matrix_sketch(a_local, row0, in_dim, sketch_dim, seed, surjective)
+    if world > 1:
+        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if bool(flag.item()):
+        conf = backend.confirm_nonfinite(operand)
+        if world > 1:
+            dist.all_reduce(conf, op=dist.ReduceOp.MAX, group=group)
+        if bool(conf.item()):
+            raise ValueError("a contains non-finite entries")
+    return backend.matrix_id(y, sketch_dim, cols, rank, rank_tol, "countsketch")
+
+
+def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketch_dim=None,
+                            seed=None, rank_tol=1e-12, group=None, backend=None):
+    """tensorsketch_id with the R terms split into column blocks: this rank
+    holds terms [col0, col0 + R_local) of the (normalized) CpTensor in
+    x_local.  Returns the TensorIdResult-like tuple (cols, coeffs,
+    new_weights, numerical_rank, rank_deficient), identical on all ranks."""
+    from .cp_tensor import check_tensor_id_args
+
+    backend = backend or DeviceBackend()
+    world, me = _world(group)
+
+    class _X:
+        rank = total_terms
+        total_entries = int(np.prod(x_local.mode_dims))
+
+    sketch_dim = check_tensor_id_args(_X, rank, sketch_dim, "tensorsketch")
+    if seed is None:
+        ent = torch.tensor([np.random.SeedSequence().entropy % (2**63)], dtype=torch.int64)
+        if world > 1:
+            dist.broadcast(ent, src=0, group=group)
+        seed = int(ent.item())
+    y_local = backend.tensor_sketch(x_local.factors, x_local.weights, x_local.mode_dims,
+                                    sketch_dim, seed)
+    if world > 1:
+        counts = [row_block(total_terms, world, r) for r in range(world)]
+        sizes = [b - a for a, b in counts]
+        width = max(sizes)
+        pad = torch.zeros((width, sketch_dim), dtype=y_local.dtype, device=y_local.device)
+        pad[: y_local.shape[0]] = y_local
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)
+        y = torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0).contiguous()
+    else:
+        y = y_local
+    d = backend.matrix_id(y, sketch_dim, total_terms, rank, rank_tol, "tensorsketch")
+    weights = np.asarray(all_weights, dtype=np.float64)
+    new_weights = weights[d.cols] * d.coeffs.sum(axis=1)
+    return d, new_weights

@@ -1,0 +1,302 @@
+"""CountSketch and TensorSketch operators on B200.
+
+Drop-in for reference ``pkg/src/idsketch/sketch.py:51-207``: same
+constructors, attributes (``bucket`` int64, ``sign`` float64 +-1, ``in_dim``,
+``out_dim``, ``surjective``; ``mode_ops``, ``seed``, ``mode_dims``),
+``from_arrays``, ``apply``, ``materialize`` and the TensorSketch composite-hash
+helpers.  The hash is drawn ON THE DEVICE (bit-exact with numpy's PCG64
+stream, ``ids_countsketch_hash``) and kept there; ``bucket``/``sign`` are
+host copies fetched on first access.  ``apply`` runs the sm_100a sketch
+kernels; host inputs return numpy arrays, CUDA-tensor inputs return CUDA
+tensors.
+"""
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _device
+from ._inputs import DenseOperand, SparseOperand, matrix_operand
+from ._native import IDS_ERETRY, IDS_FLAG_ORDERED, call, query
+
+_MAX_MATERIALIZE = 50_000_000  # sketch.py:30
+
+
+def _seed_entropy(seed):
+    """sketch.py:33-39."""
+    if seed is None:
+        return np.random.SeedSequence().entropy
+    if isinstance(seed, np.random.SeedSequence):
+        return seed.entropy
+    return int(seed)
+
+
+def seed_state(seed):
+    """The (state, inc) of the fresh PCG64 that ``np.random.default_rng(seed)``
+    builds (sketch.py:77): SeedSequence hashing is numpy's own host code."""
+    if isinstance(seed, np.random.Generator):
+        raise TypeError("pass an int or SeedSequence seed (Generator state is not replayable)")
+    st = np.random.PCG64(seed).state["state"]
+    return int(st["state"]), int(st["inc"])
+
+
+def _split(v):
+    return (v >> 64) & 0xFFFFFFFFFFFFFFFF, v & 0xFFFFFFFFFFFFFFFF
+
+
+def _check_rows(a, in_dim, kind):
+    """sketch.py:42-48."""
+    ndim = a.dim() if isinstance(a, torch.Tensor) else np.ndim(a)
+    if ndim != 2:
+        raise ValueError("sketch input must be 2-D")
+    if a.shape[0] != in_dim:
+        raise ValueError(f"{kind} expects {in_dim} input rows, got {a.shape[0]}")
+
+
+class CountSketchOp:
+    """Bucket-and-sign sketch S (reference sketch.py:51-125).
+
+    In surjective mode the bucket map is a random permutation of
+    [0..out_dim) followed by iid uniform values, so every output row receives
+    at least one input row.
+    """
+
+    def __init__(self, in_dim, out_dim, seed=None, surjective=False):
+        if in_dim < 1 or out_dim < 1:
+            raise ValueError("dimensions must be positive")
+        if surjective and out_dim > in_dim:
+            raise ValueError(
+                f"surjective mode requires out_dim <= in_dim, got {out_dim} > {in_dim}"
+            )
+        self.in_dim = int(in_dim)
+        self.out_dim = int(out_dim)
+        self.surjective = bool(surjective)
+        self._bucket_h = None
+        self._sign_h = None
+        self._index = None
+        state, inc = seed_state(seed)
+        self._bucket_d = _device.empty(self.in_dim, torch.int32)
+        self._sign_d = _device.empty(self.in_dim, torch.int8)
+        self._draws = _device.empty(4, torch.int64)
+        nbytes = query("ids_hash_workspace_bytes", self.in_dim, self.out_dim, int(self.surjective))
+        ws = _device.workspace(nbytes)
+        sh, sl = _split(state)
+        ih, il = _split(inc)
+        call(
+            "ids_countsketch_hash", sh, sl, ih, il, self.in_dim, self.out_dim,
+            int(self.surjective), _device.ptr(self._bucket_d), _device.ptr(self._sign_d),
+            _device.ptr(self._draws), _device.ptr(ws), nbytes, _device.stream_ptr(),
+        )
+        self._checked = False
+
+    @classmethod
+    def from_arrays(cls, bucket, sign, out_dim=None):
+        """Operator from explicit bucket and sign arrays (sketch.py:91-106)."""
+        bucket = np.asarray(bucket, dtype=np.int64)
+        sign = np.asarray(sign, dtype=np.float64)
+        if bucket.ndim != 1 or bucket.shape != sign.shape:
+            raise ValueError("bucket and sign must be 1-D arrays of equal length")
+        if not np.isin(sign, (-1.0, 1.0)).all():
+            raise ValueError("signs must be +-1")
+        op = cls.__new__(cls)
+        op.in_dim = bucket.size
+        op.out_dim = int(bucket.max()) + 1 if out_dim is None else int(out_dim)
+        op.surjective = bool(np.unique(bucket).size == op.out_dim)
+        if bucket.size and (bucket.min() < 0 or bucket.max() >= op.out_dim):
+            raise ValueError("bucket values must lie in [0, out_dim)")
+        op._bucket_h = bucket
+        op._sign_h = sign
+        op._bucket_d = _device.to_device(bucket.astype(np.int32))
+        op._sign_d = _device.to_device(sign.astype(np.int8))
+        op._draws = None
+        op._index = None
+        op._checked = True
+        return op
+
+    # ---- host views -------------------------------------------------------
+    def _check_draws(self):
+        if self._checked or self._draws is None:
+            return
+        status = int(self._draws[3].item())
+        if status == IDS_ERETRY:  # pragma: no cover - needs ~e^-100 luck
+            raise RuntimeError("hash draw buffer exhausted; rebuild the operator")
+        self._checked = True
+
+    @property
+    def bucket(self):
+        if self._bucket_h is None:
+            self._check_draws()
+            self._bucket_h = _device.to_host(self._bucket_d).astype(np.int64)
+        return self._bucket_h
+
+    @property
+    def sign(self):
+        if self._sign_h is None:
+            self._check_draws()
+            self._sign_h = _device.to_host(self._sign_d).astype(np.float64)
+        return self._sign_h
+
+    @property
+    def draws(self):
+        """32-bit draws consumed by (phase A, permutation, signs)."""
+        if self._draws is None:
+            return None
+        return tuple(int(v) for v in _device.to_host(self._draws)[:3])
+
+    def materialize(self):
+        """Dense L x I operator (sketch.py:124-125; test helper)."""
+        out = np.zeros((self.out_dim, self.in_dim))
+        out[self.bucket, np.arange(self.in_dim)] = self.sign
+        return out
+
+    # ---- device ------------------------------------------------------------
+    def bucket_index(self):
+        """(order_signed int32[I], bstart int64[L+1]) -- the CSR structure of S."""
+        if self._index is None:
+            order = _device.empty(self.in_dim, torch.int32)
+            bstart = _device.empty(self.out_dim + 1, torch.int64)
+            nbytes = query("ids_bucket_index_workspace_bytes", self.in_dim, self.out_dim)
+            ws = _device.workspace(nbytes)
+            call(
+                "ids_bucket_index", _device.ptr(self._bucket_d), _device.ptr(self._sign_d),
+                self.in_dim, self.out_dim, _device.ptr(order), _device.ptr(bstart),
+                _device.ptr(ws), nbytes, _device.stream_ptr(),
+            )
+            self._index = (order, bstart)
+        return self._index
+
+    def sketch_into(self, operand, y, row0=0, accumulate=False, flags=0, nonfinite=None):
+        """Y (+)= S[:, row0:row0+rows] @ operand on the current stream.
+
+        y: CUDA float64 tensor of shape (cols, out_dim) -- the col-major L x R
+        sketch.  nonfinite: optional device int32[1] flag.
+        """
+        st = _device.stream_ptr()
+        nf = _device.ptr(nonfinite)
+        if isinstance(operand, DenseOperand):
+            order, bstart = self.bucket_index()
+            nbytes = query(
+                "ids_countsketch_dense_workspace_bytes", operand.rows, operand.cols,
+                self.out_dim, operand.layout,
+            )
+            ws = _device.workspace(nbytes)
+            call(
+                "ids_countsketch_dense_f64", _device.ptr(operand.t), operand.rows, operand.cols,
+                operand.ld, operand.layout, row0, self.in_dim, _device.ptr(self._bucket_d),
+                _device.ptr(self._sign_d), _device.ptr(order), _device.ptr(bstart),
+                self.out_dim, _device.ptr(y), int(accumulate), int(flags), nf,
+                _device.ptr(ws), nbytes, st,
+            )
+        elif isinstance(operand, SparseOperand) and operand.fmt == "csc":
+            nbytes = query("ids_countsketch_csc_workspace_bytes", operand.cols, self.out_dim)
+            ws = _device.workspace(nbytes)
+            call(
+                "ids_countsketch_csc_f64", _device.ptr(operand.indptr),
+                int(operand.indptr.dtype == torch.int64), _device.ptr(operand.indices),
+                _device.ptr(operand.data), operand.rows, operand.cols, operand.nnz, row0,
+                self.in_dim, _device.ptr(self._bucket_d), _device.ptr(self._sign_d),
+                self.out_dim, _device.ptr(y), int(accumulate), nf, _device.ptr(ws), nbytes, st,
+            )
+        elif isinstance(operand, SparseOperand):
+            order, bstart = self.bucket_index()
+            nbytes = query(
+                "ids_countsketch_csr_workspace_bytes", operand.rows, operand.cols, operand.nnz,
+                self.out_dim,
+            )
+            ws = _device.workspace(nbytes)
+            call(
+                "ids_countsketch_csr_f64", _device.ptr(operand.indptr),
+                int(operand.indptr.dtype == torch.int64), _device.ptr(operand.indices),
+                _device.ptr(operand.data), operand.rows, operand.cols, operand.nnz, row0,
+                self.in_dim, _device.ptr(self._bucket_d), _device.ptr(self._sign_d),
+                _device.ptr(order), _device.ptr(bstart), self.out_dim, _device.ptr(y),
+                int(accumulate), int(flags), nf, _device.ptr(ws), nbytes, st,
+            )
+        else:  # pragma: no cover
+            raise TypeError(f"unsupported operand {type(operand)!r}")
+
+    def apply_device(self, a, flags=0, nonfinite=None):
+        """S @ a as a CUDA tensor of shape (cols, out_dim) (col-major sketch)."""
+        op = a if isinstance(a, (DenseOperand, SparseOperand)) else matrix_operand(a)
+        if op.rows != self.in_dim:
+            raise ValueError(f"CountSketch expects {self.in_dim} input rows, got {op.rows}")
+        y = _device.empty((op.cols, self.out_dim), torch.float64)
+        self.sketch_into(op, y, 0, False, flags, nonfinite)
+        return y
+
+    def apply(self, a):
+        """Sketch `a` (sparse or dense, in_dim rows); returns a dense array
+        (sketch.py:116-122).  CUDA-tensor input returns a CUDA tensor."""
+        if not sp.issparse(a):
+            _check_rows(a, self.in_dim, "CountSketch")
+        elif a.shape[0] != self.in_dim:
+            raise ValueError(f"CountSketch expects {self.in_dim} input rows, got {a.shape[0]}")
+        on_device = isinstance(a, torch.Tensor) and a.device.type == "cuda"
+        if a.shape[1] == 0:
+            return np.zeros((self.out_dim, 0))
+        op = matrix_operand(a)
+        y = self.apply_device(op, flags=IDS_FLAG_ORDERED).t()
+        if on_device:
+            return y
+        return _device.to_host(y.contiguous())
+
+
+class TensorSketchOp:
+    """CountSketch whose hash and sign factor across tensor modes
+    (reference sketch.py:128-207)."""
+
+    def __init__(self, mode_dims, out_dim, seed=None):
+        mode_dims = [int(d) for d in mode_dims]
+        if len(mode_dims) == 0:
+            raise ValueError("need at least one mode")
+        if any(d < 1 for d in mode_dims) or out_dim < 1:
+            raise ValueError("dimensions must be positive")
+        entropy = _seed_entropy(seed)
+        self.mode_dims = tuple(mode_dims)
+        self.out_dim = int(out_dim)
+        self.seed = entropy
+        self.mode_ops = [
+            CountSketchOp(d, out_dim, seed=np.random.SeedSequence([entropy, n]))
+            for n, d in enumerate(mode_dims)
+        ]
+
+    @property
+    def in_dim(self):
+        return int(np.prod(self.mode_dims))
+
+    def apply_device(self, factors, weights=None):
+        """Sketch of khatri_rao(factors) @ diag(weights) as a CUDA tensor of
+        shape (ncols, out_dim) (col-major L x R)."""
+        from .tensorsketch import tensorsketch_device
+
+        return tensorsketch_device(self, factors, weights)
+
+    def apply(self, factors, weights=None):
+        """sketch.py:156-186: numpy L x R for host factors."""
+        if len(factors) != len(self.mode_ops):
+            raise ValueError(f"expected {len(self.mode_ops)} factors, got {len(factors)}")
+        on_device = all(isinstance(f, torch.Tensor) and f.device.type == "cuda" for f in factors)
+        y = self.apply_device(factors, weights).t()
+        if on_device:
+            return y
+        return _device.to_host(y.contiguous())
+
+    def composite_bucket(self):
+        """Bucket of every Khatri-Rao row (last mode fastest), sketch.py:188-194."""
+        total = np.zeros(1, dtype=np.int64)
+        for op in self.mode_ops:
+            total = (total[:, None] + op.bucket[None, :]).ravel()
+        return total % self.out_dim
+
+    def composite_sign(self):
+        total = np.ones(1, dtype=np.float64)
+        for op in self.mode_ops:
+            total = (total[:, None] * op.sign[None, :]).ravel()
+        return total
+
+    def materialize(self):
+        if self.in_dim * self.out_dim > _MAX_MATERIALIZE:
+            raise ValueError("operator too large to materialize")
+        dense = np.zeros((self.out_dim, self.in_dim))
+        dense[self.composite_bucket(), np.arange(self.in_dim)] = self.composite_sign()
+        return dense

@@ -1,0 +1,385 @@
+"""Parity of the CUDA path against the golden fixtures (made by the real
+reference) and the CPU oracle.  Runs on a B200 (pytest -m gpu)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+
+from conftest import dense_countsketch, relerr_fro
+
+pytestmark = pytest.mark.gpu
+
+ids = pytest.importorskip("paper_1901_10559_b200")
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+TOL = 1e-10  # north_star: sketch and P within 1e-10 relative Frobenius (fp64)
+
+
+def _digest(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+# ---------------------------------------------------------------- hash -----
+def test_hash_small_bit_exact(golden):
+    data, man = golden
+    for case in man["hash_small"]:
+        op = ids.CountSketchOp(
+            case["in_dim"], case["out_dim"], seed=case["seed"], surjective=case["surjective"]
+        )
+        assert op.bucket.dtype == np.int64 and op.sign.dtype == np.float64
+        assert np.array_equal(op.bucket, data[f"hash{case['id']}_bucket"]), case
+        assert np.array_equal(op.sign, data[f"hash{case['id']}_sign"]), case
+
+
+def test_hash_config_sizes_bit_exact(golden):
+    """BASELINE.json config sizes (I = 1e4 .. 1e7), pinned by digests of the
+    reference's own arrays."""
+    _, man = golden
+    for case in man["hash_digest"]:
+        if case["mode"] is None:
+            seed = case["seed"]
+        else:
+            seed = np.random.SeedSequence([case["seed"], case["mode"]])
+        op = ids.CountSketchOp(case["in_dim"], case["out_dim"], seed=seed,
+                               surjective=case["surjective"])
+        assert _digest(op.bucket, op.sign) == case["sha256"], case
+
+
+def test_hash_draw_counts_match_oracle():
+    for I, L, seed, surj in [(100_000, 200, 7, True), (4097, 64, 12, True), (777, 5, 13, False),
+                             (1, 1, 0, True), (2, 2, 3, True), (65_600, 3, 5, True)]:
+        op = ids.CountSketchOp(I, L, seed=seed, surjective=surj)
+        o = oracle.OracleCountSketch(I, L, seed, surj)
+        assert op.draws == tuple(int(v) for v in o.draws), (I, L, seed, surj)
+        assert np.array_equal(op.bucket, o.bucket)
+        assert np.array_equal(op.sign, o.sign)
+
+
+def test_hash_random_shapes_vs_oracle():
+    rng = np.random.default_rng(5)
+    for _ in range(60):
+        I = int(rng.integers(1, 200_000))
+        L = int(rng.integers(1, min(I, 5000) + 1))
+        surj = bool(rng.integers(0, 2))
+        seed = int(rng.integers(0, 2**62))
+        op = ids.CountSketchOp(I, L, seed=seed, surjective=surj)
+        o = oracle.OracleCountSketch(I, L, seed, surj)
+        assert np.array_equal(op.bucket, o.bucket), (I, L, seed, surj)
+        assert np.array_equal(op.sign, o.sign), (I, L, seed, surj)
+
+
+def test_surjective_covers_all_buckets():
+    op = ids.CountSketchOp(1000, 10, seed=1, surjective=True)
+    assert np.unique(op.bucket).size == 10
+    op = ids.CountSketchOp(4, 4, seed=0, surjective=True)
+    assert sorted(op.bucket) == [0, 1, 2, 3]
+
+
+# ---------------------------------------------------------------- sketch ---
+def test_sketch_dense_golden_bit_exact(golden):
+    data, man = golden
+    for case in man["sketch_dense"]:
+        n = case["id"]
+        op = ids.CountSketchOp(case["in_dim"], case["out_dim"], seed=case["seed"],
+                               surjective=case["surjective"])
+        a = data[f"sd{n}_a"]
+        want = data[f"sd{n}_y"]
+        y_c = op.apply(np.ascontiguousarray(a))
+        y_f = op.apply(np.asfortranarray(a))
+        assert y_c.shape == want.shape and y_c.flags.c_contiguous
+        assert np.array_equal(y_c, want), n  # scipy's summation order, bit for bit
+        assert np.array_equal(y_f, want), n
+
+
+def test_sketch_csr_csc_golden_bit_exact(golden):
+    data, man = golden
+    for case in man["sketch_csr"]:
+        n = case["id"]
+        a = sp.csr_array(
+            (data[f"sc{n}_data"], data[f"sc{n}_indices"], data[f"sc{n}_indptr"]),
+            shape=(case["in_dim"], case["cols"]),
+        )
+        op = ids.CountSketchOp(case["in_dim"], case["out_dim"], seed=case["seed"],
+                               surjective=case["surjective"])
+        want = data[f"sc{n}_y"]
+        assert np.array_equal(op.apply(a), want), n
+        assert np.array_equal(op.apply(sp.csc_array(a)), want), n
+        assert np.array_equal(op.apply(a.tocoo()), want), n
+
+
+def test_hand_example():
+    op = ids.CountSketchOp.from_arrays([0, 1, 0, 1], [1.0, -1.0, 1.0, 1.0])
+    out = op.apply(np.eye(4))
+    assert np.array_equal(out, [[1.0, 0.0, 1.0, 0.0], [0.0, -1.0, 0.0, 1.0]])
+
+
+def test_permutation_hash_permutes_rows():
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((6, 3))
+    perm = rng.permutation(6)
+    op = ids.CountSketchOp.from_arrays(perm, np.ones(6))
+    assert np.array_equal(op.apply(a)[perm], a)
+
+
+def test_sparse_matches_densified_operator():
+    rng = np.random.default_rng(3)
+    a = sp.random_array((100, 15), density=0.05, rng=rng, format="csc")
+    op = ids.CountSketchOp(100, 20, seed=4)
+    want = dense_countsketch(op.bucket, op.sign, 20) @ a.toarray()
+    assert np.abs(op.apply(a) - want).max() <= 1e-13
+
+
+def test_linearity_and_replay():
+    rng = np.random.default_rng(34)
+    a = rng.standard_normal((25, 4))
+    b = rng.standard_normal((25, 4))
+    for surj in (False, True):
+        op = ids.CountSketchOp(25, 6, seed=31, surjective=surj)
+        assert np.abs(op.apply(a + b) - (op.apply(a) + op.apply(b))).max() <= 1e-12
+        two = ids.CountSketchOp(25, 6, seed=31, surjective=surj)
+        assert np.array_equal(op.apply(a), two.apply(a))
+
+
+def test_dimension_mismatch():
+    op = ids.CountSketchOp(10, 3, seed=0)
+    with pytest.raises(ValueError):
+        op.apply(np.eye(9))
+    with pytest.raises(ValueError):
+        op.apply(np.ones(10))
+
+
+def test_device_tensor_in_device_tensor_out():
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((500, 33))
+    op = ids.CountSketchOp(500, 20, seed=2, surjective=True)
+    yd = op.apply(torch.from_numpy(a).cuda())
+    assert yd.is_cuda and tuple(yd.shape) == (20, 33)
+    assert np.array_equal(yd.cpu().numpy(), oracle.cs_apply(op.bucket, op.sign, 20, a))
+
+
+def test_large_dense_sketch_vs_oracle_and_segmented_mode():
+    """C1 shape (10,000 x 1,000, L = 40); ordered kernel == scipy bit for bit,
+    segmented kernel within 1e-10 (and deterministic)."""
+    from paper_1901_10559_b200._inputs import dense_operand
+
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((10_000, 1_000))
+    op = ids.CountSketchOp(10_000, 40, seed=3, surjective=True)
+    want = oracle.cs_apply(op.bucket, op.sign, 40, a)
+    assert np.array_equal(op.apply(a), want)
+    y1 = op.apply_device(dense_operand(a), flags=0).t().cpu().numpy()
+    y2 = op.apply_device(dense_operand(a), flags=0).t().cpu().numpy()
+    assert relerr_fro(y1, want) <= TOL
+    assert np.array_equal(y1, y2)
+    yf = op.apply(np.asfortranarray(a))
+    assert np.array_equal(yf, want)
+
+
+def test_chunked_rows_accumulate_bit_exact():
+    """Row blocks sketched separately and accumulated equal the one-shot sketch
+    (the multi-GPU / streaming decomposition)."""
+    from paper_1901_10559_b200._inputs import dense_operand
+
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((3000, 70))
+    op = ids.CountSketchOp(3000, 50, seed=8, surjective=True)
+    want = oracle.cs_apply(op.bucket, op.sign, 50, a)
+    y = torch.zeros((70, 50), dtype=torch.float64, device="cuda")
+    for r0, r1 in [(0, 1000), (1000, 1001), (1001, 3000)]:
+        op.sketch_into(dense_operand(a[r0:r1]), y, row0=r0, accumulate=True, flags=1)
+    assert np.array_equal(y.t().cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------- ID -------
+def test_matrix_id_golden(golden):
+    data, man = golden
+    for case in man["matrix_id"]:
+        n = case["id"]
+        d = ids.matrix_id(data[f"mid{n}_y"], case["rank"])
+        assert d.cols.dtype == np.int32
+        assert np.array_equal(d.cols, data[f"mid{n}_cols"]), n
+        assert relerr_fro(d.coeffs, data[f"mid{n}_coeffs"]) <= TOL, n
+        assert d.numerical_rank == case["numerical_rank"], n
+        assert d.rank_deficient == case["rank_deficient"], n
+        assert np.array_equal(d.coeffs[:, d.cols], np.eye(case["rank"]))
+
+
+def test_countsketch_id_golden(golden):
+    data, man = golden
+    a = data["csid_a"]
+    for case in man["countsketch_id"]:
+        s = case["seed"]
+        d = ids.countsketch_id(a, case["rank"], case["sketch_dim"], seed=s)
+        assert d.method == "countsketch"
+        assert np.array_equal(d.cols, data[f"csid{s}_cols"]), s
+        assert relerr_fro(d.coeffs, data[f"csid{s}_coeffs"]) <= TOL, s
+        assert d.numerical_rank == case["numerical_rank"]
+        y = ids.matrix_sketch(a, "countsketch", case["sketch_dim"], seed=s)
+        assert np.array_equal(y, data[f"csid{s}_y"])
+    a_sp = sp.csr_array(
+        (data["csid_sp_data"], data["csid_sp_indices"], data["csid_sp_indptr"]),
+        shape=(3000, 120),
+    )
+    for m in (a_sp, sp.csc_array(a_sp)):
+        d = ids.countsketch_id(m, 12, 50, seed=21)
+        assert np.array_equal(d.cols, data["csid_sp_cols"])
+        assert relerr_fro(d.coeffs, data["csid_sp_coeffs"]) <= TOL
+
+
+def _c1_matrix(rng, rows=10_000, cols=1_000, k=10):
+    sigma = np.concatenate([np.ones(k), 10.0 ** (-np.arange(1, cols - k + 1) / 10.0)])
+    u = np.linalg.qr(rng.standard_normal((rows, cols)))[0]
+    v = np.linalg.qr(rng.standard_normal((cols, cols)))[0]
+    return (u * sigma) @ v.T
+
+
+def test_config1_full_size_vs_oracle():
+    """BASELINE.json configs[0] (10,000 x 1,000, K = 10, L = 40), seeds 0-9:
+    Y bit-exact, j identical, P within 1e-10 of the LAPACK-based oracle."""
+    a = _c1_matrix(np.random.default_rng(1))
+    for seed in range(10):
+        want = oracle.countsketch_id(a, 10, 40, seed=seed)
+        op = ids.CountSketchOp(10_000, 40, seed=seed, surjective=True)
+        assert np.array_equal(op.apply(a), want.sketch)
+        d = ids.countsketch_id(a, 10, 40, seed=seed)
+        assert np.array_equal(d.cols, want.cols), seed
+        assert relerr_fro(d.coeffs, want.coeffs) <= TOL, seed
+        # ID error within 1% of the reference's
+        err = np.linalg.norm(a[:, d.cols] @ d.coeffs - a, 2)
+        ref = np.linalg.norm(a[:, want.cols] @ want.coeffs - a, 2)
+        assert abs(err - ref) <= 0.01 * ref
+
+
+def test_id_properties_reference_suite():
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        rows = int(rng.integers(30, 80))
+        cols = int(rng.integers(5, 25))
+        k = int(rng.integers(1, cols + 1))
+        a = rng.standard_normal((rows, cols))
+        d = ids.countsketch_id(a, k, seed=trial)
+        assert np.array_equal(d.coeffs[:, d.cols], np.eye(k))
+        assert np.unique(d.cols).size == k
+        sv = np.linalg.svd(d.coeffs, compute_uv=False)
+        assert sv[-1] >= 1.0 - 1e-8
+        assert sv[0] <= np.sqrt(4.0 * k * (cols - k) + 1.0) * 10.0
+        want = oracle.countsketch_id(a, k, seed=trial)
+        assert np.array_equal(d.cols, want.cols)
+        assert relerr_fro(d.coeffs, want.coeffs) <= 1e-9
+
+
+def test_exact_rank_recovery_and_full_width():
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((80, 6)) @ rng.standard_normal((6, 30))
+    d = ids.countsketch_id(a, 6, seed=7)
+    assert relerr_fro(d.reconstruct(a), a) <= 1e-8
+    a = np.random.default_rng(4).standard_normal((60, 12))
+    d = ids.countsketch_id(a, 12, seed=8)
+    assert relerr_fro(d.reconstruct(a), a) <= 1e-10
+
+
+def test_single_nonzero_column_sparse():
+    a = np.zeros((30, 5))
+    a[:, 2] = np.arange(1.0, 31.0)
+    d = ids.countsketch_id(sp.csc_array(a), 1, seed=9)
+    assert d.cols[0] == 2
+    assert d.coeffs[0, 2] == 1.0
+    assert relerr_fro(d.reconstruct(a), a) <= 1e-12
+
+
+def test_rank_deficient_and_zero():
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((20, 4)) @ rng.standard_normal((4, 15))
+    d = ids.matrix_id(a, 10)
+    assert d.rank_deficient and d.numerical_rank == 4
+    assert np.array_equal(d.coeffs[:, d.cols], np.eye(10))
+    assert np.isfinite(d.coeffs).all()
+    assert relerr_fro(d.reconstruct(a), a) <= 1e-8
+    d = ids.matrix_id(np.zeros((5, 4)), 2)
+    assert d.rank_deficient and d.numerical_rank == 0
+    assert np.array_equal(d.coeffs[:, d.cols], np.eye(2))
+
+
+def test_errors():
+    a = np.random.default_rng(7).standard_normal((20, 10))
+    with pytest.raises(ValueError):
+        ids.countsketch_id(a, 5, sketch_dim=20, seed=0)
+    with pytest.raises(ValueError):
+        ids.countsketch_id(a, 5, sketch_dim=4, seed=0)
+    with pytest.raises(ValueError):
+        ids.countsketch_id(a, 11, seed=0)
+    bad = a.copy()
+    bad[3, 4] = np.nan
+    with pytest.raises(ValueError):
+        ids.countsketch_id(bad, 2, seed=0)
+    bad[3, 4] = np.inf
+    with pytest.raises(ValueError):
+        ids.countsketch_id(np.asfortranarray(bad), 2, seed=0)
+    with pytest.raises(ValueError):
+        ids.matrix_id(np.array([[np.nan, 1.0]]), 1)
+    sp_bad = sp.csr_array(bad)
+    with pytest.raises(ValueError):
+        ids.countsketch_id(sp_bad, 2, seed=0)
+
+
+def test_seed_determinism_sparse():
+    rng = np.random.default_rng(8)
+    a = sp.random_array((100, 20), density=0.1, rng=rng, format="csc")
+    one = ids.countsketch_id(a, 5, seed=42)
+    two = ids.countsketch_id(a, 5, seed=42)
+    assert np.array_equal(one.cols, two.cols)
+    assert np.array_equal(one.coeffs, two.coeffs)
+
+
+def test_cpqr_reference_properties():
+    f = ids.cpqr(np.eye(3), 3)
+    assert np.allclose(np.abs(f.r), np.eye(3), atol=1e-14)
+    assert f.numerical_rank == 3
+    f = ids.cpqr(np.array([[2.0, 1.0], [0.0, 0.0]]), 1)
+    assert f.perm[0] == 0 and abs(f.r[0, 0]) == pytest.approx(2.0, abs=1e-15)
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((50, 10)) @ rng.standard_normal((10, 30))
+    assert ids.cpqr(a, 30, rank_tol=1e-10).numerical_rank == 10
+    f = ids.cpqr(np.zeros((4, 3)), 2)
+    assert f.numerical_rank == 0 and np.all(f.r == 0.0)
+    for seed in range(5):
+        rng = np.random.default_rng(seed)
+        rows, cols = int(rng.integers(5, 200)), int(rng.integers(5, 200))
+        a = rng.standard_normal((rows, cols))
+        k = int(rng.integers(1, min(rows, cols) + 1))
+        f = ids.cpqr(a, k)
+        d = np.abs(np.diag(f.r))
+        assert np.all(d[:-1] >= d[1:])
+        want = oracle.cpqr(a, k)
+        assert np.array_equal(f.perm[:k], want.perm[:k])
+        full = ids.cpqr(a, min(rows, cols))
+        err = np.linalg.norm(full.q @ full.r - a[:, full.perm]) / np.linalg.norm(a)
+        assert err <= 1e-10
+        assert np.abs(full.q.T @ full.q - np.eye(full.q.shape[1])).max() <= 1e-12
+    with pytest.raises(ValueError):
+        ids.cpqr(np.eye(3), 0)
+    with pytest.raises(ValueError):
+        ids.cpqr(np.eye(3), 4)
+
+
+def test_triangular_solve():
+    rng = np.random.default_rng(4)
+    r = np.triu(rng.standard_normal((6, 6))) + 3 * np.eye(6)
+    b = rng.standard_normal((6, 4))
+    x = ids.triangular_solve(r, b)
+    assert np.allclose(r @ x, b, atol=1e-12)
+    xl = ids.triangular_solve(r.T, b, lower=True)
+    assert np.allclose(r.T @ xl, b, atol=1e-12)
+    r[2, 2] = 0.0
+    with pytest.raises(ids.SingularTriangleError):
+        ids.triangular_solve(r, b)
+    assert ids.triangular_solve(np.eye(2), np.zeros((2, 0))).shape == (2, 0)
