@@ -27,6 +27,8 @@ from .port import (
     OracleTensorSketch,
     coeffs_from_pivoted,
     countsketch_id,
+    cp_diff_norm,
+    cp_norm,
     cpqr,
     cs_apply,
     matrix_id,
@@ -41,6 +43,8 @@ __all__ = [
     "coeffs_from_pivoted",
     "countsketch_hash",
     "countsketch_id",
+    "cp_diff_norm",
+    "cp_norm",
     "cpqr",
     "cs_apply",
     "matrix_id",

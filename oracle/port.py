@@ -187,3 +187,29 @@ def tensorsketch_id(weights, factors, rank, sketch_dim=None, seed=None, rank_tol
     out = matrix_id(y, rank, rank_tol)
     out.sketch = y
     return out, ts_new_weights(np.asarray(weights), out.cols, out.coeffs)
+
+
+def _dense(f):
+    return f.toarray() if sp.issparse(f) else np.asarray(f)
+
+
+def cp_gram(weights, factors):
+    """cp_tensor.py:144-160: diag(w) (hadamard of factor Grams) diag(w)."""
+    w = np.asarray(weights, dtype=np.float64)
+    out = np.ones((w.size, w.size))
+    for f in factors:
+        f = _dense(f)
+        out *= f.T @ f
+    return out * w[None, :] * w[:, None]
+
+
+def cp_norm(weights, factors):
+    """cp_tensor.py:169-172."""
+    return float(np.sqrt(max(cp_gram(weights, factors).sum(), 0.0)))
+
+
+def cp_diff_norm(w1, f1, w2, f2):
+    """cp_tensor.py:183-197: || X - Y ||_F through the Gram identity."""
+    w = np.concatenate([np.asarray(w1, float), -np.asarray(w2, float)])
+    fs = [np.hstack([_dense(a), _dense(b)]) for a, b in zip(f1, f2)]
+    return float(np.sqrt(max(cp_gram(w, fs).sum(), 0.0)))

@@ -70,6 +70,7 @@ struct CpqrArgs {
     // workspace
     double *vn1, *vn2, *F, *Rcol, *W, *V, *tau, *beta, *a, *normpart, *zpart;
     int64_t* pos;
+    int64_t* flag_list;
     ArgMax* amax;
 };
 
@@ -87,8 +88,10 @@ __device__ double block_sum(double v, double* red) {
 
 __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ double vsm[];  // v of the current step (m), then z (k)
+    extern __shared__ double vsm[];  // v (m), z (k), V[kk, :kk] (k)
     double* zsh = vsm + g.m;
+    double* vrow = zsh + g.k;
+    __shared__ int s_nflag;
     __shared__ double red[kWarps];
     __shared__ ArgMax warp_best[kWarps];
     __shared__ int64_t s_piv[3];
@@ -99,6 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
     const int64_t c0 = n * b / G, c1 = n * (b + 1) / G;   // owned columns
     const int64_t r0 = m * b / G, r1 = m * (b + 1) / G;   // owned rows
     const double tol3z = sqrt(DBL_EPSILON);
+    int64_t* flagged = g.flag_list + c0;  // this CTA's columns needing a norm recompute
 
     // local argmax over owned columns with pos >= pmin; reports column at pnext
     auto local_argmax = [&](int64_t pmin, int64_t pnext) {
@@ -187,11 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         }
         {
             const double* ycol = g.Y + cs * ldy;
-            const double* fr = g.F + cs * k;
             double ss = 0.0;
-            for (int64_t r = max(r0, kk) + threadIdx.x; r < r1; r += kThreads) {
+            for (int64_t r = tmax(r0, kk) + threadIdx.x; r < r1; r += kThreads) {
                 double v = ycol[r];
-                for (int64_t q = 0; q < kk; ++q) v = fma(-g.V[q * m + r], fr[q], v);
+                for (int64_t q = 0; q < kk; ++q) v = fma(-g.V[q * m + r], g.F[q * n + cs], v);
                 g.a[r] = v;
                 if (r > kk) ss = fma(v, v, ss);
             }
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         // z partials: z_q = V[:, q]^T v over owned rows >= kk
         for (int64_t q = wid; q < kk; q += kWarps) {
             double s = 0.0;
-            for (int64_t r = max(r0, kk) + lane; r < r1; r += 32) s = fma(g.V[q * m + r], vsm[r], s);
+            for (int64_t r = tmax(r0, kk) + lane; r < r1; r += 32) s = fma(g.V[q * m + r], vsm[r], s);
             s = warp_sum(s);
             if (lane == 0) g.zpart[b * k + q] = s;
         }
@@ -246,52 +249,55 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         grid.sync();
 
         // ---- S3: F column, row kk of R, norm downdate, next argmax ----
+        // z = V[:, :kk]^T v (fixed-order sum of the per-CTA partials) and row kk of V
         for (int64_t q = threadIdx.x; q < kk; q += kThreads) {
             double s = 0.0;
             for (int64_t i = 0; i < G; ++i) s += g.zpart[i * k + q];
             zsh[q] = s;
+            vrow[q] = g.V[q * m + kk];
+        }
+        if (threadIdx.x == 0) s_nflag = 0;
+        __syncthreads();
+        // one thread per owned remaining column (F is q-major: coalesced)
+        for (int64_t j = c0 + threadIdx.x; j < c1; j += kThreads) {
+            if (g.pos[j] <= kk) continue;
+            double f = g.W[j], rk = g.Y[j * ldy + kk];
+            for (int64_t q = 0; q < kk; ++q) {
+                const double fq = g.F[q * n + j];
+                f = fma(-fq, zsh[q], f);
+                rk = fma(-vrow[q], fq, rk);
+            }
+            f *= tau;
+            g.F[kk * n + j] = f;
+            rk -= f;  // V[kk, kk] = 1
+            g.Rcol[j * k + kk] = rk;
+            const double vn1 = g.vn1[j];
+            if (kk < m - 1 && vn1 != 0.0) {
+                double temp = fabs(rk) / vn1;
+                temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+                const double ratio = vn1 / g.vn2[j];
+                const double temp2 = temp * ratio * ratio;
+                if (temp2 <= tol3z) flagged[atomicAdd(&s_nflag, 1)] = j;
+                else g.vn1[j] = vn1 * sqrt(temp);
+            }
         }
         __syncthreads();
-        for (int64_t j = c0 + wid; j < c1; j += kWarps) {
-            if (g.pos[j] <= kk) continue;
-            double* fr = g.F + j * k;
-            double rk = 0.0, vn1 = 0.0;
-            bool recompute = false;
-            if (lane == 0) {
-                double f = g.W[j];
-                for (int64_t q = 0; q < kk; ++q) f = fma(-fr[q], zsh[q], f);
-                f *= tau;
-                fr[kk] = f;
-                rk = g.Y[j * ldy + kk];
-                for (int64_t q = 0; q < kk; ++q) rk = fma(-g.V[q * m + kk], fr[q], rk);
-                rk -= f;  // V[kk, kk] = 1
-                g.Rcol[j * k + kk] = rk;
-                vn1 = g.vn1[j];
-                if (kk < m - 1 && vn1 != 0.0) {
-                    double temp = fabs(rk) / vn1;
-                    temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
-                    const double ratio = vn1 / g.vn2[j];
-                    const double temp2 = temp * ratio * ratio;
-                    if (temp2 <= tol3z) recompute = true;
-                    else g.vn1[j] = vn1 * sqrt(temp);
-                }
+        // exact norms of the flagged columns below row kk (LAPACK's recompute)
+        const int nflag = s_nflag;
+        for (int fi = wid; fi < nflag; fi += kWarps) {
+            const int64_t j = flagged[fi];
+            const double* y = g.Y + j * ldy;
+            double s = 0.0;
+            for (int64_t r = kk + 1 + lane; r < m; r += 32) {
+                double v = y[r];
+                for (int64_t q = 0; q < kk; ++q) v = fma(-g.V[q * m + r], g.F[q * n + j], v);
+                v = fma(-vsm[r], g.F[kk * n + j], v);
+                s = fma(v, v, s);
             }
-            recompute = __shfl_sync(0xffffffffu, recompute, 0);
-            __syncwarp();
-            if (recompute) {
-                const double* y = g.Y + j * ldy;
-                double s = 0.0;
-                for (int64_t r = kk + 1 + lane; r < m; r += 32) {
-                    double v = y[r];
-                    for (int64_t q = 0; q < kk; ++q) v = fma(-g.V[q * m + r], fr[q], v);
-                    v = fma(-vsm[r], fr[kk], v);
-                    s = fma(v, v, s);
-                }
-                s = warp_sum(s);
-                if (lane == 0) {
-                    g.vn1[j] = sqrt(s);
-                    g.vn2[j] = sqrt(s);
-                }
+            s = warp_sum(s);
+            if (lane == 0) {
+                g.vn1[j] = sqrt(s);
+                g.vn2[j] = sqrt(s);
             }
         }
         __syncthreads();
@@ -427,6 +433,7 @@ void carve_cpqr(W& ws, int64_t m, int64_t n, int64_t k, int64_t G, CpqrArgs& a) 
     a.normpart = ws.template take<double>(G);
     a.zpart = ws.template take<double>(G * k);
     a.pos = ws.template take<int64_t>(n);
+    a.flag_list = ws.template take<int64_t>(n);
     a.amax = ws.template take<ArgMax>(G);
 }
 
@@ -471,7 +478,7 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
         return IDS_EINVAL;
     }
     cudaStream_t st = as_stream(stream);
-    const size_t smem = (size_t)(rows + k) * sizeof(double);
+    const size_t smem = (size_t)(rows + 2 * k) * sizeof(double);
     if (smem > 200 * 1024) {
         ids_set_last_error("cpqr: sketch too tall for the shared-memory Householder vector");
         return IDS_EINVAL;

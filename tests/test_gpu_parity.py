@@ -204,13 +204,23 @@ def test_matrix_id_golden(golden):
     data, man = golden
     for case in man["matrix_id"]:
         n = case["id"]
-        d = ids.matrix_id(data[f"mid{n}_y"], case["rank"])
+        y = data[f"mid{n}_y"]
+        d = ids.matrix_id(y, case["rank"])
         assert d.cols.dtype == np.int32
-        assert np.array_equal(d.cols, data[f"mid{n}_cols"]), n
-        assert relerr_fro(d.coeffs, data[f"mid{n}_coeffs"]) <= TOL, n
         assert d.numerical_rank == case["numerical_rank"], n
         assert d.rank_deficient == case["rank_deficient"], n
         assert np.array_equal(d.coeffs[:, d.cols], np.eye(case["rank"]))
+        nr = case["numerical_rank"]
+        if not case["rank_deficient"]:
+            assert np.array_equal(d.cols, data[f"mid{n}_cols"]), n
+            assert relerr_fro(d.coeffs, data[f"mid{n}_coeffs"]) <= TOL, n
+        else:
+            # pivots past the numerical rank are decided by round-off (both in
+            # LAPACK and here); the independent ones and the ID quality must agree
+            assert np.array_equal(d.cols[:nr], data[f"mid{n}_cols"][:nr]), n
+            assert np.isfinite(d.coeffs).all()
+            if nr:
+                assert relerr_fro(y[:, d.cols] @ d.coeffs, y) <= 1e-8, n
 
 
 def test_countsketch_id_golden(golden):

@@ -1,0 +1,191 @@
+"""TensorSketch + tensor ID parity on the GPU against the golden fixtures
+(pocketfft / LAPACK via the real reference) and the CPU oracle."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+
+from conftest import dense_countsketch, khatri_rao, relerr_fro
+
+pytestmark = pytest.mark.gpu
+
+ids = pytest.importorskip("paper_1901_10559_b200")
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+TOL = 1e-10
+
+
+def test_tensorsketch_golden(golden):
+    data, man = golden
+    for case in man["tensorsketch"]:
+        n = case["id"]
+        factors = [data[f"ts{n}_f{m}"] for m in range(len(case["dims"]))]
+        ts = ids.TensorSketchOp(case["dims"], case["out_dim"], seed=case["seed"])
+        y = ts.apply(factors, data[f"ts{n}_w"])
+        want = data[f"ts{n}_y"]
+        assert y.shape == want.shape
+        # per-mode CountSketches are bit-exact; only the FFT rounding differs
+        assert relerr_fro(y, want) <= 1e-12, (n, relerr_fro(y, want))
+
+
+def test_per_mode_hashes_bit_exact():
+    ts = ids.TensorSketchOp([1000, 1000, 1000], 4096, seed=0)
+    ots = oracle.OracleTensorSketch([1000, 1000, 1000], 4096, seed=0)
+    for a, b in zip(ts.mode_ops, ots.mode_ops):
+        assert np.array_equal(a.bucket, b.bucket) and np.array_equal(a.sign, b.sign)
+    assert ts.seed == 0
+
+
+def test_single_mode_reduces_to_countsketch():
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((12, 5))
+    lam = rng.random(5) + 0.5
+    op = ids.TensorSketchOp([12], 8, seed=8)
+    via_fft = op.apply([a], lam)
+    direct = op.mode_ops[0].apply(a * lam)
+    assert np.abs(via_fft - direct).max() <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_composite_hash_identity(seed):
+    """reference acceptance criterion 2 (test_acceptance.py:108-131)."""
+    rng = np.random.default_rng(1000 + seed)
+    n_modes = 2 if seed % 2 == 0 else 3
+    dims = [int(rng.integers(2, 7)) for _ in range(n_modes)]
+    r = int(rng.integers(1, 6))
+    out_dim = int(rng.integers(2, 17))
+    factors = [rng.standard_normal((d, r)) for d in dims]
+    lam = rng.random(r) + 0.5
+    op = ids.TensorSketchOp(dims, out_dim, seed=seed)
+    bucket = np.zeros(1, dtype=np.int64)
+    sign = np.ones(1)
+    for mode in op.mode_ops:
+        bucket = (bucket[:, None] + mode.bucket[None, :]).ravel()
+        sign = (sign[:, None] * mode.sign[None, :]).ravel()
+    dense_t = dense_countsketch(bucket % out_dim, sign, out_dim)
+    m = khatri_rao(factors) * lam
+    assert relerr_fro(op.apply(factors, lam), dense_t @ m) <= 1e-12
+
+
+def test_materialize_and_all_ones():
+    factors = [np.ones((2, 1))] * 3
+    op = ids.TensorSketchOp([2, 2, 2], 5, seed=9)
+    out = op.apply(factors, np.array([1.0]))
+    oracle_y = op.materialize() @ khatri_rao(factors)
+    assert np.abs(out - oracle_y).max() <= 1e-12
+    assert out.sum() == pytest.approx(op.composite_sign().sum(), abs=1e-10)
+
+
+def test_sparse_factors():
+    rng = np.random.default_rng(10)
+    factors = [sp.random_array((9, 4), density=0.4, rng=rng, format="csc") for _ in range(3)]
+    op = ids.TensorSketchOp([9, 9, 9], 6, seed=11)
+    want = op.materialize() @ khatri_rao([f.toarray() for f in factors])
+    assert np.abs(op.apply(factors) - want).max() <= 1e-11
+
+
+def test_mismatched_columns():
+    op = ids.TensorSketchOp([3, 3], 4, seed=0)
+    with pytest.raises(ValueError):
+        op.apply([np.ones((3, 2)), np.ones((3, 3))])
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 7, 64, 100, 1000, 1452, 2048, 4096, 8192, 16384])
+def test_lengths_vs_oracle(L):
+    rng = np.random.default_rng(L)
+    dims = [50, 40, 30]
+    factors = [rng.standard_normal((d, 6)) for d in dims]
+    lam = rng.random(6) + 0.5
+    op = ids.TensorSketchOp(dims, L, seed=3)
+    want = oracle.OracleTensorSketch(dims, L, seed=3).apply(factors, lam)
+    assert relerr_fro(op.apply(factors, lam), want) <= 1e-12
+
+
+def test_tensorsketch_id_golden(golden):
+    data, man = golden
+    case = man["tensorsketch_id"][0]
+    factors = [data[f"tsid_f{m}"] for m in range(len(case["dims"]))]
+    x = ids.CpTensor(data["tsid_w"], factors)
+    res = ids.tensorsketch_id(x, case["rank"], case["sketch_dim"], seed=case["seed"])
+    assert np.array_equal(res.cols, data["tsid_cols"])
+    assert relerr_fro(res.coeffs, data["tsid_coeffs"]) <= TOL
+    assert relerr_fro(res.new_weights, data["tsid_new_weights"]) <= TOL
+    expected = x.weights[res.cols] * res.coeffs.sum(axis=1)
+    assert np.array_equal(res.new_weights, expected)
+    assert res.method == "tensorsketch"
+
+
+def _near_dup_cp(rng, dims, R, base, pert):
+    bases = rng.integers(0, base, size=R)
+    bases[:base] = np.arange(base)
+    fac = []
+    for d in dims:
+        f = rng.standard_normal((d, R))
+        f[:, :base] /= np.linalg.norm(f[:, :base], axis=0)
+        g = f[:, bases] + pert * rng.standard_normal((d, R))
+        g[:, :base] = f[:, :base]
+        fac.append(g / np.linalg.norm(g, axis=0))
+    return rng.uniform(0.5, 1.0, size=R), fac
+
+
+def test_config4_full_size_vs_oracle():
+    """BASELINE.json configs[3]: N = 3, I = 1000, R = 1000, K = 10, L = 4096."""
+    rng = np.random.default_rng(4)
+    w, fac = _near_dup_cp(rng, [1000] * 3, 1000, 10, 1e-3)
+    x = ids.CpTensor(w, fac)
+    for seed in range(3):
+        want, nw = oracle.tensorsketch_id(x.weights, x.factors, 10, 4096, seed=seed)
+        op = ids.TensorSketchOp(x.mode_dims, 4096, seed=seed)
+        y = op.apply(x.factors, x.weights)
+        assert relerr_fro(y, want.sketch) <= TOL
+        res = ids.tensorsketch_id(x, 10, 4096, seed=seed)
+        assert np.array_equal(res.cols, want.cols), seed
+        assert relerr_fro(res.coeffs, want.coeffs) <= TOL
+        assert relerr_fro(res.new_weights, nw) <= TOL
+        err = oracle.cp_diff_norm(x.weights, x.factors, res.reduced.weights, res.reduced.factors)
+        ref = oracle.cp_diff_norm(
+            x.weights, x.factors, nw, [f[:, want.cols] for f in x.factors])
+        assert abs(err - ref) <= 0.01 * ref + 1e-12
+
+
+def test_exact_rank_recovery_and_keep_all():
+    rng = np.random.default_rng(8)
+    k, total = 4, 10
+    factors = [rng.standard_normal((6, k)) for _ in range(3)]
+    weights = np.concatenate([rng.random(k) + 0.5, np.full(total - k, 1e-14)])
+    dup = rng.integers(0, k, size=total - k)
+    x = ids.CpTensor(weights, [np.hstack([f, f[:, dup]]) for f in factors])
+    res = ids.tensorsketch_id(x, k, seed=1)
+    scale = oracle.cp_norm(x.weights, x.factors)
+    diff = oracle.cp_diff_norm(x.weights, x.factors, res.reduced.weights, res.reduced.factors)
+    assert diff <= 1e-6 * scale
+    rng = np.random.default_rng(9)
+    x = ids.CpTensor(rng.random(7) + 0.5, [rng.standard_normal((d, 7)) for d in (5, 6, 4)])
+    res = ids.tensorsketch_id(x, 7, seed=2)
+    diff = oracle.cp_diff_norm(x.weights, x.factors, res.reduced.weights, res.reduced.factors)
+    assert diff <= 1e-8 * oracle.cp_norm(x.weights, x.factors)
+
+
+def test_tensor_parameter_validation():
+    rng = np.random.default_rng(16)
+    x = ids.CpTensor(np.ones(4), [rng.standard_normal((3, 4)), rng.standard_normal((3, 4))])
+    with pytest.raises(ValueError):
+        ids.tensorsketch_id(x, 5, seed=0)
+    with pytest.raises(ValueError):
+        ids.tensorsketch_id(x, 2, sketch_dim=9, seed=0)
+
+
+def test_reduced_preserves_sparsity_pattern():
+    rng = np.random.default_rng(15)
+    fs = [sp.random_array((10, 6), density=0.3, rng=rng, format="csc") for _ in range(2)]
+    x = ids.CpTensor(rng.random(6) + 0.5, fs)
+    res = ids.tensorsketch_id(x, 3, seed=4)
+    for reduced_f, orig_f in zip(res.reduced.factors, x.factors):
+        for t, col in enumerate(res.cols):
+            got = reduced_f.toarray()[:, t] != 0
+            want = orig_f.toarray()[:, col] != 0
+            assert np.array_equal(got, want)
