@@ -82,31 +82,39 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     for (int v = 0; v < VEC; ++v)
         acc[v] = (init_from_out && valid && c + v < cols) ? o[(c + v) * L + l] : 0.0;
 
-    const double* Abase = A + c - row0 * ld;
-    for (int64_t kb = s0; kb < s1; kb += 32) {
-        const int n = (int)tmin<int64_t>(32, s1 - kb);
-        const int32_t e = lane < n ? __ldg(order + kb + lane) : 0;
-        for (int jj = 0; jj < n; jj += UNR) {
+    // lanes past the last column read a valid column (results discarded) so
+    // that the hot loop is branch-free and all loads of a batch are in flight
+    const int64_t cl = valid ? c : (cols - VEC);
+    const double* Abase = A + cl - row0 * ld;
+    int64_t kb = s0;
+    for (; kb + 32 <= s1; kb += 32) {  // full batches: 32 rows, two rounds of 16 loads
+        const int32_t e = __ldg(order + kb + lane);
+#pragma unroll
+        for (int h = 0; h < 32; h += UNR) {
             double x[UNR][VEC];
             int32_t ev[UNR];
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
-                ev[u] = __shfl_sync(kFull, e, (jj + u) & 31);
-                if (valid && jj + u < n) {
-                    VecT<VEC>::load(Abase + (int64_t)dec_row(ev[u]) * ld, x[u]);
-                } else {
-#pragma unroll
-                    for (int v = 0; v < VEC; ++v) x[u][v] = 0.0;
-                }
+                ev[u] = __shfl_sync(kFull, e, h + u);
+                VecT<VEC>::load(Abase + (int64_t)dec_row(ev[u]) * ld, x[u]);
             }
 #pragma unroll
             for (int u = 0; u < UNR; ++u) {
-                if (jj + u < n) {
 #pragma unroll
-                    for (int v = 0; v < VEC; ++v)
-                        acc[v] = ev[u] >= 0 ? acc[v] + x[u][v] : acc[v] - x[u][v];
-                }
+                for (int v = 0; v < VEC; ++v)
+                    acc[v] = ev[u] >= 0 ? acc[v] + x[u][v] : acc[v] - x[u][v];
             }
+        }
+    }
+    if (kb < s1) {  // tail batch (< 32 rows), in order
+        const int n = (int)(s1 - kb);
+        const int32_t e = lane < n ? __ldg(order + kb + lane) : 0;
+        for (int u = 0; u < n; ++u) {
+            const int32_t ev = __shfl_sync(kFull, e, u);
+            double x[VEC];
+            VecT<VEC>::load(Abase + (int64_t)dec_row(ev) * ld, x);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] = ev >= 0 ? acc[v] + x[v] : acc[v] - x[v];
         }
     }
     if (valid) {

@@ -74,6 +74,61 @@ struct CpqrArgs {
     ArgMax* amax;
 };
 
+// Warp 0 reduces the G per-CTA argmax partials (lane-parallel loads, then a
+// shuffle tree); every CTA runs the same code, so all agree on the pivot.
+__device__ ArgMax reduce_partials_warp(const ArgMax* __restrict__ part, int64_t G) {
+    const int lane = threadIdx.x & 31;
+    ArgMax best{-1.0, INT64_MAX, -1, -1};
+    for (int64_t i = lane; i < G; i += 32) {
+        const ArgMax o = part[i];
+        if (better(o.val, o.pos, best.val, best.pos)) {
+            best.val = o.val;
+            best.pos = o.pos;
+            best.col = o.col;
+        }
+        if (o.col_at_next >= 0) best.col_at_next = o.col_at_next;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ArgMax ot;
+        ot.val = __shfl_xor_sync(0xffffffffu, best.val, o);
+        ot.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
+        ot.col = __shfl_xor_sync(0xffffffffu, best.col, o);
+        ot.col_at_next = __shfl_xor_sync(0xffffffffu, best.col_at_next, o);
+        if (better(ot.val, ot.pos, best.val, best.pos)) {
+            best.val = ot.val;
+            best.pos = ot.pos;
+            best.col = ot.col;
+        }
+        if (ot.col_at_next >= 0) best.col_at_next = ot.col_at_next;
+    }
+    return best;
+}
+
+// Fixed-order sum of G partials strided by `stride`, by one warp (all lanes
+// get the result); identical in every CTA.
+__device__ __forceinline__ double warp_sum_partials(const double* __restrict__ p, int64_t G,
+                                                    int64_t stride) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int64_t i = lane; i < G; i += 32) s += p[i * stride];
+    return warp_sum(s);
+}
+
+// y - sum_q a[q*lda] * b[q*ldb] for q < n, four independent chains.
+__device__ __forceinline__ double sub_dot(double y, const double* __restrict__ a, int64_t lda,
+                                          const double* __restrict__ b, int64_t ldb, int64_t n) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t q = 0;
+    for (; q + 4 <= n; q += 4) {
+        s0 = fma(a[q * lda], b[q * ldb], s0);
+        s1 = fma(a[(q + 1) * lda], b[(q + 1) * ldb], s1);
+        s2 = fma(a[(q + 2) * lda], b[(q + 2) * ldb], s2);
+        s3 = fma(a[(q + 3) * lda], b[(q + 3) * ldb], s3);
+    }
+    for (; q < n; ++q) s0 = fma(a[q * lda], b[q * ldb], s0);
+    return y - ((s0 + s1) + (s2 + s3));
+}
+
 // Block-wide sum of one double per thread; result valid in all threads.
 __device__ double block_sum(double v, double* red) {
     v = warp_sum(v);
@@ -92,6 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
     double* zsh = vsm + g.m;
     double* vrow = zsh + g.k;
     __shared__ int s_nflag;
+    __shared__ double s_red0;
     __shared__ double red[kWarps];
     __shared__ ArgMax warp_best[kWarps];
     __shared__ int64_t s_piv[3];
@@ -168,20 +224,13 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
 
     for (int64_t kk = 0; kk < k; ++kk) {
         // ---- S1: global pivot, position swap, distributed pivot column ----
-        if (threadIdx.x == 0) {
-            ArgMax r = g.amax[0];
-            for (int64_t i = 1; i < G; ++i) {
-                const ArgMax o = g.amax[i];
-                if (better(o.val, o.pos, r.val, r.pos)) {
-                    r.val = o.val;
-                    r.pos = o.pos;
-                    r.col = o.col;
-                }
-                if (o.col_at_next >= 0) r.col_at_next = o.col_at_next;
+        if (wid == 0) {
+            const ArgMax r = reduce_partials_warp(g.amax, G);
+            if (lane == 0) {
+                s_piv[0] = r.col;          // pivot column c*
+                s_piv[1] = r.pos;          // its position p*
+                s_piv[2] = r.col_at_next;  // column at position kk
             }
-            s_piv[0] = r.col;          // pivot column c*
-            s_piv[1] = r.pos;          // its position p*
-            s_piv[2] = r.col_at_next;  // column at position kk
         }
         __syncthreads();
         const int64_t cs = s_piv[0], ps = s_piv[1], ck = s_piv[2];
@@ -193,8 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             const double* ycol = g.Y + cs * ldy;
             double ss = 0.0;
             for (int64_t r = tmax(r0, kk) + threadIdx.x; r < r1; r += kThreads) {
-                double v = ycol[r];
-                for (int64_t q = 0; q < kk; ++q) v = fma(-g.V[q * m + r], g.F[q * n + cs], v);
+                const double v = sub_dot(ycol[r], g.V + r, m, g.F + cs, n, kk);
                 g.a[r] = v;
                 if (r > kk) ss = fma(v, v, ss);
             }
@@ -204,9 +252,12 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         grid.sync();
 
         // ---- S2: Householder vector (redundantly per CTA), z partials, GEMV ----
-        double xs = 0.0;
-        for (int64_t i = 0; i < G; ++i) xs += g.normpart[i];
-        const double xnorm = sqrt(xs);
+        if (wid == 0) {
+            const double xs = warp_sum_partials(g.normpart, G, 1);
+            if (lane == 0) s_red0 = xs;
+        }
+        __syncthreads();
+        const double xnorm = sqrt(s_red0);
         const double alpha = g.a[kk];
         double tau, beta, scal;
         if (xnorm == 0.0) {
@@ -250,23 +301,20 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
 
         // ---- S3: F column, row kk of R, norm downdate, next argmax ----
         // z = V[:, :kk]^T v (fixed-order sum of the per-CTA partials) and row kk of V
-        for (int64_t q = threadIdx.x; q < kk; q += kThreads) {
-            double s = 0.0;
-            for (int64_t i = 0; i < G; ++i) s += g.zpart[i * k + q];
-            zsh[q] = s;
-            vrow[q] = g.V[q * m + kk];
+        for (int64_t q = wid; q < kk; q += kWarps) {
+            const double zq = warp_sum_partials(g.zpart + q, G, k);
+            if (lane == 0) {
+                zsh[q] = zq;
+                vrow[q] = g.V[q * m + kk];
+            }
         }
         if (threadIdx.x == 0) s_nflag = 0;
         __syncthreads();
         // one thread per owned remaining column (F is q-major: coalesced)
         for (int64_t j = c0 + threadIdx.x; j < c1; j += kThreads) {
             if (g.pos[j] <= kk) continue;
-            double f = g.W[j], rk = g.Y[j * ldy + kk];
-            for (int64_t q = 0; q < kk; ++q) {
-                const double fq = g.F[q * n + j];
-                f = fma(-fq, zsh[q], f);
-                rk = fma(-vrow[q], fq, rk);
-            }
+            double f = sub_dot(g.W[j], g.F + j, n, zsh, 1, kk);
+            double rk = sub_dot(g.Y[j * ldy + kk], g.F + j, n, vrow, 1, kk);
             f *= tau;
             g.F[kk * n + j] = f;
             rk -= f;  // V[kk, kk] = 1
@@ -289,8 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             const double* y = g.Y + j * ldy;
             double s = 0.0;
             for (int64_t r = kk + 1 + lane; r < m; r += 32) {
-                double v = y[r];
-                for (int64_t q = 0; q < kk; ++q) v = fma(-g.V[q * m + r], g.F[q * n + j], v);
+                double v = sub_dot(y[r], g.V + r, m, g.F + j, n, kk);
                 v = fma(-vsm[r], g.F[kk * n + j], v);
                 s = fma(v, v, s);
             }
