@@ -129,6 +129,22 @@ __device__ __forceinline__ double sub_dot(double y, const double* __restrict__ a
     return y - ((s0 + s1) + (s2 + s3));
 }
 
+// sum_{r = r0 + lane, step 32, r < m} a[r] * b[r] with four independent chains
+// (one warp; result NOT yet reduced across lanes).
+__device__ __forceinline__ double lane_dot(const double* __restrict__ a, const double* __restrict__ b,
+                                           int64_t r0, int64_t m) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t r = r0 + (threadIdx.x & 31);
+    for (; r + 96 < m; r += 128) {
+        s0 = fma(a[r], b[r], s0);
+        s1 = fma(a[r + 32], b[r + 32], s1);
+        s2 = fma(a[r + 64], b[r + 64], s2);
+        s3 = fma(a[r + 96], b[r + 96], s3);
+    }
+    for (; r < m; r += 32) s0 = fma(a[r], b[r], s0);
+    return (s0 + s1) + (s2 + s3);
+}
+
 // Block-wide sum of one double per thread; result valid in all threads.
 __device__ double block_sum(double v, double* red) {
     v = warp_sum(v);
@@ -209,9 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
     // ---- prologue: column norms (dnrm2), positions ----
     for (int64_t j = c0 + wid; j < c1; j += kWarps) {
         const double* y = g.Y + j * ldy;
-        double s = 0.0;
-        for (int64_t r = lane; r < m; r += 32) s = fma(y[r], y[r], s);
-        s = warp_sum(s);
+        const double s = warp_sum(lane_dot(y, y, 0, m));
         if (lane == 0) {
             g.vn1[j] = sqrt(s);
             g.vn2[j] = sqrt(s);
@@ -291,10 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         // GEMV over owned remaining columns: W_j = Y[kk:, j]^T v
         for (int64_t j = c0 + wid; j < c1; j += kWarps) {
             if (g.pos[j] <= kk) continue;
-            const double* y = g.Y + j * ldy;
-            double s = 0.0;
-            for (int64_t r = kk + lane; r < m; r += 32) s = fma(y[r], vsm[r], s);
-            s = warp_sum(s);
+            const double s = warp_sum(lane_dot(g.Y + j * ldy, vsm, kk, m));
             if (lane == 0) g.W[j] = s;
         }
         grid.sync();
@@ -499,10 +510,10 @@ int grid_size(int64_t m, int64_t n, size_t smem) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_kernel, kThreads, smem);
     if (per_sm < 1) per_sm = 1;
-    // ~ one warp per owned column at least; tiny problems use few CTAs
-    const int64_t want = tmax<int64_t>(1, tmin<int64_t>(ceil_div(n, 2 * kWarps), (int64_t)sms));
-    const int64_t by_rows = tmax<int64_t>(1, ceil_div(m * n, 16384));
-    return (int)tmin<int64_t>((int64_t)sms * per_sm, min(want, tmax<int64_t>(by_rows, 1)));
+    // about one warp per owned column; tiny problems use few CTAs (cheap barriers)
+    const int64_t want = tmax<int64_t>(1, tmin<int64_t>(ceil_div(n, kWarps), (int64_t)sms));
+    const int64_t by_size = tmax<int64_t>(1, ceil_div(m * n, 2048));
+    return (int)tmin<int64_t>((int64_t)sms * per_sm, tmin(want, by_size));
 }
 
 constexpr int64_t kMaxG = 148;

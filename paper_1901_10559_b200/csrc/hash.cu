@@ -182,142 +182,62 @@ __global__ void __launch_bounds__(kGenThreads) sign_kernel(Seed sd, const int64_
 
 __device__ __forceinline__ uint32_t mask_of(uint32_t i) { return 0xFFFFFFFFu >> __clz(i); }
 
+// ---- phase B: the accept/reject chain of the masked Fisher-Yates draws -----
+// i runs n-1 .. 1; each 32-bit draw x gives v = x & mask(i); v <= i is
+// accepted (j[i] = v, i -= 1), otherwise it is rejected.  FyState holds the
+// exact (draw position, i) between stages.
+struct FyState {
+    int64_t pos;   // next unconsumed draw (relative to the phase-B stream)
+    int64_t i;     // current i
+    int64_t done;  // number of chunks resolved by the last stitch
+};
+
 enum { ST_DONE = 0, ST_ACC = 1, ST_REJ = 2, ST_AMB = 3 };
 
-__device__ __forceinline__ int classify(uint32_t x, int64_t i, int64_t u, uint32_t* v) {
+// Lane of a 32-draw window: the true i before it lies in [i - u, i].  Definite
+// when the mask is the same over that range, the range stays above i_stop and
+// v is outside (lo, i].
+__device__ __forceinline__ int classify(uint32_t x, int64_t i, int64_t u, int64_t i_stop,
+                                        uint32_t* v) {
     const int64_t lo = i - u;
     const uint32_t m = mask_of((uint32_t)i);
-    if (lo < 1 || mask_of((uint32_t)lo) != m) return ST_AMB;
+    if (lo <= i_stop || lo < 1 || mask_of((uint32_t)lo) != m) return ST_AMB;
     *v = x & m;
     if ((int64_t)*v <= lo) return ST_ACC;
     if ((int64_t)*v > i) return ST_REJ;
     return ST_AMB;
 }
 
-// Phase B accept/reject chain.  g: the phase-B draw stream (nbuf draws).
-// Writes jout[i] for i = n-1..1 and the number of draws consumed.
-__global__ void __launch_bounds__(1024, 1) fy_scan_kernel(const uint32_t* __restrict__ g,
-                                                          int64_t nbuf, int64_t n,
-                                                          int32_t* __restrict__ jout,
-                                                          int64_t* consumed, int64_t* status) {
-    __shared__ uint32_t s_acc[32], s_amb[32];
-    __shared__ int s_pref[32];
-    __shared__ int s_tamb, s_A, s_done;
-    __shared__ int64_t s_i, s_cons;
-    const int t = threadIdx.x, w = t >> 5, ln = t & 31;
+// One warp walks the chain exactly from st->(pos, i) until i == i_stop,
+// 32 draws per round (ambiguous lanes are settled one at a time).  When
+// i_stop == 0 the walk ends the phase and *consumed gets the draw count.
+__device__ void fy_walk_warp(const uint32_t* __restrict__ g, int64_t nbuf, int64_t i_stop,
+                             int32_t* __restrict__ jout, FyState* st, int64_t* status) {
+    const int ln = threadIdx.x & 31;
     const uint32_t lt_mask = (1u << ln) - 1u;
-    if (n <= 1) {
-        if (t == 0) *consumed = 0;
-        return;
-    }
-    int64_t i = n - 1;
-    int64_t pos = 0;
-    if (t == 0) s_done = 0;
-    __syncthreads();
-    // ---------------- block regime: 1024 draws per window -----------------
-    uint32_t x_next = (pos + t < nbuf) ? g[pos + t] : 0u;
-    while (i >= (int64_t)kBlockMin) {
+    int64_t i = st->i, pos = st->pos;
+    while (i > i_stop) {
         if (pos + 1024 > nbuf) {
-            if (t == 0) *status = IDS_ERETRY;
-            return;
-        }
-        const uint32_t x = x_next;
-        x_next = (pos + 1024 + t < nbuf) ? g[pos + 1024 + t] : 0u;
-        int b = 0;
-        while (b < 1024) {
-            uint32_t v = 0;
-            const int st = (t >= b) ? classify(x, i, t - b, &v) : ST_DONE;
-            const uint32_t accb = __ballot_sync(0xffffffffu, st == ST_ACC);
-            const uint32_t ambb = __ballot_sync(0xffffffffu, st == ST_AMB);
-            if (ln == 0) {
-                s_acc[w] = accb;
-                s_amb[w] = ambb;
-            }
-            __syncthreads();
-            if (w == 0) {
-                const uint32_t a = s_acc[ln], am = s_amb[ln];
-                const uint32_t anyamb = __ballot_sync(0xffffffffu, am != 0u);
-                const int fw = anyamb ? __ffs(anyamb) - 1 : 32;
-                const int tamb = fw < 32 ? fw * 32 + __ffs(__shfl_sync(0xffffffffu, am, fw)) - 1
-                                         : 1024;
-                int cnt;
-                if (ln < fw) cnt = __popc(a);
-                else if (ln == fw) cnt = __popc(a & ((1u << (tamb & 31)) - 1u));
-                else cnt = 0;
-                int inc = cnt;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (ln >= o) inc += y;
-                }
-                s_pref[ln] = inc - cnt;
-                if (ln == 31) {
-                    s_A = inc;
-                    s_tamb = tamb;
-                }
-            }
-            __syncthreads();
-            const int tamb = s_tamb, A = s_A;
-            if (st == ST_ACC && t < tamb) {
-                const int a_t = s_pref[w] + __popc(accb & lt_mask);
-                jout[i - a_t] = (int32_t)v;
-            }
-            if (tamb == 1024) {
-                i -= A;
-                break;
-            }
-            if (t == tamb) {
-                int64_t is = i - A;
-                if (is < 1) {
-                    s_done = 1;
-                    s_cons = pos + tamb;
-                } else {
-                    const uint32_t vv = x & mask_of((uint32_t)is);
-                    if ((int64_t)vv <= is) {
-                        jout[is] = (int32_t)vv;
-                        --is;
-                    }
-                    s_i = is;
-                    if (is == 0) {
-                        s_done = 1;
-                        s_cons = pos + tamb + 1;
-                    }
-                }
-            }
-            __syncthreads();
-            if (s_done) {
-                if (t == 0) *consumed = s_cons;
-                return;
-            }
-            i = s_i;
-            b = tamb + 1;
-        }
-        pos += 1024;
-    }
-    // ---------------- warp regime: 32 draws per window ---------------------
-    if (w != 0) return;
-    for (;;) {
-        if (pos >= nbuf) {
             if (ln == 0) *status = IDS_ERETRY;
-            return;
+            break;
         }
         uint32_t xs[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            const int64_t p = pos + 32 * k + ln;
-            xs[k] = p < nbuf ? g[p] : 0u;
-        }
+        for (int k = 0; k < 32; ++k) xs[k] = __ldg(g + pos + 32 * k + ln);
+        bool stop = false;
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
+            if (stop) break;
             const uint32_t x = xs[k];
             int b = 0;
             while (b < 32) {
                 uint32_t v = 0;
-                const int st = (ln >= b) ? classify(x, i, ln - b, &v) : ST_DONE;
-                const uint32_t accb = __ballot_sync(0xffffffffu, st == ST_ACC);
-                const uint32_t ambb = __ballot_sync(0xffffffffu, st == ST_AMB);
+                const int stt = (ln >= b) ? classify(x, i, ln - b, i_stop, &v) : ST_DONE;
+                const uint32_t accb = __ballot_sync(0xffffffffu, stt == ST_ACC);
+                const uint32_t ambb = __ballot_sync(0xffffffffu, stt == ST_AMB);
                 const int tamb = ambb ? __ffs(ambb) - 1 : 32;
                 const uint32_t before = tamb < 32 ? (accb & ((1u << tamb) - 1u)) : accb;
-                if (st == ST_ACC && ln < tamb) jout[i - __popc(before & lt_mask)] = (int32_t)v;
+                if (stt == ST_ACC && ln < tamb) jout[i - __popc(before & lt_mask)] = (int32_t)v;
                 const int A = __popc(before);
                 if (tamb == 32) {
                     i -= A;
@@ -325,24 +245,171 @@ __global__ void __launch_bounds__(1024, 1) fy_scan_kernel(const uint32_t* __rest
                 }
                 int64_t is = i - A;
                 const uint32_t xa = __shfl_sync(0xffffffffu, x, tamb);
-                if (is < 1) {
-                    if (ln == 0) *consumed = pos + 32 * k + tamb;
-                    return;
+                if (is <= i_stop) {  // stage ends before this draw
+                    pos += 32 * k + tamb;
+                    i = is;
+                    stop = true;
+                    break;
                 }
                 const uint32_t vv = xa & mask_of((uint32_t)is);
                 if ((int64_t)vv <= is) {
                     if (ln == 0) jout[is] = (int32_t)vv;
                     --is;
                 }
-                if (is == 0) {
-                    if (ln == 0) *consumed = pos + 32 * k + tamb + 1;
-                    return;
-                }
                 i = is;
                 b = tamb + 1;
+                if (i == i_stop) {
+                    pos += 32 * k + tamb + 1;
+                    stop = true;
+                    break;
+                }
             }
         }
-        pos += 1024;
+        if (!stop) pos += 1024;
+    }
+    __syncwarp();
+    if (ln == 0) {
+        st->i = i;
+        st->pos = pos;
+    }
+}
+
+__global__ void fy_walk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, int64_t i_stop,
+                               int32_t* __restrict__ jout, FyState* st, int64_t* consumed,
+                               int64_t* status) {
+    fy_walk_warp(g, nbuf, i_stop, jout, st, status);
+    if (i_stop == 0 && threadIdx.x == 0) *consumed = st->pos;
+}
+
+__global__ void fy_init_kernel(FyState* st, int64_t n) {
+    st->pos = 0;
+    st->i = n - 1;
+    st->done = 0;
+}
+
+// Speculative chunks of band [lo_band, hi_band] (mask = 2*lo_band - 1):
+// chunk c covers draws st->pos + [c*T, (c+1)*T).  Its true starting i is
+// unknown; the expected trajectory gives a window [s, s + W] that contains it
+// with overwhelming probability.  The LOWEST start s is simulated; any start
+// s + d stays exactly d above it except at "near misses", draws the base
+// rejects with gap g = v - i_base in [1, W]: a trajectory whose current
+// offset is >= g accepts there and its offset drops by one.  Recording those
+// gaps (in order) makes the chunk's end state a cheap function of the true
+// start, evaluated by the stitch below.
+constexpr int kEvMax = 24;
+struct FyChunk {
+    int64_t s;    // lowest start in the window
+    int32_t w;    // window width (-1: chunk not usable)
+    int32_t a;    // accepts of the base trajectory
+    int32_t ne;   // near-miss events recorded (-1: overflow)
+    int32_t ev[kEvMax];
+};
+
+__global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, const FyState* st,
+                                int64_t i0, int64_t lo_band, int64_t T, int64_t nchunks,
+                                FyChunk* __restrict__ ch) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    FyChunk out;
+    out.w = -1;
+    out.a = 0;
+    out.ne = 0;
+    out.s = 0;
+    const double tau = (double)(c * T);
+    const double m2 = (double)(2 * lo_band);  // mask + 1
+    const double gi = (double)(i0 + 1) * exp(-tau / m2) - 1.0;
+    const int64_t half = c == 0 ? 0 : (int64_t)(3.0 * sqrt(tau) + 16.0);
+    int64_t s = (int64_t)floor(gi) - half;
+    int64_t hi = tmin<int64_t>((int64_t)floor(gi) + half, i0);
+    if (c == 0) s = hi = i0;
+    const int64_t pos0 = st->pos + c * T;
+    if (s - T > lo_band && hi >= s && pos0 + T <= nbuf) {
+        const uint32_t m = (uint32_t)(2 * lo_band - 1);
+        const int64_t w = hi - s;
+        int64_t i = s;
+        int a = 0, ne = 0;
+        const uint32_t* x = g + pos0;
+        for (int64_t t = 0; t < T; ++t) {
+            const int64_t v = (int64_t)(__ldg(x + t) & m);
+            if (v <= i) {
+                --i;
+                ++a;
+            } else if (v - i <= w) {
+                if (ne < kEvMax) out.ev[ne] = (int32_t)(v - i);
+                ++ne;
+            }
+        }
+        out.s = s;
+        out.w = (int32_t)w;
+        out.a = a;
+        out.ne = ne <= kEvMax ? ne : -1;
+    }
+    ch[c] = out;
+}
+
+// Exact re-run of chunk c from its resolved start, writing j (one thread each).
+__global__ void fy_chunk_exact_kernel(const uint32_t* __restrict__ g, const FyState* st0,
+                                      const int64_t* __restrict__ starts, int64_t lo_band,
+                                      int64_t T, int32_t* __restrict__ jout, int64_t pos_base) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= st0->done) return;
+    const uint32_t m = (uint32_t)(2 * lo_band - 1);
+    int64_t i = starts[c];
+    const uint32_t* x = g + starts[-1] + c * T;  // starts[-1] holds the band's first draw
+    for (int64_t t = 0; t < T; ++t) {
+        const uint32_t v = __ldg(x + t) & m;
+        if ((int64_t)v <= i) {
+            jout[i] = (int32_t)v;
+            --i;
+        }
+    }
+    (void)pos_base;
+}
+
+// One warp resolves the chunks in order: the true start of chunk c gives its
+// offset d in the window; replaying the near-miss gaps gives the end state.
+// A chunk whose start falls outside its window (or overflowed) stops the
+// stitch; the exact walk then continues from there.
+__global__ void fy_stitch_kernel(FyState* st, const FyChunk* __restrict__ ch, int64_t nchunks,
+                                 int64_t T, int64_t* __restrict__ starts) {
+    const int ln = threadIdx.x & 31;
+    int64_t S = st->i;
+    const int64_t pos0 = st->pos;
+    if (ln == 0) starts[-1] = pos0;
+    int64_t done = 0;
+    bool ok = true;
+    for (int64_t c0 = 0; c0 < nchunks && ok; c0 += 32) {
+        const int64_t c = c0 + ln;
+        FyChunk mine;
+        mine.w = -1;
+        if (c < nchunks) mine = ch[c];
+        const int cnt = (int)tmin<int64_t>(32, nchunks - c0);
+        for (int l = 0; l < cnt; ++l) {
+            const int64_t s = __shfl_sync(0xffffffffu, mine.s, l);
+            const int w = __shfl_sync(0xffffffffu, mine.w, l);
+            const int ne = __shfl_sync(0xffffffffu, mine.ne, l);
+            const int64_t d = S - s;
+            if (w < 0 || ne < 0 || d < 0 || d > w) {
+                ok = false;
+                break;
+            }
+            int64_t dd = d;
+            if (ln == l) {
+                for (int e = 0; e < ne; ++e)
+                    if (dd >= mine.ev[e]) --dd;
+            }
+            dd = __shfl_sync(0xffffffffu, dd, l);
+            const int a = __shfl_sync(0xffffffffu, mine.a, l);
+            if (ln == 0) starts[c0 + l] = S;
+            S = s - a + dd;
+            ++done;
+        }
+    }
+    __syncwarp();
+    if (ln == 0) {
+        st->i = S;
+        st->pos = pos0 + done * T;
+        st->done = done;
     }
 }
 
@@ -422,8 +489,19 @@ struct HashPlan {
     int64_t I, L;
     int surj;
     int64_t n_acc, n_cand, nblk, nbuf;
+    int64_t max_chunks;
     size_t scan_bytes, scan2_bytes;
 };
+
+constexpr int kMinBand = 15;  // bands below 2^15 are walked exactly by one warp
+
+// Chunk length for band k: ~8 expected near-miss events per chunk.
+int64_t band_chunk(int k) {
+    const double want = 2.3 * pow(2.0, 0.5 * k);
+    int64_t T = 256;
+    while (T < want && T < 4096) T <<= 1;
+    return T;
+}
 
 HashPlan make_plan(int64_t I, int64_t L, int surj) {
     HashPlan p;
@@ -442,6 +520,7 @@ HashPlan make_plan(int64_t I, int64_t L, int surj) {
     if (p.nblk < 1) p.nblk = 1;
     p.nbuf = surj ? 2 * I + 16 * (int64_t)sqrt((double)I + 1.0) + 4096 : 0;
     p.nbuf = (p.nbuf + 1023) / 1024 * 1024;
+    p.max_chunks = surj ? (2 * I) / 256 + 64 : 0;
     p.scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, p.scan_bytes, (int64_t*)nullptr, (int64_t*)nullptr,
                                   (int)p.nblk);
@@ -455,7 +534,8 @@ HashPlan make_plan(int64_t I, int64_t L, int surj) {
 template <class W>
 void carve(W& ws, const HashPlan& p, int64_t** blk_cnt, int64_t** blk_off, int64_t** scal,
            void** scan_tmp, int32_t** tail, uint32_t** draws, int32_t** jarr, int32_t** first,
-           int32_t** gcount, int32_t** goff, int32_t** members) {
+           int32_t** gcount, int32_t** goff, int32_t** members, FyState** fst, FyChunk** chunks,
+           int64_t** starts) {
     *blk_cnt = ws.template take<int64_t>(p.nblk);
     *blk_off = ws.template take<int64_t>(p.nblk);
     *scal = ws.template take<int64_t>(4);
@@ -469,6 +549,9 @@ void carve(W& ws, const HashPlan& p, int64_t** blk_cnt, int64_t** blk_off, int64
         *gcount = ws.template take<int32_t>(p.I + 1);
         *goff = ws.template take<int32_t>(p.I + 1);
         *members = ws.template take<int32_t>(p.I + 1);
+        *fst = ws.template take<FyState>(1);
+        *chunks = ws.template take<FyChunk>(p.max_chunks);
+        *starts = ws.template take<int64_t>(p.max_chunks + 1);
     }
 }
 
@@ -491,7 +574,10 @@ extern "C" size_t ids_hash_workspace_bytes(int64_t in_dim, int64_t out_dim, int 
     void* d;
     int32_t *e, *g, *h, *i2, *j2, *k2;
     uint32_t* f;
-    carve(nc, p, &a, &b, &c, &d, &e, &f, &g, &h, &i2, &j2, &k2);
+    FyState* fs;
+    FyChunk* fc;
+    int64_t* sts;
+    carve(nc, p, &a, &b, &c, &d, &e, &f, &g, &h, &i2, &j2, &k2, &fs, &fc, &sts);
     return nc.off + 256;
 }
 
@@ -516,8 +602,11 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
     int32_t *tail = nullptr, *jarr = nullptr, *first = nullptr, *gcount = nullptr,
             *goff = nullptr, *members = nullptr;
     uint32_t* draws = nullptr;
+    FyState* fst = nullptr;
+    FyChunk* chunks = nullptr;
+    int64_t* starts = nullptr;
     carve(ws, p, &blk_cnt, &blk_off, &scal, &scan_tmp, &tail, &draws, &jarr, &first, &gcount,
-          &goff, &members);
+          &goff, &members, &fst, &chunks, &starts);
     if (!ws.ok()) {
         ids_set_last_error("hash: workspace too small");
         return IDS_EWORKSPACE;
@@ -553,7 +642,30 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
         const unsigned gb = (unsigned)ceil_div(p.nbuf, (int64_t)kGenThreads * kChunk);
         raw_draws_kernel<<<gb, kGenThreads, 0, st>>>(sd, d, 1, p.nbuf, draws);
         IDS_LAUNCH_CHECK();
-        fy_scan_kernel<<<1, 1024, 0, st>>>(draws, p.nbuf, I, jarr, d + 1, d + 3);
+        fy_init_kernel<<<1, 1, 0, st>>>(fst, I);
+        IDS_LAUNCH_CHECK();
+        int top = 0;
+        while ((2LL << top) <= I - 1) ++top;  // band of i = I - 1
+        for (int k = top; k >= kMinBand && I > 1; --k) {
+            const int64_t lo_band = 1LL << k;
+            const int64_t i0 = tmin<int64_t>(2 * lo_band - 1, I - 1);
+            if (i0 < lo_band) continue;
+            const int64_t T = band_chunk(k);
+            const double draws_est = (double)(2 * lo_band) * log((double)(i0 + 1) / (double)lo_band);
+            const int64_t nch = tmin<int64_t>((int64_t)(draws_est / (double)T) + 2, p.max_chunks);
+            if (nch >= 2) {
+                const unsigned gb = (unsigned)ceil_div(nch, 128);
+                fy_chunk_kernel<<<gb, 128, 0, st>>>(draws, p.nbuf, fst, i0, lo_band, T, nch, chunks);
+                IDS_LAUNCH_CHECK();
+                fy_stitch_kernel<<<1, 32, 0, st>>>(fst, chunks, nch, T, starts + 1);
+                IDS_LAUNCH_CHECK();
+                fy_chunk_exact_kernel<<<gb, 128, 0, st>>>(draws, fst, starts + 1, lo_band, T, jarr, 0);
+                IDS_LAUNCH_CHECK();
+            }
+            fy_walk_kernel<<<1, 32, 0, st>>>(draws, p.nbuf, lo_band - 1, jarr, fst, d + 1, d + 3);
+            IDS_LAUNCH_CHECK();
+        }
+        fy_walk_kernel<<<1, 32, 0, st>>>(draws, p.nbuf, 0, jarr, fst, d + 1, d + 3);
         IDS_LAUNCH_CHECK();
         if (I > 1) {
             fill_i32_kernel<<<1024, 256, 0, st>>>(first, I, kNone);

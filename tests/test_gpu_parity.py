@@ -77,6 +77,18 @@ def test_hash_random_shapes_vs_oracle():
         assert np.array_equal(op.sign, o.sign), (I, L, seed, surj)
 
 
+@pytest.mark.parametrize("I", [32768, 32769, 65535, 65536, 65537, 131071, 131072, 131073,
+                               262145, 524289, 1048577, 3_000_001])
+def test_hash_band_boundaries_vs_oracle(I):
+    # the banded speculative Fisher-Yates resolution around band edges
+    for L, seed in [(1, 1), (100, 2), (I // 3, 3)]:
+        op = ids.CountSketchOp(I, L, seed=seed, surjective=True)
+        o = oracle.OracleCountSketch(I, L, seed, True)
+        assert op.draws == tuple(int(v) for v in o.draws), (I, L, seed)
+        assert np.array_equal(op.bucket, o.bucket), (I, L, seed)
+        assert np.array_equal(op.sign, o.sign), (I, L, seed)
+
+
 def test_surjective_covers_all_buckets():
     op = ids.CountSketchOp(1000, 10, seed=1, surjective=True)
     assert np.unique(op.bucket).size == 10
