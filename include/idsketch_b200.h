@@ -70,12 +70,13 @@ int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
 /* ---------------------------------------------------------------------------
  * Bucket index: the rows of each bucket in increasing row order, i.e. the CSR
  * structure of the L x I operator S that sketch.py:108-114 (`_matrix`) builds.
- * order_signed[k] = row (sign +1) or ~row (sign -1); bstart int64[L+1].
+ * order_signed[k] = row (sign +1) or ~row (sign -1); bstart int64[L+1];
+ * sorted_bucket (may be NULL): int32[I], the bucket of order_signed[k].
  * ------------------------------------------------------------------------- */
 size_t ids_bucket_index_workspace_bytes(int64_t in_dim, int64_t out_dim);
 int ids_bucket_index(const int32_t* bucket, const int8_t* sign, int64_t in_dim,
                      int64_t out_dim, int32_t* order_signed, int64_t* bstart,
-                     void* workspace, size_t ws_bytes, void* stream);
+                     int32_t* sorted_bucket, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Dense CountSketch Y (+)= S[:, row0:row0+rows] @ A.  Replaces sketch.py:119
@@ -148,7 +149,8 @@ int ids_countsketch_csr_f64(const void* indptr, int indptr64, const int32_t* ind
  * x weights).  Never forms Khatri-Rao columns.
  *   n_modes, and HOST arrays of per-mode DEVICE pointers:
  *   factors[n]: col-major dims[n] x ncols with leading dimension lds[n];
- *   order_signed[n], bstart[n]: bucket index of mode n (out_dim buckets).
+ *   order_signed[n], sorted_bucket[n]: bucket index of mode n (out_dim
+ *   buckets; see ids_bucket_index).
  *   weights: device double[ncols] or NULL.  Y: col-major out_dim x ncols.
  *   colnorm2 (may be NULL): ||Y[:,r]||^2 per column.
  * ------------------------------------------------------------------------- */
@@ -156,9 +158,10 @@ size_t ids_tensorsketch_workspace_bytes(int n_modes, const int64_t* dims, int64_
                                         int64_t out_dim);
 int ids_tensorsketch_f64(int n_modes, const double* const* factors, const int64_t* dims,
                          const int64_t* lds, int64_t ncols,
-                         const int32_t* const* order_signed, const int64_t* const* bstart,
-                         int64_t out_dim, const double* weights, double* Y,
-                         double* colnorm2, void* workspace, size_t ws_bytes, void* stream);
+                         const int32_t* const* order_signed,
+                         const int32_t* const* sorted_bucket, int64_t out_dim,
+                         const double* weights, double* Y, double* colnorm2, void* workspace,
+                         size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Truncated column-pivoted Householder QR (k steps).  Replaces linalg.py:97-102

@@ -33,7 +33,9 @@ SIGNATURES = {
          _c_p],
     ),
     "ids_bucket_index_workspace_bytes": (_c_sz, [_c_i64, _c_i64]),
-    "ids_bucket_index": (_c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "ids_bucket_index": (
+        _c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]
+    ),
     "ids_countsketch_dense_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_i64, _c_int]),
     "ids_countsketch_dense_f64": (
         _c_int,

@@ -59,7 +59,8 @@ extern "C" size_t ids_bucket_index_workspace_bytes(int64_t in_dim, int64_t out_d
 
 extern "C" int ids_bucket_index(const int32_t* bucket, const int8_t* sign, int64_t in_dim,
                                 int64_t out_dim, int32_t* order_signed, int64_t* bstart,
-                                void* workspace, size_t ws_bytes, void* stream) {
+                                int32_t* sorted_bucket, void* workspace, size_t ws_bytes,
+                                void* stream) {
     if (in_dim < 1 || out_dim < 1 || in_dim > 0x7fffffffLL) {
         ids_set_last_error("bucket index: dimensions out of range");
         return IDS_EINVAL;
@@ -67,7 +68,8 @@ extern "C" int ids_bucket_index(const int32_t* bucket, const int8_t* sign, int64
     cudaStream_t st = as_stream(stream);
     WsCarve ws(workspace, ws_bytes);
     int32_t* vals = ws.take<int32_t>(in_dim);
-    int32_t* keys_out = ws.take<int32_t>(in_dim);
+    int32_t* keys_tmp = ws.take<int32_t>(in_dim);
+    int32_t* keys_out = sorted_bucket ? sorted_bucket : keys_tmp;
     const size_t sb = sort_bytes(in_dim, out_dim);
     void* tmp = ws.take<char>(sb);
     if (!ws.ok()) {

@@ -33,7 +33,6 @@ namespace {
 
 constexpr int kGenThreads = 256;
 constexpr int kChunk = 32;  // 32-bit draws per thread in the parallel phases
-constexpr uint32_t kBlockMin = 65536;
 constexpr int32_t kNone = 0x7fffffff;
 
 __device__ __forceinline__ u128 ld128(const uint64_t v[2]) {
@@ -192,93 +191,137 @@ struct FyState {
     int64_t done;  // number of chunks resolved by the last stitch
 };
 
-enum { ST_DONE = 0, ST_ACC = 1, ST_REJ = 2, ST_AMB = 3 };
+// One warp walks the chain EXACTLY over draws [pos, limit) from a known i,
+// until i == i_stop: 256 draws per window, 8 consecutive draws per lane.
+// Round: every unfinished lane classifies its draws assuming between 0 and
+// 8*(lanes before it) accepts precede it; draws whose fate does not depend on
+// that count are definite.  The first lane holding an ambiguous draw ends
+// the round: the lanes before it are exact (prefix sum of their accepts) and
+// it walks its own 8 draws exactly from the now exact start.  Optionally
+// writes j[i] for accepted draws and records "near misses" (rejections with
+// gap v - i in [1, w], in draw order) for the speculative chunks.
+struct WalkOut {
+    int64_t i, pos;
+    int nev;
+};
 
-// Lane of a 32-draw window: the true i before it lies in [i - u, i].  Definite
-// when the mask is the same over that range, the range stays above i_stop and
-// v is outside (lo, i].
-__device__ __forceinline__ int classify(uint32_t x, int64_t i, int64_t u, int64_t i_stop,
-                                        uint32_t* v) {
-    const int64_t lo = i - u;
-    const uint32_t m = mask_of((uint32_t)i);
-    if (lo <= i_stop || lo < 1 || mask_of((uint32_t)lo) != m) return ST_AMB;
-    *v = x & m;
-    if ((int64_t)*v <= lo) return ST_ACC;
-    if ((int64_t)*v > i) return ST_REJ;
-    return ST_AMB;
-}
-
-// One warp walks the chain exactly from st->(pos, i) until i == i_stop,
-// 32 draws per round (ambiguous lanes are settled one at a time).  When
-// i_stop == 0 the walk ends the phase and *consumed gets the draw count.
-__device__ void fy_walk_warp(const uint32_t* __restrict__ g, int64_t nbuf, int64_t i_stop,
-                             int32_t* __restrict__ jout, FyState* st, int64_t* status) {
+__device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_t limit,
+                             int64_t i, int64_t i_stop, int32_t* __restrict__ jout, int64_t w,
+                             int32_t* __restrict__ ev, int evmax) {
     const int ln = threadIdx.x & 31;
-    const uint32_t lt_mask = (1u << ln) - 1u;
-    int64_t i = st->i, pos = st->pos;
-    while (i > i_stop) {
-        if (pos + 1024 > nbuf) {
-            if (ln == 0) *status = IDS_ERETRY;
-            break;
+    int nev = 0;
+    while (i > i_stop && pos < limit) {
+        uint32_t x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t p = pos + 8 * ln + q;
+            x[q] = p < limit ? __ldg(g + p) : 0u;
         }
-        uint32_t xs[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) xs[k] = __ldg(g + pos + 32 * k + ln);
+        int b = 0;
+        int64_t ib = i;
         bool stop = false;
+        int64_t pos_final = 0;
+        while (b < 32) {
+            // -- speculative classification of this lane's draws
+            int a = 0;
+            bool amb = false;
+            if (ln >= b) {
+                const int64_t umax = 8 * (ln - b);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            if (stop) break;
-            const uint32_t x = xs[k];
-            int b = 0;
-            while (b < 32) {
-                uint32_t v = 0;
-                const int stt = (ln >= b) ? classify(x, i, ln - b, i_stop, &v) : ST_DONE;
-                const uint32_t accb = __ballot_sync(0xffffffffu, stt == ST_ACC);
-                const uint32_t ambb = __ballot_sync(0xffffffffu, stt == ST_AMB);
-                const int tamb = ambb ? __ffs(ambb) - 1 : 32;
-                const uint32_t before = tamb < 32 ? (accb & ((1u << tamb) - 1u)) : accb;
-                if (stt == ST_ACC && ln < tamb) jout[i - __popc(before & lt_mask)] = (int32_t)v;
-                const int A = __popc(before);
-                if (tamb == 32) {
-                    i -= A;
-                    break;
-                }
-                int64_t is = i - A;
-                const uint32_t xa = __shfl_sync(0xffffffffu, x, tamb);
-                if (is <= i_stop) {  // stage ends before this draw
-                    pos += 32 * k + tamb;
-                    i = is;
-                    stop = true;
-                    break;
-                }
-                const uint32_t vv = xa & mask_of((uint32_t)is);
-                if ((int64_t)vv <= is) {
-                    if (ln == 0) jout[is] = (int32_t)vv;
-                    --is;
-                }
-                i = is;
-                b = tamb + 1;
-                if (i == i_stop) {
-                    pos += 32 * k + tamb + 1;
-                    stop = true;
-                    break;
+                for (int q = 0; q < 8; ++q) {
+                    if (!amb) {
+                        const int64_t hi = ib - a, lo = hi - umax;
+                        const int64_t p = pos + 8 * ln + q;
+                        if (p >= limit || lo <= i_stop || lo < 1 ||
+                            mask_of((uint32_t)lo) != mask_of((uint32_t)hi)) {
+                            amb = true;
+                        } else {
+                            const int64_t v = (int64_t)(x[q] & mask_of((uint32_t)hi));
+                            if (v <= lo) ++a;
+                            else if (v <= hi) amb = true;
+                        }
+                    }
                 }
             }
+            const uint32_t ambb = __ballot_sync(0xffffffffu, amb);
+            const int ls = ambb ? __ffs(ambb) - 1 : 32;
+            const int cnt = (ln >= b && ln < ls) ? a : 0;
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (ln >= o) incl += y;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            // -- exact walk of lanes [b, ls]
+            int64_t ii = ib - (incl - cnt);
+            int endq = 8;
+            int ne = 0;
+            int32_t gaps[8];
+            if (ln >= b && ln <= ls) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (endq == 8) {
+                        const int64_t p = pos + 8 * ln + q;
+                        if (p >= limit || ii <= i_stop) {
+                            endq = q;
+                        } else {
+                            const int64_t v = (int64_t)(x[q] & mask_of((uint32_t)ii));
+                            if (v <= ii) {
+                                if (jout) jout[ii] = (int32_t)v;
+                                --ii;
+                            } else if (v - ii <= w) {
+                                gaps[ne++] = (int32_t)(v - ii);
+                            }
+                        }
+                    }
+                }
+            }
+            if (w > 0 && __ballot_sync(0xffffffffu, ne > 0)) {
+                int einc = ne;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, einc, o);
+                    if (ln >= o) einc += y;
+                }
+                const int base = nev + einc - ne;
+                for (int e = 0; e < ne; ++e)
+                    if (base + e < evmax) ev[base + e] = gaps[e];
+                nev += __shfl_sync(0xffffffffu, einc, 31);
+            }
+            if (ls == 32) {
+                ib -= total;
+                break;
+            }
+            ib = __shfl_sync(0xffffffffu, ii, ls);
+            const int eq = __shfl_sync(0xffffffffu, endq, ls);
+            b = ls + 1;
+            if (eq < 8) {
+                stop = true;
+                pos_final = pos + 8 * ls + eq;
+                break;
+            }
         }
-        if (!stop) pos += 1024;
+        i = ib;
+        if (stop) {
+            pos = pos_final;
+            break;
+        }
+        pos += 256;
     }
-    __syncwarp();
-    if (ln == 0) {
-        st->i = i;
-        st->pos = pos;
-    }
+    return WalkOut{i, tmin<int64_t>(pos, limit), nev};
 }
 
 __global__ void fy_walk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, int64_t i_stop,
                                int32_t* __restrict__ jout, FyState* st, int64_t* consumed,
                                int64_t* status) {
-    fy_walk_warp(g, nbuf, i_stop, jout, st, status);
-    if (i_stop == 0 && threadIdx.x == 0) *consumed = st->pos;
+    const WalkOut r = warp_walk(g, st->pos, nbuf, st->i, i_stop, jout, 0, nullptr, 0);
+    if (threadIdx.x == 0) {
+        if (r.i > i_stop) *status = IDS_ERETRY;  // ran out of buffered draws
+        st->i = r.i;
+        st->pos = r.pos;
+        if (i_stop == 0) *consumed = r.pos;
+    }
 }
 
 __global__ void fy_init_kernel(FyState* st, int64_t n) {
@@ -308,13 +351,11 @@ struct FyChunk {
 __global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, const FyState* st,
                                 int64_t i0, int64_t lo_band, int64_t T, int64_t nchunks,
                                 FyChunk* __restrict__ ch) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int ln = threadIdx.x & 31;
     if (c >= nchunks) return;
-    FyChunk out;
-    out.w = -1;
-    out.a = 0;
-    out.ne = 0;
-    out.s = 0;
+    __shared__ int32_t evs[4][kEvMax];
+    int32_t* ev = evs[(threadIdx.x >> 5) & 3];
     const double tau = (double)(c * T);
     const double m2 = (double)(2 * lo_band);  // mask + 1
     const double gi = (double)(i0 + 1) * exp(-tau / m2) - 1.0;
@@ -323,47 +364,32 @@ __global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, co
     int64_t hi = tmin<int64_t>((int64_t)floor(gi) + half, i0);
     if (c == 0) s = hi = i0;
     const int64_t pos0 = st->pos + c * T;
+    FyChunk out;
+    out.w = -1;
+    out.a = 0;
+    out.ne = 0;
+    out.s = 0;
     if (s - T > lo_band && hi >= s && pos0 + T <= nbuf) {
-        const uint32_t m = (uint32_t)(2 * lo_band - 1);
         const int64_t w = hi - s;
-        int64_t i = s;
-        int a = 0, ne = 0;
-        const uint32_t* x = g + pos0;
-        for (int64_t t = 0; t < T; ++t) {
-            const int64_t v = (int64_t)(__ldg(x + t) & m);
-            if (v <= i) {
-                --i;
-                ++a;
-            } else if (v - i <= w) {
-                if (ne < kEvMax) out.ev[ne] = (int32_t)(v - i);
-                ++ne;
-            }
-        }
+        const WalkOut r = warp_walk(g, pos0, pos0 + T, s, s - T - 1, nullptr, w, ev, kEvMax);
+        __syncwarp();
         out.s = s;
         out.w = (int32_t)w;
-        out.a = a;
-        out.ne = ne <= kEvMax ? ne : -1;
+        out.a = (int32_t)(s - r.i);
+        out.ne = r.nev <= kEvMax ? r.nev : -1;
+        for (int e = 0; e < kEvMax; ++e) out.ev[e] = e < r.nev ? ev[e] : 0;
     }
-    ch[c] = out;
+    if (ln == 0) ch[c] = out;
 }
 
-// Exact re-run of chunk c from its resolved start, writing j (one thread each).
+// Exact re-run of chunk c from its resolved start, writing j (one warp each).
 __global__ void fy_chunk_exact_kernel(const uint32_t* __restrict__ g, const FyState* st0,
                                       const int64_t* __restrict__ starts, int64_t lo_band,
-                                      int64_t T, int32_t* __restrict__ jout, int64_t pos_base) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                                      int64_t T, int32_t* __restrict__ jout) {
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (c >= st0->done) return;
-    const uint32_t m = (uint32_t)(2 * lo_band - 1);
-    int64_t i = starts[c];
-    const uint32_t* x = g + starts[-1] + c * T;  // starts[-1] holds the band's first draw
-    for (int64_t t = 0; t < T; ++t) {
-        const uint32_t v = __ldg(x + t) & m;
-        if ((int64_t)v <= i) {
-            jout[i] = (int32_t)v;
-            --i;
-        }
-    }
-    (void)pos_base;
+    const int64_t p0 = starts[-1] + c * T;  // starts[-1] holds the band's first draw
+    warp_walk(g, p0, p0 + T, starts[c], lo_band, jout, 0, nullptr, 0);
 }
 
 // One warp resolves the chunks in order: the true start of chunk c gives its
@@ -654,12 +680,12 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
             const double draws_est = (double)(2 * lo_band) * log((double)(i0 + 1) / (double)lo_band);
             const int64_t nch = tmin<int64_t>((int64_t)(draws_est / (double)T) + 2, p.max_chunks);
             if (nch >= 2) {
-                const unsigned gb = (unsigned)ceil_div(nch, 128);
+                const unsigned gb = (unsigned)ceil_div(nch, 4);  // one warp per chunk
                 fy_chunk_kernel<<<gb, 128, 0, st>>>(draws, p.nbuf, fst, i0, lo_band, T, nch, chunks);
                 IDS_LAUNCH_CHECK();
                 fy_stitch_kernel<<<1, 32, 0, st>>>(fst, chunks, nch, T, starts + 1);
                 IDS_LAUNCH_CHECK();
-                fy_chunk_exact_kernel<<<gb, 128, 0, st>>>(draws, fst, starts + 1, lo_band, T, jarr, 0);
+                fy_chunk_exact_kernel<<<gb, 128, 0, st>>>(draws, fst, starts + 1, lo_band, T, jarr);
                 IDS_LAUNCH_CHECK();
             }
             fy_walk_kernel<<<1, 32, 0, st>>>(draws, p.nbuf, lo_band - 1, jarr, fst, d + 1, d + 3);

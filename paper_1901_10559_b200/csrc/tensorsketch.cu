@@ -36,7 +36,8 @@ struct TsArgs {
     const double* factors[kMaxModes];
     int64_t lds[kMaxModes];
     const int32_t* order[kMaxModes];
-    const int64_t* bstart[kMaxModes];
+    const int32_t* keys[kMaxModes];   // bucket of each sorted entry
+    int64_t dims[kMaxModes];
     int64_t ncols, L, M, N2;
     int linear;  // 1: zero-pad + fold (L not a power of two)
     const double* weights;
@@ -178,20 +179,26 @@ __global__ void __launch_bounds__(512) tensorsketch_kernel(TsArgs g) {
     for (int64_t r = blockIdx.x; r < g.ncols; r += gridDim.x) {
         for (int n = 0; n < g.n_modes; ++n) {
             // ---- per-mode CountSketch of column r, into the packed buffer ----
+            // zero the M slots, then one thread per bucket run of the sorted
+            // index sums its rows in increasing row order (scipy's order)
             const double* col = g.factors[n] + r * g.lds[n];
             const int32_t* ord = g.order[n];
-            const int64_t* bs = g.bstart[n];
-            for (int l = t; l < M; l += T) {
+            const int32_t* key = g.keys[n];
+            const int In = (int)g.dims[n];
+            for (int l = t; l < M; l += T) dbuf[2 * pad(l >> 1) + (l & 1)] = 0.0;
+            __syncthreads();
+            for (int k = t; k < In; k += T) {
+                const int32_t bkt = __ldg(key + k);
+                if (k > 0 && __ldg(key + k - 1) == bkt) continue;  // not a run head
                 double acc = 0.0;
-                if (l < L) {
-                    const int64_t k1 = bs[l + 1];
-                    for (int64_t k = bs[l]; k < k1; ++k) {
-                        const int32_t e = __ldg(ord + k);
-                        const double x = __ldg(col + dec_row(e));
-                        acc = e >= 0 ? acc + x : acc - x;
-                    }
-                }
-                dbuf[2 * pad(l >> 1) + (l & 1)] = acc;
+                int kk = k;
+                do {
+                    const int32_t e = __ldg(ord + kk);
+                    const double x = __ldg(col + dec_row(e));
+                    acc = e >= 0 ? acc + x : acc - x;
+                    ++kk;
+                } while (kk < In && __ldg(key + kk) == bkt);
+                dbuf[2 * pad(bkt >> 1) + (bkt & 1)] = acc;
             }
             __syncthreads();
             fft_forward<EPT>(buf, N2, M, g.tw);
@@ -315,7 +322,7 @@ extern "C" size_t ids_tensorsketch_workspace_bytes(int n_modes, const int64_t* d
 extern "C" int ids_tensorsketch_f64(int n_modes, const double* const* factors, const int64_t* dims,
                                     const int64_t* lds, int64_t ncols,
                                     const int32_t* const* order_signed,
-                                    const int64_t* const* bstart, int64_t out_dim,
+                                    const int32_t* const* sorted_bucket, int64_t out_dim,
                                     const double* weights, double* Y, double* colnorm2,
                                     void* workspace, size_t ws_bytes, void* stream) {
     if (n_modes < 1 || n_modes > kMaxModes || ncols < 0 || out_dim < 1) {
@@ -349,7 +356,8 @@ extern "C" int ids_tensorsketch_f64(int n_modes, const double* const* factors, c
         a.factors[n] = factors[n];
         a.lds[n] = lds[n];
         a.order[n] = order_signed[n];
-        a.bstart[n] = bstart[n];
+        a.keys[n] = sorted_bucket[n];
+        a.dims[n] = dims[n];
     }
     a.ncols = ncols;
     a.L = out_dim;

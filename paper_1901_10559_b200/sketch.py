@@ -152,17 +152,22 @@ class CountSketchOp:
     # ---- device ------------------------------------------------------------
     def bucket_index(self):
         """(order_signed int32[I], bstart int64[L+1]) -- the CSR structure of S."""
+        return self._bucket_index()[:2]
+
+    def _bucket_index(self):
+        """(order_signed, bstart, sorted_bucket) on the device."""
         if self._index is None:
             order = _device.empty(self.in_dim, torch.int32)
             bstart = _device.empty(self.out_dim + 1, torch.int64)
+            keys = _device.empty(self.in_dim, torch.int32)
             nbytes = query("ids_bucket_index_workspace_bytes", self.in_dim, self.out_dim)
             ws = _device.workspace(nbytes)
             call(
                 "ids_bucket_index", _device.ptr(self._bucket_d), _device.ptr(self._sign_d),
                 self.in_dim, self.out_dim, _device.ptr(order), _device.ptr(bstart),
-                _device.ptr(ws), nbytes, _device.stream_ptr(),
+                _device.ptr(keys), _device.ptr(ws), nbytes, _device.stream_ptr(),
             )
-            self._index = (order, bstart)
+            self._index = (order, bstart, keys)
         return self._index
 
     def sketch_into(self, operand, y, row0=0, accumulate=False, flags=0, nonfinite=None):

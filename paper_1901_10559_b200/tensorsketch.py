@@ -65,10 +65,10 @@ def tensorsketch_device(op, factors, weights=None):
     dev_f = [factor_to_device(f) for f in factors]
     n = len(dev_f)
     L = op.out_dim
-    idx = [m.bucket_index() for m in op.mode_ops]
+    idx = [m._bucket_index() for m in op.mode_ops]
     fac_p = (ctypes.c_void_p * n)(*[_device.ptr(t) for t in dev_f])
-    ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _ in idx])
-    bst_p = (ctypes.c_void_p * n)(*[_device.ptr(b) for _, b in idx])
+    ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _, _ in idx])
+    key_p = (ctypes.c_void_p * n)(*[_device.ptr(k) for _, _, k in idx])
     dims = (ctypes.c_int64 * n)(*[int(d) for d in op.mode_dims])
     lds = (ctypes.c_int64 * n)(*[int(t.shape[1]) for t in dev_f])
     y = _device.empty((ncols, L), torch.float64)
@@ -78,7 +78,7 @@ def tensorsketch_device(op, factors, weights=None):
     ws = _device.workspace(nbytes)
     call(
         "ids_tensorsketch_f64", n, ctypes.addressof(fac_p), ctypes.addressof(dims),
-        ctypes.addressof(lds), ncols, ctypes.addressof(ord_p), ctypes.addressof(bst_p), L,
+        ctypes.addressof(lds), ncols, ctypes.addressof(ord_p), ctypes.addressof(key_p), L,
         _device.ptr(w), _device.ptr(y), None, _device.ptr(ws), nbytes, _device.stream_ptr(),
     )
     # dev_f may be freed now: the caching allocator reuses memory in stream order
