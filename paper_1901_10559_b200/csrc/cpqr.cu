@@ -63,6 +63,7 @@ __device__ __forceinline__ double dlapy2(double x, double y) {
 struct CpqrArgs {
     const double* Y;
     int64_t m, n, ldy, k;
+    int small;  // m small: pivot column and z computed redundantly by every CTA
     double rank_tol;
     int32_t* perm;
     double* Rtop;
@@ -252,7 +253,22 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             if (ck >= c0 && ck < c1 && ck != cs) g.pos[ck] = ps;
             if (cs >= c0 && cs < c1) g.pos[cs] = kk;
         }
-        {
+        double alpha;
+        if (g.small) {
+            // short sketch: every CTA builds the whole pivot column itself
+            const double* ycol = g.Y + cs * ldy;
+            double ss = 0.0;
+            for (int64_t r = kk + threadIdx.x; r < m; r += kThreads) {
+                const double v = sub_dot(ycol[r], g.V + r, m, g.F + cs, n, kk);
+                vsm[r] = v;
+                if (r > kk) ss = fma(v, v, ss);
+            }
+            ss = block_sum(ss, red);
+            if (threadIdx.x == 0) s_red0 = ss;
+            __syncthreads();
+            alpha = vsm[kk];
+            __syncthreads();
+        } else {
             const double* ycol = g.Y + cs * ldy;
             double ss = 0.0;
             for (int64_t r = tmax(r0, kk) + threadIdx.x; r < r1; r += kThreads) {
@@ -262,17 +278,17 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             }
             ss = block_sum(ss, red);
             if (threadIdx.x == 0) g.normpart[b] = ss;
+            grid.sync();
+            if (wid == 0) {
+                const double xs = warp_sum_partials(g.normpart, G, 1);
+                if (lane == 0) s_red0 = xs;
+            }
+            __syncthreads();
+            alpha = g.a[kk];
         }
-        grid.sync();
 
-        // ---- S2: Householder vector (redundantly per CTA), z partials, GEMV ----
-        if (wid == 0) {
-            const double xs = warp_sum_partials(g.normpart, G, 1);
-            if (lane == 0) s_red0 = xs;
-        }
-        __syncthreads();
+        // ---- S2: Householder vector (redundantly per CTA), z, GEMV ----
         const double xnorm = sqrt(s_red0);
-        const double alpha = g.a[kk];
         double tau, beta, scal;
         if (xnorm == 0.0) {
             tau = 0.0;
@@ -284,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             scal = 1.0 / (alpha - beta);
         }
         for (int64_t r = kk + threadIdx.x; r < m; r += kThreads)
-            vsm[r] = (r == kk) ? 1.0 : g.a[r] * scal;
+            vsm[r] = (r == kk) ? 1.0 : (g.small ? vsm[r] : g.a[r]) * scal;
         __syncthreads();
         if (b == 0) {
             for (int64_t r = threadIdx.x; r < m; r += kThreads)
@@ -295,12 +311,18 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             }
         }
         if (threadIdx.x == 0 && cs >= c0 && cs < c1) g.Rcol[cs * k + kk] = beta;
-        // z partials: z_q = V[:, q]^T v over owned rows >= kk
+        // z_q = V[:, q]^T v: whole columns (small) or owned-row partials
         for (int64_t q = wid; q < kk; q += kWarps) {
-            double s = 0.0;
-            for (int64_t r = tmax(r0, kk) + lane; r < r1; r += 32) s = fma(g.V[q * m + r], vsm[r], s);
-            s = warp_sum(s);
-            if (lane == 0) g.zpart[b * k + q] = s;
+            if (g.small) {
+                const double s = warp_sum(lane_dot(g.V + q * m, vsm, kk, m));
+                if (lane == 0) zsh[q] = s;
+            } else {
+                double s = 0.0;
+                for (int64_t r = tmax(r0, kk) + lane; r < r1; r += 32)
+                    s = fma(g.V[q * m + r], vsm[r], s);
+                s = warp_sum(s);
+                if (lane == 0) g.zpart[b * k + q] = s;
+            }
         }
         // GEMV over owned remaining columns: W_j = Y[kk:, j]^T v
         for (int64_t j = c0 + wid; j < c1; j += kWarps) {
@@ -308,14 +330,15 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             const double s = warp_sum(lane_dot(g.Y + j * ldy, vsm, kk, m));
             if (lane == 0) g.W[j] = s;
         }
-        grid.sync();
+        if (g.small) __syncthreads();
+        else grid.sync();
 
         // ---- S3: F column, row kk of R, norm downdate, next argmax ----
         // z = V[:, :kk]^T v (fixed-order sum of the per-CTA partials) and row kk of V
         for (int64_t q = wid; q < kk; q += kWarps) {
-            const double zq = warp_sum_partials(g.zpart + q, G, k);
+            const double zq = g.small ? 0.0 : warp_sum_partials(g.zpart + q, G, k);
             if (lane == 0) {
-                zsh[q] = zq;
+                if (!g.small) zsh[q] = zq;
                 vrow[q] = g.V[q * m + kk];
             }
         }
@@ -552,6 +575,7 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
     a.ldy = ldy;
     a.k = k;
     a.rank_tol = rank_tol;
+    a.small = rows <= 1024 ? 1 : 0;
     a.perm = perm;
     a.Rtop = Rtop;
     a.numerical_rank = numerical_rank;
