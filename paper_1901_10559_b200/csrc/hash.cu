@@ -339,14 +339,16 @@ __global__ void fy_init_kernel(FyState* st, int64_t n) {
 // offset is >= g accepts there and its offset drops by one.  Recording those
 // gaps (in order) makes the chunk's end state a cheap function of the true
 // start, evaluated by the stitch below.
-constexpr int kEvMax = 24;
+constexpr int kEvMax = 26;
 struct FyChunk {
     int64_t s;    // lowest start in the window
     int32_t w;    // window width (-1: chunk not usable)
     int32_t a;    // accepts of the base trajectory
     int32_t ne;   // near-miss events recorded (-1: overflow)
     int32_t ev[kEvMax];
+    int32_t pad_;
 };
+static_assert(sizeof(FyChunk) % 16 == 0, "FyChunk is staged with 16-byte copies");
 
 __global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, const FyState* st,
                                 int64_t i0, int64_t lo_band, int64_t T, int64_t nchunks,
@@ -392,48 +394,57 @@ __global__ void fy_chunk_exact_kernel(const uint32_t* __restrict__ g, const FySt
     warp_walk(g, p0, p0 + T, starts[c], lo_band, jout, 0, nullptr, 0);
 }
 
-// One warp resolves the chunks in order: the true start of chunk c gives its
-// offset d in the window; replaying the near-miss gaps gives the end state.
-// A chunk whose start falls outside its window (or overflowed) stops the
-// stitch; the exact walk then continues from there.
-__global__ void fy_stitch_kernel(FyState* st, const FyChunk* __restrict__ ch, int64_t nchunks,
-                                 int64_t T, int64_t* __restrict__ starts) {
-    const int ln = threadIdx.x & 31;
-    int64_t S = st->i;
+// The chunks are resolved in order by ONE thread: the true start of chunk c
+// gives its offset d in the window; replaying the near-miss gaps gives the
+// end state.  The block stages the chunk summaries in shared memory so the
+// sequential loop only touches on-chip data.  A chunk whose start falls
+// outside its window (or overflowed) stops the stitch; the exact walk then
+// continues from there.
+constexpr int kStitchBatch = 128;
+__global__ void __launch_bounds__(256) fy_stitch_kernel(FyState* st, const FyChunk* __restrict__ ch,
+                                                        int64_t nchunks, int64_t T,
+                                                        int64_t* __restrict__ starts) {
+    __shared__ FyChunk sm[kStitchBatch];
+    __shared__ int64_t s_S;
+    __shared__ int s_ok;
     const int64_t pos0 = st->pos;
-    if (ln == 0) starts[-1] = pos0;
+    if (threadIdx.x == 0) {
+        s_S = st->i;
+        s_ok = 1;
+        starts[-1] = pos0;
+    }
     int64_t done = 0;
-    bool ok = true;
-    for (int64_t c0 = 0; c0 < nchunks && ok; c0 += 32) {
-        const int64_t c = c0 + ln;
-        FyChunk mine;
-        mine.w = -1;
-        if (c < nchunks) mine = ch[c];
-        const int cnt = (int)tmin<int64_t>(32, nchunks - c0);
-        for (int l = 0; l < cnt; ++l) {
-            const int64_t s = __shfl_sync(0xffffffffu, mine.s, l);
-            const int w = __shfl_sync(0xffffffffu, mine.w, l);
-            const int ne = __shfl_sync(0xffffffffu, mine.ne, l);
-            const int64_t d = S - s;
-            if (w < 0 || ne < 0 || d < 0 || d > w) {
-                ok = false;
-                break;
+    for (int64_t c0 = 0; c0 < nchunks; c0 += kStitchBatch) {
+        const int cnt = (int)tmin<int64_t>(kStitchBatch, nchunks - c0);
+        __syncthreads();
+        if (!s_ok) break;
+        const int words = (int)(cnt * sizeof(FyChunk) / sizeof(int4));
+        const int4* src = reinterpret_cast<const int4*>(ch + c0);
+        int4* dst = reinterpret_cast<int4*>(sm);
+        for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t S = s_S;
+            int l = 0;
+            for (; l < cnt; ++l) {
+                const FyChunk& cc = sm[l];
+                const int64_t d = S - cc.s;
+                if (cc.w < 0 || cc.ne < 0 || d < 0 || d > cc.w) {
+                    s_ok = 0;
+                    break;
+                }
+                int64_t dd = d;
+                for (int e = 0; e < cc.ne; ++e) dd -= (dd >= cc.ev[e]) ? 1 : 0;
+                starts[c0 + l] = S;
+                S = cc.s - cc.a + dd;
             }
-            int64_t dd = d;
-            if (ln == l) {
-                for (int e = 0; e < ne; ++e)
-                    if (dd >= mine.ev[e]) --dd;
-            }
-            dd = __shfl_sync(0xffffffffu, dd, l);
-            const int a = __shfl_sync(0xffffffffu, mine.a, l);
-            if (ln == 0) starts[c0 + l] = S;
-            S = s - a + dd;
-            ++done;
+            s_S = S;
+            done += l;
         }
     }
-    __syncwarp();
-    if (ln == 0) {
-        st->i = S;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st->i = s_S;
         st->pos = pos0 + done * T;
         st->done = done;
     }
@@ -519,7 +530,7 @@ struct HashPlan {
     size_t scan_bytes, scan2_bytes;
 };
 
-constexpr int kMinBand = 15;  // bands below 2^15 are walked exactly by one warp
+constexpr int kMinBand = 12;  // bands below 2^12 are walked exactly by one warp
 
 // Chunk length for band k: ~8 expected near-miss events per chunk.
 int64_t band_chunk(int k) {
@@ -683,7 +694,7 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
                 const unsigned gb = (unsigned)ceil_div(nch, 4);  // one warp per chunk
                 fy_chunk_kernel<<<gb, 128, 0, st>>>(draws, p.nbuf, fst, i0, lo_band, T, nch, chunks);
                 IDS_LAUNCH_CHECK();
-                fy_stitch_kernel<<<1, 32, 0, st>>>(fst, chunks, nch, T, starts + 1);
+                fy_stitch_kernel<<<1, 256, 0, st>>>(fst, chunks, nch, T, starts + 1);
                 IDS_LAUNCH_CHECK();
                 fy_chunk_exact_kernel<<<gb, 128, 0, st>>>(draws, fst, starts + 1, lo_band, T, jarr);
                 IDS_LAUNCH_CHECK();

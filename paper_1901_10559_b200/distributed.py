@@ -31,6 +31,9 @@ def row_block(n, world, rank):
 class DeviceBackend:
     """sm_100a kernels through the C ABI (the product path)."""
 
+    def __init__(self, prefetcher=None):
+        self.prefetcher = prefetcher
+
     def matrix_sketch(self, a_local, row0, in_dim, sketch_dim, seed, surjective):
         from . import _device
         from ._inputs import DenseOperand, SparseOperand, matrix_operand
@@ -41,7 +44,11 @@ class DeviceBackend:
             operand = a_local
         else:
             operand = matrix_operand(a_local)
-        op = CountSketchOp(in_dim, sketch_dim, seed=seed, surjective=surjective)
+        op = None
+        if self.prefetcher is not None:
+            op = self.prefetcher.take(in_dim, sketch_dim, seed, surjective)
+        if op is None:
+            op = CountSketchOp(in_dim, sketch_dim, seed=seed, surjective=surjective)
         y = _device.empty((operand.cols, sketch_dim), torch.float64)
         flag = _device.zeros(1, torch.int32)
         op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,

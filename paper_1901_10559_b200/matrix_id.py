@@ -161,16 +161,47 @@ def _raise_if_nonfinite(flag, operand):
 
 
 def countsketch_device(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL,
-                       surjective=True, flags=IDS_FLAG_ORDERED, check_finite=True):
-    """The device half of countsketch_id: returns (DeviceId, sketch (cols, L))."""
+                       surjective=True, flags=IDS_FLAG_ORDERED, check_finite=True,
+                       prefetcher=None):
+    """The device half of countsketch_id: returns (DeviceId, sketch (cols, L)).
+
+    prefetcher: optional sketch.HashPrefetcher holding this trial's operator
+    (drawn ahead on a side stream)."""
     operand = a if isinstance(a, (DenseOperand, SparseOperand)) else matrix_operand(a)
     sketch_dim = check_matrix_id_args(operand, rank, sketch_dim, "countsketch")
-    op = CountSketchOp(operand.rows, sketch_dim, seed=seed, surjective=surjective)
+    op = None
+    if prefetcher is not None and seed is not None:
+        op = prefetcher.take(operand.rows, sketch_dim, seed, surjective)
+    if op is None:
+        op = CountSketchOp(operand.rows, sketch_dim, seed=seed, surjective=surjective)
     nonfinite = _device.zeros(1, torch.int32) if check_finite else None
     y = op.apply_device(operand, flags=flags, nonfinite=nonfinite)
     if check_finite:
         _raise_if_nonfinite(nonfinite, operand)
     return device_matrix_id(y, sketch_dim, operand.cols, rank, rank_tol), y
+
+
+def countsketch_id_trials(a, rank, sketch_dim=None, seeds=(0,), rank_tol=DEFAULT_RANK_TOL,
+                          surjective=True):
+    """countsketch_id of one matrix for several seeds (the paper averages 10
+    trials).  A is uploaded once; the hash of trial t+1 is drawn on a side
+    stream while trial t sketches.  Returns a list of
+    InterpolativeDecomposition, identical to separate countsketch_id calls."""
+    from .sketch import HashPrefetcher
+
+    operand = a if isinstance(a, (DenseOperand, SparseOperand)) else matrix_operand(a)
+    L = check_matrix_id_args(operand, rank, sketch_dim, "countsketch")
+    seeds = list(seeds)
+    pf = HashPrefetcher()
+    outs = []
+    for t, s in enumerate(seeds):
+        if t == 0:
+            pf.request(operand.rows, L, s, surjective)
+        if t + 1 < len(seeds):
+            pf.request(operand.rows, L, seeds[t + 1], surjective)
+        d, _ = countsketch_device(operand, rank, L, s, rank_tol, surjective, prefetcher=pf)
+        outs.append(d)
+    return [d.to_host("countsketch") for d in outs]
 
 
 def countsketch_id(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL, surjective=True):
@@ -192,6 +223,7 @@ __all__ = [
     "check_matrix_id_args",
     "countsketch_device",
     "countsketch_id",
+    "countsketch_id_trials",
     "device_matrix_id",
     "matrix_id",
     "matrix_sketch",

@@ -113,6 +113,16 @@ class CountSketchOp:
         op._checked = True
         return op
 
+    def record_stream(self, stream):
+        """Mark the operator's device arrays as used on `stream` (they may have
+        been drawn on another stream, see HashPrefetcher)."""
+        for t in (self._bucket_d, self._sign_d, self._draws):
+            if t is not None:
+                t.record_stream(stream)
+        if self._index is not None:
+            for t in self._index:
+                t.record_stream(stream)
+
     # ---- host views -------------------------------------------------------
     def _check_draws(self):
         if self._checked or self._draws is None:
@@ -305,3 +315,40 @@ class TensorSketchOp:
         dense = np.zeros((self.out_dim, self.in_dim))
         dense[self.composite_bucket(), np.arange(self.in_dim)] = self.composite_sign()
         return dense
+
+
+class HashPrefetcher:
+    """Draws CountSketch hashes ahead of time on a side stream.
+
+    The hash draw (and bucket index) depends only on (in_dim, out_dim, seed,
+    surjective), not on the data, and its kernels are latency-bound and
+    light.  Requesting the NEXT trial's operator before sketching the
+    current one lets the draw overlap the HBM-bound sketch kernel
+    (repeated IDs of one matrix, e.g. the paper's 10 trials per config)."""
+
+    def __init__(self):
+        self.side = torch.cuda.Stream(device=_device.device())
+        self.cache = {}
+
+    def request(self, in_dim, out_dim, seed, surjective):
+        key = (int(in_dim), int(out_dim), seed, bool(surjective))
+        if key in self.cache:
+            return
+        self.side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.side):
+            op = CountSketchOp(in_dim, out_dim, seed=seed, surjective=surjective)
+            op._bucket_index()
+            ev = torch.cuda.Event()
+            ev.record(self.side)
+        self.cache[key] = (op, ev)
+
+    def take(self, in_dim, out_dim, seed, surjective):
+        """The prefetched operator (waited on by the current stream), or None."""
+        item = self.cache.pop((int(in_dim), int(out_dim), seed, bool(surjective)), None)
+        if item is None:
+            return None
+        op, ev = item
+        cur = torch.cuda.current_stream()
+        cur.wait_event(ev)
+        op.record_stream(cur)
+        return op

@@ -21,6 +21,7 @@ p.add_argument("--L", type=int, default=100)
 p.add_argument("--steps", type=int, default=2)
 p.add_argument("--fortran", action="store_true")
 p.add_argument("--tensor", default="")  # e.g. "3,1000,1000,4096,10" = N,I,R,L,K
+p.add_argument("--csr", default="")  # e.g. "10000000,10000,100000000,200,20" = I,R,nnz,L,K
 args = p.parse_args()
 
 torch.cuda.set_device(0)
@@ -32,6 +33,22 @@ if args.tensor:
     for s in range(args.steps + 1):
         y = op.apply_device([f.t() for f in fac], w)
         device_matrix_id(y, L, R, K).to_host("tensorsketch")
+    torch.cuda.synchronize()
+    sys.exit(0)
+if args.csr:
+    from paper_1901_10559_b200._inputs import SparseOperand
+    I, R, nnz, L, K = (int(v) for v in args.csr.split(","))
+    per = nnz // I
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    indptr = torch.arange(0, I + 1, dtype=torch.int64, device="cuda") * per
+    idx = torch.randint(0, R, (I * per,), generator=g, device="cuda", dtype=torch.int64)
+    idx = idx.view(I, per).sort(dim=1).values.to(torch.int32).reshape(-1)
+    data = torch.randn(I * per, generator=g, device="cuda", dtype=torch.float64)
+    op = SparseOperand("csr", indptr, idx, data, I, R, I * per)
+    for s in range(args.steps + 1):
+        d, _ = countsketch_device(op, K, L, seed=s)
+        d.to_host("countsketch")
     torch.cuda.synchronize()
     sys.exit(0)
 a = torch.randn(args.rows, args.cols, dtype=torch.float64, device="cuda")
