@@ -119,6 +119,60 @@ def countsketch_id_sharded(a_local, row0, in_dim, rank, sketch_dim=None, seed=No
     return backend.matrix_id(y, sketch_dim, cols, rank, rank_tol, "countsketch")
 
 
+def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, seeds=(0,),
+                                  rank_tol=1e-12, surjective=True, group=None):
+    """countsketch_id_sharded for several seeds, fully queued on the device:
+    trial t+1's hash is drawn on a side stream during trial t, the sketch
+    all-reduce and the ID are enqueued back to back, and the host only
+    synchronizes once at the end (non-finite input is checked then, for all
+    trials at once).  Every rank returns the same list."""
+    from ._inputs import DenseOperand, SparseOperand, matrix_operand
+    from ._native import IDS_FLAG_ORDERED
+    from .matrix_id import check_matrix_id_args, device_matrix_id
+    from .sketch import CountSketchOp, HashPrefetcher
+
+    world, _ = _world(group)
+    operand = a_local if isinstance(a_local, (DenseOperand, SparseOperand)) else \
+        matrix_operand(a_local)
+    cols = operand.cols
+
+    class _Shape:
+        shape = (in_dim, cols)
+
+    L = check_matrix_id_args(_Shape, rank, sketch_dim, "countsketch")
+    seeds = list(seeds)
+    pf = HashPrefetcher()
+    outs, flags = [], []
+    if seeds:
+        pf.request(in_dim, L, seeds[0], surjective)
+    for t, s in enumerate(seeds):
+        if t + 1 < len(seeds):
+            pf.request(in_dim, L, seeds[t + 1], surjective)
+        op = pf.take(in_dim, L, s, surjective)
+        if op is None:  # pragma: no cover
+            op = CountSketchOp(in_dim, L, seed=s, surjective=surjective)
+        y = torch.empty((cols, L), dtype=torch.float64, device=torch.cuda.current_device())
+        flag = torch.zeros(1, dtype=torch.int32, device=y.device)
+        op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,
+                       nonfinite=flag)
+        if world > 1:
+            dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+        outs.append(device_matrix_id(y, L, cols, rank, rank_tol).fetch_async())
+        flags.append(flag)
+    if flags:
+        bad = torch.stack(flags).max()
+        if world > 1:
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=group)
+        if bool(bad.item()):
+            conf = DeviceBackend().confirm_nonfinite(operand)
+            if world > 1:
+                dist.all_reduce(conf, op=dist.ReduceOp.MAX, group=group)
+            if bool(conf.item()):
+                raise ValueError("a contains non-finite entries")
+    torch.cuda.current_stream().synchronize()
+    return [d.host_result("countsketch") for d in outs]
+
+
 def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketch_dim=None,
                             seed=None, rank_tol=1e-12, group=None, backend=None):
     """tensorsketch_id with the R terms split into column blocks: this rank

@@ -78,6 +78,22 @@ class DeviceId:
             numerical_rank=int(nr[0]), rank_deficient=bool(de[0]),
         )
 
+    def fetch_async(self):
+        """Queue the device->host copies into pinned buffers (no sync)."""
+        self._host = [
+            torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t, non_blocking=True)
+            for t in (self.cols, self.coeffs, self.numerical_rank, self.deficient)
+        ]
+        return self
+
+    def host_result(self, method):
+        """InterpolativeDecomposition from fetch_async() buffers (after a sync)."""
+        cols, coeffs, nr, de = (t.numpy() for t in self._host)
+        return InterpolativeDecomposition(
+            coeffs=coeffs, cols=cols.copy(), rank=self.rank, method=method,
+            numerical_rank=int(nr[0]), rank_deficient=bool(de[0]),
+        )
+
 
 def device_matrix_id(y_cm, rows, cols, rank, rank_tol=DEFAULT_RANK_TOL, ld=None):
     """ID of the col-major rows x cols sketch in y_cm, on the device
@@ -185,23 +201,14 @@ def countsketch_id_trials(a, rank, sketch_dim=None, seeds=(0,), rank_tol=DEFAULT
                           surjective=True):
     """countsketch_id of one matrix for several seeds (the paper averages 10
     trials).  A is uploaded once; the hash of trial t+1 is drawn on a side
-    stream while trial t sketches.  Returns a list of
-    InterpolativeDecomposition, identical to separate countsketch_id calls."""
-    from .sketch import HashPrefetcher
+    stream while trial t sketches, and nothing waits on the host until every
+    trial is queued.  Returns a list of InterpolativeDecomposition, identical
+    to separate countsketch_id calls."""
+    from .distributed import countsketch_id_sharded_trials
 
     operand = a if isinstance(a, (DenseOperand, SparseOperand)) else matrix_operand(a)
-    L = check_matrix_id_args(operand, rank, sketch_dim, "countsketch")
-    seeds = list(seeds)
-    pf = HashPrefetcher()
-    outs = []
-    for t, s in enumerate(seeds):
-        if t == 0:
-            pf.request(operand.rows, L, s, surjective)
-        if t + 1 < len(seeds):
-            pf.request(operand.rows, L, seeds[t + 1], surjective)
-        d, _ = countsketch_device(operand, rank, L, s, rank_tol, surjective, prefetcher=pf)
-        outs.append(d)
-    return [d.to_host("countsketch") for d in outs]
+    return countsketch_id_sharded_trials(operand, 0, operand.rows, rank, sketch_dim, seeds,
+                                         rank_tol, surjective)
 
 
 def countsketch_id(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL, surjective=True):

@@ -405,3 +405,21 @@ def test_triangular_solve():
     with pytest.raises(ids.SingularTriangleError):
         ids.triangular_solve(r, b)
     assert ids.triangular_solve(np.eye(2), np.zeros((2, 0))).shape == (2, 0)
+
+
+def test_trials_api_matches_single_calls_and_checks_nan():
+    from paper_1901_10559_b200.matrix_id import countsketch_id_trials
+
+    rng = np.random.default_rng(21)
+    a = rng.standard_normal((5000, 12)) @ rng.standard_normal((12, 300))
+    a += 1e-6 * rng.standard_normal(a.shape)
+    seeds = [3, 4, 5, 3]
+    many = countsketch_id_trials(a, 12, 40, seeds=seeds)
+    for s, d in zip(seeds, many):
+        one = ids.countsketch_id(a, 12, 40, seed=s)
+        assert np.array_equal(d.cols, one.cols)
+        assert np.array_equal(d.coeffs, one.coeffs)
+    bad = a.copy()
+    bad[17, 5] = np.inf
+    with pytest.raises(ValueError):
+        countsketch_id_trials(bad, 12, 40, seeds=[1, 2])

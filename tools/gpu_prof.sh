@@ -13,3 +13,10 @@ if [ -n "$FULL_KERNEL" ]; then
       -o gpurun_out/prof_full python tools/prof_step.py --steps 1 $FULL_ARGS > gpurun_out/ncu_full.log 2>&1
 fi
 echo "prof done"
+if [ -n "$EXTRA" ]; then
+python tools/prof_step.py --steps 1 --tensor 4,10000,2000,16384,20 > gpurun_out/prof_c5_plain.log 2>&1 && \
+  ncu $M --log-file gpurun_out/launches_c5.csv python tools/prof_step.py --steps 1 --tensor 4,10000,2000,16384,20 > gpurun_out/ncu_c5.log 2>&1
+python tools/prof_step.py --steps 1 --csr 10000000,10000,100000000,200,20 > gpurun_out/prof_c3_plain.log 2>&1 && \
+  ncu $M --log-file gpurun_out/launches_c3.csv python tools/prof_step.py --steps 1 --csr 10000000,10000,100000000,200,20 > gpurun_out/ncu_c3.log 2>&1
+echo extra done
+fi
