@@ -248,7 +248,12 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             }
         }
         __syncthreads();
-        const int64_t cs = s_piv[0], ps = s_piv[1], ck = s_piv[2];
+        int64_t cs = s_piv[0], ps = s_piv[1];
+        const int64_t ck = s_piv[2];
+        if (cs < 0) {  // every remaining norm is NaN (non-finite input): keep position kk
+            cs = ck;
+            ps = kk;
+        }
         if (threadIdx.x == 0) {
             if (ck >= c0 && ck < c1 && ck != cs) g.pos[ck] = ps;
             if (cs >= c0 && cs < c1) g.pos[cs] = kk;

@@ -157,7 +157,7 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
                        nonfinite=flag)
         if world > 1:
             dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
-        outs.append(device_matrix_id(y, L, cols, rank, rank_tol).fetch_async())
+        outs.append(device_matrix_id(y, L, cols, rank, rank_tol).packed())
         flags.append(flag)
     if flags:
         bad = torch.stack(flags).max()
@@ -169,8 +169,10 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
                 dist.all_reduce(conf, op=dist.ReduceOp.MAX, group=group)
             if bool(conf.item()):
                 raise ValueError("a contains non-finite entries")
-    torch.cuda.current_stream().synchronize()
-    return [d.host_result("countsketch") for d in outs]
+    from .matrix_id import DeviceId
+
+    host = torch.stack(outs).cpu().numpy() if outs else []  # one copy for all trials
+    return [DeviceId.unpack(v, rank, cols, "countsketch") for v in host]
 
 
 def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketch_dim=None,

@@ -78,21 +78,20 @@ class DeviceId:
             numerical_rank=int(nr[0]), rank_deficient=bool(de[0]),
         )
 
-    def fetch_async(self):
-        """Queue the device->host copies into pinned buffers (no sync)."""
-        self._host = [
-            torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t, non_blocking=True)
-            for t in (self.cols, self.coeffs, self.numerical_rank, self.deficient)
-        ]
-        return self
+    def packed(self):
+        """cols, numerical_rank, deficient and coeffs packed in one float64
+        device vector (indices are exact in float64), for one batched copy."""
+        head = torch.cat([self.cols.to(torch.float64), self.numerical_rank.to(torch.float64),
+                          self.deficient.to(torch.float64)])
+        return torch.cat([head, self.coeffs.reshape(-1)])
 
-    def host_result(self, method):
-        """InterpolativeDecomposition from fetch_async() buffers (after a sync)."""
-        cols, coeffs, nr, de = (t.numpy() for t in self._host)
-        return InterpolativeDecomposition(
-            coeffs=coeffs, cols=cols.copy(), rank=self.rank, method=method,
-            numerical_rank=int(nr[0]), rank_deficient=bool(de[0]),
-        )
+    @staticmethod
+    def unpack(vec, rank, ncols, method):
+        cols = vec[:rank].astype(np.int32)
+        nr, de = int(vec[rank]), bool(vec[rank + 1])
+        coeffs = vec[rank + 2:].reshape(rank, ncols).copy()
+        return InterpolativeDecomposition(coeffs=coeffs, cols=cols, rank=rank, method=method,
+                                          numerical_rank=nr, rank_deficient=de)
 
 
 def device_matrix_id(y_cm, rows, cols, rank, rank_tol=DEFAULT_RANK_TOL, ld=None):
