@@ -401,7 +401,7 @@ __global__ void fy_chunk_exact_kernel(const uint32_t* __restrict__ g, const FySt
 // outside its window (or overflowed) stops the stitch; the exact walk then
 // continues from there.
 constexpr int kStitchBatch = 128;
-__global__ void __launch_bounds__(256) fy_stitch_kernel(FyState* st, const FyChunk* __restrict__ ch,
+__global__ void __launch_bounds__(32) fy_stitch_kernel(FyState* st, const FyChunk* __restrict__ ch,
                                                         int64_t nchunks, int64_t T,
                                                         int64_t* __restrict__ starts) {
     __shared__ FyChunk sm[kStitchBatch];
@@ -694,7 +694,7 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
                 const unsigned gb = (unsigned)ceil_div(nch, 4);  // one warp per chunk
                 fy_chunk_kernel<<<gb, 128, 0, st>>>(draws, p.nbuf, fst, i0, lo_band, T, nch, chunks);
                 IDS_LAUNCH_CHECK();
-                fy_stitch_kernel<<<1, 256, 0, st>>>(fst, chunks, nch, T, starts + 1);
+                fy_stitch_kernel<<<1, 32, 0, st>>>(fst, chunks, nch, T, starts + 1);
                 IDS_LAUNCH_CHECK();
                 fy_chunk_exact_kernel<<<gb, 128, 0, st>>>(draws, fst, starts + 1, lo_band, T, jarr);
                 IDS_LAUNCH_CHECK();

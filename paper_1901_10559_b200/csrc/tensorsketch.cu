@@ -102,10 +102,20 @@ __device__ __forceinline__ void dft<8>(double2* x) {
     x[7] = csub(b6, b7);
 }
 
+// exp(-2 pi i m / M) from two small shared-memory tables:
+// coarse[m >> 7] * fine[m & 127]  (M a power of two).
+struct Twiddle {
+    const double2* coarse;
+    const double2* fine;
+    __device__ __forceinline__ double2 operator()(int m) const {
+        return cmul(coarse[m >> 7], fine[m & 127]);
+    }
+};
+
 // One in-place Stockham pass of radix R over the N2-point buffer; every
 // thread holds EPT >= N2 / blockDim.x points in registers across the barrier.
 template <int R, int EPT>
-__device__ void stockham_pass(double2* buf, int N2, int Ns, int M, const double2* __restrict__ tw) {
+__device__ void stockham_pass(double2* buf, int N2, int Ns, int M, const Twiddle tw) {
     const int B = N2 / R;
     const int T = blockDim.x;
     constexpr int kSlots = EPT / R;  // butterflies per thread
@@ -118,7 +128,7 @@ __device__ void stockham_pass(double2* buf, int N2, int Ns, int M, const double2
             for (int r = 0; r < R; ++r) v[s][r] = buf[pad(j + r * B)];
             const int k = j % Ns;
             if (Ns > 1 && k != 0) {
-                const double2 w1 = __ldg(tw + (int64_t)k * (M / (Ns * R)));
+                const double2 w1 = tw(k * (M / (Ns * R)));
                 double2 w = w1;
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
@@ -143,12 +153,15 @@ __device__ void stockham_pass(double2* buf, int N2, int Ns, int M, const double2
     __syncthreads();
 }
 
+// Radix-8 passes while each thread holds 8 points; with 16 points per thread
+// (the longest transforms) radix-4 passes keep the live set in registers.
 template <int EPT>
-__device__ void fft_forward(double2* buf, int N2, int M, const double2* tw) {
+__device__ __forceinline__ void fft_forward(double2* buf, int N2, int M, const Twiddle tw) {
     int Ns = 1;
-    while (Ns * 8 <= N2) {
-        stockham_pass<8, EPT>(buf, N2, Ns, M, tw);
-        Ns *= 8;
+    constexpr int RMAX = EPT >= 16 ? 4 : 8;
+    while (Ns * RMAX <= N2) {
+        stockham_pass<RMAX, EPT>(buf, N2, Ns, M, tw);
+        Ns *= RMAX;
     }
     const int rem = N2 / Ns;
     if (rem == 4) stockham_pass<4, EPT>(buf, N2, Ns, M, tw);
@@ -165,53 +178,100 @@ __global__ void twiddle_kernel(double2* tw, int64_t M) {
 }
 
 template <int EPT>
-__global__ void __launch_bounds__(512) tensorsketch_kernel(TsArgs g) {
+__global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     extern __shared__ double2 buf[];
+    __shared__ double2 tw_coarse[kMaxHalf * 2 / 128 + 1];
+    __shared__ double2 tw_fine[128];
+    __shared__ const double* s_fac[kMaxModes];
+    __shared__ const int32_t* s_ord[kMaxModes];
+    __shared__ const int32_t* s_key[kMaxModes];
+    __shared__ int64_t s_ld[kMaxModes];
+    __shared__ int s_dim[kMaxModes];
     double* dbuf = reinterpret_cast<double*>(buf);
     const int T = blockDim.x, t = threadIdx.x;
     const int N2 = (int)g.N2, M = (int)g.M;
     const int L = (int)g.L;
+    if (t == 0) {
+#pragma unroll
+        for (int q = 0; q < kMaxModes; ++q) {  // static indexing: no local copy of g
+            s_fac[q] = g.factors[q];
+            s_ord[q] = g.order[q];
+            s_key[q] = g.keys[q];
+            s_ld[q] = g.lds[q];
+            s_dim[q] = (int)g.dims[q];
+        }
+    }
+    for (int m = t; m < 128; m += T) {
+        double sn, cs;
+        sincospi(2.0 * (double)m / (double)M, &sn, &cs);
+        tw_fine[m] = make_double2(cs, -sn);
+    }
+    for (int q = t; q * 128 < M; q += T) {
+        double sn, cs;
+        sincospi(2.0 * (double)q * 128.0 / (double)M, &sn, &cs);
+        tw_coarse[q] = make_double2(cs, -sn);
+    }
+    __syncthreads();
+    const Twiddle tw{tw_coarse, tw_fine};
     const int npairs = N2 / 2 + 1;  // pairs (p, N2 - p), p = 0..N2/2
     // running spectrum S[0..N2]: after the padded FFT buffer in smem, or in
     // this CTA's global (L2-resident) slice
     double2* spec = g.spec_in_smem ? buf + (N2 + N2 / 8 + 1)
                                    : g.spec_glob + (int64_t)blockIdx.x * (N2 + 1);
     for (int64_t r = blockIdx.x; r < g.ncols; r += gridDim.x) {
-        for (int n = 0; n < g.n_modes; ++n) {
-            // ---- per-mode CountSketch of column r, into the packed buffer ----
-            // zero the M slots, then one thread per bucket run of the sorted
-            // index sums its rows in increasing row order (scipy's order)
-            const double* col = g.factors[n] + r * g.lds[n];
-            const int32_t* ord = g.order[n];
-            const int32_t* key = g.keys[n];
-            const int In = (int)g.dims[n];
-            for (int l = t; l < M; l += T) dbuf[2 * pad(l >> 1) + (l & 1)] = 0.0;
-            __syncthreads();
-            for (int k = t; k < In; k += T) {
-                const int32_t bkt = __ldg(key + k);
-                if (k > 0 && __ldg(key + k - 1) == bkt) continue;  // not a run head
-                double acc = 0.0;
-                int kk = k;
-                do {
-                    const int32_t e = __ldg(ord + kk);
-                    const double x = __ldg(col + dec_row(e));
-                    acc = e >= 0 ? acc + x : acc - x;
-                    ++kk;
-                } while (kk < In && __ldg(key + kk) == bkt);
-                dbuf[2 * pad(bkt >> 1) + (bkt & 1)] = acc;
+        // passes 0..N-1: forward transform of mode n's CountSketch, product into S;
+        // pass N: inverse transform of S (one inlined FFT for all passes)
+        for (int n = 0; n <= g.n_modes; ++n) {
+            if (n < g.n_modes) {
+                // ---- per-mode CountSketch of column r, into the packed buffer ----
+                // zero the M slots, then one thread per bucket run of the sorted
+                // index sums its rows in increasing row order (scipy's order)
+                const double* col = s_fac[n] + r * s_ld[n];
+                const int32_t* ord = s_ord[n];
+                const int32_t* key = s_key[n];
+                const int In = s_dim[n];
+                for (int l = t; l < M; l += T) dbuf[2 * pad(l >> 1) + (l & 1)] = 0.0;
+                __syncthreads();
+                for (int k = t; k < In; k += T) {
+                    const int32_t bkt = __ldg(key + k);
+                    if (k > 0 && __ldg(key + k - 1) == bkt) continue;  // not a run head
+                    double acc = 0.0;
+                    int kk = k;
+                    do {
+                        const int32_t e = __ldg(ord + kk);
+                        const double x = __ldg(col + dec_row(e));
+                        acc = e >= 0 ? acc + x : acc - x;
+                        ++kk;
+                    } while (kk < In && __ldg(key + kk) == bkt);
+                    dbuf[2 * pad(bkt >> 1) + (bkt & 1)] = acc;
+                }
+            } else {
+                // ---- inverse: pack conj(Z) from S, forward FFT, conj ----
+                for (int p = t; p < npairs; p += T) {
+                    const double2 xk = spec[p], xm = spec[N2 - p];  // S[p], S[N2 - p]
+                    const double2 w = tw(p);
+                    const double2 e = make_double2(0.5 * (xk.x + xm.x), 0.5 * (xk.y - xm.y));
+                    const double2 d = make_double2(0.5 * (xk.x - xm.x), 0.5 * (xk.y + xm.y));
+                    const double2 o = cmul(d, conj2(w));
+                    // Z[p] = E + iO ; Z[N2-p] = conj(E) + i conj(O); stored conjugated
+                    const double2 zlo = make_double2(e.x - o.y, e.y + o.x);
+                    const double2 zhi = make_double2(e.x + o.y, -e.y + o.x);
+                    if (p < N2) buf[pad(p)] = conj2(zlo);
+                    const int pm = N2 - p;
+                    if (pm != p && pm < N2 && pm > 0) buf[pad(pm)] = conj2(zhi);
+                }
             }
             __syncthreads();
-            fft_forward<EPT>(buf, N2, M, g.tw);
-            // ---- untangle the real spectrum, multiply into S ----
-            for (int p = t; p < npairs; p += T) {
-                {
+            fft_forward<EPT>(buf, N2, M, tw);
+            if (n < g.n_modes) {
+                // ---- untangle the real spectrum, multiply into S ----
+                for (int p = t; p < npairs; p += T) {
                     const double2 zk = buf[pad(p % N2)];
                     const double2 zm = buf[pad((N2 - p) % N2)];
                     const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
                     const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // zk - conj(zm)
                     const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);   // d * (-i/2)
-                    const double2 w = __ldg(g.tw + p);
-                    const double2 wo = cmul(w, o);
+                    const double2 wo = cmul(tw(p), o);
                     const double2 xlo = cadd(e, wo);
                     const double2 xhi = conj2(csub(e, wo));
                     if (n == 0) {
@@ -222,27 +282,9 @@ __global__ void __launch_bounds__(512) tensorsketch_kernel(TsArgs g) {
                         if (N2 - p != p) spec[N2 - p] = cmul(spec[N2 - p], xhi);
                     }
                 }
-            }
-            __syncthreads();
-        }
-        // ---- inverse: pack conj(Z), forward FFT, conj -> half-length IFFT ----
-        for (int p = t; p < npairs; p += T) {
-            {
-                const double2 xk = spec[p], xm = spec[N2 - p];  // S[p], S[N2 - p]
-                const double2 w = __ldg(g.tw + p);
-                const double2 e = make_double2(0.5 * (xk.x + xm.x), 0.5 * (xk.y - xm.y));
-                const double2 d = make_double2(0.5 * (xk.x - xm.x), 0.5 * (xk.y + xm.y));
-                const double2 o = cmul(d, conj2(w));
-                // Z[p] = E + iO ; Z[N2-p] = conj(E) + i conj(O); stored conjugated
-                const double2 zlo = make_double2(e.x - o.y, e.y + o.x);
-                const double2 zhi = make_double2(e.x + o.y, -e.y + o.x);
-                if (p < N2) buf[pad(p)] = conj2(zlo);
-                const int pm = N2 - p;
-                if (pm != p && pm < N2 && pm > 0) buf[pad(pm)] = conj2(zhi);
+                __syncthreads();
             }
         }
-        __syncthreads();
-        fft_forward<EPT>(buf, N2, M, g.tw);
         // y[2m] = Re z[m], y[2m+1] = Im z[m], z = conj(FFT(conj Z)) / N2
         const double scale = 1.0 / (double)N2;
         const double wr = g.weights ? g.weights[r] : 1.0;
@@ -257,12 +299,12 @@ __global__ void __launch_bounds__(512) tensorsketch_kernel(TsArgs g) {
             }
         } else {
             for (int j = t; j < L; j += T) {
-                double s = 0.0;
+                double sacc = 0.0;
                 for (int u = j; u < M; u += L) {
                     const double2 z = buf[pad(u >> 1)];
-                    s += ((u & 1) ? -z.y : z.x) * scale;
+                    sacc += ((u & 1) ? -z.y : z.x) * scale;
                 }
-                const double v = s * wr;
+                const double v = sacc * wr;
                 y[j] = v;
                 nrm = fma(v, v, nrm);
             }
