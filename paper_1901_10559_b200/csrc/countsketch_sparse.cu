@@ -201,9 +201,7 @@ extern "C" int ids_countsketch_csc_f64(const void* colptr, int colptr64, const i
     return IDS_OK;
 }
 
-extern "C" size_t ids_countsketch_csr_workspace_bytes(int64_t rows, int64_t cols, int64_t nnz,
-                                                      int64_t out_dim) {
-    (void)rows;
+static size_t csr_transpose_ws(int64_t cols, int64_t nnz, int64_t out_dim) {
     WsCount c;
     c.take<int32_t>(nnz);  // row_of
     c.take<int32_t>(nnz);  // iota
@@ -217,23 +215,17 @@ extern "C" size_t ids_countsketch_csr_workspace_bytes(int64_t rows, int64_t cols
     return c.off + 256;
 }
 
-extern "C" int ids_countsketch_csr_f64(const void* indptr, int indptr64, const int32_t* indices,
-                                       const double* data, int64_t rows, int64_t cols,
-                                       int64_t nnz, int64_t row0, int64_t in_dim,
-                                       const int32_t* bucket, const int8_t* sign,
-                                       const int32_t* order_signed, const int64_t* bstart,
-                                       int64_t out_dim, double* Y, int accumulate, int flags,
-                                       int32_t* nonfinite, void* workspace, size_t ws_bytes,
-                                       void* stream) {
-    (void)order_signed;
-    (void)bstart;
-    (void)flags;
+static int csr_transpose_path(const void* indptr, int indptr64, const int32_t* indices,
+                              const double* data, int64_t rows, int64_t cols, int64_t nnz,
+                              int64_t row0, int64_t in_dim, const int32_t* bucket,
+                              const int8_t* sign, int64_t out_dim, double* Y, int accumulate,
+                              int32_t* nonfinite, void* workspace, size_t ws_bytes,
+                              cudaStream_t st) {
     if (rows < 1 || cols < 1 || nnz < 0 || nnz > 0x7fffffffLL || out_dim < 1 || row0 < 0 ||
         row0 + rows > in_dim) {
         ids_set_last_error("csr countsketch: bad arguments");
         return IDS_EINVAL;
     }
-    cudaStream_t st = as_stream(stream);
     WsCarve ws(workspace, ws_bytes);
     int32_t* row_of = ws.take<int32_t>(nnz);
     int32_t* iota = ws.take<int32_t>(nnz);
@@ -279,6 +271,243 @@ extern "C" int ids_countsketch_csr_f64(const void* indptr, int indptr64, const i
         // with ids_values_has_nonfinite before raising
         const unsigned g = (unsigned)tmin<int64_t>(ceil_div(out_dim * cols, 256), 148 * 4);
         nonfinite_values_kernel<<<g, 256, 0, st>>>(Y, out_dim * cols, nonfinite);
+        IDS_LAUNCH_CHECK();
+    }
+    return IDS_OK;
+}
+
+// ---- direct CSR kernel ------------------------------------------------------
+// One CTA per (bucket l, segment of the bucket's rows).  The CTA walks its
+// rows in increasing order (the bucket index) in batches, gathers their
+// nonzeros (coalesced within a row), and accumulates into an R-wide fp64
+// accumulator in shared memory.  Determinism without atomics: the column
+// range is split into 8 tiles, each owned by one warp; a stable block-wide
+// counting sort routes every staged nonzero to its tile's list in row order,
+// and the owner warp adds them with same-column lanes serialized by
+// __match_any_sync rank.  Each Y entry therefore sums its rows in increasing
+// row order (scipy's order: bit-identical with one segment per bucket).
+constexpr int kCsrThreads = 256;
+constexpr int kCsrOwners = 8;
+constexpr int kCsrRows = 256;
+constexpr int kCsrCap = 2048;  // staged nonzeros per sub-batch (8 per thread)
+constexpr int64_t kCsrMaxCols = 16384;
+
+__device__ __forceinline__ int64_t lower_bound_rows_csr(const int32_t* __restrict__ order,
+                                                        int64_t lo, int64_t hi, int64_t row) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)dec_row(order[mid]) < row) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <class IP>
+__global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
+    const IP* __restrict__ indptr, const int32_t* __restrict__ indices,
+    const double* __restrict__ data, int64_t cols, int64_t row0, int64_t rows,
+    int restrict_rows, const int32_t* __restrict__ order, const int64_t* __restrict__ bstart,
+    int64_t L, int nseg, double* __restrict__ out, int64_t seg_stride, int init_from_out) {
+    extern __shared__ double acc[];  // cols
+    __shared__ int64_t s_p0[kCsrRows];
+    __shared__ int s_off[kCsrRows + 1];
+    __shared__ int8_t s_sg[kCsrRows];
+    __shared__ int s_col[kCsrCap];
+    __shared__ double s_val[kCsrCap];
+    __shared__ int s_base[kCsrOwners * 8 * kCsrOwners];  // [owner][q][warp]
+    __shared__ int s_ostart[kCsrOwners + 1];
+    typedef cub::BlockScan<int, kCsrThreads> BS;
+    __shared__ typename BS::TempStorage scan_tmp;
+
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int64_t l = blockIdx.x / nseg;
+    const int seg = (int)(blockIdx.x % nseg);
+    int64_t k0 = bstart[l], k1 = bstart[l + 1];
+    if (restrict_rows) {
+        const int64_t a = lower_bound_rows_csr(order, k0, k1, row0);
+        k1 = lower_bound_rows_csr(order, a, k1, row0 + rows);
+        k0 = a;
+    }
+    const int64_t len = k1 - k0;
+    const int64_t s0 = k0 + len * seg / nseg, s1 = k0 + len * (seg + 1) / nseg;
+    const int tw = (int)((cols + kCsrOwners - 1) / kCsrOwners);
+    double* o = out + (int64_t)seg * seg_stride;
+    for (int64_t c = t; c < cols; c += kCsrThreads) acc[c] = init_from_out ? o[c * L + l] : 0.0;
+
+    for (int64_t kb = s0; kb < s1; kb += kCsrRows) {
+        const int nr = (int)tmin<int64_t>(kCsrRows, s1 - kb);
+        int cnt = 0;
+        if (t < nr) {
+            const int32_t e = __ldg(order + kb + t);
+            const int64_t row = (int64_t)dec_row(e) - row0;
+            const int64_t p0 = (int64_t)indptr[row], p1 = (int64_t)indptr[row + 1];
+            s_p0[t] = p0;
+            s_sg[t] = e >= 0 ? 1 : -1;
+            cnt = (int)(p1 - p0);
+        }
+        int off, E;
+        BS(scan_tmp).ExclusiveSum(cnt, off, E);
+        if (t < nr) s_off[t] = off;
+        if (t == 0) s_off[nr] = E;
+        __syncthreads();
+        for (int f0 = 0; f0 < E; f0 += kCsrCap) {
+            const int nE = min(kCsrCap, E - f0);
+            int myo[8], myc[8], rk[8];
+            double myv[8];
+            for (int i = t; i < kCsrOwners * 8 * kCsrOwners; i += kCsrThreads) s_base[i] = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int f = f0 + q * kCsrThreads + t;
+                myo[q] = -1;
+                myc[q] = 0;
+                myv[q] = 0.0;
+                if (f < f0 + nE) {
+                    int lo = 0, hi = nr;  // row tr with s_off[tr] <= f < s_off[tr + 1]
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (s_off[mid] <= f) lo = mid;
+                        else hi = mid;
+                    }
+                    const int64_t p = s_p0[lo] + (f - s_off[lo]);
+                    myc[q] = __ldg(indices + p);
+                    const double v = __ldcs(data + p);
+                    myv[q] = s_sg[lo] < 0 ? -v : v;
+                    myo[q] = myc[q] / tw;
+                }
+            }
+            __syncthreads();  // s_base zeroed
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t peers = __match_any_sync(0xffffffffu, myo[q]);
+                rk[q] = __popc(peers & lt);
+                if (myo[q] >= 0 && rk[q] == 0)
+                    s_base[(myo[q] * 8 + q) * kCsrOwners + w] = __popc(peers);
+            }
+            __syncthreads();
+            {  // exclusive scan over (owner, q, warp): 512 counters, 2 per thread
+                const int a0 = s_base[2 * t], a1 = s_base[2 * t + 1];
+                int ex, tot;
+                BS(scan_tmp).ExclusiveSum(a0 + a1, ex, tot);
+                __syncthreads();
+                s_base[2 * t] = ex;
+                s_base[2 * t + 1] = ex + a0;
+            }
+            __syncthreads();
+            if (t <= kCsrOwners) s_ostart[t] = t < kCsrOwners ? s_base[t * 8 * kCsrOwners] : nE;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (myo[q] >= 0) {
+                    const int pos = s_base[(myo[q] * 8 + q) * kCsrOwners + w] + rk[q];
+                    s_col[pos] = myc[q];
+                    s_val[pos] = myv[q];
+                }
+            }
+            __syncthreads();
+            {  // owner warp w adds its tile's entries in row order
+                const int a = s_ostart[w], b = s_ostart[w + 1];
+                for (int ib = a; ib < b; ib += 32) {
+                    const int i = ib + lane;
+                    const bool act = i < b;
+                    const int c = act ? s_col[i] : -1 - lane;
+                    const double v = act ? s_val[i] : 0.0;
+                    const uint32_t peers = __match_any_sync(0xffffffffu, c);
+                    const int r = __popc(peers & lt);
+                    const int maxr = (int)__reduce_max_sync(0xffffffffu, (unsigned)(act ? r : 0));
+                    for (int rr = 0; rr <= maxr; ++rr) {
+                        if (act && r == rr) acc[c] += v;
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    for (int64_t c = t; c < cols; c += kCsrThreads) o[c * L + l] = acc[c];
+}
+
+__global__ void csr_seg_reduce_kernel(const double* __restrict__ part, int nseg, int64_t n,
+                                      double* __restrict__ Y, int accumulate) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double a = accumulate ? Y[e] : 0.0;
+        for (int s = 0; s < nseg; ++s) a += part[(int64_t)s * n + e];
+        Y[e] = a;
+    }
+}
+
+static int csr_nseg(int64_t out_dim, int flags) {
+    if (flags & IDS_FLAG_ORDERED) return 1;
+    const int64_t want = (148 * 2 * 2 + out_dim - 1) / out_dim;  // ~2 waves of 2 CTAs/SM
+    return (int)tmax<int64_t>(1, tmin<int64_t>(want, 16));
+}
+
+extern "C" size_t ids_countsketch_csr_workspace_bytes(int64_t rows, int64_t cols, int64_t nnz,
+                                                      int64_t out_dim) {
+    (void)rows;
+    if (cols <= kCsrMaxCols) {
+        WsCount c;
+        c.take<double>((size_t)csr_nseg(out_dim, 0) * cols * out_dim);
+        return c.off + 256;
+    }
+    return csr_transpose_ws(cols, nnz, out_dim);
+}
+
+extern "C" int ids_countsketch_csr_f64(const void* indptr, int indptr64, const int32_t* indices,
+                                       const double* data, int64_t rows, int64_t cols,
+                                       int64_t nnz, int64_t row0, int64_t in_dim,
+                                       const int32_t* bucket, const int8_t* sign,
+                                       const int32_t* order_signed, const int64_t* bstart,
+                                       int64_t out_dim, double* Y, int accumulate, int flags,
+                                       int32_t* nonfinite, void* workspace, size_t ws_bytes,
+                                       void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (cols > kCsrMaxCols || !order_signed || !bstart)
+        return csr_transpose_path(indptr, indptr64, indices, data, rows, cols, nnz, row0, in_dim,
+                                  bucket, sign, out_dim, Y, accumulate, nonfinite, workspace,
+                                  ws_bytes, st);
+    if (rows < 1 || cols < 1 || nnz < 0 || out_dim < 1 || row0 < 0 || row0 + rows > in_dim) {
+        ids_set_last_error("csr countsketch: bad arguments");
+        return IDS_EINVAL;
+    }
+    const int nseg = csr_nseg(out_dim, flags);
+    WsCarve ws(workspace, ws_bytes);
+    double* part = nseg > 1 ? ws.take<double>((size_t)nseg * cols * out_dim) : nullptr;
+    if (!ws.ok()) {
+        ids_set_last_error("csr countsketch: workspace too small");
+        return IDS_EWORKSPACE;
+    }
+    double* out = nseg > 1 ? part : Y;
+    const int64_t stride = cols * out_dim;
+    const int init = (nseg == 1 && accumulate) ? 1 : 0;
+    const int restrict_rows = (row0 != 0 || rows != in_dim) ? 1 : 0;
+    const size_t smem = (size_t)cols * sizeof(double);
+    const unsigned grid = (unsigned)(out_dim * nseg);
+    if (indptr64) {
+        if (smem > 48 * 1024)
+            IDS_CUDA_TRY(cudaFuncSetAttribute(cs_csr_bucket_kernel<int64_t>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cs_csr_bucket_kernel<int64_t><<<grid, kCsrThreads, smem, st>>>(
+            static_cast<const int64_t*>(indptr), indices, data, cols, row0, rows, restrict_rows,
+            order_signed, bstart, out_dim, nseg, out, stride, init);
+    } else {
+        if (smem > 48 * 1024)
+            IDS_CUDA_TRY(cudaFuncSetAttribute(cs_csr_bucket_kernel<int32_t>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cs_csr_bucket_kernel<int32_t><<<grid, kCsrThreads, smem, st>>>(
+            static_cast<const int32_t*>(indptr), indices, data, cols, row0, rows, restrict_rows,
+            order_signed, bstart, out_dim, nseg, out, stride, init);
+    }
+    IDS_LAUNCH_CHECK();
+    if (nseg > 1) {
+        const unsigned g = (unsigned)tmin<int64_t>(ceil_div(stride, 256), 148 * 8);
+        csr_seg_reduce_kernel<<<g, 256, 0, st>>>(part, nseg, stride, Y, accumulate);
+        IDS_LAUNCH_CHECK();
+    }
+    if (nonfinite) {
+        const unsigned g = (unsigned)tmin<int64_t>(ceil_div(stride, 256), 148 * 4);
+        nonfinite_values_kernel<<<g, 256, 0, st>>>(Y, stride, nonfinite);
         IDS_LAUNCH_CHECK();
     }
     return IDS_OK;

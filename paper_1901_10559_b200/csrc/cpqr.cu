@@ -134,16 +134,14 @@ __device__ __forceinline__ double sub_dot(double y, const double* __restrict__ a
 // (one warp; result NOT yet reduced across lanes).
 __device__ __forceinline__ double lane_dot(const double* __restrict__ a, const double* __restrict__ b,
                                            int64_t r0, int64_t m) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     int64_t r = r0 + (threadIdx.x & 31);
-    for (; r + 96 < m; r += 128) {
-        s0 = fma(a[r], b[r], s0);
-        s1 = fma(a[r + 32], b[r + 32], s1);
-        s2 = fma(a[r + 64], b[r + 64], s2);
-        s3 = fma(a[r + 96], b[r + 96], s3);
+    for (; r + 224 < m; r += 256) {  // eight loads in flight per lane
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] = fma(a[r + 32 * u], b[r + 32 * u], s[u]);
     }
-    for (; r < m; r += 32) s0 = fma(a[r], b[r], s0);
-    return (s0 + s1) + (s2 + s3);
+    for (; r < m; r += 32) s[0] = fma(a[r], b[r], s[0]);
+    return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
 // Block-wide sum of one double per thread; result valid in all threads.
@@ -329,8 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
                 if (lane == 0) g.zpart[b * k + q] = s;
             }
         }
-        // GEMV over owned remaining columns: W_j = Y[kk:, j]^T v
-        for (int64_t j = c0 + wid; j < c1; j += kWarps) {
+        // GEMV over owned remaining columns: W_j = Y[kk:, j]^T v.  Odd steps walk
+        // the columns backwards so the tail read last (still in L2) comes first.
+        for (int64_t jw = wid; jw < c1 - c0; jw += kWarps) {
+            const int64_t j = (kk & 1) ? c1 - 1 - jw : c0 + jw;
             if (g.pos[j] <= kk) continue;
             const double s = warp_sum(lane_dot(g.Y + j * ldy, vsm, kk, m));
             if (lane == 0) g.W[j] = s;
@@ -405,6 +405,277 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             for (int64_t q = 0; q < k; ++q) nr += fabs(g.beta[q]) > g.rank_tol * lead ? 1 : 0;
         *g.numerical_rank = nr;
     }
+}
+
+// ---- short sketches: one thread-block CLUSTER, Y resident in shared memory --
+// For L x R sketches small enough to split over the SMs of one cluster (the
+// matrix configs: 40 x 1000, 100 x 2000), each CTA keeps its column slice of
+// Y, its rows of F and R, and a private copy of V in shared memory.  A step
+// then needs one hardware cluster barrier: the per-CTA argmax candidates are
+// exchanged through distributed shared memory (double-buffered by step
+// parity), the pivot column and its F row are read from the owner CTA's
+// shared memory, and every CTA builds the Householder vector itself.
+constexpr int kClusterMax = 16;
+
+struct ClusterArgs {
+    const double* Y;
+    int64_t m, n, ldy, k;
+    double rank_tol;
+    int32_t* perm;
+    double* Rtop;
+    int32_t* numerical_rank;
+    double* Vout;    // V (m x k) and tau for form_q_kernel, written by CTA 0
+    double* tauout;
+    int ncl;         // columns per CTA (max)
+};
+
+struct ClusterSmem {  // carve of the dynamic shared memory
+    double *Ys, *Fs, *Rs, *V, *v, *z, *vn1, *vn2, *W, *tau, *beta;
+    int* pos;
+};
+
+__device__ ClusterSmem carve_cluster(double* base, int64_t m, int64_t k, int ncl) {
+    ClusterSmem c;
+    c.Ys = base;
+    c.Fs = c.Ys + (int64_t)m * ncl;  // F: k x ncl (q-major)
+    c.Rs = c.Fs + k * ncl;           // R rows: k x ncl
+    c.V = c.Rs + k * ncl;            // m x k col-major
+    c.v = c.V + m * k;
+    c.z = c.v + m;
+    c.vn1 = c.z + k;
+    c.vn2 = c.vn1 + ncl;
+    c.W = c.vn2 + ncl;
+    c.tau = c.W + ncl;
+    c.beta = c.tau + k;
+    c.pos = reinterpret_cast<int*>(c.beta + k);
+    return c;
+}
+
+size_t cluster_smem_bytes(int64_t m, int64_t k, int ncl) {
+    return sizeof(double) * ((size_t)m * ncl + 2 * k * ncl + m * k + m + k + 3 * ncl + 2 * k) +
+           sizeof(int) * ncl + 64;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g) {
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ double dyn[];
+    __shared__ ArgMax slot[2];           // this CTA's candidate, by step parity
+    __shared__ ArgMax warp_best[kWarps];
+    __shared__ double red[kWarps];
+    __shared__ int64_t s_piv[3];
+    __shared__ double s_ab[2];
+    const int CS = (int)cluster.num_blocks();
+    const int b = (int)cluster.block_rank();
+    const int64_t m = g.m, n = g.n, k = g.k;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c0 = n * b / CS, c1 = n * (b + 1) / CS;
+    const int nc = (int)(c1 - c0);
+    const ClusterSmem S = carve_cluster(dyn, m, k, g.ncl);
+    const double tol3z = sqrt(DBL_EPSILON);
+
+    // load the Y slice, norms, positions
+    for (int64_t e = threadIdx.x; e < (int64_t)nc * m; e += kThreads) {
+        const int64_t jj = e / m, r = e % m;
+        S.Ys[jj * m + r] = g.Y[(c0 + jj) * g.ldy + r];
+    }
+    __syncthreads();
+    for (int jj = wid; jj < nc; jj += kWarps) {
+        const double s2 = warp_sum(lane_dot(S.Ys + (int64_t)jj * m, S.Ys + (int64_t)jj * m, 0, m));
+        if (lane == 0) {
+            S.vn1[jj] = sqrt(s2);
+            S.vn2[jj] = sqrt(s2);
+            S.pos[jj] = (int)(c0 + jj);
+        }
+    }
+    __syncthreads();
+
+    auto local_argmax = [&](int64_t pmin, int64_t pnext, int par) {
+        ArgMax best{-1.0, INT64_MAX, -1, -1};
+        for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
+            const int64_t pj = S.pos[jj];
+            if (pj == pnext) best.col_at_next = c0 + jj;
+            if (pj >= pmin && better(S.vn1[jj], pj, best.val, best.pos)) {
+                best.val = S.vn1[jj];
+                best.pos = pj;
+                best.col = c0 + jj;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            ArgMax ot;
+            ot.val = __shfl_xor_sync(0xffffffffu, best.val, o);
+            ot.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
+            ot.col = __shfl_xor_sync(0xffffffffu, best.col, o);
+            ot.col_at_next = __shfl_xor_sync(0xffffffffu, best.col_at_next, o);
+            if (better(ot.val, ot.pos, best.val, best.pos)) {
+                best.val = ot.val;
+                best.pos = ot.pos;
+                best.col = ot.col;
+            }
+            if (ot.col_at_next >= 0) best.col_at_next = ot.col_at_next;
+        }
+        if (lane == 0) warp_best[wid] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ArgMax r = warp_best[0];
+            for (int i = 1; i < kWarps; ++i) {
+                const ArgMax o = warp_best[i];
+                if (better(o.val, o.pos, r.val, r.pos)) {
+                    r.val = o.val;
+                    r.pos = o.pos;
+                    r.col = o.col;
+                }
+                if (o.col_at_next >= 0) r.col_at_next = o.col_at_next;
+            }
+            slot[par] = r;
+        }
+    };
+    local_argmax(0, 0, 0);
+    cluster.sync();
+
+    for (int64_t kk = 0; kk < k; ++kk) {
+        const int par = (int)(kk & 1);
+        // ---- pivot from every CTA's candidate (DSMEM), fixed rank order ----
+        if (threadIdx.x == 0) {
+            ArgMax r{-1.0, INT64_MAX, -1, -1};
+            for (int q = 0; q < CS; ++q) {
+                const ArgMax o = *cluster.map_shared_rank(&slot[par], q);
+                if (better(o.val, o.pos, r.val, r.pos)) {
+                    r.val = o.val;
+                    r.pos = o.pos;
+                    r.col = o.col;
+                }
+                if (o.col_at_next >= 0) r.col_at_next = o.col_at_next;
+            }
+            if (r.col < 0) {  // all-NaN norms (non-finite input): keep position kk
+                r.col = r.col_at_next;
+                r.pos = kk;
+            }
+            s_piv[0] = r.col;
+            s_piv[1] = r.pos;
+            s_piv[2] = r.col_at_next;
+        }
+        __syncthreads();
+        const int64_t cs = s_piv[0], ps = s_piv[1], ck = s_piv[2];
+        if (threadIdx.x == 0) {
+            if (ck >= c0 && ck < c1 && ck != cs) S.pos[ck - c0] = (int)ps;
+            if (cs >= c0 && cs < c1) S.pos[cs - c0] = (int)kk;
+        }
+        // ---- pivot column from the owner's shared memory, Householder ----
+        int owner = 0;
+        while (owner + 1 < CS && n * (owner + 1) / CS <= cs) ++owner;
+        const int64_t oc0 = n * owner / CS;
+        const double* ycol = cluster.map_shared_rank(S.Ys, owner) + (cs - oc0) * m;
+        const double* fown = cluster.map_shared_rank(S.Fs, owner) + (cs - oc0);
+        double ss = 0.0;
+        for (int64_t r = kk + threadIdx.x; r < m; r += kThreads) {
+            double acc = ycol[r];
+            for (int64_t q = 0; q < kk; ++q) acc = fma(-S.V[q * m + r], fown[q * g.ncl], acc);
+            S.v[r] = acc;
+            if (r > kk) ss = fma(acc, acc, ss);
+        }
+        ss = block_sum(ss, red);
+        if (threadIdx.x == 0) {
+            s_ab[0] = S.v[kk];
+            s_ab[1] = ss;
+        }
+        __syncthreads();
+        const double alpha = s_ab[0], xnorm = sqrt(s_ab[1]);
+        double tau, beta, scal;
+        if (xnorm == 0.0) {
+            tau = 0.0;
+            beta = alpha;
+            scal = 0.0;
+        } else {
+            beta = -copysign(dlapy2(alpha, xnorm), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        for (int64_t r = threadIdx.x; r < m; r += kThreads) {
+            const double vr = r < kk ? 0.0 : (r == kk ? 1.0 : S.v[r] * scal);
+            S.v[r] = vr;
+            S.V[kk * m + r] = vr;
+        }
+        if (threadIdx.x == 0) {
+            S.tau[kk] = tau;
+            S.beta[kk] = beta;
+            if (cs >= c0 && cs < c1) S.Rs[kk * g.ncl + (cs - c0)] = beta;
+        }
+        __syncthreads();
+        // z = V[:, :kk]^T v
+        for (int64_t q = wid; q < kk; q += kWarps) {
+            const double zq = warp_sum(lane_dot(S.V + q * m, S.v, kk, m));
+            if (lane == 0) S.z[q] = zq;
+        }
+        // GEMV over owned remaining columns
+        for (int jj = wid; jj < nc; jj += kWarps) {
+            if (S.pos[jj] <= kk) continue;
+            const double w = warp_sum(lane_dot(S.Ys + (int64_t)jj * m, S.v, kk, m));
+            if (lane == 0) S.W[jj] = w;
+        }
+        __syncthreads();
+        // F, row kk of R, norm downdate (thread per column), flagged recompute (warp per column)
+        for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
+            if (S.pos[jj] <= kk) continue;
+            double f = S.W[jj], rk = S.Ys[(int64_t)jj * m + kk];
+            for (int64_t q = 0; q < kk; ++q) {
+                const double fq = S.Fs[q * g.ncl + jj];
+                f = fma(-fq, S.z[q], f);
+                rk = fma(-S.V[q * m + kk], fq, rk);
+            }
+            f *= tau;
+            S.Fs[kk * g.ncl + jj] = f;
+            rk -= f;
+            S.Rs[kk * g.ncl + jj] = rk;
+            const double vn1 = S.vn1[jj];
+            S.W[jj] = 0.0;  // recompute flag
+            if (kk < m - 1 && vn1 != 0.0) {
+                double temp = fabs(rk) / vn1;
+                temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+                const double ratio = vn1 / S.vn2[jj];
+                if (temp * ratio * ratio <= tol3z) S.W[jj] = 1.0;
+                else S.vn1[jj] = vn1 * sqrt(temp);
+            }
+        }
+        __syncthreads();
+        for (int jj = wid; jj < nc; jj += kWarps) {
+            if (S.pos[jj] <= kk || S.W[jj] == 0.0) continue;
+            double s2 = 0.0;
+            for (int64_t r = kk + 1 + lane; r < m; r += 32) {
+                double v = S.Ys[(int64_t)jj * m + r];
+                for (int64_t q = 0; q <= kk; ++q) v = fma(-S.V[q * m + r], S.Fs[q * g.ncl + jj], v);
+                s2 = fma(v, v, s2);
+            }
+            s2 = warp_sum(s2);
+            if (lane == 0) {
+                S.vn1[jj] = sqrt(s2);
+                S.vn2[jj] = sqrt(s2);
+            }
+        }
+        __syncthreads();
+        local_argmax(kk + 1, kk + 1, par ^ 1);
+        cluster.sync();
+    }
+
+    // ---- outputs ----
+    for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
+        const int64_t p = S.pos[jj];
+        g.perm[p] = (int32_t)(c0 + jj);
+        for (int64_t q = 0; q < k; ++q) g.Rtop[q * n + p] = (p >= q) ? S.Rs[q * g.ncl + jj] : 0.0;
+    }
+    if (b == 0) {
+        if (g.Vout) {
+            for (int64_t e = threadIdx.x; e < m * k; e += kThreads) g.Vout[e] = S.V[e];
+            for (int64_t q = threadIdx.x; q < k; q += kThreads) g.tauout[q] = S.tau[q];
+        }
+        if (threadIdx.x == 0) {
+            const double lead = fabs(S.beta[0]);
+            int32_t nr = 0;
+            if (lead != 0.0)
+                for (int64_t q = 0; q < k; ++q) nr += fabs(S.beta[q]) > g.rank_tol * lead ? 1 : 0;
+            *g.numerical_rank = nr;
+        }
+    }
+    cluster.sync();  // keep every CTA's shared memory alive until remote reads finish
 }
 
 // Q[:, c] = H_0 H_1 ... H_c e_c  (dorgqr's explicit Q, first k columns)
@@ -564,6 +835,60 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
         return IDS_EINVAL;
     }
     cudaStream_t st = as_stream(stream);
+    {   // short sketch: one cluster with Y in shared memory
+        for (int csz : {8, 16}) {
+            const int ncl = (int)ceil_div(cols, csz);
+            const size_t cs_smem = cluster_smem_bytes(rows, k, ncl);
+            if (cols < 2 * csz || cs_smem > 200 * 1024) continue;
+            if (rows * cols < 4096) break;  // tiny: the cooperative kernel is fine
+            ClusterArgs ca{};
+            ca.Y = Y;
+            ca.m = rows;
+            ca.n = cols;
+            ca.ldy = ldy;
+            ca.k = k;
+            ca.rank_tol = rank_tol;
+            ca.perm = perm;
+            ca.Rtop = Rtop;
+            ca.numerical_rank = numerical_rank;
+            ca.ncl = ncl;
+            WsCarve wsc(workspace, ws_bytes);
+            ca.Vout = wsc.take<double>((size_t)rows * k);
+            ca.tauout = wsc.take<double>((size_t)k);
+            if (!wsc.ok()) break;
+            IDS_CUDA_TRY(cudaFuncSetAttribute(cpqr_cluster_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)cs_smem));
+            if (csz > 8)
+                IDS_CUDA_TRY(cudaFuncSetAttribute(cpqr_cluster_kernel,
+                                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(csz);
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = cs_smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = csz;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int clusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&clusters, cpqr_cluster_kernel, &cfg) != cudaSuccess ||
+                clusters < 1) {
+                cudaGetLastError();
+                continue;
+            }
+            IDS_CUDA_TRY(cudaLaunchKernelEx(&cfg, cpqr_cluster_kernel, ca));
+            ids_count_launch();
+            if (Q) {
+                form_q_kernel<<<(unsigned)k, kThreads, 0, st>>>(ca.Vout, ca.tauout, rows, k, Q);
+                IDS_LAUNCH_CHECK();
+            }
+            return IDS_OK;
+        }
+    }
     const size_t smem = (size_t)(rows + 2 * k) * sizeof(double);
     if (smem > 200 * 1024) {
         ids_set_last_error("cpqr: sketch too tall for the shared-memory Householder vector");

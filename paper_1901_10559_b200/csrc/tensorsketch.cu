@@ -30,6 +30,7 @@ namespace {
 
 constexpr int kMaxModes = 8;
 constexpr int kMaxHalf = 8192;  // largest half-length transform kept in shared memory
+constexpr int kStage = 2048;    // sorted CountSketch entries staged per round
 
 struct TsArgs {
     int n_modes;
@@ -218,6 +219,9 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     // this CTA's global (L2-resident) slice
     double2* spec = g.spec_in_smem ? buf + (N2 + N2 / 8 + 1)
                                    : g.spec_glob + (int64_t)blockIdx.x * (N2 + 1);
+    double* st_val = reinterpret_cast<double*>(buf + (N2 + N2 / 8 + 1) +
+                                               (g.spec_in_smem ? (N2 + 1) : 0));
+    int32_t* st_key = reinterpret_cast<int32_t*>(st_val + kStage);
     for (int64_t r = blockIdx.x; r < g.ncols; r += gridDim.x) {
         // passes 0..N-1: forward transform of mode n's CountSketch, product into S;
         // pass N: inverse transform of S (one inlined FFT for all passes)
@@ -231,19 +235,36 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 const int32_t* key = s_key[n];
                 const int In = s_dim[n];
                 for (int l = t; l < M; l += T) dbuf[2 * pad(l >> 1) + (l & 1)] = 0.0;
-                __syncthreads();
-                for (int k = t; k < In; k += T) {
-                    const int32_t bkt = __ldg(key + k);
-                    if (k > 0 && __ldg(key + k - 1) == bkt) continue;  // not a run head
-                    double acc = 0.0;
-                    int kk = k;
-                    do {
-                        const int32_t e = __ldg(ord + kk);
+                // stage kStage sorted entries at a time: bucket + signed value,
+                // all loads independent (coalesced index reads, column gather)
+                for (int c0 = 0; c0 < In; c0 += kStage) {
+                    const int cn = min(kStage, In - c0);
+                    for (int q = t; q < cn; q += T) {
+                        const int32_t e = __ldg(ord + c0 + q);
                         const double x = __ldg(col + dec_row(e));
-                        acc = e >= 0 ? acc + x : acc - x;
-                        ++kk;
-                    } while (kk < In && __ldg(key + kk) == bkt);
-                    dbuf[2 * pad(bkt >> 1) + (bkt & 1)] = acc;
+                        st_key[q] = __ldg(key + c0 + q);
+                        st_val[q] = e >= 0 ? x : -x;
+                    }
+                    __syncthreads();
+                    // run heads sum their bucket's rows in increasing row order
+                    for (int q = t; q < cn; q += T) {
+                        const int32_t bkt = st_key[q];
+                        const bool head = q > 0 ? st_key[q - 1] != bkt
+                                                : (c0 == 0 || __ldg(key + c0 - 1) != bkt);
+                        if (!head) continue;
+                        double acc = 0.0;
+                        int kk = q;
+                        while (kk < cn && st_key[kk] == bkt) acc += st_val[kk++];
+                        int kg = c0 + kk;  // run continues past the staged block (rare)
+                        while (kg < In && __ldg(key + kg) == bkt) {
+                            const int32_t e = __ldg(ord + kg);
+                            const double x = __ldg(col + dec_row(e));
+                            acc = e >= 0 ? acc + x : acc - x;
+                            ++kg;
+                        }
+                        dbuf[2 * pad(bkt >> 1) + (bkt & 1)] = acc;
+                    }
+                    __syncthreads();
                 }
             } else {
                 // ---- inverse: pack conj(Z) from S, forward FFT, conj ----
@@ -345,8 +366,9 @@ TsPlan plan_ts(int n_modes, int64_t L) {
     p.threads = (int)T;
     const size_t fft_bytes = (size_t)(p.N2 + p.N2 / 8 + 1) * sizeof(double2);
     const size_t spec_bytes = (size_t)(p.N2 + 1) * sizeof(double2);
-    p.spec_in_smem = fft_bytes + spec_bytes <= 200 * 1024;
-    p.smem = fft_bytes + (p.spec_in_smem ? spec_bytes : 0);
+    const size_t stage_bytes = (size_t)kStage * (sizeof(double) + sizeof(int32_t));
+    p.spec_in_smem = fft_bytes + spec_bytes + stage_bytes <= 200 * 1024;
+    p.smem = fft_bytes + (p.spec_in_smem ? spec_bytes : 0) + stage_bytes;
     return p;
 }
 
