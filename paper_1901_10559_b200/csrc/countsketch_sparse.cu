@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
                     myc[q] = __ldg(indices + p);
                     const double v = __ldcs(data + p);
                     myv[q] = s_sg[lo] < 0 ? -v : v;
-                    myo[q] = myc[q] / tw;
+                    myo[q] = (int)((uint32_t)myc[q] / (uint32_t)tw);
                 }
             }
             __syncthreads();  // s_base zeroed

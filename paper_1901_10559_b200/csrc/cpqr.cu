@@ -535,24 +535,31 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
     for (int64_t kk = 0; kk < k; ++kk) {
         const int par = (int)(kk & 1);
         // ---- pivot from every CTA's candidate (DSMEM), fixed rank order ----
-        if (threadIdx.x == 0) {
+        if (wid == 0) {  // lane q reads CTA q's candidate, then a shuffle tree
             ArgMax r{-1.0, INT64_MAX, -1, -1};
-            for (int q = 0; q < CS; ++q) {
-                const ArgMax o = *cluster.map_shared_rank(&slot[par], q);
-                if (better(o.val, o.pos, r.val, r.pos)) {
-                    r.val = o.val;
-                    r.pos = o.pos;
-                    r.col = o.col;
+            if (lane < CS) r = *cluster.map_shared_rank(&slot[par], lane);
+            for (int o = 16; o > 0; o >>= 1) {
+                ArgMax ot;
+                ot.val = __shfl_xor_sync(0xffffffffu, r.val, o);
+                ot.pos = __shfl_xor_sync(0xffffffffu, r.pos, o);
+                ot.col = __shfl_xor_sync(0xffffffffu, r.col, o);
+                ot.col_at_next = __shfl_xor_sync(0xffffffffu, r.col_at_next, o);
+                if (better(ot.val, ot.pos, r.val, r.pos)) {
+                    r.val = ot.val;
+                    r.pos = ot.pos;
+                    r.col = ot.col;
                 }
-                if (o.col_at_next >= 0) r.col_at_next = o.col_at_next;
+                if (ot.col_at_next >= 0) r.col_at_next = ot.col_at_next;
             }
-            if (r.col < 0) {  // all-NaN norms (non-finite input): keep position kk
-                r.col = r.col_at_next;
-                r.pos = kk;
+            if (lane == 0) {
+                if (r.col < 0) {  // all-NaN norms (non-finite input): keep position kk
+                    r.col = r.col_at_next;
+                    r.pos = kk;
+                }
+                s_piv[0] = r.col;
+                s_piv[1] = r.pos;
+                s_piv[2] = r.col_at_next;
             }
-            s_piv[0] = r.col;
-            s_piv[1] = r.pos;
-            s_piv[2] = r.col_at_next;
         }
         __syncthreads();
         const int64_t cs = s_piv[0], ps = s_piv[1], ck = s_piv[2];
@@ -564,12 +571,16 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
         int owner = 0;
         while (owner + 1 < CS && n * (owner + 1) / CS <= cs) ++owner;
         const int64_t oc0 = n * owner / CS;
-        const double* ycol = cluster.map_shared_rank(S.Ys, owner) + (cs - oc0) * m;
-        const double* fown = cluster.map_shared_rank(S.Fs, owner) + (cs - oc0);
+        {   // copy the pivot column and its F row from the owner (one remote read each)
+            const double* ycol = cluster.map_shared_rank(S.Ys, owner) + (cs - oc0) * m;
+            const double* fown = cluster.map_shared_rank(S.Fs, owner) + (cs - oc0);
+            for (int64_t r = kk + threadIdx.x; r < m; r += kThreads) S.v[r] = ycol[r];
+            for (int64_t q = threadIdx.x; q < kk; q += kThreads) S.z[q] = fown[q * g.ncl];
+        }
+        __syncthreads();
         double ss = 0.0;
         for (int64_t r = kk + threadIdx.x; r < m; r += kThreads) {
-            double acc = ycol[r];
-            for (int64_t q = 0; q < kk; ++q) acc = fma(-S.V[q * m + r], fown[q * g.ncl], acc);
+            const double acc = sub_dot(S.v[r], S.V + r, m, S.z, 1, kk);
             S.v[r] = acc;
             if (r > kk) ss = fma(acc, acc, ss);
         }
@@ -601,16 +612,26 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
             if (cs >= c0 && cs < c1) S.Rs[kk * g.ncl + (cs - c0)] = beta;
         }
         __syncthreads();
+        __syncthreads();  // z (F row copy) consumed, S.z reused below
+        // GEMV over owned remaining columns, one thread per column (short m)
+        for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
+            if (S.pos[jj] <= kk) continue;
+            const double* yc = S.Ys + (int64_t)jj * m;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int64_t r = kk;
+            for (; r + 3 < m; r += 4) {
+                a0 = fma(yc[r], S.v[r], a0);
+                a1 = fma(yc[r + 1], S.v[r + 1], a1);
+                a2 = fma(yc[r + 2], S.v[r + 2], a2);
+                a3 = fma(yc[r + 3], S.v[r + 3], a3);
+            }
+            for (; r < m; ++r) a0 = fma(yc[r], S.v[r], a0);
+            S.W[jj] = (a0 + a1) + (a2 + a3);
+        }
         // z = V[:, :kk]^T v
         for (int64_t q = wid; q < kk; q += kWarps) {
             const double zq = warp_sum(lane_dot(S.V + q * m, S.v, kk, m));
             if (lane == 0) S.z[q] = zq;
-        }
-        // GEMV over owned remaining columns
-        for (int jj = wid; jj < nc; jj += kWarps) {
-            if (S.pos[jj] <= kk) continue;
-            const double w = warp_sum(lane_dot(S.Ys + (int64_t)jj * m, S.v, kk, m));
-            if (lane == 0) S.W[jj] = w;
         }
         __syncthreads();
         // F, row kk of R, norm downdate (thread per column), flagged recompute (warp per column)

@@ -239,11 +239,28 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 // all loads independent (coalesced index reads, column gather)
                 for (int c0 = 0; c0 < In; c0 += kStage) {
                     const int cn = min(kStage, In - c0);
-                    for (int q = t; q < cn; q += T) {
-                        const int32_t e = __ldg(ord + c0 + q);
-                        const double x = __ldg(col + dec_row(e));
-                        st_key[q] = __ldg(key + c0 + q);
-                        st_val[q] = e >= 0 ? x : -x;
+                    for (int qb = 0; qb < cn; qb += 4 * T) {  // 4 entries per thread in flight
+                        int32_t e[4], kq[4];
+                        double x[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int q = qb + u * T + t;
+                            e[u] = q < cn ? __ldg(ord + c0 + q) : 0;
+                            kq[u] = q < cn ? __ldg(key + c0 + q) : 0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int q = qb + u * T + t;
+                            x[u] = q < cn ? __ldg(col + dec_row(e[u])) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int q = qb + u * T + t;
+                            if (q < cn) {
+                                st_key[q] = kq[u];
+                                st_val[q] = e[u] >= 0 ? x[u] : -x[u];
+                            }
+                        }
                     }
                     __syncthreads();
                     // run heads sum their bucket's rows in increasing row order

@@ -20,6 +20,10 @@ from ._inputs import DenseOperand, SparseOperand, matrix_operand
 from ._native import IDS_ERETRY, IDS_FLAG_ORDERED, call, query
 
 _MAX_MATERIALIZE = 50_000_000  # sketch.py:30
+# Above this many nonzeros the CSR kernel splits each bucket into row segments
+# (fixed-order partial sums): deterministic run to run and within ~1e-16 of
+# scipy, but no longer bit-identical to its sequential order.
+ORDERED_SPARSE_MAX_NNZ = 1 << 24
 
 
 def _seed_entropy(seed):
@@ -214,6 +218,8 @@ class CountSketchOp:
             )
         elif isinstance(operand, SparseOperand):
             order, bstart = self.bucket_index()
+            if operand.nnz > ORDERED_SPARSE_MAX_NNZ:
+                flags &= ~IDS_FLAG_ORDERED  # segmented: deterministic, not bit-for-bit scipy
             nbytes = query(
                 "ids_countsketch_csr_workspace_bytes", operand.rows, operand.cols, operand.nnz,
                 self.out_dim,

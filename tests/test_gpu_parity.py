@@ -423,3 +423,22 @@ def test_trials_api_matches_single_calls_and_checks_nan():
     bad[17, 5] = np.inf
     with pytest.raises(ValueError):
         countsketch_id_trials(bad, 12, 40, seeds=[1, 2])
+
+
+@pytest.mark.parametrize("shape,k", [((100, 2000), 20), ((40, 1000), 10), ((200, 3000), 20),
+                                     ((300, 700), 64), ((4096, 300), 10)])
+def test_matrix_id_paths_vs_oracle(shape, k):
+    """Cluster (short sketches), cooperative-small and cooperative-tall CPQR
+    paths: j identical to LAPACK's dgeqp3, P within 1e-10."""
+    rng = np.random.default_rng(shape[0] + shape[1])
+    m, n = shape
+    base = rng.standard_normal((m, k + 5)) @ rng.standard_normal((k + 5, n))
+    y = base + 1e-3 * rng.standard_normal((m, n))
+    d = ids.matrix_id(y, k)
+    want = oracle.matrix_id(y, k)
+    assert np.array_equal(d.cols, want.cols)
+    assert relerr_fro(d.coeffs, want.coeffs) <= TOL
+    f = ids.cpqr(y, k)
+    assert np.array_equal(f.perm[:k], want.cols)
+    err = np.linalg.norm(f.q @ f.r - y[:, f.perm]) / np.linalg.norm(y)
+    assert err <= 1e-3 * 10  # rank-k truncation error of this matrix

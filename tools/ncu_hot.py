@@ -1,0 +1,26 @@
+"""Top stall-sampled SASS lines (+ CUDA source line) of an ncu report."""
+import csv
+import subprocess
+import sys
+
+rep = sys.argv[1]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout.splitlines()
+rows = list(csv.reader(out))
+start = 2 if rows and rows[0] and rows[0][0].startswith("Kernel") else 1
+hdr = rows[start - 1]
+ci = hdr.index("Warp Stall Sampling (All Samples)")
+si = hdr.index("Source")
+data = [(int(r[ci]) if r[ci].isdigit() else 0, i, r[si]) for i, r in enumerate(rows[start:]) if len(r) > ci]
+tot = sum(d[0] for d in data)
+print("total samples", tot)
+for c, i, src in sorted(data, reverse=True)[:n]:
+    print(f"{c:7d} {100.0 * c / max(tot, 1):5.1f}% {i:6d}  {src[:90]}")
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
+r2 = list(csv.reader(raw))
+for i, h in enumerate(r2[0]):
+    if h in ("gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "dram__bytes_read.sum",
+             "dram__bytes_write.sum", "smsp__warps_active.avg.per_cycle_active",
+             "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers"):
+        print(h, r2[1][i], r2[2][i])
