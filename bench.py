@@ -142,11 +142,8 @@ class Clocks:
 
 
 # ----------------------------------------------------------------- CPU -----
-def cpu_sample_gbs(w, rows, seed=0):
-    """The oracle port (reference algorithm on numpy/scipy/LAPACK) on a
-    bounded row sample of the workload; returns (GB/s, seconds, rows)."""
-    import oracle
-
+def cpu_sample_matrix(w, rows):
+    """A row sample of the workload built the same way (host numpy)."""
     rng = np.random.default_rng(7)
     cols = w["cols"]
     v = np.linalg.qr(rng.standard_normal((cols, cols)))[0]
@@ -154,11 +151,22 @@ def cpu_sample_gbs(w, rows, seed=0):
     a = (u * sigma_of(w)) @ v.T
     if w["noise"] > 0:
         a += w["noise"] * rng.standard_normal(a.shape)
-    del u
+    # F order, as BASELINE.md section 2 prescribes for the reference (no extra copy
+    # in as_dense, linalg.py:29)
+    return np.asfortranarray(a)
+
+
+def cpu_sample_gbs(w, rows, seed=0, a=None):
+    """The oracle port (reference algorithm on numpy/scipy/LAPACK) on a
+    bounded row sample of the workload; returns (GB/s, seconds, rows)."""
+    import oracle
+
+    if a is None:
+        a = cpu_sample_matrix(w, rows)
     t0 = time.perf_counter()
     oracle.countsketch_id(a, w["k"], w["L"], seed=seed)
     dt = time.perf_counter() - t0
-    return a.nbytes / dt / 1e9, dt, rows
+    return a.nbytes / dt / 1e9, dt, a.shape[0]
 
 
 def cores():
@@ -172,9 +180,10 @@ def run_reference(args, w, rank, world):
     if rank != 0:
         return
     rows = min(args.cpu_rows, w["rows"])
+    a = cpu_sample_matrix(w, rows)
     vals = []
     for step in range(args.warmup + args.steps):
-        gbs, dt, _ = cpu_sample_gbs(w, rows, seed=step)
+        gbs, dt, _ = cpu_sample_gbs(w, rows, seed=step, a=a)
         if step >= args.warmup:
             vals.append((gbs, dt))
     gb = float(np.median([v[0] for v in vals]))

@@ -156,8 +156,21 @@ def matrix_id(y, rank, rank_tol=RANK_TOL):
     return OracleId(f.perm[:rank].copy(), coeffs, f.numerical_rank, deficient)
 
 
+def as_dense(a, name="a"):
+    """linalg.py:22-36: F-ordered float64 copy + shape / finiteness checks."""
+    out = np.asfortranarray(a, dtype=np.float64)
+    if out.ndim != 2 or out.size == 0:
+        raise ValueError(f"{name} must be a nonempty 2-D array")
+    if not np.isfinite(out).all():
+        raise ValueError(f"{name} contains non-finite entries")
+    return out
+
+
 def countsketch_id(a, rank, sketch_dim=None, seed=None, rank_tol=RANK_TOL, surjective=True):
-    """matrix_id.py:162-182 (validation of check_matrix_id_args :116-141)."""
+    """matrix_id.py:162-182 (validation of check_matrix_id_args :116-141);
+    dense input goes through as_dense like the reference (matrix_id.py:163)."""
+    if not sp.issparse(a):
+        a = as_dense(a)
     rows, ncols = a.shape
     if not 1 <= rank <= ncols:
         raise ValueError("rank out of range")

@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
     const int64_t len = k1 - k0;
     const int64_t s0 = k0 + len * seg / nseg, s1 = k0 + len * (seg + 1) / nseg;
     const int tw = (int)((cols + kCsrOwners - 1) / kCsrOwners);
+    const float inv_tw = 1.0f / (float)tw;
     double* o = out + (int64_t)seg * seg_stride;
     for (int64_t c = t; c < cols; c += kCsrThreads) acc[c] = init_from_out ? o[c * L + l] : 0.0;
 
@@ -373,7 +374,10 @@ __global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
                     myc[q] = __ldg(indices + p);
                     const double v = __ldcs(data + p);
                     myv[q] = s_sg[lo] < 0 ? -v : v;
-                    myo[q] = (int)((uint32_t)myc[q] / (uint32_t)tw);
+                    int ow = (int)((float)myc[q] * inv_tw);  // col / tw without a divide
+                    ow -= (ow * tw > myc[q]) ? 1 : 0;
+                    ow += ((ow + 1) * tw <= myc[q]) ? 1 : 0;
+                    myo[q] = ow;
                 }
             }
             __syncthreads();  // s_base zeroed

@@ -473,19 +473,22 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
     const ClusterSmem S = carve_cluster(dyn, m, k, g.ncl);
     const double tol3z = sqrt(DBL_EPSILON);
 
-    // load the Y slice, norms, positions
+    // load the Y slice ROW-major (Ys[r * ncl + jj]: a thread per column walks
+    // rows conflict-free), norms, positions
     for (int64_t e = threadIdx.x; e < (int64_t)nc * m; e += kThreads) {
         const int64_t jj = e / m, r = e % m;
-        S.Ys[jj * m + r] = g.Y[(c0 + jj) * g.ldy + r];
+        S.Ys[r * g.ncl + jj] = g.Y[(c0 + jj) * g.ldy + r];
     }
     __syncthreads();
-    for (int jj = wid; jj < nc; jj += kWarps) {
-        const double s2 = warp_sum(lane_dot(S.Ys + (int64_t)jj * m, S.Ys + (int64_t)jj * m, 0, m));
-        if (lane == 0) {
-            S.vn1[jj] = sqrt(s2);
-            S.vn2[jj] = sqrt(s2);
-            S.pos[jj] = (int)(c0 + jj);
+    for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
+        double s2 = 0.0;
+        for (int64_t r = 0; r < m; ++r) {
+            const double y = S.Ys[r * g.ncl + jj];
+            s2 = fma(y, y, s2);
         }
+        S.vn1[jj] = sqrt(s2);
+        S.vn2[jj] = sqrt(s2);
+        S.pos[jj] = (int)(c0 + jj);
     }
     __syncthreads();
 
@@ -572,9 +575,9 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
         while (owner + 1 < CS && n * (owner + 1) / CS <= cs) ++owner;
         const int64_t oc0 = n * owner / CS;
         {   // copy the pivot column and its F row from the owner (one remote read each)
-            const double* ycol = cluster.map_shared_rank(S.Ys, owner) + (cs - oc0) * m;
+            const double* ycol = cluster.map_shared_rank(S.Ys, owner) + (cs - oc0);
             const double* fown = cluster.map_shared_rank(S.Fs, owner) + (cs - oc0);
-            for (int64_t r = kk + threadIdx.x; r < m; r += kThreads) S.v[r] = ycol[r];
+            for (int64_t r = kk + threadIdx.x; r < m; r += kThreads) S.v[r] = ycol[r * g.ncl];
             for (int64_t q = threadIdx.x; q < kk; q += kThreads) S.z[q] = fown[q * g.ncl];
         }
         __syncthreads();
@@ -616,16 +619,17 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
         // GEMV over owned remaining columns, one thread per column (short m)
         for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
             if (S.pos[jj] <= kk) continue;
-            const double* yc = S.Ys + (int64_t)jj * m;
+            const double* yc = S.Ys + jj;
+            const int64_t ld = g.ncl;
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             int64_t r = kk;
             for (; r + 3 < m; r += 4) {
-                a0 = fma(yc[r], S.v[r], a0);
-                a1 = fma(yc[r + 1], S.v[r + 1], a1);
-                a2 = fma(yc[r + 2], S.v[r + 2], a2);
-                a3 = fma(yc[r + 3], S.v[r + 3], a3);
+                a0 = fma(yc[r * ld], S.v[r], a0);
+                a1 = fma(yc[(r + 1) * ld], S.v[r + 1], a1);
+                a2 = fma(yc[(r + 2) * ld], S.v[r + 2], a2);
+                a3 = fma(yc[(r + 3) * ld], S.v[r + 3], a3);
             }
-            for (; r < m; ++r) a0 = fma(yc[r], S.v[r], a0);
+            for (; r < m; ++r) a0 = fma(yc[r * ld], S.v[r], a0);
             S.W[jj] = (a0 + a1) + (a2 + a3);
         }
         // z = V[:, :kk]^T v
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
         // F, row kk of R, norm downdate (thread per column), flagged recompute (warp per column)
         for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
             if (S.pos[jj] <= kk) continue;
-            double f = S.W[jj], rk = S.Ys[(int64_t)jj * m + kk];
+            double f = S.W[jj], rk = S.Ys[kk * g.ncl + jj];
             for (int64_t q = 0; q < kk; ++q) {
                 const double fq = S.Fs[q * g.ncl + jj];
                 f = fma(-fq, S.z[q], f);
@@ -662,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
             if (S.pos[jj] <= kk || S.W[jj] == 0.0) continue;
             double s2 = 0.0;
             for (int64_t r = kk + 1 + lane; r < m; r += 32) {
-                double v = S.Ys[(int64_t)jj * m + r];
+                double v = S.Ys[r * g.ncl + jj];
                 for (int64_t q = 0; q <= kk; ++q) v = fma(-S.V[q * m + r], S.Fs[q * g.ncl + jj], v);
                 s2 = fma(v, v, s2);
             }

@@ -441,4 +441,4 @@ def test_matrix_id_paths_vs_oracle(shape, k):
     f = ids.cpqr(y, k)
     assert np.array_equal(f.perm[:k], want.cols)
     err = np.linalg.norm(f.q @ f.r - y[:, f.perm]) / np.linalg.norm(y)
-    assert err <= 1e-3 * 10  # rank-k truncation error of this matrix
+    assert err <= 1e-2  # rank-k truncation of a rank-k matrix plus 1e-3 noise
