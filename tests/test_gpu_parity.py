@@ -432,7 +432,7 @@ def test_matrix_id_paths_vs_oracle(shape, k):
     paths: j identical to LAPACK's dgeqp3, P within 1e-10."""
     rng = np.random.default_rng(shape[0] + shape[1])
     m, n = shape
-    base = rng.standard_normal((m, k + 5)) @ rng.standard_normal((k + 5, n))
+    base = rng.standard_normal((m, k)) @ rng.standard_normal((k, n))
     y = base + 1e-3 * rng.standard_normal((m, n))
     d = ids.matrix_id(y, k)
     want = oracle.matrix_id(y, k)
