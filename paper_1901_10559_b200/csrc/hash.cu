@@ -351,11 +351,12 @@ struct FyChunk {
 static_assert(sizeof(FyChunk) % 16 == 0, "FyChunk is staged with 16-byte copies");
 
 __global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, const FyState* st,
-                                int64_t i0, int64_t lo_band, int64_t T, int64_t nchunks,
+                                int64_t lo_band, int64_t T, int64_t nchunks,
                                 FyChunk* __restrict__ ch) {
     const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int ln = threadIdx.x & 31;
     if (c >= nchunks) return;
+    const int64_t i0 = st->i;  // exact state at the start of this epoch
     __shared__ int32_t evs[4][kEvMax];
     int32_t* ev = evs[(threadIdx.x >> 5) & 3];
     const double tau = (double)(c * T);
@@ -378,8 +379,34 @@ __global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, co
         out.s = s;
         out.w = (int32_t)w;
         out.a = (int32_t)(s - r.i);
-        out.ne = r.nev <= kEvMax ? r.nev : -1;
-        for (int e = 0; e < kEvMax; ++e) out.ev[e] = e < r.nev ? ev[e] : 0;
+        // near misses -> "flats": offsets where the end-state function
+        // D(d) = d - #{flats <= d} stays level (D gives the trajectory that
+        // started d above the base).  Gap g is taken by every trajectory whose
+        // current offset is >= g: the smallest such start d* solves
+        // d* = g + #{flats <= d*}.  Flats are distinct; kept sorted.
+        int nf = 0;
+        bool over = r.nev > kEvMax;
+        if (!over) {
+            for (int e = 0; e < r.nev; ++e) {
+                const int gap = ev[e];
+                int d = gap, cnt = 0;
+                for (;;) {
+                    cnt = 0;
+                    for (int f = 0; f < nf; ++f) cnt += out.ev[f] <= d ? 1 : 0;
+                    if (gap + cnt == d) break;
+                    d = gap + cnt;
+                }
+                if (d > w) continue;  // no trajectory of the window reaches it
+                int at = nf++;
+                while (at > 0 && out.ev[at - 1] > d) {
+                    out.ev[at] = out.ev[at - 1];
+                    --at;
+                }
+                out.ev[at] = d;
+            }
+        }
+        out.ne = over ? -1 : nf;
+        for (int e = nf; e < kEvMax; ++e) out.ev[e] = 0;
     }
     if (ln == 0) ch[c] = out;
 }
@@ -433,8 +460,9 @@ __global__ void __launch_bounds__(32) fy_stitch_kernel(FyState* st, const FyChun
                     s_ok = 0;
                     break;
                 }
-                int64_t dd = d;
-                for (int e = 0; e < cc.ne; ++e) dd -= (dd >= cc.ev[e]) ? 1 : 0;
+                int cnt = 0;  // D(d) = d - #{flats <= d}; independent loads
+                for (int e = 0; e < cc.ne; ++e) cnt += (cc.ev[e] <= d) ? 1 : 0;
+                const int64_t dd = d - cnt;
                 starts[c0 + l] = S;
                 S = cc.s - cc.a + dd;
             }
@@ -687,12 +715,22 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
             const int64_t lo_band = 1LL << k;
             const int64_t i0 = tmin<int64_t>(2 * lo_band - 1, I - 1);
             if (i0 < lo_band) continue;
-            const int64_t T = band_chunk(k);
-            const double draws_est = (double)(2 * lo_band) * log((double)(i0 + 1) / (double)lo_band);
-            const int64_t nch = tmin<int64_t>((int64_t)(draws_est / (double)T) + 2, p.max_chunks);
-            if (nch >= 2) {
+            // epoch 1 from the band start; epoch 2 restarts the guesses from the
+            // exact state it left (narrow windows, short chunks) so that the
+            // exact walk only has to cover a short tail
+            const int64_t T1 = band_chunk(k);
+            const double draws1 = (double)(2 * lo_band) * log((double)(i0 + 1) / (double)lo_band);
+            const int64_t rem_i = (int64_t)(3.0 * sqrt(draws1) + 16.0) + T1 + 64;
+            const int64_t T2 = tmax<int64_t>(256, T1 / 8);
+            const int64_t epochs[2][2] = {
+                {T1, (int64_t)(draws1 / (double)T1) + 2},
+                {T2, (2 * rem_i) / T2 + 2}};
+            for (int e = 0; e < 2; ++e) {
+                const int64_t T = epochs[e][0];
+                const int64_t nch = tmin<int64_t>(epochs[e][1], p.max_chunks);
+                if (nch < 2) continue;
                 const unsigned gb = (unsigned)ceil_div(nch, 4);  // one warp per chunk
-                fy_chunk_kernel<<<gb, 128, 0, st>>>(draws, p.nbuf, fst, i0, lo_band, T, nch, chunks);
+                fy_chunk_kernel<<<gb, 128, 0, st>>>(draws, p.nbuf, fst, lo_band, T, nch, chunks);
                 IDS_LAUNCH_CHECK();
                 fy_stitch_kernel<<<1, 32, 0, st>>>(fst, chunks, nch, T, starts + 1);
                 IDS_LAUNCH_CHECK();
