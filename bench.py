@@ -399,8 +399,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(args, w, world),
             "id_seconds": single_ms * 1e-3,
-            "pipelined_hash": "K trials (seeds) queued back to back; trial t+1's hash drawn on "
-                              "a side stream during trial t's sketch; one host sync at the end",
+            "trials": "K trials (seeds) of the same A queued back to back, one host sync at "
+                      "the end; each trial draws its own hash on the device",
             "phases_ms": {"hash_and_index": hash_ms, "sketch": sk_ms, "cpqr_and_coeffs": id_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

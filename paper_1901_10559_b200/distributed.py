@@ -122,14 +122,13 @@ def countsketch_id_sharded(a_local, row0, in_dim, rank, sketch_dim=None, seed=No
 def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, seeds=(0,),
                                   rank_tol=1e-12, surjective=True, group=None):
     """countsketch_id_sharded for several seeds, fully queued on the device:
-    trial t+1's hash is drawn on a side stream during trial t, the sketch
-    all-reduce and the ID are enqueued back to back, and the host only
-    synchronizes once at the end (non-finite input is checked then, for all
-    trials at once).  Every rank returns the same list."""
+    hash, sketch, all-reduce and ID of every trial are enqueued back to back
+    and the host synchronizes once at the end (non-finite input is checked
+    then, for all trials at once).  Every rank returns the same list."""
     from ._inputs import DenseOperand, SparseOperand, matrix_operand
     from ._native import IDS_FLAG_ORDERED
     from .matrix_id import check_matrix_id_args, device_matrix_id
-    from .sketch import CountSketchOp, HashPrefetcher
+    from .sketch import CountSketchOp
 
     world, _ = _world(group)
     operand = a_local if isinstance(a_local, (DenseOperand, SparseOperand)) else \
@@ -141,16 +140,11 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
 
     L = check_matrix_id_args(_Shape, rank, sketch_dim, "countsketch")
     seeds = list(seeds)
-    pf = HashPrefetcher()
     outs, flags = [], []
-    if seeds:
-        pf.request(in_dim, L, seeds[0], surjective)
-    for t, s in enumerate(seeds):
-        if t + 1 < len(seeds):
-            pf.request(in_dim, L, seeds[t + 1], surjective)
-        op = pf.take(in_dim, L, s, surjective)
-        if op is None:  # pragma: no cover
-            op = CountSketchOp(in_dim, L, seed=s, surjective=surjective)
+    for s in seeds:
+        # (drawing the next trial's hash on a side stream was measured to slow
+        # the one-wave sketch kernel down more than it hid: kept sequential)
+        op = CountSketchOp(in_dim, L, seed=s, surjective=surjective)
         y = torch.empty((cols, L), dtype=torch.float64, device=torch.cuda.current_device())
         flag = torch.zeros(1, dtype=torch.int32, device=y.device)
         op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,
@@ -169,9 +163,10 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
                 dist.all_reduce(conf, op=dist.ReduceOp.MAX, group=group)
             if bool(conf.item()):
                 raise ValueError("a contains non-finite entries")
+    packed = torch.stack(outs) if outs else None
     from .matrix_id import DeviceId
 
-    host = torch.stack(outs).cpu().numpy() if outs else []  # one copy for all trials
+    host = packed.cpu().numpy() if packed is not None else []  # one copy for all trials
     return [DeviceId.unpack(v, rank, cols, "countsketch") for v in host]
 
 

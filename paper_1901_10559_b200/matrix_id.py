@@ -199,8 +199,7 @@ def countsketch_device(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RAN
 def countsketch_id_trials(a, rank, sketch_dim=None, seeds=(0,), rank_tol=DEFAULT_RANK_TOL,
                           surjective=True):
     """countsketch_id of one matrix for several seeds (the paper averages 10
-    trials).  A is uploaded once; the hash of trial t+1 is drawn on a side
-    stream while trial t sketches, and nothing waits on the host until every
+    trials).  A is uploaded once and nothing waits on the host until every
     trial is queued.  Returns a list of InterpolativeDecomposition, identical
     to separate countsketch_id calls."""
     from .distributed import countsketch_id_sharded_trials

@@ -340,7 +340,6 @@ class HashPrefetcher:
         key = (int(in_dim), int(out_dim), seed, bool(surjective))
         if key in self.cache:
             return
-        self.side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.side):
             op = CountSketchOp(in_dim, out_dim, seed=seed, surjective=surjective)
             op._bucket_index()
