@@ -20,9 +20,12 @@
 //   * the Fisher-Yates swaps themselves are applied in parallel: the value
 //     that lands at position i is found by chasing "first later swap that
 //     targeted this position" links (see fy_final_kernel), O(I) work.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 #define PCG_TABLE_QUAL __constant__
 #include "pcg_tables.h"
@@ -312,53 +315,31 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
     return WalkOut{i, tmin<int64_t>(pos, limit), nev};
 }
 
-__global__ void fy_walk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, int64_t i_stop,
-                               int32_t* __restrict__ jout, FyState* st, int64_t* consumed,
-                               int64_t* status) {
-    const WalkOut r = warp_walk(g, st->pos, nbuf, st->i, i_stop, jout, 0, nullptr, 0);
-    if (threadIdx.x == 0) {
-        if (r.i > i_stop) *status = IDS_ERETRY;  // ran out of buffered draws
-        st->i = r.i;
-        st->pos = r.pos;
-        if (i_stop == 0) *consumed = r.pos;
-    }
-}
-
-__global__ void fy_init_kernel(FyState* st, int64_t n) {
-    st->pos = 0;
-    st->i = n - 1;
-    st->done = 0;
-}
-
 // Speculative chunks of band [lo_band, hi_band] (mask = 2*lo_band - 1):
 // chunk c covers draws st->pos + [c*T, (c+1)*T).  Its true starting i is
 // unknown; the expected trajectory gives a window [s, s + W] that contains it
 // with overwhelming probability.  The LOWEST start s is simulated; any start
 // s + d stays exactly d above it except at "near misses", draws the base
 // rejects with gap g = v - i_base in [1, W]: a trajectory whose current
-// offset is >= g accepts there and its offset drops by one.  Recording those
-// gaps (in order) makes the chunk's end state a cheap function of the true
-// start, evaluated by the stitch below.
+// offset is >= g accepts there and its offset drops by one.  The gaps are
+// folded into sorted "flats" of the end-state function
+// D(d) = d - #{flats <= d}, evaluated by the stitch.
 constexpr int kEvMax = 26;
 struct FyChunk {
     int64_t s;    // lowest start in the window
     int32_t w;    // window width (-1: chunk not usable)
     int32_t a;    // accepts of the base trajectory
-    int32_t ne;   // near-miss events recorded (-1: overflow)
+    int32_t ne;   // flats (-1: overflow)
     int32_t ev[kEvMax];
     int32_t pad_;
 };
 static_assert(sizeof(FyChunk) % 16 == 0, "FyChunk is staged with 16-byte copies");
 
-__global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, const FyState* st,
-                                int64_t lo_band, int64_t T, int64_t nchunks,
-                                FyChunk* __restrict__ ch) {
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// One warp: the summary of chunk c of the current epoch (state = epoch start).
+__device__ void chunk_work(const uint32_t* __restrict__ g, int64_t nbuf, int64_t i0, int64_t pos,
+                           int64_t lo_band, int64_t T, int64_t c, FyChunk* __restrict__ ch,
+                           int32_t* ev) {
     const int ln = threadIdx.x & 31;
-    if (c >= nchunks) return;
-    const int64_t i0 = st->i;  // exact state at the start of this epoch
-    __shared__ int32_t evs[4][kEvMax];
-    int32_t* ev = evs[(threadIdx.x >> 5) & 3];
     const double tau = (double)(c * T);
     const double m2 = (double)(2 * lo_band);  // mask + 1
     const double gi = (double)(i0 + 1) * exp(-tau / m2) - 1.0;
@@ -366,7 +347,7 @@ __global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, co
     int64_t s = (int64_t)floor(gi) - half;
     int64_t hi = tmin<int64_t>((int64_t)floor(gi) + half, i0);
     if (c == 0) s = hi = i0;
-    const int64_t pos0 = st->pos + c * T;
+    const int64_t pos0 = pos + c * T;
     FyChunk out;
     out.w = -1;
     out.a = 0;
@@ -379,19 +360,16 @@ __global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, co
         out.s = s;
         out.w = (int32_t)w;
         out.a = (int32_t)(s - r.i);
-        // near misses -> "flats": offsets where the end-state function
-        // D(d) = d - #{flats <= d} stays level (D gives the trajectory that
-        // started d above the base).  Gap g is taken by every trajectory whose
-        // current offset is >= g: the smallest such start d* solves
-        // d* = g + #{flats <= d*}.  Flats are distinct; kept sorted.
+        // gap g is taken by every trajectory whose current offset is >= g: the
+        // smallest such start d* solves d* = g + #{flats <= d*}
         int nf = 0;
-        bool over = r.nev > kEvMax;
+        const bool over = r.nev > kEvMax;
         if (!over) {
             for (int e = 0; e < r.nev; ++e) {
                 const int gap = ev[e];
-                int d = gap, cnt = 0;
+                int d = gap;
                 for (;;) {
-                    cnt = 0;
+                    int cnt = 0;
                     for (int f = 0; f < nf; ++f) cnt += out.ev[f] <= d ? 1 : 0;
                     if (gap + cnt == d) break;
                     d = gap + cnt;
@@ -407,40 +385,26 @@ __global__ void fy_chunk_kernel(const uint32_t* __restrict__ g, int64_t nbuf, co
         }
         out.ne = over ? -1 : nf;
         for (int e = nf; e < kEvMax; ++e) out.ev[e] = 0;
+        __syncwarp();
     }
     if (ln == 0) ch[c] = out;
 }
 
-// Exact re-run of chunk c from its resolved start, writing j (one warp each).
-__global__ void fy_chunk_exact_kernel(const uint32_t* __restrict__ g, const FyState* st0,
-                                      const int64_t* __restrict__ starts, int64_t lo_band,
-                                      int64_t T, int32_t* __restrict__ jout) {
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (c >= st0->done) return;
-    const int64_t p0 = starts[-1] + c * T;  // starts[-1] holds the band's first draw
-    warp_walk(g, p0, p0 + T, starts[c], lo_band, jout, 0, nullptr, 0);
-}
-
-// The chunks are resolved in order by ONE thread: the true start of chunk c
-// gives its offset d in the window; replaying the near-miss gaps gives the
-// end state.  The block stages the chunk summaries in shared memory so the
-// sequential loop only touches on-chip data.  A chunk whose start falls
-// outside its window (or overflowed) stops the stitch; the exact walk then
-// continues from there.
-constexpr int kStitchBatch = 128;
-__global__ void __launch_bounds__(32) fy_stitch_kernel(FyState* st, const FyChunk* __restrict__ ch,
-                                                        int64_t nchunks, int64_t T,
-                                                        int64_t* __restrict__ starts) {
-    __shared__ FyChunk sm[kStitchBatch];
-    __shared__ int64_t s_S;
+// One block (thread 0 walks, the block stages summaries in shared memory):
+// resolves the chunks in order from the exact epoch start; stops at the first
+// chunk whose start leaves its window (the exact walk continues from there).
+constexpr int kStitchBatch = 64;
+__device__ void stitch_block(FyState* st, const FyChunk* __restrict__ ch, int64_t nchunks,
+                             int64_t T, int64_t* __restrict__ starts, FyChunk* sm) {
+    __shared__ int64_t s_S, s_done;
     __shared__ int s_ok;
     const int64_t pos0 = st->pos;
     if (threadIdx.x == 0) {
         s_S = st->i;
         s_ok = 1;
+        s_done = 0;
         starts[-1] = pos0;
     }
-    int64_t done = 0;
     for (int64_t c0 = 0; c0 < nchunks; c0 += kStitchBatch) {
         const int cnt = (int)tmin<int64_t>(kStitchBatch, nchunks - c0);
         __syncthreads();
@@ -460,21 +424,104 @@ __global__ void __launch_bounds__(32) fy_stitch_kernel(FyState* st, const FyChun
                     s_ok = 0;
                     break;
                 }
-                int cnt = 0;  // D(d) = d - #{flats <= d}; independent loads
-                for (int e = 0; e < cc.ne; ++e) cnt += (cc.ev[e] <= d) ? 1 : 0;
-                const int64_t dd = d - cnt;
+                int nflat = 0;  // D(d) = d - #{flats <= d}: independent loads
+                for (int e = 0; e < cc.ne; ++e) nflat += (cc.ev[e] <= d) ? 1 : 0;
                 starts[c0 + l] = S;
-                S = cc.s - cc.a + dd;
+                S = cc.s - cc.a + (d - nflat);
             }
             s_S = S;
-            done += l;
+            s_done += l;
         }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         st->i = s_S;
-        st->pos = pos0 + done * T;
-        st->done = done;
+        st->pos = pos0 + s_done * T;
+        st->done = s_done;
+    }
+}
+
+__device__ __forceinline__ int64_t band_chunk_dev(int k) {
+    const double want = 2.3 * exp2(0.5 * k);
+    int64_t T = 256;
+    while (T < want && T < 4096) T <<= 1;
+    return T;
+}
+
+// The whole phase-B chain in ONE persistent cooperative kernel: per band two
+// speculative epochs (chunks -> stitch -> exact re-runs) and an exact warp
+// walk of the band's tail, then a walk of the small bands; grid barriers
+// separate the stages.
+constexpr int kPbThreads = 128;
+__global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
+    const uint32_t* __restrict__ g, int64_t nbuf, int64_t n, int32_t* __restrict__ jout,
+    FyState* st, FyChunk* __restrict__ ch, int64_t* __restrict__ starts, int64_t max_chunks,
+    int kmin, int64_t* consumed, int64_t* status) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int32_t evs[kPbThreads / 32][kEvMax];
+    __shared__ FyChunk sm[kStitchBatch];
+    const int wib = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * (kPbThreads / 32) + wib;
+    const int64_t nw = (int64_t)gridDim.x * (kPbThreads / 32);
+    const bool lead_warp = blockIdx.x == 0 && wib == 0;
+    if (n <= 1) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) *consumed = 0;
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->pos = 0;
+        st->i = n - 1;
+        st->done = 0;
+    }
+    grid.sync();
+    int top = 0;
+    while ((2LL << top) <= n - 1) ++top;
+    for (int k = top; k >= kmin; --k) {
+        const int64_t lo_band = 1LL << k;
+        const int64_t i0 = tmin<int64_t>(2 * lo_band - 1, n - 1);
+        if (i0 < lo_band) continue;
+        const int64_t T1 = band_chunk_dev(k);
+        const double draws1 = (double)(2 * lo_band) * log((double)(i0 + 1) / (double)lo_band);
+        const int64_t rem_i = (int64_t)(3.0 * sqrt(draws1) + 16.0) + T1 + 64;
+        const int64_t T2 = tmax<int64_t>(256, T1 / 8);
+        for (int e = 0; e < 2; ++e) {
+            const int64_t T = e == 0 ? T1 : T2;
+            const int64_t nch = tmin<int64_t>(e == 0 ? (int64_t)(draws1 / (double)T1) + 2
+                                                      : (2 * rem_i) / T2 + 2,
+                                              max_chunks);
+            if (nch < 2) continue;
+            const int64_t ei = st->i, ep = st->pos;
+            for (int64_t c = gw; c < nch; c += nw) chunk_work(g, nbuf, ei, ep, lo_band, T, c, ch, evs[wib]);
+            grid.sync();
+            if (blockIdx.x == 0) stitch_block(st, ch, nch, T, starts, sm);
+            grid.sync();
+            const int64_t done = st->done;
+            for (int64_t c = gw; c < done; c += nw) {
+                const int64_t p0 = starts[-1] + c * T;
+                warp_walk(g, p0, p0 + T, starts[c], lo_band, jout, 0, nullptr, 0);
+            }
+            // the next epoch's chunk stage only reads st and writes ch; the
+            // stitch that rewrites `starts` is behind the next grid barrier
+        }
+        grid.sync();  // exact re-runs may still write j; st is final for the walk
+        if (lead_warp) {
+            const WalkOut r = warp_walk(g, st->pos, nbuf, st->i, lo_band - 1, jout, 0, nullptr, 0);
+            if (threadIdx.x == 0) {
+                if (r.i > lo_band - 1) *status = IDS_ERETRY;
+                st->i = r.i;
+                st->pos = r.pos;
+            }
+        }
+        grid.sync();
+    }
+    if (lead_warp) {
+        const WalkOut r = warp_walk(g, st->pos, nbuf, st->i, 0, jout, 0, nullptr, 0);
+        if (threadIdx.x == 0) {
+            if (r.i > 0) *status = IDS_ERETRY;
+            st->i = r.i;
+            st->pos = r.pos;
+            *consumed = r.pos;
+        }
     }
 }
 
@@ -560,13 +607,6 @@ struct HashPlan {
 
 constexpr int kMinBand = 12;  // bands below 2^12 are walked exactly by one warp
 
-// Chunk length for band k: ~8 expected near-miss events per chunk.
-int64_t band_chunk(int k) {
-    const double want = 2.3 * pow(2.0, 0.5 * k);
-    int64_t T = 256;
-    while (T < want && T < 4096) T <<= 1;
-    return T;
-}
 
 HashPlan make_plan(int64_t I, int64_t L, int surj) {
     HashPlan p;
@@ -707,41 +747,23 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
         const unsigned gb = (unsigned)ceil_div(p.nbuf, (int64_t)kGenThreads * kChunk);
         raw_draws_kernel<<<gb, kGenThreads, 0, st>>>(sd, d, 1, p.nbuf, draws);
         IDS_LAUNCH_CHECK();
-        fy_init_kernel<<<1, 1, 0, st>>>(fst, I);
-        IDS_LAUNCH_CHECK();
-        int top = 0;
-        while ((2LL << top) <= I - 1) ++top;  // band of i = I - 1
-        for (int k = top; k >= kMinBand && I > 1; --k) {
-            const int64_t lo_band = 1LL << k;
-            const int64_t i0 = tmin<int64_t>(2 * lo_band - 1, I - 1);
-            if (i0 < lo_band) continue;
-            // epoch 1 from the band start; epoch 2 restarts the guesses from the
-            // exact state it left (narrow windows, short chunks) so that the
-            // exact walk only has to cover a short tail
-            const int64_t T1 = band_chunk(k);
-            const double draws1 = (double)(2 * lo_band) * log((double)(i0 + 1) / (double)lo_band);
-            const int64_t rem_i = (int64_t)(3.0 * sqrt(draws1) + 16.0) + T1 + 64;
-            const int64_t T2 = tmax<int64_t>(256, T1 / 8);
-            const int64_t epochs[2][2] = {
-                {T1, (int64_t)(draws1 / (double)T1) + 2},
-                {T2, (2 * rem_i) / T2 + 2}};
-            for (int e = 0; e < 2; ++e) {
-                const int64_t T = epochs[e][0];
-                const int64_t nch = tmin<int64_t>(epochs[e][1], p.max_chunks);
-                if (nch < 2) continue;
-                const unsigned gb = (unsigned)ceil_div(nch, 4);  // one warp per chunk
-                fy_chunk_kernel<<<gb, 128, 0, st>>>(draws, p.nbuf, fst, lo_band, T, nch, chunks);
-                IDS_LAUNCH_CHECK();
-                fy_stitch_kernel<<<1, 32, 0, st>>>(fst, chunks, nch, T, starts + 1);
-                IDS_LAUNCH_CHECK();
-                fy_chunk_exact_kernel<<<gb, 128, 0, st>>>(draws, fst, starts + 1, lo_band, T, jarr);
-                IDS_LAUNCH_CHECK();
-            }
-            fy_walk_kernel<<<1, 32, 0, st>>>(draws, p.nbuf, lo_band - 1, jarr, fst, d + 1, d + 3);
-            IDS_LAUNCH_CHECK();
+        {
+            int dev = 0, sms = 148, per_sm = 1;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fy_phaseb_kernel, kPbThreads, 0);
+            const int G = tmax(1, sms * tmin(per_sm, 2));
+            const uint32_t* dr = draws;
+            int64_t nbuf = p.nbuf, nI = I, mc = p.max_chunks;
+            int kmin = kMinBand;
+            int64_t* sts = starts + 1;
+            int64_t* cons = d + 1;
+            int64_t* stat = d + 3;
+            void* args[] = {&dr, &nbuf, &nI, &jarr, &fst, &chunks, &sts, &mc, &kmin, &cons, &stat};
+            IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fy_phaseb_kernel, dim3(G),
+                                                     dim3(kPbThreads), args, 0, st));
+            ids_count_launch();
         }
-        fy_walk_kernel<<<1, 32, 0, st>>>(draws, p.nbuf, 0, jarr, fst, d + 1, d + 3);
-        IDS_LAUNCH_CHECK();
         if (I > 1) {
             fill_i32_kernel<<<1024, 256, 0, st>>>(first, I, kNone);
             IDS_LAUNCH_CHECK();
