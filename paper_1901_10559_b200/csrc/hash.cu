@@ -325,7 +325,7 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
 // folded into sorted "flats" of the end-state function
 // D(d) = d - #{flats <= d}, evaluated by the stitch.
 constexpr int kEvMax = 26;
-struct FyChunk {
+struct __align__(16) FyChunk {
     int64_t s;    // lowest start in the window
     int32_t w;    // window width (-1: chunk not usable)
     int32_t a;    // accepts of the base trajectory
