@@ -213,12 +213,19 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
                              int32_t* __restrict__ ev, int evmax) {
     const int ln = threadIdx.x & 31;
     int nev = 0;
+    uint32_t xn[8];  // next window, loaded one window ahead
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int64_t p = pos + 8 * ln + q;
+        xn[q] = p < limit ? __ldg(g + p) : 0u;
+    }
     while (i > i_stop && pos < limit) {
         uint32_t x[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int64_t p = pos + 8 * ln + q;
-            x[q] = p < limit ? __ldg(g + p) : 0u;
+            x[q] = xn[q];
+            const int64_t p = pos + 256 + 8 * ln + q;
+            xn[q] = p < limit ? __ldg(g + p) : 0u;
         }
         int b = 0;
         int64_t ib = i;
