@@ -101,6 +101,7 @@ class Clocks:
     def __init__(self, enabled):
         self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        self.t0 = time.time()
         if not enabled:
             return
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
@@ -285,6 +286,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clocks = Clocks(rank == 0)
+    time.sleep(1.5)  # let nvidia-smi/NVML initialize before the timed region
     n0 = lib.ids_launch_count()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
