@@ -267,10 +267,11 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
             int64_t ii = ib - (incl - cnt);
             int endq = 8;
             int ne = 0;
-            int32_t gaps[8];
+            int32_t gaps[8];  // gaps[q] (statically indexed): near miss at draw q, or 0
             if (ln >= b && ln <= ls) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
+                    gaps[q] = 0;
                     if (endq == 8) {
                         const int64_t p = pos + 8 * ln + q;
                         if (p >= limit || ii <= i_stop) {
@@ -281,11 +282,15 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
                                 if (jout) jout[ii] = (int32_t)v;
                                 --ii;
                             } else if (v - ii <= w) {
-                                gaps[ne++] = (int32_t)(v - ii);
+                                gaps[q] = (int32_t)(v - ii);
+                                ++ne;
                             }
                         }
                     }
                 }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) gaps[q] = 0;
             }
             if (w > 0 && __ballot_sync(0xffffffffu, ne > 0)) {
                 int einc = ne;
@@ -294,9 +299,14 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
                     const int y = __shfl_up_sync(0xffffffffu, einc, o);
                     if (ln >= o) einc += y;
                 }
-                const int base = nev + einc - ne;
-                for (int e = 0; e < ne; ++e)
-                    if (base + e < evmax) ev[base + e] = gaps[e];
+                int at = nev + einc - ne;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (gaps[q] != 0) {
+                        if (at < evmax) ev[at] = gaps[q];
+                        ++at;
+                    }
+                }
                 nev += __shfl_sync(0xffffffffu, einc, 31);
             }
             if (ls == 32) {
@@ -320,6 +330,79 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
         pos += 256;
     }
     return WalkOut{i, tmin<int64_t>(pos, limit), nev};
+}
+
+// Small-i variant of warp_walk: one draw per lane (32-draw windows, read 1024
+// draws ahead), so the uncertainty of a lane's i is at most 31 -- better when
+// i is small and wide windows would be mostly ambiguous.
+__device__ WalkOut warp_walk1(const uint32_t* __restrict__ g, int64_t pos, int64_t limit, int64_t i,
+                              int64_t i_stop, int32_t* __restrict__ jout) {
+    const int ln = threadIdx.x & 31;
+    const uint32_t lt = (1u << ln) - 1u;
+    while (i > i_stop && pos < limit) {
+        uint32_t xs[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const int64_t p = pos + 32 * k + ln;
+            xs[k] = p < limit ? __ldg(g + p) : 0u;
+        }
+        bool stop = false;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            if (stop) break;
+            const uint32_t x = xs[k];
+            int b = 0;
+            while (b < 32) {
+                int stt = 0;  // 0 done, 1 accept, 2 reject, 3 ambiguous
+                uint32_t v = 0;
+                if (ln >= b) {
+                    const int64_t hi = i, lo = i - (ln - b);
+                    const int64_t p = pos + 32 * k + ln;
+                    if (p >= limit || lo <= i_stop || lo < 1 ||
+                        mask_of((uint32_t)lo) != mask_of((uint32_t)hi)) {
+                        stt = 3;
+                    } else {
+                        v = x & mask_of((uint32_t)hi);
+                        stt = (int64_t)v <= lo ? 1 : ((int64_t)v > hi ? 2 : 3);
+                    }
+                }
+                const uint32_t accb = __ballot_sync(0xffffffffu, stt == 1);
+                const uint32_t ambb = __ballot_sync(0xffffffffu, stt == 3);
+                const int tamb = ambb ? __ffs(ambb) - 1 : 32;
+                const uint32_t before = tamb < 32 ? (accb & ((1u << tamb) - 1u)) : accb;
+                if (stt == 1 && ln < tamb && jout) jout[i - __popc(before & lt)] = (int32_t)v;
+                const int A = __popc(before);
+                if (tamb == 32) {
+                    i -= A;
+                    break;
+                }
+                int64_t is = i - A;
+                const uint32_t xa = __shfl_sync(0xffffffffu, x, tamb);
+                const int64_t pa = pos + 32 * k + tamb;
+                if (pa >= limit || is <= i_stop) {
+                    pos = pa;
+                    i = is;
+                    stop = true;
+                    break;
+                }
+                const uint32_t vv = xa & mask_of((uint32_t)is);
+                if ((int64_t)vv <= is) {
+                    if (ln == 0 && jout) jout[is] = (int32_t)vv;
+                    --is;
+                }
+                i = is;
+                b = tamb + 1;
+                if (i == i_stop) {
+                    pos = pa + 1;
+                    stop = true;
+                    break;
+                }
+            }
+        }
+        if (stop) break;
+        pos += 1024;
+    }
+    return WalkOut{i, tmin<int64_t>(pos, limit), 0};
 }
 
 // Speculative chunks of band [lo_band, hi_band] (mask = 2*lo_band - 1):
@@ -421,23 +504,35 @@ __device__ void stitch_block(FyState* st, const FyChunk* __restrict__ ch, int64_
         int4* dst = reinterpret_cast<int4*>(sm);
         for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x < 32) {  // warp 0: lane e holds flat e; one ballot per chunk
+            const int ln = threadIdx.x;
             int64_t S = s_S;
             int l = 0;
+            // chunk l's fields are loaded before chunk l-1 is resolved
+            int64_t cs = sm[0].s;
+            int cw = sm[0].w, cne = sm[0].ne, ca = sm[0].a;
+            int32_t cf = (ln < kEvMax && ln < cne) ? sm[0].ev[ln] : 0x7fffffff;
             for (; l < cnt; ++l) {
-                const FyChunk& cc = sm[l];
-                const int64_t d = S - cc.s;
-                if (cc.w < 0 || cc.ne < 0 || d < 0 || d > cc.w) {
-                    s_ok = 0;
-                    break;
-                }
-                int nflat = 0;  // D(d) = d - #{flats <= d}: independent loads
-                for (int e = 0; e < cc.ne; ++e) nflat += (cc.ev[e] <= d) ? 1 : 0;
-                starts[c0 + l] = S;
-                S = cc.s - cc.a + (d - nflat);
+                const int nl = l + 1 < cnt ? l + 1 : l;
+                const int64_t ns = sm[nl].s;
+                const int nw = sm[nl].w, nne = sm[nl].ne, na = sm[nl].a;
+                const int32_t nf = (ln < kEvMax && ln < nne) ? sm[nl].ev[ln] : 0x7fffffff;
+                const int64_t d = S - cs;
+                if (cw < 0 || cne < 0 || d < 0 || d > cw) break;
+                const int nflat = __popc(__ballot_sync(0xffffffffu, cf <= d));
+                if (ln == 0) starts[c0 + l] = S;
+                S = cs - ca + (d - nflat);
+                cs = ns;
+                cw = nw;
+                cne = nne;
+                ca = na;
+                cf = nf;
             }
-            s_S = S;
-            s_done += l;
+            if (ln == 0) {
+                if (l < cnt) s_ok = 0;
+                s_S = S;
+                s_done += l;
+            }
         }
     }
     __syncthreads();
@@ -463,8 +558,18 @@ constexpr int kPbThreads = 128;
 __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
     const uint32_t* __restrict__ g, int64_t nbuf, int64_t n, int32_t* __restrict__ jout,
     FyState* st, FyChunk* __restrict__ ch, int64_t* __restrict__ starts, int64_t max_chunks,
-    int kmin, int64_t* consumed, int64_t* status) {
+    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog) {
     cg::grid_group grid = cg::this_grid();
+    int tl = 0;  // optional stage timestamps (globaltimer, ns) written by block 0
+    auto stamp = [&](int tag) {
+        if (tlog && blockIdx.x == 0 && threadIdx.x == 0 && tl < 254) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            tlog[2 * tl] = tag;
+            tlog[2 * tl + 1] = (int64_t)t;
+            ++tl;
+        }
+    };
     __shared__ int32_t evs[kPbThreads / 32][kEvMax];
     __shared__ FyChunk sm[kStitchBatch];
     const int wib = threadIdx.x >> 5;
@@ -481,6 +586,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         st->done = 0;
     }
     grid.sync();
+    stamp(0);
     int top = 0;
     while ((2LL << top) <= n - 1) ++top;
     for (int k = top; k >= kmin; --k) {
@@ -499,9 +605,13 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
             if (nch < 2) continue;
             const int64_t ei = st->i, ep = st->pos;
             for (int64_t c = gw; c < nch; c += nw) chunk_work(g, nbuf, ei, ep, lo_band, T, c, ch, evs[wib]);
+            stamp(100 * k + 10 * e + 1);
             grid.sync();
+            stamp(100 * k + 10 * e + 2);
             if (blockIdx.x == 0) stitch_block(st, ch, nch, T, starts, sm);
+            stamp(100 * k + 10 * e + 3);
             grid.sync();
+            stamp(100 * k + 10 * e + 4);
             const int64_t done = st->done;
             for (int64_t c = gw; c < done; c += nw) {
                 const int64_t p0 = starts[-1] + c * T;
@@ -510,19 +620,26 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
             // the next epoch's chunk stage only reads st and writes ch; the
             // stitch that rewrites `starts` is behind the next grid barrier
         }
+        stamp(100 * k + 5);
         grid.sync();  // exact re-runs may still write j; st is final for the walk
+        stamp(100 * k + 6);
         if (lead_warp) {
-            const WalkOut r = warp_walk(g, st->pos, nbuf, st->i, lo_band - 1, jout, 0, nullptr, 0);
+            const WalkOut r = lo_band < 16384
+                                  ? warp_walk1(g, st->pos, nbuf, st->i, lo_band - 1, jout)
+                                  : warp_walk(g, st->pos, nbuf, st->i, lo_band - 1, jout, 0, nullptr, 0);
             if (threadIdx.x == 0) {
                 if (r.i > lo_band - 1) *status = IDS_ERETRY;
                 st->i = r.i;
                 st->pos = r.pos;
             }
         }
+        stamp(100 * k + 7);
         grid.sync();
     }
+    stamp(9000);
     if (lead_warp) {
-        const WalkOut r = warp_walk(g, st->pos, nbuf, st->i, 0, jout, 0, nullptr, 0);
+        const WalkOut r = st->i < 16384 ? warp_walk1(g, st->pos, nbuf, st->i, 0, jout)
+                                        : warp_walk(g, st->pos, nbuf, st->i, 0, jout, 0, nullptr, 0);
         if (threadIdx.x == 0) {
             if (r.i > 0) *status = IDS_ERETRY;
             st->i = r.i;
@@ -530,6 +647,8 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
             *consumed = r.pos;
         }
     }
+    stamp(9999);
+    if (tlog && blockIdx.x == 0 && threadIdx.x == 0) tlog[2 * tl] = -1;
 }
 
 // ---- parallel application of the Fisher-Yates swaps --------------------------
@@ -603,6 +722,8 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_
         bucket[i] = out;
     }
 }
+
+int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel
 
 struct HashPlan {
     int64_t I, L;
@@ -766,7 +887,9 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
             int64_t* sts = starts + 1;
             int64_t* cons = d + 1;
             int64_t* stat = d + 3;
-            void* args[] = {&dr, &nbuf, &nI, &jarr, &fst, &chunks, &sts, &mc, &kmin, &cons, &stat};
+            int64_t* tlog = g_fy_tlog;
+            void* args[] = {&dr, &nbuf, &nI, &jarr, &fst, &chunks, &sts, &mc, &kmin, &cons, &stat,
+                            &tlog};
             IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fy_phaseb_kernel, dim3(G),
                                                      dim3(kPbThreads), args, 0, st));
             ids_count_launch();
@@ -803,3 +926,7 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
     }
     return IDS_OK;
 }
+
+// Debug hook: record phase-B stage timestamps into `buf` (device int64[512])
+// for the next hash draws; NULL disables.
+extern "C" void ids_debug_phaseb_timing(int64_t* buf) { g_fy_tlog = buf; }
