@@ -200,6 +200,34 @@ int ids_id_coeffs_f64(const double* Rtop, const int32_t* perm, int64_t k, int64_
 int ids_triangular_solve_f64(const double* r, const double* b, int64_t n, int64_t m,
                              int lower, double* x, int64_t* bad_index, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Error metric: the operator passes of est_spectral_norm
+ * through id_residual_operator / matrix_operator (estimators.py:91-121):
+ * `a @ x` and `a.T @ y` on device-resident A.  Deterministic summation order.
+ *
+ * Dense: y = A x (trans = 0; x[cols], y[rows]) or y = A^T x (trans = 1;
+ * x[rows], y[cols]); A rows x cols with leading dimension ld in `layout`.
+ * ------------------------------------------------------------------------- */
+size_t ids_dense_gemv_workspace_bytes(int64_t rows, int64_t cols, int layout, int trans);
+int ids_dense_gemv_f64(const double* A, int64_t rows, int64_t cols, int64_t ld, int layout,
+                       int trans, const double* x, double* y, void* workspace,
+                       size_t ws_bytes, void* stream);
+
+/* CSR y = A x (x[cols], y[rows]).  For A^T x pass the CSR of A^T, built once
+ * by ids_csr_transpose_f64 (estimators.py:99-109 `a_t @ y`). */
+int ids_csr_spmv_f64(const void* indptr, int indptr64, const int32_t* indices,
+                     const double* data, int64_t rows, int64_t cols, int64_t nnz,
+                     const double* x, double* y, void* stream);
+
+/* CSR of A^T (= CSC of A) from the CSR of A: t_indptr int64[cols+1],
+ * t_indices int32[nnz] (row ids, increasing within each column), t_data[nnz]
+ * (linalg.py:39-53 as_csc without the canonicalization checks). */
+size_t ids_csr_transpose_workspace_bytes(int64_t rows, int64_t cols, int64_t nnz);
+int ids_csr_transpose_f64(const void* indptr, int indptr64, const int32_t* indices,
+                          const double* data, int64_t rows, int64_t cols, int64_t nnz,
+                          int64_t* t_indptr, int32_t* t_indices, double* t_data,
+                          void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,8 @@ Contents
   ``oracle/Makefile``): plain-C restatement of the PCG64 / Lemire /
   Fisher-Yates draw sequence behind ``CountSketchOp.__init__``
   (reference ``pkg/src/idsketch/sketch.py:77-84``).
+* ``estimators.py``: the reference's error metric for matrix trials
+  (``estimators.py:26-121``, ``bench.py:116-145``).
 * ``port.py``: numpy/scipy restatement of the reference's sketch + ID path
   (``sketch.py:116-186``, ``linalg.py:76-147``, ``matrix_id.py:56-182``,
   ``cp_tensor.py:215-276``), calling the same third-party kernels the
@@ -22,10 +24,12 @@ real reference package (``tests/golden/make_golden.py``) in
 """
 
 from .cs_hash import countsketch_hash, pcg64_stream32, seed_state
+from .estimators import derive_seed, est_spectral_norm, id_residual_operator, matrix_operator
 from .port import (
     OracleCountSketch,
     OracleTensorSketch,
     coeffs_from_pivoted,
+    cp_gram,
     countsketch_id,
     cp_diff_norm,
     cp_norm,
@@ -41,12 +45,17 @@ __all__ = [
     "OracleCountSketch",
     "OracleTensorSketch",
     "coeffs_from_pivoted",
+    "cp_gram",
     "countsketch_hash",
     "countsketch_id",
     "cp_diff_norm",
     "cp_norm",
     "cpqr",
     "cs_apply",
+    "derive_seed",
+    "est_spectral_norm",
+    "id_residual_operator",
+    "matrix_operator",
     "matrix_id",
     "pcg64_stream32",
     "seed_state",

@@ -13,10 +13,20 @@ from .cp_tensor import (
     CpTensor,
     TensorIdResult,
     check_tensor_id_args,
+    cp_diff_norm,
+    cp_norm,
+    gram_hadamard,
     tensor_id_from_sketch,
     tensorsketch_id,
 )
 from .errors import SingularTriangleError
+from .estimators import (
+    NormEstimate,
+    derive_seed,
+    est_spectral_norm,
+    id_residual_operator,
+    matrix_operator,
+)
 from .linalg import DEFAULT_RANK_TOL, PivotedQr, cpqr, triangular_solve
 from .matrix_id import (
     InterpolativeDecomposition,
@@ -34,6 +44,7 @@ __all__ = [
     "CpTensor",
     "DEFAULT_RANK_TOL",
     "InterpolativeDecomposition",
+    "NormEstimate",
     "PivotedQr",
     "SingularTriangleError",
     "TensorIdResult",
@@ -41,8 +52,15 @@ __all__ = [
     "check_matrix_id_args",
     "check_tensor_id_args",
     "countsketch_id",
+    "cp_diff_norm",
+    "cp_norm",
     "cpqr",
+    "derive_seed",
+    "est_spectral_norm",
+    "gram_hadamard",
+    "id_residual_operator",
     "matrix_id",
+    "matrix_operator",
     "matrix_sketch",
     "tensor_id_from_sketch",
     "tensorsketch_id",

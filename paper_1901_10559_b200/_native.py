@@ -75,6 +75,19 @@ SIGNATURES = {
     "ids_triangular_solve_f64": (
         _c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p]
     ),
+    "ids_dense_gemv_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_int, _c_int]),
+    "ids_dense_gemv_f64": (
+        _c_int,
+        [_c_p, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_p, _c_p, _c_p, _c_sz, _c_p],
+    ),
+    "ids_csr_spmv_f64": (
+        _c_int, [_c_p, _c_int, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p]
+    ),
+    "ids_csr_transpose_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_i64]),
+    "ids_csr_transpose_f64": (
+        _c_int,
+        [_c_p, _c_int, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p],
+    ),
 }
 
 _lib = None

@@ -212,11 +212,53 @@ def tensorsketch_id(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_T
     return _assemble(x, d.to_host("tensorsketch"), "tensorsketch")
 
 
+# ---- error metric for tensor trials --------------------------
+def _gram_device(weights, factor_lists):
+    """diag(w) (hadamard of factor Grams) diag(w) on the device (cp_tensor.py:
+    143-160).  Each entry of factor_lists is the list of column blocks of one
+    mode (concatenated); the Grams are plain cuBLAS DGEMMs."""
+    import torch
+
+    from . import _device
+    from .tensorsketch import factor_to_device
+
+    out = None
+    for blocks in factor_lists:
+        t = torch.cat([factor_to_device(b) for b in blocks], 0)  # (R, I_n)
+        g = t @ t.T
+        out = g if out is None else out.mul_(g)
+    w = _device.to_device(np.asarray(weights, dtype=np.float64), torch.float64)
+    return out.mul_(w[None, :]).mul_(w[:, None])
+
+
+def gram_hadamard(x):
+    """Gram matrix of the flattened weighted rank-1 terms (cp_tensor.py:163-166)."""
+    return _gram_device(x.weights, [[f] for f in x.factors]).cpu().numpy()
+
+
+def cp_norm(x):
+    """Exact Frobenius norm of a CP tensor via the Gram identity (cp_tensor.py:169-172)."""
+    total = float(_gram_device(x.weights, [[f] for f in x.factors]).sum())
+    return float(np.sqrt(max(total, 0.0)))
+
+
+def cp_diff_norm(x, y):
+    """Exact Frobenius norm of x - y for CP tensors (cp_tensor.py:183-197)."""
+    if tuple(x.mode_dims) != tuple(y.mode_dims):
+        raise ValueError(f"mode dimensions disagree: {x.mode_dims} vs {y.mode_dims}")
+    weights = np.concatenate([x.weights, -np.asarray(y.weights)])
+    total = float(_gram_device(weights, [[a, b] for a, b in zip(x.factors, y.factors)]).sum())
+    return float(np.sqrt(max(total, 0.0)))
+
+
 __all__ = [
     "CpTensor",
     "TENSOR_METHODS",
     "TensorIdResult",
     "check_tensor_id_args",
+    "cp_diff_norm",
+    "cp_norm",
+    "gram_hadamard",
     "tensor_id_from_sketch",
     "tensorsketch_device",
     "tensorsketch_id",

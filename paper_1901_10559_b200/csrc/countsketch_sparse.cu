@@ -215,6 +215,37 @@ static size_t csr_transpose_ws(int64_t cols, int64_t nnz, int64_t out_dim) {
     return c.off + 256;
 }
 
+// CSR -> CSC on the device: stable radix sort of the entries by column (row
+// order kept inside each column), then gather rows/values and column starts.
+static int build_csc(const void* indptr, int indptr64, const int32_t* indices, const double* data,
+                     int64_t rows, int64_t cols, int64_t nnz, int32_t* row_of, int32_t* iota,
+                     int32_t* keys, int32_t* perm, void* tmp, size_t sb, int32_t* crow,
+                     double* cval, int64_t* colptr, cudaStream_t st) {
+    if (nnz > 0) {
+        const unsigned g = (unsigned)tmin<int64_t>(ceil_div(rows, 256), 148 * 16);
+        if (indptr64)
+            row_of_entry_kernel<<<g, 256, 0, st>>>(static_cast<const int64_t*>(indptr), rows,
+                                                   row_of, iota);
+        else
+            row_of_entry_kernel<<<g, 256, 0, st>>>(static_cast<const int32_t*>(indptr), rows,
+                                                   row_of, iota);
+        IDS_LAUNCH_CHECK();
+        size_t b = sb;
+        IDS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(
+            tmp, b, reinterpret_cast<const uint32_t*>(indices), reinterpret_cast<uint32_t*>(keys),
+            iota, perm, (int)nnz, 0, key_bits(cols), st));
+        const unsigned g2 = (unsigned)tmin<int64_t>(ceil_div(nnz, 256), 148 * 16);
+        gather_csc_kernel<<<g2, 256, 0, st>>>(perm, row_of, data, nnz, crow, cval);
+        IDS_LAUNCH_CHECK();
+        colptr_kernel<<<(unsigned)tmin<int64_t>(ceil_div(cols + 1, 256), 1024), 256, 0, st>>>(
+            keys, nnz, cols, colptr);
+        IDS_LAUNCH_CHECK();
+    } else {
+        IDS_CUDA_TRY(cudaMemsetAsync(colptr, 0, sizeof(int64_t) * (cols + 1), st));
+    }
+    return IDS_OK;
+}
+
 static int csr_transpose_path(const void* indptr, int indptr64, const int32_t* indices,
                               const double* data, int64_t rows, int64_t cols, int64_t nnz,
                               int64_t row0, int64_t in_dim, const int32_t* bucket,
@@ -241,27 +272,10 @@ static int csr_transpose_path(const void* indptr, int indptr64, const int32_t* i
         ids_set_last_error("csr countsketch: workspace too small");
         return IDS_EWORKSPACE;
     }
-    if (nnz > 0) {
-        const unsigned g = (unsigned)tmin<int64_t>(ceil_div(rows, 256), 148 * 16);
-        if (indptr64)
-            row_of_entry_kernel<<<g, 256, 0, st>>>(static_cast<const int64_t*>(indptr), rows,
-                                                   row_of, iota);
-        else
-            row_of_entry_kernel<<<g, 256, 0, st>>>(static_cast<const int32_t*>(indptr), rows,
-                                                   row_of, iota);
-        IDS_LAUNCH_CHECK();
-        size_t b = sb;
-        IDS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(
-            tmp, b, reinterpret_cast<const uint32_t*>(indices), reinterpret_cast<uint32_t*>(keys),
-            iota, perm, (int)nnz, 0, key_bits(cols), st));
-        const unsigned g2 = (unsigned)tmin<int64_t>(ceil_div(nnz, 256), 148 * 16);
-        gather_csc_kernel<<<g2, 256, 0, st>>>(perm, row_of, data, nnz, crow, cval);
-        IDS_LAUNCH_CHECK();
-        colptr_kernel<<<(unsigned)tmin<int64_t>(ceil_div(cols + 1, 256), 1024), 256, 0, st>>>(
-            keys, nnz, cols, colptr);
-        IDS_LAUNCH_CHECK();
-    } else {
-        IDS_CUDA_TRY(cudaMemsetAsync(colptr, 0, sizeof(int64_t) * (cols + 1), st));
+    {
+        const int rc = build_csc(indptr, indptr64, indices, data, rows, cols, nnz, row_of, iota, keys,
+                                 perm, tmp, sb, crow, cval, colptr, st);
+        if (rc != IDS_OK) return rc;
     }
     int rc = launch_csc(colptr, crow, cval, cols, row0, bucket, sign, out_dim, Y, accumulate,
                         gacc, st);
@@ -524,4 +538,36 @@ extern "C" int ids_values_has_nonfinite(const double* v, int64_t n, int32_t* fla
     nonfinite_values_kernel<<<g, 256, 0, as_stream(stream)>>>(v, n, flag);
     IDS_LAUNCH_CHECK();
     return IDS_OK;
+}
+
+// ---- public transpose (CSR of A^T, i.e. CSC of A) ---------------------------
+extern "C" size_t ids_csr_transpose_workspace_bytes(int64_t rows, int64_t cols, int64_t nnz) {
+    (void)rows;
+    WsCount c;
+    for (int i = 0; i < 4; ++i) c.take<int32_t>(nnz);
+    c.take<char>(sort_bytes(nnz, cols));
+    return c.off + 256;
+}
+
+extern "C" int ids_csr_transpose_f64(const void* indptr, int indptr64, const int32_t* indices,
+                                     const double* data, int64_t rows, int64_t cols, int64_t nnz,
+                                     int64_t* t_indptr, int32_t* t_indices, double* t_data,
+                                     void* workspace, size_t ws_bytes, void* stream) {
+    if (rows < 0 || cols < 1 || nnz < 0 || nnz > 0x7fffffffLL) {
+        ids_set_last_error("csr transpose: bad arguments");
+        return IDS_EINVAL;
+    }
+    WsCarve ws(workspace, ws_bytes);
+    int32_t* row_of = ws.take<int32_t>(nnz);
+    int32_t* iota = ws.take<int32_t>(nnz);
+    int32_t* keys = ws.take<int32_t>(nnz);
+    int32_t* perm = ws.take<int32_t>(nnz);
+    const size_t sb = sort_bytes(nnz, cols);
+    void* tmp = ws.take<char>(sb);
+    if (!ws.ok()) {
+        ids_set_last_error("csr transpose: workspace too small");
+        return IDS_EWORKSPACE;
+    }
+    return build_csc(indptr, indptr64, indices, data, rows, cols, nnz, row_of, iota, keys, perm,
+                     tmp, sb, t_indices, t_data, t_indptr, as_stream(stream));
 }

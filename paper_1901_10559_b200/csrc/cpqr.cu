@@ -33,6 +33,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kSeg = 512;                // GEMV unit: rows per (column, segment)
+constexpr int kSegLoads = kSeg / 32;     // loads per lane per unit
 
 struct ArgMax {
     double val;
@@ -64,6 +66,7 @@ struct CpqrArgs {
     const double* Y;
     int64_t m, n, ldy, k;
     int small;  // m small: pivot column and z computed redundantly by every CTA
+    int vsmem;  // Householder vector kept in shared memory (else read from a)
     double rank_tol;
     int32_t* perm;
     double* Rtop;
@@ -73,7 +76,14 @@ struct CpqrArgs {
     int64_t* pos;
     int64_t* flag_list;
     ArgMax* amax;
+    int64_t* tlog;  // debug: per-phase ns accumulated by CTA 0 (NULL: off)
 };
+
+__device__ __forceinline__ int64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (int64_t)t;
+}
 
 // Warp 0 reduces the G per-CTA argmax partials (lane-parallel loads, then a
 // shuffle tree); every CTA runs the same code, so all agree on the pivot.
@@ -135,12 +145,19 @@ __device__ __forceinline__ double sub_dot(double y, const double* __restrict__ a
 __device__ __forceinline__ double lane_dot(const double* __restrict__ a, const double* __restrict__ b,
                                            int64_t r0, int64_t m) {
     double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int64_t r = r0 + (threadIdx.x & 31);
-    for (; r + 224 < m; r += 256) {  // eight loads in flight per lane
+    // eight loads in flight per lane; the last batch is clamped and zero-weighted
+    for (int64_t r = r0 + (threadIdx.x & 31); r < m; r += 256) {
+        double x[8], y[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) s[u] = fma(a[r + 32 * u], b[r + 32 * u], s[u]);
+        for (int u = 0; u < 8; ++u) {
+            const int64_t rr = r + 32 * u;
+            const int64_t rc = rr < m ? rr : m - 1;
+            x[u] = a[rc];
+            y[u] = rr < m ? b[rc] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] = fma(x[u], y[u], s[u]);
     }
-    for (; r < m; r += 32) s[0] = fma(a[r], b[r], s[0]);
     return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
@@ -159,7 +176,8 @@ __device__ double block_sum(double v, double* red) {
 __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double vsm[];  // v (m), z (k), V[kk, :kk] (k)
-    double* zsh = vsm + g.m;
+    const int64_t mpad = (g.m + kSeg - 1) / kSeg * kSeg;  // v padded with zeros
+    double* zsh = vsm + (g.vsmem ? mpad : 0);
     double* vrow = zsh + g.k;
     __shared__ int s_nflag;
     __shared__ double s_red0;
@@ -221,7 +239,9 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         __syncthreads();
     };
 
-    // ---- prologue: column norms (dnrm2), positions ----
+    // ---- prologue: column norms (dnrm2), positions; zero padding of a ----
+    if (b == 0)
+        for (int64_t r = m + threadIdx.x; r < mpad; r += kThreads) g.a[r] = 0.0;
     for (int64_t j = c0 + wid; j < c1; j += kWarps) {
         const double* y = g.Y + j * ldy;
         const double s = warp_sum(lane_dot(y, y, 0, m));
@@ -235,6 +255,15 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
     local_argmax(0, 0);
     grid.sync();
 
+    const bool tl = g.tlog && b == 0 && threadIdx.x == 0;
+    int64_t tprev = tl ? gtimer() : 0;
+    auto stamp = [&](int phase) {
+        if (tl) {
+            const int64_t t = gtimer();
+            g.tlog[phase] += t - tprev;
+            tprev = t;
+        }
+    };
     for (int64_t kk = 0; kk < k; ++kk) {
         // ---- S1: global pivot, position swap, distributed pivot column ----
         if (wid == 0) {
@@ -274,14 +303,20 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         } else {
             const double* ycol = g.Y + cs * ldy;
             double ss = 0.0;
-            for (int64_t r = tmax(r0, kk) + threadIdx.x; r < r1; r += kThreads) {
+            for (int64_t r = r0 + threadIdx.x; r < r1; r += kThreads) {
+                if (r < kk) {
+                    g.a[r] = 0.0;  // rows above kk read as v = 0 by the GEMV
+                    continue;
+                }
                 const double v = sub_dot(ycol[r], g.V + r, m, g.F + cs, n, kk);
                 g.a[r] = v;
                 if (r > kk) ss = fma(v, v, ss);
             }
             ss = block_sum(ss, red);
             if (threadIdx.x == 0) g.normpart[b] = ss;
+            stamp(0);
             grid.sync();
+            stamp(1);
             if (wid == 0) {
                 const double xs = warp_sum_partials(g.normpart, G, 1);
                 if (lane == 0) s_red0 = xs;
@@ -302,12 +337,36 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             tau = (beta - alpha) / beta;
             scal = 1.0 / (alpha - beta);
         }
-        for (int64_t r = kk + threadIdx.x; r < m; r += kThreads)
-            vsm[r] = (r == kk) ? 1.0 : (g.small ? vsm[r] : g.a[r]) * scal;
-        __syncthreads();
+        // v: in shared memory (vsm), or for very tall sketches read on the fly
+        // as a[r] * scal from the distributed pivot column (identical values)
+        const bool vs = g.vsmem;
+        auto vval = [&](int64_t r) -> double {
+            return vs ? vsm[r] : (r == kk ? 1.0 : g.a[r] * scal);
+        };
+        if (vs) {  // v with zeros above row kk and in the padding
+            if (g.small) {
+                for (int64_t r = threadIdx.x; r < mpad; r += kThreads)
+                    vsm[r] = (r < kk || r >= m) ? 0.0 : (r == kk) ? 1.0 : vsm[r] * scal;
+            } else {
+                // a[] already holds zeros above kk and in the padding; eight
+                // independent loads per thread per pass (mpad is a multiple of 512)
+                for (int64_t r0v = 8 * threadIdx.x - threadIdx.x % 8 * 7; r0v < mpad;
+                     r0v += 8 * kThreads) {
+                    double t[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) t[u] = g.a[r0v + 8 * u];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t r = r0v + 8 * u;
+                        vsm[r] = (r == kk) ? 1.0 : t[u] * scal;
+                    }
+                }
+            }
+            __syncthreads();
+        }
         if (b == 0) {
             for (int64_t r = threadIdx.x; r < m; r += kThreads)
-                g.V[kk * m + r] = r < kk ? 0.0 : vsm[r];
+                g.V[kk * m + r] = r < kk ? 0.0 : vval(r);
             if (threadIdx.x == 0) {
                 g.tau[kk] = tau;
                 g.beta[kk] = beta;
@@ -322,21 +381,56 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             } else {
                 double s = 0.0;
                 for (int64_t r = tmax(r0, kk) + lane; r < r1; r += 32)
-                    s = fma(g.V[q * m + r], vsm[r], s);
+                    s = fma(g.V[q * m + r], vval(r), s);
                 s = warp_sum(s);
                 if (lane == 0) g.zpart[b * k + q] = s;
             }
         }
-        // GEMV over owned remaining columns: W_j = Y[kk:, j]^T v.  Odd steps walk
-        // the columns backwards so the tail read last (still in L2) comes first.
-        for (int64_t jw = wid; jw < c1 - c0; jw += kWarps) {
-            const int64_t j = (kk & 1) ? c1 - 1 - jw : c0 + jw;
-            if (g.pos[j] <= kk) continue;
-            const double s = warp_sum(lane_dot(g.Y + j * ldy, vsm, kk, m));
-            if (lane == 0) g.W[j] = s;
+        // GEMV W_j = Y[kk:, j]^T v in units of (column j, kSeg-row segment s),
+        // two units per warp at a time (2 x 16 independent loads per lane);
+        // partial dots go to W[s * n + j] and are summed in fixed order in S3.
+        // Small sketches: this CTA's columns and warps; tall: the whole grid.
+        {
+            const int64_t nseg = (m + kSeg - 1) / kSeg, s0 = kk / kSeg, ns = nseg - s0;
+            const int64_t cA = g.small ? c0 : 0, cB = g.small ? c1 : n;
+            const int64_t U = (cB - cA) * ns;
+            const int64_t wi = g.small ? wid : b * kWarps + wid;
+            const int64_t WN = g.small ? kWarps : G * kWarps;
+            for (int64_t u = wi; u < U; u += 2 * WN) {
+                double y1[kSegLoads], y2[kSegLoads];
+                const int64_t j1 = cA + u / ns, sg1 = s0 + u % ns;
+                const int64_t u2 = u + WN;
+                const bool h2 = u2 < U;
+                const int64_t j2 = h2 ? cA + u2 / ns : j1, sg2 = h2 ? s0 + u2 % ns : sg1;
+                const bool a1 = g.pos[j1] > kk, a2 = h2 && g.pos[j2] > kk;
+                const double* p1 = g.Y + j1 * ldy;
+                const double* p2 = g.Y + j2 * ldy;
+                // branch-free: clamped rows (v is zero there and above kk)
+                const int64_t b1 = sg1 * kSeg + lane, b2 = sg2 * kSeg + lane;
+#pragma unroll
+                for (int t = 0; t < kSegLoads; ++t) {
+                    y1[t] = p1[tmin(b1 + 32 * t, m - 1)];
+                    y2[t] = p2[tmin(b2 + 32 * t, m - 1)];
+                }
+                double s1 = 0.0, s2 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll
+                for (int t = 0; t < kSegLoads; t += 2) {
+                    s1 = fma(y1[t], vval(b1 + 32 * t), s1);
+                    t1 = fma(y1[t + 1], vval(b1 + 32 * t + 32), t1);
+                    s2 = fma(y2[t], vval(b2 + 32 * t), s2);
+                    t2 = fma(y2[t + 1], vval(b2 + 32 * t + 32), t2);
+                }
+                const double w1 = warp_sum(s1 + t1), w2 = warp_sum(s2 + t2);
+                if (lane == 0) {
+                    if (a1) g.W[sg1 * n + j1] = w1;
+                    if (a2) g.W[sg2 * n + j2] = w2;
+                }
+            }
         }
+        stamp(2);
         if (g.small) __syncthreads();
         else grid.sync();
+        stamp(3);
 
         // ---- S3: F column, row kk of R, norm downdate, next argmax ----
         // z = V[:, :kk]^T v (fixed-order sum of the per-CTA partials) and row kk of V
@@ -352,7 +446,20 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         // one thread per owned remaining column (F is q-major: coalesced)
         for (int64_t j = c0 + threadIdx.x; j < c1; j += kThreads) {
             if (g.pos[j] <= kk) continue;
-            double f = sub_dot(g.W[j], g.F + j, n, zsh, 1, kk);
+            double wj = 0.0;  // fixed-order sum of the segment partials
+            {
+                const int64_t nseg = mpad / kSeg;
+                int64_t sg = kk / kSeg;
+                for (; sg + 8 <= nseg; sg += 8) {
+                    double t[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) t[u] = g.W[(sg + u) * n + j];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) wj += t[u];
+                }
+                for (; sg < nseg; ++sg) wj += g.W[sg * n + j];
+            }
+            double f = sub_dot(wj, g.F + j, n, zsh, 1, kk);
             double rk = sub_dot(g.Y[j * ldy + kk], g.F + j, n, vrow, 1, kk);
             f *= tau;
             g.F[kk * n + j] = f;
@@ -369,15 +476,17 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             }
         }
         __syncthreads();
+        stamp(4);
         // exact norms of the flagged columns below row kk (LAPACK's recompute)
         const int nflag = s_nflag;
+        if (g.tlog && threadIdx.x == 0) atomicAdd((unsigned long long*)&g.tlog[15], (unsigned long long)nflag);
         for (int fi = wid; fi < nflag; fi += kWarps) {
             const int64_t j = flagged[fi];
             const double* y = g.Y + j * ldy;
             double s = 0.0;
             for (int64_t r = kk + 1 + lane; r < m; r += 32) {
                 double v = sub_dot(y[r], g.V + r, m, g.F + j, n, kk);
-                v = fma(-vsm[r], g.F[kk * n + j], v);
+                v = fma(-vval(r), g.F[kk * n + j], v);
                 s = fma(v, v, s);
             }
             s = warp_sum(s);
@@ -387,8 +496,11 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             }
         }
         __syncthreads();
+        stamp(5);
         local_argmax(kk + 1, kk + 1);
+        stamp(6);
         grid.sync();
+        stamp(7);
     }
 
     // ---- outputs: perm, Rtop, numerical rank ----
@@ -807,11 +919,11 @@ void carve_cpqr(W& ws, int64_t m, int64_t n, int64_t k, int64_t G, CpqrArgs& a) 
     a.vn2 = ws.template take<double>(n);
     a.F = ws.template take<double>(n * k);
     a.Rcol = ws.template take<double>(n * k);
-    a.W = ws.template take<double>(n);
+    a.W = ws.template take<double>(n * ceil_div(m, (int64_t)kSeg));
     a.V = ws.template take<double>(m * k);
     a.tau = ws.template take<double>(k);
     a.beta = ws.template take<double>(k);
-    a.a = ws.template take<double>(m);
+    a.a = ws.template take<double>(ceil_div(m, (int64_t)kSeg) * kSeg);
     a.normpart = ws.template take<double>(G);
     a.zpart = ws.template take<double>(G * k);
     a.pos = ws.template take<int64_t>(n);
@@ -835,14 +947,22 @@ int grid_size(int64_t m, int64_t n, size_t smem) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_kernel, kThreads, smem);
     if (per_sm < 1) per_sm = 1;
     // about one warp per owned column; tiny problems use few CTAs (cheap barriers)
-    const int64_t want = tmax<int64_t>(1, tmin<int64_t>(ceil_div(n, kWarps), (int64_t)sms));
+    // (tall sketches: the whole GPU, the GEMV units are spread over every warp)
+    const int64_t want = m > 1024 ? (int64_t)sms
+                                  : tmax<int64_t>(1, tmin<int64_t>(ceil_div(n, kWarps), (int64_t)sms));
     const int64_t by_size = tmax<int64_t>(1, ceil_div(m * n, 2048));
     return (int)tmin<int64_t>((int64_t)sms * per_sm, tmin(want, by_size));
 }
 
 constexpr int64_t kMaxG = 148;
 
+int64_t* g_cpqr_tlog = nullptr;  // debug: per-phase timing of the cooperative kernel
+
 }  // namespace
+
+// Debug hook: accumulate per-phase ns of cpqr_kernel into `buf` (device
+// int64[16], [15] = flagged-column count); NULL disables.
+extern "C" void ids_debug_cpqr_timing(int64_t* buf) { g_cpqr_tlog = buf; }
 
 extern "C" size_t ids_cpqr_workspace_bytes(int64_t rows, int64_t cols, int64_t k) {
     CountCarve c;
@@ -914,9 +1034,12 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
             return IDS_OK;
         }
     }
-    const size_t smem = (size_t)(rows + 2 * k) * sizeof(double);
+    // v lives in shared memory unless the sketch is very tall
+    const int64_t mpad = ceil_div(rows, (int64_t)kSeg) * kSeg;
+    const bool vsmem = (size_t)(mpad + 2 * k) * sizeof(double) <= 160 * 1024;
+    const size_t smem = (size_t)((vsmem ? mpad : 0) + 2 * k) * sizeof(double);
     if (smem > 200 * 1024) {
-        ids_set_last_error("cpqr: sketch too tall for the shared-memory Householder vector");
+        ids_set_last_error("cpqr: rank too large for the shared-memory z buffer");
         return IDS_EINVAL;
     }
     if (smem > 48 * 1024)
@@ -931,9 +1054,11 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
     a.k = k;
     a.rank_tol = rank_tol;
     a.small = rows <= 1024 ? 1 : 0;
+    a.vsmem = vsmem ? 1 : 0;
     a.perm = perm;
     a.Rtop = Rtop;
     a.numerical_rank = numerical_rank;
+    a.tlog = g_cpqr_tlog;
     WsCarve ws(workspace, ws_bytes);
     carve_cpqr(ws, rows, cols, k, kMaxG, a);
     if (!ws.ok()) {

@@ -47,7 +47,14 @@ struct TsArgs {
     const double2* tw;    // tw[m] = exp(-2 pi i m / M), m < M
     double2* spec_glob;   // per-CTA running spectrum (N2 + 1 bins) when not in smem
     int spec_in_smem;
+    int64_t* tlog;        // debug: per-phase ns accumulated by CTA 0 (NULL: off)
 };
+
+__device__ __forceinline__ int64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return (int64_t)t;
+}
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
 
@@ -222,6 +229,15 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     double* st_val = reinterpret_cast<double*>(buf + (N2 + N2 / 8 + 1) +
                                                (g.spec_in_smem ? (N2 + 1) : 0));
     int32_t* st_key = reinterpret_cast<int32_t*>(st_val + kStage);
+    const bool tl = g.tlog && blockIdx.x == 0 && t == 0;
+    int64_t tprev = tl ? gtimer() : 0;
+    auto stamp = [&](int phase) {
+        if (tl) {
+            const int64_t tn = gtimer();
+            g.tlog[phase] += tn - tprev;
+            tprev = tn;
+        }
+    };
     for (int64_t r = blockIdx.x; r < g.ncols; r += gridDim.x) {
         // passes 0..N-1: forward transform of mode n's CountSketch, product into S;
         // pass N: inverse transform of S (one inlined FFT for all passes)
@@ -235,6 +251,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 const int32_t* key = s_key[n];
                 const int In = s_dim[n];
                 for (int l = t; l < M; l += T) dbuf[2 * pad(l >> 1) + (l & 1)] = 0.0;
+                stamp(0);
                 // stage kStage sorted entries at a time: bucket + signed value,
                 // all loads independent (coalesced index reads, column gather)
                 for (int c0 = 0; c0 < In; c0 += kStage) {
@@ -263,6 +280,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                         }
                     }
                     __syncthreads();
+                    stamp(1);
                     // run heads sum their bucket's rows in increasing row order
                     for (int q = t; q < cn; q += T) {
                         const int32_t bkt = st_key[q];
@@ -282,6 +300,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                         dbuf[2 * pad(bkt >> 1) + (bkt & 1)] = acc;
                     }
                     __syncthreads();
+                    stamp(2);
                 }
             } else {
                 // ---- inverse: pack conj(Z) from S, forward FFT, conj ----
@@ -300,7 +319,9 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 }
             }
             __syncthreads();
+            stamp(3);
             fft_forward<EPT>(buf, N2, M, tw);
+            stamp(4);
             if (n < g.n_modes) {
                 // ---- untangle the real spectrum, multiply into S ----
                 for (int p = t; p < npairs; p += T) {
@@ -321,6 +342,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                     }
                 }
                 __syncthreads();
+                stamp(5);
             }
         }
         // y[2m] = Re z[m], y[2m+1] = Im z[m], z = conj(FFT(conj Z)) / N2
@@ -352,8 +374,11 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
             if ((t & 31) == 0) atomicAdd(g.colnorm2 + r, nrm);
         }
         __syncthreads();
+        stamp(6);
     }
 }
+
+int64_t* g_ts_tlog = nullptr;  // debug: per-phase timing of tensorsketch_kernel
 
 struct TsPlan {
     int64_t M, N2;
@@ -390,6 +415,10 @@ TsPlan plan_ts(int n_modes, int64_t L) {
 }
 
 }  // namespace
+
+// Debug hook: accumulate per-phase ns of tensorsketch_kernel (CTA 0) into
+// `buf` (device int64[8]); NULL disables.
+extern "C" void ids_debug_ts_timing(int64_t* buf) { g_ts_tlog = buf; }
 
 extern "C" size_t ids_tensorsketch_workspace_bytes(int n_modes, const int64_t* dims,
                                                    int64_t ncols, int64_t out_dim) {
@@ -451,6 +480,7 @@ extern "C" int ids_tensorsketch_f64(int n_modes, const double* const* factors, c
     a.tw = tw;
     a.spec_glob = specg;
     a.spec_in_smem = p.spec_in_smem;
+    a.tlog = g_ts_tlog;
     if (colnorm2) IDS_CUDA_TRY(cudaMemsetAsync(colnorm2, 0, sizeof(double) * ncols, st));
     auto kern = p.ept == 16 ? tensorsketch_kernel<16> : tensorsketch_kernel<8>;
     if (p.smem > 48 * 1024)

@@ -25,7 +25,10 @@ import scipy.sparse as sp
 REF = "/root/reference/pkg/src"
 sys.path.insert(0, REF)
 
-from idsketch.cp_tensor import CpTensor, tensorsketch_id  # noqa: E402
+from idsketch.bench import derive_seed  # noqa: E402
+from idsketch.cp_tensor import CpTensor, cp_diff_norm, cp_norm, tensorsketch_id  # noqa: E402
+from idsketch.estimators import (  # noqa: E402
+    est_spectral_norm, id_residual_operator, matrix_operator)
 from idsketch.matrix_id import countsketch_id, matrix_id, matrix_sketch  # noqa: E402
 from idsketch.sketch import CountSketchOp, TensorSketchOp  # noqa: E402
 
@@ -58,6 +61,7 @@ def main():
         "matrix_id": [],
         "countsketch_id": [],
         "tensorsketch_id": [],
+        "error_estimates": [],
     }
 
     # ---- hash: full arrays for small cases -------------------------------
@@ -178,6 +182,13 @@ def main():
             {"seed": seed, "rank": 10, "sketch_dim": 40,
              "numerical_rank": int(d.numerical_rank)}
         )
+        # the reference's own error metric for a matrix trial (bench.py:137-145)
+        ap, adj = id_residual_operator(a_c1, d)
+        est = est_spectral_norm(ap, adj, cols=a_c1.shape[1], iters=10, probes=2,
+                                seed=derive_seed(seed, 0xE57))
+        manifest["error_estimates"].append(
+            {"case": "csid", "seed": seed, "est_seed": derive_seed(seed, 0xE57),
+             "value": est.value})
     a_sp = sp.random_array((3000, 120), density=0.02, rng=np.random.default_rng(3),
                            format="csr")
     arrays["csid_sp_indptr"] = a_sp.indptr.astype(np.int64)
@@ -186,6 +197,14 @@ def main():
     d = countsketch_id(a_sp, 12, 50, seed=21)
     arrays["csid_sp_cols"] = d.cols
     arrays["csid_sp_coeffs"] = d.coeffs
+    ap, adj = id_residual_operator(a_sp, d)
+    est = est_spectral_norm(ap, adj, cols=a_sp.shape[1], seed=derive_seed(21, 0xE57))
+    manifest["error_estimates"].append(
+        {"case": "csid_sp", "seed": 21, "est_seed": derive_seed(21, 0xE57), "value": est.value})
+    ap, adj = matrix_operator(a_c1)
+    est = est_spectral_norm(ap, adj, cols=a_c1.shape[1], iters=5, probes=3, seed=7)
+    manifest["error_estimates"].append(
+        {"case": "matrix_operator", "iters": 5, "probes": 3, "est_seed": 7, "value": est.value})
 
     # ---- tensorsketch_id (C4-shaped construction, reduced size) ------------
     trng = np.random.default_rng(4)
@@ -211,7 +230,8 @@ def main():
     arrays["tsid_new_weights"] = res.new_weights
     manifest["tensorsketch_id"].append(
         {"dims": list(dims), "terms": R, "rank": k, "sketch_dim": L, "seed": 11,
-         "numerical_rank": int(res.numerical_rank)}
+         "numerical_rank": int(res.numerical_rank),
+         "cp_diff_norm": cp_diff_norm(x, res.reduced), "cp_norm": cp_norm(x)}
     )
 
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)

@@ -151,3 +151,35 @@ def test_tensorsketch_id_golden(golden):
     assert np.array_equal(d.cols, data["tsid_cols"])
     assert np.array_equal(d.coeffs, data["tsid_coeffs"])
     assert np.array_equal(nw, data["tsid_new_weights"])
+
+
+def test_error_estimates_golden(golden):
+    """The reference's error metric (estimators.py, bench.py:137-145) restated."""
+    data, man = golden
+    a = data["csid_a"]
+    a_sp = sp.csr_array(
+        (data["csid_sp_data"], data["csid_sp_indices"], data["csid_sp_indptr"]),
+        shape=(3000, 120),
+    )
+    for case in man["error_estimates"]:
+        if case["case"] == "csid":
+            s = case["seed"]
+            assert oracle.derive_seed(s, 0xE57) == case["est_seed"]
+            ap, adj = oracle.id_residual_operator(a, data[f"csid{s}_cols"], data[f"csid{s}_coeffs"])
+            v = oracle.est_spectral_norm(ap, adj, a.shape[1], seed=case["est_seed"])
+        elif case["case"] == "csid_sp":
+            assert oracle.derive_seed(21, 0xE57) == case["est_seed"]
+            ap, adj = oracle.id_residual_operator(a_sp, data["csid_sp_cols"], data["csid_sp_coeffs"])
+            v = oracle.est_spectral_norm(ap, adj, a_sp.shape[1], seed=case["est_seed"])
+        else:
+            ap, adj = oracle.matrix_operator(a)
+            v = oracle.est_spectral_norm(ap, adj, a.shape[1], iters=case["iters"],
+                                         probes=case["probes"], seed=case["est_seed"])
+        assert v == case["value"], case
+    tcase = man["tensorsketch_id"][0]
+    factors = [data[f"tsid_f{m}"] for m in range(len(tcase["dims"]))]
+    w = data["tsid_w"]
+    cols = data["tsid_cols"]
+    err = oracle.cp_diff_norm(w, factors, data["tsid_new_weights"], [f[:, cols] for f in factors])
+    assert abs(err - tcase["cp_diff_norm"]) <= 1e-12 * tcase["cp_norm"]
+    assert abs(oracle.cp_norm(w, factors) - tcase["cp_norm"]) <= 1e-12 * tcase["cp_norm"]

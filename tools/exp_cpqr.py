@@ -1,0 +1,47 @@
+"""Per-phase timing of the cooperative CPQR kernel on C4/C5-shaped sketches
+(debug hook ids_debug_cpqr_timing).  Usage: python tools/exp_cpqr.py"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1901_10559_b200 as ids
+from paper_1901_10559_b200 import _native
+from paper_1901_10559_b200.linalg import device_cpqr
+
+lib = _native.load()
+lib.ids_debug_cpqr_timing.argtypes = [ctypes.c_void_p]
+NAMES = ["pivot col", "sync norm", "hh+z+gemv", "sync gemv", "F/R/downdate",
+         "recompute", "argmax", "sync step"]
+
+
+def near_dup(m, n, base, pert, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    b = torch.randn(m, base, generator=g, device="cuda", dtype=torch.float64)
+    idx = torch.randint(0, base, (n,), generator=g, device="cuda")
+    idx[:base] = torch.arange(base, device="cuda")
+    y = b[:, idx] + pert * torch.randn(m, n, generator=g, device="cuda", dtype=torch.float64)
+    return y.t().contiguous()  # (n, m) == col-major m x n
+
+
+for name, m, n, k, base, pert in (("C4", 4096, 1000, 10, 10, 1e-3),
+                                  ("C5", 16384, 2000, 20, 20, 1e-4),
+                                  ("C3", 200, 10000, 20, 20, 1e-2)):
+    y = near_dup(m, n, base, pert, 1)
+    for _ in range(3):
+        device_cpqr(y, m, n, k)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        device_cpqr(y, m, n, k)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    buf = torch.zeros(16, dtype=torch.int64, device="cuda")
+    lib.ids_debug_cpqr_timing(buf.data_ptr())
+    device_cpqr(y, m, n, k)
+    torch.cuda.synchronize()
+    lib.ids_debug_cpqr_timing(None)
+    t = buf.cpu().numpy()
+    print(f"{name}: {m}x{n} k={k}: {ms * 1e3:.1f} us per call; flagged {t[15]}")
+    for i, nm in enumerate(NAMES):
+        print(f"   {nm:14s} {t[i] / 1e3:9.1f} us  ({t[i] / 1e3 / k:6.2f}/step)")
