@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kMaxModes = 8;
 constexpr int kMaxHalf = 8192;  // largest half-length transform kept in shared memory
-constexpr int kStage = 2048;    // sorted CountSketch entries staged per round
+constexpr int kStageExt = 64;   // look-ahead entries staged past a stage's last head
 
 struct TsArgs {
     int n_modes;
@@ -47,6 +47,7 @@ struct TsArgs {
     const double2* tw;    // tw[m] = exp(-2 pi i m / M), m < M
     double2* spec_glob;   // per-CTA running spectrum (N2 + 1 bins) when not in smem
     int spec_in_smem;
+    int stage_cap;        // staged CountSketch entries (shared memory) per round
     int64_t* tlog;        // debug: per-phase ns accumulated by CTA 0 (NULL: off)
 };
 
@@ -56,7 +57,10 @@ __device__ __forceinline__ int64_t gtimer() {
     return (int64_t)t;
 }
 
-__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
+// Shared-memory index padding against bank conflicts: one extra slot every
+// 2^PS complex entries (PS = 3 for radix-8 passes, 4 for radix-16 passes).
+template <int PS>
+__device__ __forceinline__ int pad(int i) { return i + (i >> PS); }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -110,6 +114,41 @@ __device__ __forceinline__ void dft<8>(double2* x) {
     x[7] = csub(b6, b7);
 }
 
+// 16-point DFT in registers: 4 x DFT4, internal twiddles W16^(n2 k1), 4 x DFT4.
+__device__ __forceinline__ void dft16(double2* x) {
+    const double c = 0.92387953251128675613, s = 0.38268343236508977173;
+    const double h = 0.70710678118654752440;
+    double2 a[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+        double2 t[4] = {x[n2], x[4 + n2], x[8 + n2], x[12 + n2]};
+        dft<4>(t);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) a[n2][k1] = t[k1];
+    }
+    a[1][1] = cmul(a[1][1], make_double2(c, -s));   // W^1
+    a[1][2] = cmul(a[1][2], make_double2(h, -h));   // W^2
+    a[1][3] = cmul(a[1][3], make_double2(s, -c));   // W^3
+    a[2][1] = cmul(a[2][1], make_double2(h, -h));   // W^2
+    a[2][2] = mul_mi(a[2][2]);                      // W^4 = -i
+    a[2][3] = cmul(a[2][3], make_double2(-h, -h));  // W^6
+    a[3][1] = cmul(a[3][1], make_double2(s, -c));   // W^3
+    a[3][2] = cmul(a[3][2], make_double2(-h, -h));  // W^6
+    a[3][3] = cmul(a[3][3], make_double2(-c, s));   // W^9
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        double2 t[4] = {a[0][k1], a[1][k1], a[2][k1], a[3][k1]};
+        dft<4>(t);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = t[k2];
+    }
+}
+
+template <>
+__device__ __forceinline__ void dft<16>(double2* v) {
+    dft16(v);
+}
+
 // exp(-2 pi i m / M) from two small shared-memory tables:
 // coarse[m >> 7] * fine[m & 127]  (M a power of two).
 struct Twiddle {
@@ -122,7 +161,7 @@ struct Twiddle {
 
 // One in-place Stockham pass of radix R over the N2-point buffer; every
 // thread holds EPT >= N2 / blockDim.x points in registers across the barrier.
-template <int R, int EPT>
+template <int R, int EPT, int PS>
 __device__ void stockham_pass(double2* buf, int N2, int Ns, int M, const Twiddle tw) {
     const int B = N2 / R;
     const int T = blockDim.x;
@@ -133,7 +172,7 @@ __device__ void stockham_pass(double2* buf, int N2, int Ns, int M, const Twiddle
         const int j = threadIdx.x + s * T;
         if (j < B) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[s][r] = buf[pad(j + r * B)];
+            for (int r = 0; r < R; ++r) v[s][r] = buf[pad<PS>(j + r * B)];
             const int k = j % Ns;
             if (Ns > 1 && k != 0) {
                 const double2 w1 = tw(k * (M / (Ns * R)));
@@ -155,25 +194,104 @@ __device__ void stockham_pass(double2* buf, int N2, int Ns, int M, const Twiddle
             const int k = j % Ns;
             const int base = (j / Ns) * Ns * R + k;
 #pragma unroll
-            for (int r = 0; r < R; ++r) buf[pad(base + r * Ns)] = v[s][r];
+            for (int r = 0; r < R; ++r) buf[pad<PS>(base + r * Ns)] = v[s][r];
         }
     }
     __syncthreads();
 }
 
-// Radix-8 passes while each thread holds 8 points; with 16 points per thread
-// (the longest transforms) radix-4 passes keep the live set in registers.
+// The last Stockham pass (Ns * R == N2): butterfly j reads and writes the
+// same slots j + r * Ns, so each completes on its own -- no barrier between
+// loads and stores and one live butterfly per thread.
+template <int R, int PS>
+__device__ void stockham_last(double2* buf, int N2, int M, const Twiddle tw) {
+    const int B = N2 / R, Ns = B;
+    for (int j = threadIdx.x; j < B; j += blockDim.x) {
+        double2 u[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) u[r] = buf[pad<PS>(j + r * B)];
+        if (Ns > 1 && j != 0) {
+            const double2 w1 = tw(j * (M / (Ns * R)));
+            double2 w = w1;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                u[r] = cmul(u[r], w);
+                if (r + 1 < R) w = cmul(w, w1);
+            }
+        }
+        dft<R>(u);
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad<PS>(j + r * B)] = u[r];
+    }
+    __syncthreads();
+}
+
+// One radix-16 Stockham pass, one butterfly per thread (N2 = 16 * blockDim.x).
+// Twiddles w^r: w, w^2, w^4, w^8 from the tables, the rest as products.
+__device__ void stockham_pass16(double2* buf, int N2, int Ns, int M, const Twiddle tw) {
+    const int B = N2 / 16;
+    const int j = threadIdx.x;
+    double2 v[16];
+    if (j < B) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = buf[pad<4>(j + r * B)];
+        const int k = j % Ns;
+        if (Ns > 1 && k != 0) {
+            const int m1 = k * (M / (Ns * 16));
+            const double2 w1 = tw(m1), w2 = tw(2 * m1), w4 = tw(4 * m1), w8 = tw(8 * m1);
+            v[1] = cmul(v[1], w1);
+            v[2] = cmul(v[2], w2);
+            v[4] = cmul(v[4], w4);
+            v[8] = cmul(v[8], w8);
+            const double2 w3 = cmul(w1, w2);
+            v[3] = cmul(v[3], w3);
+            v[5] = cmul(v[5], cmul(w1, w4));
+            const double2 w6 = cmul(w2, w4);
+            v[6] = cmul(v[6], w6);
+            const double2 w7 = cmul(w3, w4);
+            v[7] = cmul(v[7], w7);
+            v[9] = cmul(v[9], cmul(w1, w8));
+            v[10] = cmul(v[10], cmul(w2, w8));
+            v[11] = cmul(v[11], cmul(w3, w8));
+            v[12] = cmul(v[12], cmul(w4, w8));
+            v[13] = cmul(v[13], cmul(cmul(w1, w4), w8));
+            v[14] = cmul(v[14], cmul(w6, w8));
+            v[15] = cmul(v[15], cmul(w7, w8));
+        }
+        dft16(v);
+    }
+    __syncthreads();
+    if (j < B) {
+        const int k = j % Ns;
+        const int base = (j / Ns) * Ns * 16 + k;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) buf[pad<4>(base + r * Ns)] = v[r];
+    }
+    __syncthreads();
+}
+
+// 8 points per thread: radix-8 passes (+ one radix-4/2).  16 points per thread
+// (N2 = 8192, the longest transform): radix-16 passes in registers + radix-2.
 template <int EPT>
 __device__ __forceinline__ void fft_forward(double2* buf, int N2, int M, const Twiddle tw) {
+    constexpr int PS = EPT >= 16 ? 4 : 3;
     int Ns = 1;
-    constexpr int RMAX = EPT >= 16 ? 4 : 8;
-    while (Ns * RMAX <= N2) {
-        stockham_pass<RMAX, EPT>(buf, N2, Ns, M, tw);
-        Ns *= RMAX;
+    if constexpr (EPT >= 16) {
+        while (Ns * 16 < N2) {
+            stockham_pass16(buf, N2, Ns, M, tw);
+            Ns *= 16;
+        }
+    } else {
+        while (Ns * 8 < N2) {
+            stockham_pass<8, EPT, PS>(buf, N2, Ns, M, tw);
+            Ns *= 8;
+        }
     }
-    const int rem = N2 / Ns;
-    if (rem == 4) stockham_pass<4, EPT>(buf, N2, Ns, M, tw);
-    else if (rem == 2) stockham_pass<2, EPT>(buf, N2, Ns, M, tw);
+    const int rem = N2 / Ns;  // the last pass, in place
+    if (rem == 16) stockham_last<16, PS>(buf, N2, M, tw);
+    else if (rem == 8) stockham_last<8, PS>(buf, N2, M, tw);
+    else if (rem == 4) stockham_last<4, PS>(buf, N2, M, tw);
+    else if (rem == 2) stockham_last<2, PS>(buf, N2, M, tw);
 }
 
 __global__ void twiddle_kernel(double2* tw, int64_t M) {
@@ -187,6 +305,7 @@ __global__ void twiddle_kernel(double2* tw, int64_t M) {
 
 template <int EPT>
 __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
+    constexpr int PS = EPT >= 16 ? 4 : 3;
     extern __shared__ double2 buf[];
     __shared__ double2 tw_coarse[kMaxHalf * 2 / 128 + 1];
     __shared__ double2 tw_fine[128];
@@ -222,13 +341,14 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     __syncthreads();
     const Twiddle tw{tw_coarse, tw_fine};
     const int npairs = N2 / 2 + 1;  // pairs (p, N2 - p), p = 0..N2/2
+    const int fft_slots = N2 + (N2 >> PS) + 1;
     // running spectrum S[0..N2]: after the padded FFT buffer in smem, or in
     // this CTA's global (L2-resident) slice
-    double2* spec = g.spec_in_smem ? buf + (N2 + N2 / 8 + 1)
-                                   : g.spec_glob + (int64_t)blockIdx.x * (N2 + 1);
-    double* st_val = reinterpret_cast<double*>(buf + (N2 + N2 / 8 + 1) +
-                                               (g.spec_in_smem ? (N2 + 1) : 0));
-    int32_t* st_key = reinterpret_cast<int32_t*>(st_val + kStage);
+    double2* spec = g.spec_in_smem ? buf + fft_slots : g.spec_glob + (int64_t)blockIdx.x * (N2 + 1);
+    double* st_val = reinterpret_cast<double*>(buf + fft_slots + (g.spec_in_smem ? (N2 + 1) : 0));
+    int32_t* st_key = reinterpret_cast<int32_t*>(st_val + g.stage_cap);
+    // heads resolved per stage; the rest of the staged block is look-ahead
+    const int stage_heads = g.stage_cap - kStageExt - 1;
     const bool tl = g.tlog && blockIdx.x == 0 && t == 0;
     int64_t tprev = tl ? gtimer() : 0;
     auto stamp = [&](int phase) {
@@ -250,30 +370,32 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 const int32_t* ord = s_ord[n];
                 const int32_t* key = s_key[n];
                 const int In = s_dim[n];
-                for (int l = t; l < M; l += T) dbuf[2 * pad(l >> 1) + (l & 1)] = 0.0;
+                for (int l = t; l < M; l += T) dbuf[2 * pad<PS>(l >> 1) + (l & 1)] = 0.0;
                 stamp(0);
-                // stage kStage sorted entries at a time: bucket + signed value,
-                // all loads independent (coalesced index reads, column gather)
-                for (int c0 = 0; c0 < In; c0 += kStage) {
-                    const int cn = min(kStage, In - c0);
-                    for (int qb = 0; qb < cn; qb += 4 * T) {  // 4 entries per thread in flight
-                        int32_t e[4], kq[4];
-                        double x[4];
+                for (int c0 = 0; c0 < In; c0 += stage_heads) {
+                    // stage [c0 - 1, c0 + cn + kStageExt): the entry before the
+                    // stage (run-head test) and a look-ahead past its last head;
+                    // eight independent loads in flight per thread
+                    const int cn = min(stage_heads, In - c0);
+                    const int off = c0 > 0 ? 1 : 0;
+                    const int sbeg = c0 - off;
+                    const int ns = min(In, c0 + cn + kStageExt) - sbeg;
+                    for (int qb = 0; qb < ns; qb += 8 * T) {
+                        int32_t e[8], kq[8];
+                        double x[8];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < 8; ++u) {
                             const int q = qb + u * T + t;
-                            e[u] = q < cn ? __ldg(ord + c0 + q) : 0;
-                            kq[u] = q < cn ? __ldg(key + c0 + q) : 0;
+                            const int qc = q < ns ? q : ns - 1;
+                            e[u] = __ldg(ord + sbeg + qc);
+                            kq[u] = __ldg(key + sbeg + qc);
                         }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int q = qb + u * T + t;
-                            x[u] = q < cn ? __ldg(col + dec_row(e[u])) : 0.0;
-                        }
+                        for (int u = 0; u < 8; ++u) x[u] = __ldg(col + dec_row(e[u]));
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < 8; ++u) {
                             const int q = qb + u * T + t;
-                            if (q < cn) {
+                            if (q < ns) {
                                 st_key[q] = kq[u];
                                 st_val[q] = e[u] >= 0 ? x[u] : -x[u];
                             }
@@ -283,39 +405,49 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                     stamp(1);
                     // run heads sum their bucket's rows in increasing row order
                     for (int q = t; q < cn; q += T) {
-                        const int32_t bkt = st_key[q];
-                        const bool head = q > 0 ? st_key[q - 1] != bkt
-                                                : (c0 == 0 || __ldg(key + c0 - 1) != bkt);
-                        if (!head) continue;
+                        const int sq = q + off;
+                        const int32_t bkt = st_key[sq];
+                        if (sq > 0 && st_key[sq - 1] == bkt) continue;  // not a run head
                         double acc = 0.0;
-                        int kk = q;
-                        while (kk < cn && st_key[kk] == bkt) acc += st_val[kk++];
-                        int kg = c0 + kk;  // run continues past the staged block (rare)
-                        while (kg < In && __ldg(key + kg) == bkt) {
-                            const int32_t e = __ldg(ord + kg);
-                            const double x = __ldg(col + dec_row(e));
-                            acc = e >= 0 ? acc + x : acc - x;
-                            ++kg;
+                        int kk = sq;
+                        while (kk < ns && st_key[kk] == bkt) acc += st_val[kk++];
+                        if (kk == ns) {  // run continues past the look-ahead (rare)
+                            for (int kg = sbeg + kk; kg < In && __ldg(key + kg) == bkt; ++kg) {
+                                const int32_t e = __ldg(ord + kg);
+                                const double x = __ldg(col + dec_row(e));
+                                acc = e >= 0 ? acc + x : acc - x;
+                            }
                         }
-                        dbuf[2 * pad(bkt >> 1) + (bkt & 1)] = acc;
+                        dbuf[2 * pad<PS>(bkt >> 1) + (bkt & 1)] = acc;
                     }
                     __syncthreads();
                     stamp(2);
                 }
             } else {
                 // ---- inverse: pack conj(Z) from S, forward FFT, conj ----
-                for (int p = t; p < npairs; p += T) {
-                    const double2 xk = spec[p], xm = spec[N2 - p];  // S[p], S[N2 - p]
-                    const double2 w = tw(p);
-                    const double2 e = make_double2(0.5 * (xk.x + xm.x), 0.5 * (xk.y - xm.y));
-                    const double2 d = make_double2(0.5 * (xk.x - xm.x), 0.5 * (xk.y + xm.y));
-                    const double2 o = cmul(d, conj2(w));
-                    // Z[p] = E + iO ; Z[N2-p] = conj(E) + i conj(O); stored conjugated
-                    const double2 zlo = make_double2(e.x - o.y, e.y + o.x);
-                    const double2 zhi = make_double2(e.x + o.y, -e.y + o.x);
-                    if (p < N2) buf[pad(p)] = conj2(zlo);
-                    const int pm = N2 - p;
-                    if (pm != p && pm < N2 && pm > 0) buf[pad(pm)] = conj2(zhi);
+                for (int p0 = t; p0 < npairs; p0 += 4 * T) {
+                    double2 xk[4], xm[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {  // independent spectrum loads first
+                        const int p = min(p0 + u * T, npairs - 1);
+                        xk[u] = spec[p];
+                        xm[u] = spec[N2 - p];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int p = p0 + u * T;
+                        if (p >= npairs) break;
+                        const double2 w = tw(p);
+                        const double2 e = make_double2(0.5 * (xk[u].x + xm[u].x), 0.5 * (xk[u].y - xm[u].y));
+                        const double2 d = make_double2(0.5 * (xk[u].x - xm[u].x), 0.5 * (xk[u].y + xm[u].y));
+                        const double2 o = cmul(d, conj2(w));
+                        // Z[p] = E + iO ; Z[N2-p] = conj(E) + i conj(O); stored conjugated
+                        const double2 zlo = make_double2(e.x - o.y, e.y + o.x);
+                        const double2 zhi = make_double2(e.x + o.y, -e.y + o.x);
+                        if (p < N2) buf[pad<PS>(p)] = conj2(zlo);
+                        const int pm = N2 - p;
+                        if (pm != p && pm < N2 && pm > 0) buf[pad<PS>(pm)] = conj2(zhi);
+                    }
                 }
             }
             __syncthreads();
@@ -324,21 +456,35 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
             stamp(4);
             if (n < g.n_modes) {
                 // ---- untangle the real spectrum, multiply into S ----
-                for (int p = t; p < npairs; p += T) {
-                    const double2 zk = buf[pad(p % N2)];
-                    const double2 zm = buf[pad((N2 - p) % N2)];
-                    const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-                    const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // zk - conj(zm)
-                    const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);   // d * (-i/2)
-                    const double2 wo = cmul(tw(p), o);
-                    const double2 xlo = cadd(e, wo);
-                    const double2 xhi = conj2(csub(e, wo));
-                    if (n == 0) {
-                        spec[p] = xlo;
-                        if (N2 - p != p) spec[N2 - p] = xhi;
-                    } else {
-                        spec[p] = cmul(spec[p], xlo);
-                        if (N2 - p != p) spec[N2 - p] = cmul(spec[N2 - p], xhi);
+                for (int p0 = t; p0 < npairs; p0 += 4 * T) {
+                    double2 sk[4], sm[4];
+                    if (n > 0) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {  // independent spectrum loads first
+                            const int p = min(p0 + u * T, npairs - 1);
+                            sk[u] = spec[p];
+                            sm[u] = spec[N2 - p];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int p = p0 + u * T;
+                        if (p >= npairs) break;
+                        const double2 zk = buf[pad<PS>(p % N2)];
+                        const double2 zm = buf[pad<PS>((N2 - p) % N2)];
+                        const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+                        const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // zk - conj(zm)
+                        const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);   // d * (-i/2)
+                        const double2 wo = cmul(tw(p), o);
+                        const double2 xlo = cadd(e, wo);
+                        const double2 xhi = conj2(csub(e, wo));
+                        if (n == 0) {
+                            spec[p] = xlo;
+                            if (N2 - p != p) spec[N2 - p] = xhi;
+                        } else {
+                            spec[p] = cmul(sk[u], xlo);
+                            if (N2 - p != p) spec[N2 - p] = cmul(sm[u], xhi);
+                        }
                     }
                 }
                 __syncthreads();
@@ -352,7 +498,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
         double nrm = 0.0;
         if (!g.linear) {
             for (int j = t; j < L; j += T) {
-                const double2 z = buf[pad(j >> 1)];
+                const double2 z = buf[pad<PS>(j >> 1)];
                 const double v = ((j & 1) ? -z.y : z.x) * scale * wr;
                 y[j] = v;
                 nrm = fma(v, v, nrm);
@@ -361,7 +507,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
             for (int j = t; j < L; j += T) {
                 double sacc = 0.0;
                 for (int u = j; u < M; u += L) {
-                    const double2 z = buf[pad(u >> 1)];
+                    const double2 z = buf[pad<PS>(u >> 1)];
                     sacc += ((u & 1) ? -z.y : z.x) * scale;
                 }
                 const double v = sacc * wr;
@@ -386,6 +532,7 @@ struct TsPlan {
     int threads;
     int ept;
     int spec_in_smem;
+    int stage_cap;
     size_t smem;
 };
 
@@ -406,9 +553,11 @@ TsPlan plan_ts(int n_modes, int64_t L) {
     int64_t T = p.N2 / p.ept;
     if (T < 32) T = 32;
     p.threads = (int)T;
-    const size_t fft_bytes = (size_t)(p.N2 + p.N2 / 8 + 1) * sizeof(double2);
+    const int ps = p.ept >= 16 ? 4 : 3;  // padding shift of the FFT buffer (pad<PS>)
+    const size_t fft_bytes = (size_t)(p.N2 + (p.N2 >> ps) + 1) * sizeof(double2);
     const size_t spec_bytes = (size_t)(p.N2 + 1) * sizeof(double2);
-    const size_t stage_bytes = (size_t)kStage * (sizeof(double) + sizeof(int32_t));
+    p.stage_cap = p.N2 >= 8192 ? 4096 : 2048;
+    const size_t stage_bytes = (size_t)p.stage_cap * (sizeof(double) + sizeof(int32_t));
     p.spec_in_smem = fft_bytes + spec_bytes + stage_bytes <= 200 * 1024;
     p.smem = fft_bytes + (p.spec_in_smem ? spec_bytes : 0) + stage_bytes;
     return p;
@@ -480,6 +629,7 @@ extern "C" int ids_tensorsketch_f64(int n_modes, const double* const* factors, c
     a.tw = tw;
     a.spec_glob = specg;
     a.spec_in_smem = p.spec_in_smem;
+    a.stage_cap = p.stage_cap;
     a.tlog = g_ts_tlog;
     if (colnorm2) IDS_CUDA_TRY(cudaMemsetAsync(colnorm2, 0, sizeof(double) * ncols, st));
     auto kern = p.ept == 16 ? tensorsketch_kernel<16> : tensorsketch_kernel<8>;

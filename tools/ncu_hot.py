@@ -5,7 +5,8 @@ import sys
 
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+view = sys.argv[3] if len(sys.argv) > 3 else "sass"  # or "cuda" (needs -lineinfo)
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", view],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
 start = 2 if rows and rows[0] and rows[0][0].startswith("Kernel") else 1
