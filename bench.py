@@ -251,15 +251,10 @@ def main():
             dist.barrier()
 
     from paper_1901_10559_b200.distributed import DeviceBackend
-    from paper_1901_10559_b200.sketch import HashPrefetcher
 
-    pf = HashPrefetcher()
-    backend = DeviceBackend(prefetcher=pf)
+    backend = DeviceBackend()
 
-    def step(seed, next_seed=None):
-        # the next trial's hash is drawn on a side stream while this one sketches
-        if next_seed is not None:
-            pf.request(w["rows"], w["L"], next_seed, True)
+    def step(seed):
         return countsketch_id_sharded(operand, r0, w["rows"], w["k"], w["L"], seed=seed,
                                       backend=backend)
 
@@ -281,8 +276,10 @@ def main():
     from paper_1901_10559_b200.distributed import countsketch_id_sharded_trials
 
     # ---- device-resident steps (value): K trials queued back to back ----
+    # warm-up: at least one full batch of ten trials (the side streams the
+    # trials API draws hashes on, and their cached allocations)
     countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
-                                  seeds=list(range(args.warmup)))
+                                  seeds=list(range(max(args.warmup, min(args.steps, 10)))))
     torch.cuda.synchronize()
     barrier()
     clocks = Clocks(rank == 0)

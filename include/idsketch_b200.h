@@ -66,6 +66,11 @@ int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                          int surjective, int32_t* bucket, int8_t* sign,
                          int64_t* draws_out, void* workspace, size_t ws_bytes,
                          void* stream);
+/* Concurrency hint for ids_countsketch_hash: cap the Fisher-Yates resolution
+ * grid at `ctas` CTAs (0 = whole GPU) so that several hash draws issued on
+ * different streams (independent trials) run side by side.  Process-wide;
+ * read when a draw is enqueued. */
+void ids_set_hash_grid_cap(int ctas);
 
 /* ---------------------------------------------------------------------------
  * Bucket index: the rows of each bucket in increasing row order, i.e. the CSR

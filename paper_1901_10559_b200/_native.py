@@ -75,6 +75,7 @@ SIGNATURES = {
     "ids_triangular_solve_f64": (
         _c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p]
     ),
+    "ids_set_hash_grid_cap": (None, [_c_int]),
     "ids_dense_gemv_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_int, _c_int]),
     "ids_dense_gemv_f64": (
         _c_int,

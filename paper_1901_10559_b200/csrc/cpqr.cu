@@ -539,6 +539,7 @@ struct ClusterArgs {
     double* Vout;    // V (m x k) and tau for form_q_kernel, written by CTA 0
     double* tauout;
     int ncl;         // columns per CTA (max)
+    int64_t* tlog;   // debug: per-phase ns accumulated by CTA 0 (NULL: off)
 };
 
 struct ClusterSmem {  // carve of the dynamic shared memory
@@ -647,6 +648,15 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
     local_argmax(0, 0, 0);
     cluster.sync();
 
+    const bool tl = g.tlog && b == 0 && threadIdx.x == 0;
+    int64_t tprev = tl ? gtimer() : 0;
+    auto stamp = [&](int phase) {
+        if (tl) {
+            const int64_t tn = gtimer();
+            g.tlog[phase] += tn - tprev;
+            tprev = tn;
+        }
+    };
     for (int64_t kk = 0; kk < k; ++kk) {
         const int par = (int)(kk & 1);
         // ---- pivot from every CTA's candidate (DSMEM), fixed rank order ----
@@ -682,6 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
             if (ck >= c0 && ck < c1 && ck != cs) S.pos[ck - c0] = (int)ps;
             if (cs >= c0 && cs < c1) S.pos[cs - c0] = (int)kk;
         }
+        stamp(0);
         // ---- pivot column from the owner's shared memory, Householder ----
         int owner = 0;
         while (owner + 1 < CS && n * (owner + 1) / CS <= cs) ++owner;
@@ -693,6 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
             for (int64_t q = threadIdx.x; q < kk; q += kThreads) S.z[q] = fown[q * g.ncl];
         }
         __syncthreads();
+        stamp(1);
         double ss = 0.0;
         for (int64_t r = kk + threadIdx.x; r < m; r += kThreads) {
             const double acc = sub_dot(S.v[r], S.V + r, m, S.z, 1, kk);
@@ -726,8 +738,8 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
             S.beta[kk] = beta;
             if (cs >= c0 && cs < c1) S.Rs[kk * g.ncl + (cs - c0)] = beta;
         }
-        __syncthreads();
-        __syncthreads();  // z (F row copy) consumed, S.z reused below
+        __syncthreads();  // v complete; z (the F row copy) consumed, S.z reused below
+        stamp(2);
         // GEMV over owned remaining columns, one thread per column (short m)
         for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
             if (S.pos[jj] <= kk) continue;
@@ -750,7 +762,9 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
             if (lane == 0) S.z[q] = zq;
         }
         __syncthreads();
+        stamp(3);
         // F, row kk of R, norm downdate (thread per column), flagged recompute (warp per column)
+        int any_flag = 0;
         for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
             if (S.pos[jj] <= kk) continue;
             double f = S.W[jj], rk = S.Ys[kk * g.ncl + jj];
@@ -769,12 +783,17 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
                 double temp = fabs(rk) / vn1;
                 temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
                 const double ratio = vn1 / S.vn2[jj];
-                if (temp * ratio * ratio <= tol3z) S.W[jj] = 1.0;
-                else S.vn1[jj] = vn1 * sqrt(temp);
+                if (temp * ratio * ratio <= tol3z) {
+                    S.W[jj] = 1.0;
+                    any_flag = 1;
+                } else {
+                    S.vn1[jj] = vn1 * sqrt(temp);
+                }
             }
         }
-        __syncthreads();
-        for (int jj = wid; jj < nc; jj += kWarps) {
+        any_flag = __syncthreads_or(any_flag);
+        stamp(4);
+        for (int jj = wid; any_flag && jj < nc; jj += kWarps) {
             if (S.pos[jj] <= kk || S.W[jj] == 0.0) continue;
             double s2 = 0.0;
             for (int64_t r = kk + 1 + lane; r < m; r += 32) {
@@ -788,9 +807,12 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
                 S.vn2[jj] = sqrt(s2);
             }
         }
-        __syncthreads();
+        if (any_flag) __syncthreads();
+        stamp(5);
         local_argmax(kk + 1, kk + 1, par ^ 1);
+        stamp(6);
         cluster.sync();
+        stamp(7);
     }
 
     // ---- outputs ----
@@ -997,6 +1019,7 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
             ca.Rtop = Rtop;
             ca.numerical_rank = numerical_rank;
             ca.ncl = ncl;
+            ca.tlog = g_cpqr_tlog;
             WsCarve wsc(workspace, ws_bytes);
             ca.Vout = wsc.take<double>((size_t)rows * k);
             ca.tauout = wsc.take<double>((size_t)k);

@@ -724,6 +724,7 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_
 }
 
 int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel
+int g_fy_grid_cap = 0;         // >0: cap on the phase-B grid (CTAs)
 
 struct HashPlan {
     int64_t I, L;
@@ -880,7 +881,8 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fy_phaseb_kernel, kPbThreads, 0);
-            const int G = tmax(1, sms * tmin(per_sm, 2));
+            int G = tmax(1, sms * tmin(per_sm, 2));
+            if (g_fy_grid_cap > 0) G = tmin(G, g_fy_grid_cap);
             const uint32_t* dr = draws;
             int64_t nbuf = p.nbuf, nI = I, mc = p.max_chunks;
             int kmin = kMinBand;
@@ -930,3 +932,7 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
 // Debug hook: record phase-B stage timestamps into `buf` (device int64[512])
 // for the next hash draws; NULL disables.
 extern "C" void ids_debug_phaseb_timing(int64_t* buf) { g_fy_tlog = buf; }
+
+// Cap the phase-B grid at `ctas` CTAs (0 = whole GPU); lets several hash
+// streams share the GPU.
+extern "C" void ids_set_hash_grid_cap(int ctas) { g_fy_grid_cap = ctas > 0 ? ctas : 0; }

@@ -22,6 +22,7 @@
 // M = 2^ceil(log2(N(L-1)+1)), the product gives their LINEAR convolution
 // exactly, and it is folded mod L -- the same cyclic convolution the
 // reference's length-L rfft/irfft computes (sketch.py:176-178).
+#include <limits.h>
 #include <math.h>
 
 #include "common.cuh"
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     __shared__ const int32_t* s_key[kMaxModes];
     __shared__ int64_t s_ld[kMaxModes];
     __shared__ int s_dim[kMaxModes];
+    __shared__ int32_t s_prevkey;
     double* dbuf = reinterpret_cast<double*>(buf);
     const int T = blockDim.x, t = threadIdx.x;
     const int N2 = (int)g.N2, M = (int)g.M;
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     double* st_val = reinterpret_cast<double*>(buf + fft_slots + (g.spec_in_smem ? (N2 + 1) : 0));
     int32_t* st_key = reinterpret_cast<int32_t*>(st_val + g.stage_cap);
     // heads resolved per stage; the rest of the staged block is look-ahead
-    const int stage_heads = g.stage_cap - kStageExt - 1;
+    const int stage_heads = g.stage_cap - kStageExt;  // stage_cap == 8 * blockDim.x
     const bool tl = g.tlog && blockIdx.x == 0 && t == 0;
     int64_t tprev = tl ? gtimer() : 0;
     auto stamp = [&](int phase) {
@@ -370,55 +372,87 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 const int32_t* ord = s_ord[n];
                 const int32_t* key = s_key[n];
                 const int In = s_dim[n];
-                for (int l = t; l < M; l += T) dbuf[2 * pad<PS>(l >> 1) + (l & 1)] = 0.0;
+                if (n == 0)  // later modes find the buffer zeroed by the untangle
+                    for (int l = t; l < N2; l += T) buf[pad<PS>(l)] = make_double2(0.0, 0.0);
                 stamp(0);
                 for (int c0 = 0; c0 < In; c0 += stage_heads) {
-                    // stage [c0 - 1, c0 + cn + kStageExt): the entry before the
-                    // stage (run-head test) and a look-ahead past its last head;
-                    // eight independent loads in flight per thread
+                    // stage entries [c0, c0 + ns): the heads below cn and a
+                    // look-ahead; thread t owns the 8 consecutive entries
+                    // [8t, 8t + 8) (one round: ns <= 8T), loaded with eight
+                    // independent gathers in flight and kept in registers
                     const int cn = min(stage_heads, In - c0);
-                    const int off = c0 > 0 ? 1 : 0;
-                    const int sbeg = c0 - off;
-                    const int ns = min(In, c0 + cn + kStageExt) - sbeg;
-                    for (int qb = 0; qb < ns; qb += 8 * T) {
-                        int32_t e[8], kq[8];
-                        double x[8];
+                    const int ns = min(In - c0, cn + kStageExt);
+                    const int gb = 8 * t;
+                    int32_t kq[8];
+                    double x[8];
+                    {
+                        int32_t e[8];
+                        const bool vec = ((reinterpret_cast<uintptr_t>(ord) |
+                                           reinterpret_cast<uintptr_t>(key)) & 15) == 0;
+                        if (vec && gb + 8 <= ns) {  // 2 x 16-byte loads per array (c0 % 4 == 0)
+                            const int4* o4 = reinterpret_cast<const int4*>(ord + c0 + gb);
+                            const int4* k4 = reinterpret_cast<const int4*>(key + c0 + gb);
+                            const int4 oa = __ldg(o4), ob = __ldg(o4 + 1);
+                            const int4 ka = __ldg(k4), kb = __ldg(k4 + 1);
+                            e[0] = oa.x; e[1] = oa.y; e[2] = oa.z; e[3] = oa.w;
+                            e[4] = ob.x; e[5] = ob.y; e[6] = ob.z; e[7] = ob.w;
+                            kq[0] = ka.x; kq[1] = ka.y; kq[2] = ka.z; kq[3] = ka.w;
+                            kq[4] = kb.x; kq[5] = kb.y; kq[6] = kb.z; kq[7] = kb.w;
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const int qc = min(gb + u, ns - 1);
+                                e[u] = __ldg(ord + c0 + qc);
+                                kq[u] = __ldg(key + c0 + qc);
+                            }
+                        }
+                        if (t == 0) s_prevkey = c0 > 0 ? __ldg(key + c0 - 1) : -1;
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            const int q = qb + u * T + t;
-                            const int qc = q < ns ? q : ns - 1;
-                            e[u] = __ldg(ord + sbeg + qc);
-                            kq[u] = __ldg(key + sbeg + qc);
+                            const double v = __ldg(col + dec_row(e[u]));
+                            x[u] = e[u] >= 0 ? v : -v;
                         }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) x[u] = __ldg(col + dec_row(e[u]));
-#pragma unroll
                         for (int u = 0; u < 8; ++u) {
-                            const int q = qb + u * T + t;
-                            if (q < ns) {
-                                st_key[q] = kq[u];
-                                st_val[q] = e[u] >= 0 ? x[u] : -x[u];
+                            if (gb + u < ns) {
+                                st_key[gb + u] = kq[u];
+                                st_val[gb + u] = x[u];
+                            } else {
+                                kq[u] = INT_MIN;  // past the staged block
                             }
                         }
                     }
                     __syncthreads();
                     stamp(1);
-                    // run heads sum their bucket's rows in increasing row order
-                    for (int q = t; q < cn; q += T) {
-                        const int sq = q + off;
-                        const int32_t bkt = st_key[sq];
-                        if (sq > 0 && st_key[sq - 1] == bkt) continue;  // not a run head
+                    // runs of equal bucket: the thread holding a run's head sums it
+                    // in increasing row order (its registers, then the following
+                    // threads' entries from shared memory)
+                    if (gb < cn) {
+                        int32_t cur = gb > 0 ? st_key[gb - 1] : s_prevkey;
+                        bool own = false;
                         double acc = 0.0;
-                        int kk = sq;
-                        while (kk < ns && st_key[kk] == bkt) acc += st_val[kk++];
-                        if (kk == ns) {  // run continues past the look-ahead (rare)
-                            for (int kg = sbeg + kk; kg < In && __ldg(key + kg) == bkt; ++kg) {
-                                const int32_t e = __ldg(ord + kg);
-                                const double x = __ldg(col + dec_row(e));
-                                acc = e >= 0 ? acc + x : acc - x;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (kq[u] != cur) {  // a run starts at gb + u
+                                if (own) dbuf[2 * pad<PS>(cur >> 1) + (cur & 1)] = acc;
+                                own = gb + u < cn && kq[u] != INT_MIN;
+                                cur = kq[u];
+                                acc = 0.0;
                             }
+                            if (own) acc += x[u];
                         }
-                        dbuf[2 * pad<PS>(bkt >> 1) + (bkt & 1)] = acc;
+                        if (own) {  // the last run may continue past this thread
+                            int q = gb + 8;
+                            while (q < ns && st_key[q] == cur) acc += st_val[q++];
+                            if (q == ns) {  // ... and past the look-ahead (rare)
+                                for (int kg = c0 + q; kg < In && __ldg(key + kg) == cur; ++kg) {
+                                    const int32_t e = __ldg(ord + kg);
+                                    const double v = __ldg(col + dec_row(e));
+                                    acc = e >= 0 ? acc + v : acc - v;
+                                }
+                            }
+                            dbuf[2 * pad<PS>(cur >> 1) + (cur & 1)] = acc;
+                        }
                     }
                     __syncthreads();
                     stamp(2);
@@ -472,6 +506,10 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                         if (p >= npairs) break;
                         const double2 zk = buf[pad<PS>(p % N2)];
                         const double2 zm = buf[pad<PS>((N2 - p) % N2)];
+                        // each slot is read by exactly one pair: clear it for the
+                        // next mode's CountSketch (the inverse overwrites it anyway)
+                        buf[pad<PS>(p % N2)] = make_double2(0.0, 0.0);
+                        buf[pad<PS>((N2 - p) % N2)] = make_double2(0.0, 0.0);
                         const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
                         const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // zk - conj(zm)
                         const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);   // d * (-i/2)
@@ -556,7 +594,7 @@ TsPlan plan_ts(int n_modes, int64_t L) {
     const int ps = p.ept >= 16 ? 4 : 3;  // padding shift of the FFT buffer (pad<PS>)
     const size_t fft_bytes = (size_t)(p.N2 + (p.N2 >> ps) + 1) * sizeof(double2);
     const size_t spec_bytes = (size_t)(p.N2 + 1) * sizeof(double2);
-    p.stage_cap = p.N2 >= 8192 ? 4096 : 2048;
+    p.stage_cap = 8 * p.threads;  // one staging round: 8 consecutive entries per thread
     const size_t stage_bytes = (size_t)p.stage_cap * (sizeof(double) + sizeof(int32_t));
     p.spec_in_smem = fft_bytes + spec_bytes + stage_bytes <= 200 * 1024;
     p.smem = fft_bytes + (p.spec_in_smem ? spec_bytes : 0) + stage_bytes;

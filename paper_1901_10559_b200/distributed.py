@@ -31,9 +31,6 @@ def row_block(n, world, rank):
 class DeviceBackend:
     """sm_100a kernels through the C ABI (the product path)."""
 
-    def __init__(self, prefetcher=None):
-        self.prefetcher = prefetcher
-
     def matrix_sketch(self, a_local, row0, in_dim, sketch_dim, seed, surjective):
         from . import _device
         from ._inputs import DenseOperand, SparseOperand, matrix_operand
@@ -44,11 +41,7 @@ class DeviceBackend:
             operand = a_local
         else:
             operand = matrix_operand(a_local)
-        op = None
-        if self.prefetcher is not None:
-            op = self.prefetcher.take(in_dim, sketch_dim, seed, surjective)
-        if op is None:
-            op = CountSketchOp(in_dim, sketch_dim, seed=seed, surjective=surjective)
+        op = CountSketchOp(in_dim, sketch_dim, seed=seed, surjective=surjective)
         y = _device.empty((operand.cols, sketch_dim), torch.float64)
         flag = _device.zeros(1, torch.int32)
         op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,
@@ -128,7 +121,7 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     from ._inputs import DenseOperand, SparseOperand, matrix_operand
     from ._native import IDS_FLAG_ORDERED
     from .matrix_id import check_matrix_id_args, device_matrix_id
-    from .sketch import CountSketchOp
+    from .sketch import draw_operators
 
     world, _ = _world(group)
     operand = a_local if isinstance(a_local, (DenseOperand, SparseOperand)) else \
@@ -141,10 +134,13 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     L = check_matrix_id_args(_Shape, rank, sketch_dim, "countsketch")
     seeds = list(seeds)
     outs, flags = [], []
-    for s in seeds:
-        # (drawing the next trial's hash on a side stream was measured to slow
-        # the one-wave sketch kernel down more than it hid: kept sequential)
-        op = CountSketchOp(in_dim, L, seed=s, surjective=surjective)
+    # every trial's hash first, drawn side by side on all SMs; the sketches then
+    # run back to back (overlapping a draw with the one-wave, HBM-bound sketch
+    # kernel was measured to slow the sketch down more than it hid)
+    # (batches of ten trials bound the live hash/index memory)
+    ops = (op for b in range(0, len(seeds), 10)
+           for op in draw_operators(in_dim, L, seeds[b:b + 10], surjective))
+    for op in ops:
         y = torch.empty((cols, L), dtype=torch.float64, device=torch.cuda.current_device())
         flag = torch.zeros(1, dtype=torch.int32, device=y.device)
         op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,

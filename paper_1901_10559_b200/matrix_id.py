@@ -176,19 +176,11 @@ def _raise_if_nonfinite(flag, operand):
 
 
 def countsketch_device(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL,
-                       surjective=True, flags=IDS_FLAG_ORDERED, check_finite=True,
-                       prefetcher=None):
-    """The device half of countsketch_id: returns (DeviceId, sketch (cols, L)).
-
-    prefetcher: optional sketch.HashPrefetcher holding this trial's operator
-    (drawn ahead on a side stream)."""
+                       surjective=True, flags=IDS_FLAG_ORDERED, check_finite=True):
+    """The device half of countsketch_id: returns (DeviceId, sketch (cols, L))."""
     operand = a if isinstance(a, (DenseOperand, SparseOperand)) else matrix_operand(a)
     sketch_dim = check_matrix_id_args(operand, rank, sketch_dim, "countsketch")
-    op = None
-    if prefetcher is not None and seed is not None:
-        op = prefetcher.take(operand.rows, sketch_dim, seed, surjective)
-    if op is None:
-        op = CountSketchOp(operand.rows, sketch_dim, seed=seed, surjective=surjective)
+    op = CountSketchOp(operand.rows, sketch_dim, seed=seed, surjective=surjective)
     nonfinite = _device.zeros(1, torch.int32) if check_finite else None
     y = op.apply_device(operand, flags=flags, nonfinite=nonfinite)
     if check_finite:

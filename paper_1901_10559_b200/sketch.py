@@ -17,7 +17,7 @@ import torch
 
 from . import _device
 from ._inputs import DenseOperand, SparseOperand, matrix_operand
-from ._native import IDS_ERETRY, IDS_FLAG_ORDERED, call, query
+from ._native import IDS_ERETRY, IDS_FLAG_ORDERED, call, load, query
 
 _MAX_MATERIALIZE = 50_000_000  # sketch.py:30
 # Above this many nonzeros the CSR kernel splits each bucket into row segments
@@ -119,7 +119,7 @@ class CountSketchOp:
 
     def record_stream(self, stream):
         """Mark the operator's device arrays as used on `stream` (they may have
-        been drawn on another stream, see HashPrefetcher)."""
+        been drawn on another stream, see draw_operators)."""
         for t in (self._bucket_d, self._sign_d, self._draws):
             if t is not None:
                 t.record_stream(stream)
@@ -323,37 +323,49 @@ class TensorSketchOp:
         return dense
 
 
-class HashPrefetcher:
-    """Draws CountSketch hashes ahead of time on a side stream.
+_HASH_STREAMS = {}
 
-    The hash draw (and bucket index) depends only on (in_dim, out_dim, seed,
-    surjective), not on the data, and its kernels are latency-bound and
-    light.  Requesting the NEXT trial's operator before sketching the
-    current one lets the draw overlap the HBM-bound sketch kernel
-    (repeated IDs of one matrix, e.g. the paper's 10 trials per config)."""
 
-    def __init__(self):
-        self.side = torch.cuda.Stream(device=_device.device())
-        self.cache = {}
+def draw_operators(in_dim, out_dim, seeds, surjective=False):
+    """CountSketchOps (hash + bucket index) for several seeds, drawn side by side.
 
-    def request(self, in_dim, out_dim, seed, surjective):
-        key = (int(in_dim), int(out_dim), seed, bool(surjective))
-        if key in self.cache:
-            return
-        with torch.cuda.stream(self.side):
-            op = CountSketchOp(in_dim, out_dim, seed=seed, surjective=surjective)
+    A draw depends only on (in_dim, out_dim, seed, surjective), and its
+    Fisher-Yates resolution is latency-bound: on its own it keeps only part of
+    the GPU busy.  Independent trials are therefore issued on up to ten side
+    streams with the resolution grid capped (ids_set_hash_grid_cap) so that
+    they run concurrently -- about three times the throughput of back-to-back
+    draws at I = 1e6.  The current stream waits for all of them."""
+    seeds = list(seeds)
+    if len(seeds) <= 1:
+        ops = [CountSketchOp(in_dim, out_dim, seed=s, surjective=surjective) for s in seeds]
+        for op in ops:
             op._bucket_index()
-            ev = torch.cuda.Event()
-            ev.record(self.side)
-        self.cache[key] = (op, ev)
-
-    def take(self, in_dim, out_dim, seed, surjective):
-        """The prefetched operator (waited on by the current stream), or None."""
-        item = self.cache.pop((int(in_dim), int(out_dim), seed, bool(surjective)), None)
-        if item is None:
-            return None
-        op, ev = item
-        cur = torch.cuda.current_stream()
-        cur.wait_event(ev)
-        op.record_stream(cur)
-        return op
+        return ops
+    dev = _device.device()
+    main = torch.cuda.current_stream()
+    n = min(len(seeds), 10)
+    pool = _HASH_STREAMS.setdefault(dev.index, [])
+    while len(pool) < n:
+        pool.append(torch.cuda.Stream(device=dev))
+    streams = pool[:n]
+    start = torch.cuda.Event()
+    start.record(main)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    lib = load()
+    lib.ids_set_hash_grid_cap(max(16, 2 * sms // n))
+    ops = []
+    try:
+        for st in streams:
+            st.wait_event(start)
+        for i, s in enumerate(seeds):
+            with torch.cuda.stream(streams[i % n]):
+                op = CountSketchOp(in_dim, out_dim, seed=s, surjective=surjective)
+                op._bucket_index()
+            ops.append(op)
+    finally:
+        lib.ids_set_hash_grid_cap(0)
+    for st in streams:
+        main.wait_stream(st)
+    for op in ops:
+        op.record_stream(main)
+    return ops

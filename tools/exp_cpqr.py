@@ -22,7 +22,10 @@ def near_dup(m, n, base, pert, seed):
     return y.t().contiguous()  # (n, m) == col-major m x n
 
 
-for name, m, n, k, base, pert in (("C4", 4096, 1000, 10, 10, 1e-3),
+CLUSTER = ["pivot select", "pivot col", "householder", "gemv+z", "F/R/downdate",
+           "recompute", "argmax", "cluster sync"]
+for name, m, n, k, base, pert in (("C2", 100, 2000, 20, 20, 1e-2), ("C1", 40, 1000, 10, 10, 1e-2),
+                                  ("C4", 4096, 1000, 10, 10, 1e-3),
                                   ("C5", 16384, 2000, 20, 20, 1e-4),
                                   ("C3", 200, 10000, 20, 20, 1e-2)):
     y = near_dup(m, n, base, pert, 1)
@@ -43,5 +46,5 @@ for name, m, n, k, base, pert in (("C4", 4096, 1000, 10, 10, 1e-3),
     lib.ids_debug_cpqr_timing(None)
     t = buf.cpu().numpy()
     print(f"{name}: {m}x{n} k={k}: {ms * 1e3:.1f} us per call; flagged {t[15]}")
-    for i, nm in enumerate(NAMES):
+    for i, nm in enumerate(CLUSTER if m <= 1024 and name in ("C2", "C1") else NAMES):
         print(f"   {nm:14s} {t[i] / 1e3:9.1f} us  ({t[i] / 1e3 / k:6.2f}/step)")
