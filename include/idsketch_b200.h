@@ -233,6 +233,35 @@ int ids_csr_transpose_f64(const void* indptr, int indptr64, const int32_t* indic
                           int64_t* t_indptr, int32_t* t_indices, double* t_data,
                           void* workspace, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Column-distributed truncated CPQR (replaces linalg.py:97 for
+ * sketches whose COLUMNS are split across ranks, e.g. the term-sharded tensor
+ * path).  This rank holds columns [col0, col0 + ncols) of the L x R sketch:
+ * Y col-major rows x ncols (ld = ldy).  The caller drives k steps:
+ *   init  -> cand (device double[4]: value, position, global column, global
+ *            column at the step's position; position -1 if no finite value);
+ *   per step kk: pick the global pivot (cs, ps, ck) from every rank's cand
+ *            (largest value, ties to the lowest position);
+ *            ids_dcpqr_pivot_f64 on every rank (position swap; the rank owning
+ *            cs also writes the residual pivot column a[rows]); broadcast a
+ *            from the owner; ids_dcpqr_step_f64 on every rank -> next cand.
+ *   results: positions (int64[ncols]), R rows k x ncols (row-major, by local
+ *            column), beta[k] (= R diagonal, replicated).
+ * All state lives in the caller's workspace (ids_dcpqr_workspace_bytes).
+ * ------------------------------------------------------------------------- */
+size_t ids_dcpqr_workspace_bytes(int64_t rows, int64_t ncols, int64_t k);
+int ids_dcpqr_init_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy, int64_t k,
+                       int64_t col0, double* cand, void* workspace, size_t ws_bytes,
+                       void* stream);
+int ids_dcpqr_pivot_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy, int64_t k,
+                        int64_t col0, int64_t kk, int64_t cs, int64_t ps, int64_t ck,
+                        double* a, void* workspace, size_t ws_bytes, void* stream);
+int ids_dcpqr_step_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy, int64_t k,
+                       int64_t col0, int64_t kk, int64_t cs, const double* a, double* cand,
+                       void* workspace, size_t ws_bytes, void* stream);
+int ids_dcpqr_results_f64(int64_t rows, int64_t ncols, int64_t k, int64_t* pos, double* R,
+                          double* beta, void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,6 +13,9 @@ Contents
   (reference ``pkg/src/idsketch/sketch.py:77-84``).
 * ``estimators.py``: the reference's error metric for matrix trials
   (``estimators.py:26-121``, ``bench.py:116-145``).
+* ``dcpqr.py``: one rank's share of the column-distributed CPQR (the
+  interface of ``distributed.DeviceCpqrShard``), for gloo tests of the host
+  driver.
 * ``port.py``: numpy/scipy restatement of the reference's sketch + ID path
   (``sketch.py:116-186``, ``linalg.py:76-147``, ``matrix_id.py:56-182``,
   ``cp_tensor.py:215-276``), calling the same third-party kernels the
@@ -24,6 +27,7 @@ real reference package (``tests/golden/make_golden.py``) in
 """
 
 from .cs_hash import countsketch_hash, pcg64_stream32, seed_state
+from .dcpqr import OracleCpqrShard
 from .estimators import derive_seed, est_spectral_norm, id_residual_operator, matrix_operator
 from .port import (
     OracleCountSketch,
@@ -43,6 +47,7 @@ from .port import (
 
 __all__ = [
     "OracleCountSketch",
+    "OracleCpqrShard",
     "OracleTensorSketch",
     "coeffs_from_pivoted",
     "cp_gram",

@@ -76,6 +76,23 @@ SIGNATURES = {
         _c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p]
     ),
     "ids_set_hash_grid_cap": (None, [_c_int]),
+    "ids_dcpqr_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_i64]),
+    "ids_dcpqr_init_f64": (
+        _c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_sz, _c_p]
+    ),
+    "ids_dcpqr_pivot_f64": (
+        _c_int,
+        [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_p,
+         _c_p, _c_sz, _c_p],
+    ),
+    "ids_dcpqr_step_f64": (
+        _c_int,
+        [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_sz,
+         _c_p],
+    ),
+    "ids_dcpqr_results_f64": (
+        _c_int, [_c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]
+    ),
     "ids_dense_gemv_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_int, _c_int]),
     "ids_dense_gemv_f64": (
         _c_int,

@@ -11,7 +11,11 @@ this module adds the two partitionings SURVEY.md section 8(e) derives:
   rank, so no broadcast of j / P is needed;
 * CP tensors: the R rank-1 terms are split into column blocks; column r of
   the TensorSketch depends only on column r of each factor, so each rank
-  sketches its block independently and one all-gather assembles Y.
+  sketches its block independently.  The ID then runs as a COLUMN-distributed
+  truncated CPQR (``cpqr_columns_sharded``): per step one
+  all-gather of 4-double pivot candidates and one broadcast of the L-double
+  pivot column, so the L x R sketch (262 MB for configs[4]) is never
+  gathered; ``cpqr="gather"`` keeps the all-gather + redundant CPQR variant.
 
 The arithmetic goes through a backend object so the partitioning and the
 collectives can be exercised on CPU with gloo (tests/test_distributed_gloo.py,
@@ -47,6 +51,27 @@ class DeviceBackend:
         op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,
                        nonfinite=flag)
         return y, flag, operand
+
+    def cpqr_shard(self, y_local, col0, k):
+        return DeviceCpqrShard(y_local, col0, k)
+
+    def coeffs_from_factors(self, rtop, perm, k, ncols, rank_tol, numerical_rank):
+        """P from the assembled truncated factorization (ids_id_coeffs_f64)."""
+        from . import _device
+        from ._native import call, query
+        from .matrix_id import DeviceId
+
+        rt = _device.to_device(np.ascontiguousarray(rtop), torch.float64)
+        pm = _device.to_device(np.asarray(perm, dtype=np.int32))
+        nr = _device.to_device(np.array([numerical_rank], dtype=np.int32))
+        p = _device.empty((k, ncols), torch.float64)
+        de = _device.empty(1, torch.int32)
+        nbytes = query("ids_id_coeffs_workspace_bytes", k, ncols)
+        ws = _device.workspace(nbytes)
+        call("ids_id_coeffs_f64", _device.ptr(rt), _device.ptr(pm), k, ncols, float(rank_tol),
+             _device.ptr(nr), _device.ptr(p), _device.ptr(de), _device.ptr(ws), nbytes,
+             _device.stream_ptr())
+        return DeviceId(pm[:k], p, nr, de, k).to_host("tensorsketch")
 
     def confirm_nonfinite(self, operand):
         from . import _device
@@ -167,7 +192,8 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
 
 
 def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketch_dim=None,
-                            seed=None, rank_tol=1e-12, group=None, backend=None):
+                            seed=None, rank_tol=1e-12, group=None, backend=None,
+                            cpqr="columns"):
     """tensorsketch_id with the R terms split into column blocks: this rank
     holds terms [col0, col0 + R_local) of the (normalized) CpTensor in
     x_local.  Returns the TensorIdResult-like tuple (cols, coeffs,
@@ -189,6 +215,10 @@ def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketc
         seed = int(ent.item())
     y_local = backend.tensor_sketch(x_local.factors, x_local.weights, x_local.mode_dims,
                                     sketch_dim, seed)
+    if world > 1 and cpqr == "columns":
+        d = cpqr_columns_sharded(y_local, col0, total_terms, rank, rank_tol, group, backend)
+        weights = np.asarray(all_weights, dtype=np.float64)
+        return d, weights[d.cols] * d.coeffs.sum(axis=1)
     if world > 1:
         counts = [row_block(total_terms, world, r) for r in range(world)]
         sizes = [b - a for a, b in counts]
@@ -204,3 +234,141 @@ def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketc
     weights = np.asarray(all_weights, dtype=np.float64)
     new_weights = weights[d.cols] * d.coeffs.sum(axis=1)
     return d, new_weights
+
+
+# ---- column-distributed truncated CPQR ---------------------
+class DeviceCpqrShard:
+    """This rank's column block of an L x R sketch for the column-distributed
+    CPQR (ids_dcpqr_*): y is a CUDA (ncols, L) tensor, i.e. col-major L x
+    ncols, holding global columns [col0, col0 + ncols)."""
+
+    def __init__(self, y, col0, k):
+        from . import _device
+        from ._native import call, query
+
+        self._d, self._call = _device, call
+        self.y = y.contiguous()
+        self.n, self.m = (int(v) for v in self.y.shape)
+        self.col0, self.k = int(col0), int(k)
+        self.nbytes = query("ids_dcpqr_workspace_bytes", self.m, self.n, self.k)
+        self.ws = _device.workspace(self.nbytes)
+        self.cand = _device.empty(4, torch.float64)
+        self.a = _device.zeros(self.m, torch.float64)
+        call("ids_dcpqr_init_f64", _device.ptr(self.y), self.m, self.n, self.m, self.k,
+             self.col0, _device.ptr(self.cand), _device.ptr(self.ws), self.nbytes,
+             _device.stream_ptr())
+
+    def owns(self, col):
+        return self.col0 <= col < self.col0 + self.n
+
+    def pivot(self, kk, cs, ps, ck):
+        d = self._d
+        self._call("ids_dcpqr_pivot_f64", d.ptr(self.y), self.m, self.n, self.m, self.k,
+                   self.col0, kk, cs, ps, ck, d.ptr(self.a), d.ptr(self.ws), self.nbytes,
+                   d.stream_ptr())
+        return self.a
+
+    def step(self, kk, cs, a):
+        d = self._d
+        self._call("ids_dcpqr_step_f64", d.ptr(self.y), self.m, self.n, self.m, self.k,
+                   self.col0, kk, cs, d.ptr(a), d.ptr(self.cand), d.ptr(self.ws), self.nbytes,
+                   d.stream_ptr())
+
+    def results(self):
+        d = self._d
+        pos = d.empty(max(self.n, 1), torch.int64)[: self.n]
+        r = d.empty((self.k, max(self.n, 1)), torch.float64)[:, : self.n].contiguous()
+        beta = d.empty(self.k, torch.float64)
+        self._call("ids_dcpqr_results_f64", self.m, self.n, self.k, d.ptr(pos), d.ptr(r),
+                   d.ptr(beta), d.ptr(self.ws), self.nbytes, d.stream_ptr())
+        return pos, r, beta
+
+
+def pick_pivot(cands, kk):
+    """Global pivot from the per-shard candidates (rows: value, position,
+    column, column at position kk) in shard order: largest value, ties to the
+    lowest position (dgeqp3 / idamax); all-NaN norms keep position kk."""
+    best, ck = None, -1
+    for val, pos, col, nxt in np.asarray(cands, dtype=np.float64):
+        if nxt >= 0:
+            ck = int(nxt)
+        if col < 0:
+            continue
+        if best is None or val > best[0] or (val == best[0] and pos < best[1]):
+            best = (val, pos, col)
+    if best is None:
+        return ck, kk, ck
+    return int(best[2]), int(best[1]), ck
+
+
+def dcpqr_steps(shards, k, gather, broadcast):
+    """Run the k steps over this process's shards.  gather(list of device
+    cand tensors) -> host (S_total, 4) array in global shard order;
+    broadcast(a_list, owner_col) makes every local shard's a equal to the
+    owner's."""
+    for kk in range(k):
+        cs, ps, ck = pick_pivot(gather([sh.cand for sh in shards]), kk)
+        a_list = [sh.pivot(kk, cs, ps, ck) for sh in shards]
+        broadcast(a_list, cs)
+        for sh, a in zip(shards, a_list):
+            sh.step(kk, cs, a)
+
+
+def assemble_pivoted(pos_all, r_all, beta, k, rank_tol):
+    """perm (int64[R]), Rtop (k x R, pivoted order) and numerical_rank from
+    the gathered per-column positions and R rows (global column order)."""
+    pos_all = np.asarray(pos_all, dtype=np.int64)
+    ncols = pos_all.size
+    perm = np.empty(ncols, dtype=np.int64)
+    perm[pos_all] = np.arange(ncols)
+    rtop = np.zeros((k, ncols))
+    r_all = np.asarray(r_all, dtype=np.float64)
+    q = np.arange(k)[:, None]
+    rtop[:, pos_all] = np.where(pos_all[None, :] >= q, r_all, 0.0)
+    beta = np.asarray(beta, dtype=np.float64)
+    lead = abs(beta[0])
+    nr = int(np.sum(np.abs(beta) > rank_tol * lead)) if lead != 0.0 else 0
+    return perm, rtop, nr
+
+
+def cpqr_columns_sharded(y_local, col0, total_cols, rank, rank_tol=1e-12, group=None,
+                         backend=None):
+    """ID of an L x R sketch whose columns [col0, col0 + R_local) live on this
+    rank (y_local: (R_local, L)), by the column-distributed truncated CPQR;
+    the same InterpolativeDecomposition on every rank."""
+    backend = backend or DeviceBackend()
+    world, me = _world(group)
+    blocks = [row_block(total_cols, world, r) for r in range(world)]
+    shard = backend.cpqr_shard(y_local, col0, rank)
+
+    def gather(cands):
+        c = cands[0].reshape(1, 4)
+        if world > 1:
+            parts = [torch.empty_like(c) for _ in range(world)]
+            dist.all_gather(parts, c, group=group)
+            c = torch.cat(parts)
+        return c.cpu().numpy()
+
+    def broadcast(a_list, cs):
+        if world > 1:
+            owner = next(r for r, (b0, b1) in enumerate(blocks) if b0 <= cs < b1)
+            dist.broadcast(a_list[0], src=owner, group=group)
+
+    dcpqr_steps([shard], rank, gather, broadcast)
+    pos, r, beta = shard.results()
+    if world > 1:
+        width = max(b1 - b0 for b0, b1 in blocks)
+        pp = torch.zeros(width, dtype=torch.int64, device=pos.device)
+        rp = torch.zeros((rank, width), dtype=torch.float64, device=r.device)
+        pp[: pos.numel()] = pos
+        rp[:, : r.shape[1]] = r
+        pparts = [torch.empty_like(pp) for _ in range(world)]
+        rparts = [torch.empty_like(rp) for _ in range(world)]
+        dist.all_gather(pparts, pp, group=group)
+        dist.all_gather(rparts, rp, group=group)
+        sizes = [b1 - b0 for b0, b1 in blocks]
+        pos = torch.cat([p[:s] for p, s in zip(pparts, sizes)])
+        r = torch.cat([q[:, :s] for q, s in zip(rparts, sizes)], dim=1)
+    perm, rtop, nr = assemble_pivoted(pos.cpu().numpy(), r.cpu().numpy(), beta.cpu().numpy(),
+                                      rank, rank_tol)
+    return backend.coeffs_from_factors(rtop, perm, rank, total_cols, rank_tol, nr)

@@ -1,0 +1,95 @@
+"""The column-distributed CPQR kernels (csrc/cpqr_dist.cu) on
+the GPU: one shard (world 1) and several shards driven in one process with
+the real step driver (the collectives replaced by local copies), against
+LAPACK's pivots and the reference's coefficients (CPU oracle)."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+from conftest import relerr_fro
+
+pytestmark = pytest.mark.gpu
+
+ids = pytest.importorskip("paper_1901_10559_b200")
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_1901_10559_b200.distributed import (  # noqa: E402
+    DeviceBackend,
+    DeviceCpqrShard,
+    assemble_pivoted,
+    cpqr_columns_sharded,
+    dcpqr_steps,
+)
+
+
+def _near_dup(rng, m, n, base, pert):
+    b = rng.standard_normal((m, base))
+    idx = rng.integers(0, base, size=n)
+    idx[:base] = np.arange(base)
+    return b[:, idx] + pert * rng.standard_normal((m, n))
+
+
+def _run_local_shards(y, k, bounds):
+    shards = [DeviceCpqrShard(torch.from_numpy(np.ascontiguousarray(y[:, a:b].T)).cuda(), a, k)
+              for a, b in zip(bounds[:-1], bounds[1:])]
+
+    def gather(cands):
+        return torch.stack(cands).cpu().numpy()
+
+    def broadcast(a_list, cs):
+        src = next(i for i, sh in enumerate(shards) if sh.owns(cs))
+        for i, a in enumerate(a_list):
+            if i != src:
+                a.copy_(a_list[src])
+
+    dcpqr_steps(shards, k, gather, broadcast)
+    parts = [sh.results() for sh in shards]
+    pos = np.concatenate([p[0].cpu().numpy() for p in parts])
+    r = np.concatenate([p[1].cpu().numpy() for p in parts], axis=1)
+    return assemble_pivoted(pos, r, parts[0][2].cpu().numpy(), k, 1e-12)
+
+
+@pytest.mark.parametrize("m,n,k,base,pert", [(4096, 1000, 10, 10, 1e-3), (100, 2000, 20, 20, 1e-2),
+                                             (16384, 300, 20, 20, 1e-4), (40, 37, 5, 9, 1e-2)])
+def test_single_shard_matches_oracle(m, n, k, base, pert):
+    y = _near_dup(np.random.default_rng(m + n), m, n, base, pert)
+    d = cpqr_columns_sharded(torch.from_numpy(np.ascontiguousarray(y.T)).cuda(), 0, n, k)
+    want = oracle.matrix_id(y, k)
+    assert np.array_equal(d.cols, want.cols)
+    assert relerr_fro(d.coeffs, want.coeffs) <= 1e-10
+    assert d.numerical_rank == want.numerical_rank
+
+
+@pytest.mark.parametrize("bounds", [[0, 300, 600, 1000], [0, 1, 500, 999, 1000], [0, 1000]])
+def test_several_shards_match_oracle(bounds):
+    y = _near_dup(np.random.default_rng(3), 4096, 1000, 10, 1e-3)
+    k = 10
+    perm, rtop, nr = _run_local_shards(y, k, bounds)
+    want = oracle.cpqr(y, k)
+    assert np.array_equal(perm[:k], want.perm[:k])
+    mine = np.abs(rtop)[:, np.argsort(perm)]
+    ref = np.abs(want.r)[:, np.argsort(want.perm)]
+    assert relerr_fro(mine, ref) <= 1e-10
+    assert nr == want.numerical_rank
+    d = DeviceBackend().coeffs_from_factors(rtop, perm, k, 1000, 1e-12, nr)
+    w = oracle.matrix_id(y, k)
+    assert np.array_equal(d.cols, w.cols)
+    assert relerr_fro(d.coeffs, w.coeffs) <= 1e-10
+
+
+def test_zero_and_deficient_sketches():
+    y = np.zeros((64, 30))
+    d = cpqr_columns_sharded(torch.zeros((30, 64), dtype=torch.float64, device="cuda"), 0, 30, 4)
+    assert d.numerical_rank == 0 and d.rank_deficient
+    assert np.all(np.isfinite(d.coeffs))
+    want = oracle.matrix_id(y, 4)
+    assert np.array_equal(d.cols, want.cols)
+    y = _near_dup(np.random.default_rng(5), 64, 40, 5, 0.0)  # exact rank 5 < k
+    perm, rtop, nr = _run_local_shards(y, 12, [0, 13, 40])
+    w = oracle.matrix_id(y, 12)
+    assert nr == w.numerical_rank
+    assert np.array_equal(perm[:nr], w.cols[:nr])

@@ -1,0 +1,94 @@
+"""Summaries for profiles/ from the ncu outputs of a gpurun (gpurun_out/).
+
+usage: python tools/make_profiles.py ROUND   (e.g. r01)
+
+Writes, when the inputs exist:
+  profiles/ROUND_bench_launches.csv          ncu launch list of the bench command
+  profiles/ROUND_bench_launches_summary.txt  per-kernel counts / mean / total
+  profiles/ROUND_step_launches_cN.txt        one countsketch_id / tensorsketch_id
+                                             step per config (tools/prof_step.py)
+  profiles/ROUND_<kernel>_ncu_full.txt       key metrics + top stall lines of the
+                                             --set full captures
+"""
+import csv
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+
+METRICS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+    "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+]
+
+
+def run(cmd):
+    return subprocess.run(cmd, capture_output=True, text=True).stdout
+
+
+def launches(src, dst, title):
+    txt = run([sys.executable, os.path.join(ROOT, "tools", "launches.py"), src])
+    with open(dst, "w") as fh:
+        fh.write(f"# {title}\n# ncu --metrics gpu__time_duration.sum --clock-control none "
+                 "(serialized, cold-cache per-launch times)\n")
+        fh.write(txt)
+    print("wrote", dst)
+
+
+def full(rep, dst, title):
+    raw = list(csv.reader(run(["ncu", "-i", rep, "--page", "raw", "--csv"]).splitlines()))
+    if len(raw) < 3:
+        return
+    hdr, units, vals = raw[0], raw[1], raw[2]
+    lines = [f"# {title}", f"# report: {os.path.relpath(rep, ROOT)}", ""]
+    for m in METRICS:
+        if m in hdr:
+            i = hdr.index(m)
+            lines.append(f"{m:70s} {vals[i]:>20s} {units[i]}")
+    stalls = [(h, vals[i]) for i, h in enumerate(hdr)
+              if h.startswith("smsp__pcsamp_warps_issue_stalled_") and vals[i].replace(".", "").isdigit()]
+    stalls.sort(key=lambda t: -float(t[1]))
+    lines += ["", "# top warp-stall reasons (samples)"]
+    lines += [f"{h:70s} {v:>20s}" for h, v in stalls[:8]]
+    hot = run([sys.executable, os.path.join(ROOT, "tools", "ncu_hot.py"), rep, "25", "cuda"])
+    lines += ["", "# top CUDA source lines by warp-stall samples", hot]
+    with open(dst, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+    print("wrote", dst)
+
+
+if os.path.exists(os.path.join(OUT, "ev_launches_bench.csv")):
+    shutil.copy(os.path.join(OUT, "ev_launches_bench.csv"), os.path.join(PROF, f"{rnd}_bench_launches.csv"))
+    launches(os.path.join(OUT, "ev_launches_bench.csv"), os.path.join(PROF, f"{rnd}_bench_launches_summary.txt"),
+             "python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e (whole process: data "
+             "generation, warm-up, timed trials, roofline and phase timers)")
+for cfg, what in (("c2", "C2 countsketch_id, dense 1e6 x 2000, K=20, L=100"),
+                  ("c3", "C3 countsketch_id, CSR 1e7 x 1e4, nnz 1e8, K=20, L=200"),
+                  ("c4", "C4 tensorsketch_id, N=3, I=1000, R=1000, K=10, L=4096"),
+                  ("c5", "C5 tensorsketch_id, N=4, I=1e4, R=2000, K=20, L=16384")):
+    src = os.path.join(OUT, f"launches_{cfg}.csv")
+    if os.path.exists(src):
+        launches(src, os.path.join(PROF, f"{rnd}_step_launches_{cfg}.txt"),
+                 f"{what}: tools/prof_step.py (warm-up call + one step)")
+for rep, name, title in (("ev_rowmajor.ncu-rep", "cs_rowmajor", "cs_rowmajor_kernel<2,8>, C2 sketch"),
+                         ("full_tensorsketch_kernel.ncu-rep", "tensorsketch_c5",
+                          "tensorsketch_kernel<16>, C5 (N=4, I=1e4, R=2000, L=16384)"),
+                         ("full_cs_csr_bucket.ncu-rep", "cs_csr_bucket", "cs_csr_bucket_kernel, C3"),
+                         ("full_cpqr_kernel.ncu-rep", "cpqr_kernel", "cpqr_kernel (tall sketch)"),
+                         ("full_fy_phaseb.ncu-rep", "fy_phaseb", "fy_phaseb_kernel, I=1e6")):
+    p = os.path.join(OUT, rep)
+    if os.path.exists(p):
+        full(p, os.path.join(PROF, f"{rnd}_{name}_ncu_full.txt"), title)
