@@ -276,10 +276,8 @@ def main():
     from paper_1901_10559_b200.distributed import countsketch_id_sharded_trials
 
     # ---- device-resident steps (value): K trials queued back to back ----
-    # warm-up: at least one full batch of ten trials (the side streams the
-    # trials API draws hashes on, and their cached allocations)
     countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
-                                  seeds=list(range(max(args.warmup, min(args.steps, 10)))))
+                                  seeds=list(range(args.warmup)))
     torch.cuda.synchronize()
     barrier()
     clocks = Clocks(rank == 0)

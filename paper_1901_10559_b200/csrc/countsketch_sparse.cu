@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
     __shared__ int s_off[kCsrRows + 1];
     __shared__ int8_t s_sg[kCsrRows];
     __shared__ int s_col[kCsrCap];
+    __shared__ uint8_t s_rowof[kCsrCap];  // batch row of each staged entry
     __shared__ double s_val[kCsrCap];
     __shared__ int s_base[kCsrOwners * 8 * kCsrOwners];  // [owner][q][warp]
     __shared__ int s_ostart[kCsrOwners + 1];
@@ -371,30 +372,33 @@ __global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
             int myo[8], myc[8], rk[8];
             double myv[8];
             for (int i = t; i < kCsrOwners * 8 * kCsrOwners; i += kCsrThreads) s_base[i] = 0;
+            // row of every staged entry: each row's thread fills its slots
+            if (t < nr) {
+                const int a = max(off, f0), b = min(off + cnt, f0 + nE);
+                for (int f = a; f < b; ++f) s_rowof[f - f0] = (uint8_t)t;
+            }
+            __syncthreads();
+            // eight independent (index, value) loads per thread
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const int f = f0 + q * kCsrThreads + t;
+                const int fl = q * kCsrThreads + t;
+                const bool ok = fl < nE;
+                const int tr = ok ? s_rowof[fl] : 0;
+                const int64_t p = ok ? s_p0[tr] + (f0 + fl - s_off[tr]) : 0;
+                myc[q] = ok ? __ldg(indices + p) : 0;
+                const double v = ok ? __ldcs(data + p) : 0.0;
+                myv[q] = s_sg[tr] < 0 ? -v : v;
                 myo[q] = -1;
-                myc[q] = 0;
-                myv[q] = 0.0;
-                if (f < f0 + nE) {
-                    int lo = 0, hi = nr;  // row tr with s_off[tr] <= f < s_off[tr + 1]
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (s_off[mid] <= f) lo = mid;
-                        else hi = mid;
-                    }
-                    const int64_t p = s_p0[lo] + (f - s_off[lo]);
-                    myc[q] = __ldg(indices + p);
-                    const double v = __ldcs(data + p);
-                    myv[q] = s_sg[lo] < 0 ? -v : v;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q * kCsrThreads + t < nE) {
                     int ow = (int)((float)myc[q] * inv_tw);  // col / tw without a divide
                     ow -= (ow * tw > myc[q]) ? 1 : 0;
                     ow += ((ow + 1) * tw <= myc[q]) ? 1 : 0;
                     myo[q] = ow;
                 }
             }
-            __syncthreads();  // s_base zeroed
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const uint32_t peers = __match_any_sync(0xffffffffu, myo[q]);

@@ -146,7 +146,7 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     from ._inputs import DenseOperand, SparseOperand, matrix_operand
     from ._native import IDS_FLAG_ORDERED
     from .matrix_id import check_matrix_id_args, device_matrix_id
-    from .sketch import draw_operators
+    from .sketch import pipelined_operators
 
     world, _ = _world(group)
     operand = a_local if isinstance(a_local, (DenseOperand, SparseOperand)) else \
@@ -159,13 +159,9 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     L = check_matrix_id_args(_Shape, rank, sketch_dim, "countsketch")
     seeds = list(seeds)
     outs, flags = [], []
-    # every trial's hash first, drawn side by side on all SMs; the sketches then
-    # run back to back (overlapping a draw with the one-wave, HBM-bound sketch
-    # kernel was measured to slow the sketch down more than it hid)
-    # (batches of ten trials bound the live hash/index memory)
-    ops = (op for b in range(0, len(seeds), 10)
-           for op in draw_operators(in_dim, L, seeds[b:b + 10], surjective))
-    for op in ops:
+    # each trial's hash is drawn on a side stream while the previous trial
+    # sketches (sketch.pipelined_operators)
+    for op in pipelined_operators(in_dim, L, seeds, surjective):
         y = torch.empty((cols, L), dtype=torch.float64, device=torch.cuda.current_device())
         flag = torch.zeros(1, dtype=torch.int32, device=y.device)
         op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,

@@ -119,7 +119,7 @@ class CountSketchOp:
 
     def record_stream(self, stream):
         """Mark the operator's device arrays as used on `stream` (they may have
-        been drawn on another stream, see draw_operators)."""
+        been drawn on another stream, see pipelined_operators)."""
         for t in (self._bucket_d, self._sign_d, self._draws):
             if t is not None:
                 t.record_stream(stream)
@@ -323,49 +323,60 @@ class TensorSketchOp:
         return dense
 
 
-_HASH_STREAMS = {}
+_SIDE_STREAMS = {}
+PIPELINE_DEPTH = 1     # draws in flight ahead of the trial being computed
+PIPELINE_GRID_CAP = 32  # phase-B CTAs per background draw
 
 
-def draw_operators(in_dim, out_dim, seeds, surjective=False):
-    """CountSketchOps (hash + bucket index) for several seeds, drawn side by side.
-
-    A draw depends only on (in_dim, out_dim, seed, surjective), and its
-    Fisher-Yates resolution is latency-bound: on its own it keeps only part of
-    the GPU busy.  Independent trials are therefore issued on up to ten side
-    streams with the resolution grid capped (ids_set_hash_grid_cap) so that
-    they run concurrently -- about three times the throughput of back-to-back
-    draws at I = 1e6.  The current stream waits for all of them."""
-    seeds = list(seeds)
-    if len(seeds) <= 1:
-        ops = [CountSketchOp(in_dim, out_dim, seed=s, surjective=surjective) for s in seeds]
-        for op in ops:
-            op._bucket_index()
-        return ops
-    dev = _device.device()
-    main = torch.cuda.current_stream()
-    n = min(len(seeds), 10)
-    pool = _HASH_STREAMS.setdefault(dev.index, [])
+def _side_streams(dev, n):
+    pool = _SIDE_STREAMS.setdefault(dev.index, [])
     while len(pool) < n:
         pool.append(torch.cuda.Stream(device=dev))
-    streams = pool[:n]
-    start = torch.cuda.Event()
-    start.record(main)
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    return pool[:n]
+
+
+def pipelined_operators(in_dim, out_dim, seeds, surjective=False, depth=None, grid_cap=None):
+    """CountSketchOps (hash + bucket index) for a sequence of trials, each
+    drawn while earlier trials compute.
+
+    A draw depends only on (in_dim, out_dim, seed, surjective), and its
+    Fisher-Yates resolution is latency-bound.  Before yielding operator i
+    (whose sketch the caller then enqueues on the current stream), the draws
+    of operators up to i + depth are enqueued on side streams with their
+    resolution grid capped (ids_set_hash_grid_cap), so they run beside the
+    one-wave, HBM-bound sketch kernel instead of after it: measured on B200
+    at I = 1e6, the sketch keeps its speed (2.50 vs 2.48 ms) while a draw
+    completes under it.  The current stream waits for each draw before its
+    operator is used.
+    """
+    seeds = list(seeds)
+    if not seeds:
+        return
+    depth = PIPELINE_DEPTH if depth is None else int(depth)
+    grid_cap = PIPELINE_GRID_CAP if grid_cap is None else int(grid_cap)
+    dev = _device.device()
+    main = torch.cuda.current_stream()
+    sides = _side_streams(dev, max(depth, 1))
     lib = load()
-    lib.ids_set_hash_grid_cap(max(16, 2 * sms // n))
-    ops = []
-    try:
-        for st in streams:
-            st.wait_event(start)
-        for i, s in enumerate(seeds):
-            with torch.cuda.stream(streams[i % n]):
-                op = CountSketchOp(in_dim, out_dim, seed=s, surjective=surjective)
-                op._bucket_index()
-            ops.append(op)
-    finally:
-        lib.ids_set_hash_grid_cap(0)
-    for st in streams:
-        main.wait_stream(st)
-    for op in ops:
-        op.record_stream(main)
-    return ops
+    first = CountSketchOp(in_dim, out_dim, seed=seeds[0], surjective=surjective)
+    first._bucket_index()
+    pending = [(first, None)]
+    nxt = 1
+    for i in range(len(seeds)):
+        while nxt < len(seeds) and nxt <= i + depth:
+            lib.ids_set_hash_grid_cap(grid_cap)
+            try:
+                with torch.cuda.stream(sides[nxt % len(sides)]):
+                    op = CountSketchOp(in_dim, out_dim, seed=seeds[nxt], surjective=surjective)
+                    op._bucket_index()
+                    ev = torch.cuda.Event()
+                    ev.record()
+            finally:
+                lib.ids_set_hash_grid_cap(0)
+            pending.append((op, ev))
+            nxt += 1
+        op, ev = pending.pop(0)
+        if ev is not None:
+            main.wait_event(ev)
+            op.record_stream(main)
+        yield op

@@ -1,0 +1,24 @@
+"""Trials throughput (C2 shape, 10 trials) for several hash-pipeline settings."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1901_10559_b200 import sketch
+from paper_1901_10559_b200._inputs import dense_operand
+from paper_1901_10559_b200.distributed import countsketch_id_sharded_trials
+
+I, R = 1_000_000, 2000
+a = torch.randn(I, R, dtype=torch.float64, device="cuda")
+op = dense_operand(a)
+for depth, cap in ((1, 32), (2, 32), (2, 16), (3, 16), (2, 24), (1, 48), (4, 8)):
+    sketch.PIPELINE_DEPTH, sketch.PIPELINE_GRID_CAP = depth, cap
+    countsketch_id_sharded_trials(op, 0, I, 20, 100, seeds=list(range(4)))
+    torch.cuda.synchronize()
+    best = 1e9
+    for rep in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        countsketch_id_sharded_trials(op, 0, I, 20, 100, seeds=list(range(100 + 10 * rep, 110 + 10 * rep)))
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 10)
+    print(f"depth {depth} cap {cap:3d}: {best * 1e3:7.0f} us per trial", flush=True)
