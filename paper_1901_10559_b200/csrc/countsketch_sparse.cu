@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
     const IP* __restrict__ indptr, const int32_t* __restrict__ indices,
     const double* __restrict__ data, int64_t cols, int64_t row0, int64_t rows,
     int restrict_rows, const int32_t* __restrict__ order, const int64_t* __restrict__ bstart,
-    int64_t L, int nseg, double* __restrict__ out, int64_t seg_stride, int init_from_out) {
+    int64_t L, int nseg, double* __restrict__ out, int64_t seg_stride, int init_from_out,
+    int rpb) {
     extern __shared__ double acc[];  // cols
     __shared__ int64_t s_p0[kCsrRows];
     __shared__ int s_off[kCsrRows + 1];
@@ -351,17 +352,34 @@ __global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
     double* o = out + (int64_t)seg * seg_stride;
     for (int64_t c = t; c < cols; c += kCsrThreads) acc[c] = init_from_out ? o[c * L + l] : 0.0;
 
-    for (int64_t kb = s0; kb < s1; kb += kCsrRows) {
-        const int nr = (int)tmin<int64_t>(kCsrRows, s1 - kb);
+    // rpb rows per batch; the row pointers of batch b + 1 and the order entries
+    // of batch b + 2 are loaded while batch b is processed
+    auto batch_rows = [&](int64_t kb) { return kb < s1 ? (int)tmin<int64_t>(rpb, s1 - kb) : 0; };
+    int32_t e_cur = t < batch_rows(s0) ? __ldg(order + s0 + t) : 0;
+    int64_t q0 = 0, q1 = 0;
+    if (t < batch_rows(s0)) {
+        const int64_t row = (int64_t)dec_row(e_cur) - row0;
+        q0 = (int64_t)indptr[row];
+        q1 = (int64_t)indptr[row + 1];
+    }
+    int32_t e_nxt = t < batch_rows(s0 + rpb) ? __ldg(order + s0 + rpb + t) : 0;
+    for (int64_t kb = s0; kb < s1; kb += rpb) {
+        const int nr = batch_rows(kb);
         int cnt = 0;
         if (t < nr) {
-            const int32_t e = __ldg(order + kb + t);
-            const int64_t row = (int64_t)dec_row(e) - row0;
-            const int64_t p0 = (int64_t)indptr[row], p1 = (int64_t)indptr[row + 1];
-            s_p0[t] = p0;
-            s_sg[t] = e >= 0 ? 1 : -1;
-            cnt = (int)(p1 - p0);
+            s_p0[t] = q0;
+            s_sg[t] = e_cur >= 0 ? 1 : -1;
+            cnt = (int)(q1 - q0);
         }
+        int64_t n0 = 0, n1 = 0;
+        if (t < batch_rows(kb + rpb)) {
+            const int64_t row = (int64_t)dec_row(e_nxt) - row0;
+            n0 = (int64_t)indptr[row];
+            n1 = (int64_t)indptr[row + 1];
+        }
+        const int32_t e_nn = t < batch_rows(kb + 2 * rpb) ? __ldg(order + kb + 2 * rpb + t) : 0;
+        e_cur = e_nxt;
+        e_nxt = e_nn;
         int off, E;
         BS(scan_tmp).ExclusiveSum(cnt, off, E);
         if (t < nr) s_off[t] = off;
@@ -444,6 +462,8 @@ __global__ void __launch_bounds__(kCsrThreads) cs_csr_bucket_kernel(
             }
             __syncthreads();
         }
+        q0 = n0;
+        q1 = n1;
     }
     __syncthreads();
     for (int64_t c = t; c < cols; c += kCsrThreads) o[c * L + l] = acc[c];
@@ -459,10 +479,29 @@ __global__ void csr_seg_reduce_kernel(const double* __restrict__ part, int nseg,
     }
 }
 
-static int csr_nseg(int64_t out_dim, int flags) {
+// Segments per bucket for the unordered mode: the grid is out_dim * nseg
+// CTAs over `slots` resident CTAs; pick the nseg in [1, 16] that minimizes the
+// (wave-quantized) time waves / nseg -- the fewest segments within 5% of the
+// best (less partial traffic) -- keeping the partials under 1 GB.
+static int csr_nseg(int64_t out_dim, int64_t cols, int flags) {
     if (flags & IDS_FLAG_ORDERED) return 1;
-    const int64_t want = (148 * 2 * 2 + out_dim - 1) / out_dim;  // ~2 waves of 2 CTAs/SM
-    return (int)tmax<int64_t>(1, tmin<int64_t>(want, 16));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t per_sm = tmax<int64_t>(1, tmin<int64_t>(2, (227 * 1024) / (cols * 8 + 34 * 1024)));
+    const int64_t slots = sms * per_sm;
+    double t[17];
+    int nmax = 1;
+    double best_t = 1e30;
+    for (int n = 1; n <= 16; ++n) {
+        if (n > 1 && (double)n * cols * out_dim * 8.0 > 1e9) break;
+        t[n] = (double)ceil_div(out_dim * n, slots) / n;
+        best_t = fmin(best_t, t[n]);
+        nmax = n;
+    }
+    for (int n = 1; n <= nmax; ++n)  // fewest segments within 5% of the best
+        if (t[n] <= 1.05 * best_t) return n;
+    return 1;
 }
 
 extern "C" size_t ids_countsketch_csr_workspace_bytes(int64_t rows, int64_t cols, int64_t nnz,
@@ -470,7 +509,7 @@ extern "C" size_t ids_countsketch_csr_workspace_bytes(int64_t rows, int64_t cols
     (void)rows;
     if (cols <= kCsrMaxCols) {
         WsCount c;
-        c.take<double>((size_t)csr_nseg(out_dim, 0) * cols * out_dim);
+        c.take<double>((size_t)csr_nseg(out_dim, cols, 0) * cols * out_dim);
         return c.off + 256;
     }
     return csr_transpose_ws(cols, nnz, out_dim);
@@ -493,7 +532,7 @@ extern "C" int ids_countsketch_csr_f64(const void* indptr, int indptr64, const i
         ids_set_last_error("csr countsketch: bad arguments");
         return IDS_EINVAL;
     }
-    const int nseg = csr_nseg(out_dim, flags);
+    const int nseg = csr_nseg(out_dim, cols, flags);
     WsCarve ws(workspace, ws_bytes);
     double* part = nseg > 1 ? ws.take<double>((size_t)nseg * cols * out_dim) : nullptr;
     if (!ws.ok()) {
@@ -506,20 +545,23 @@ extern "C" int ids_countsketch_csr_f64(const void* indptr, int indptr64, const i
     const int restrict_rows = (row0 != 0 || rows != in_dim) ? 1 : 0;
     const size_t smem = (size_t)cols * sizeof(double);
     const unsigned grid = (unsigned)(out_dim * nseg);
+    // rows per batch: about 0.85 of a staging round of nonzeros on average
+    const double avg = rows > 0 ? (double)nnz / (double)rows : 1.0;
+    const int rpb = (int)tmax<int64_t>(32, tmin<int64_t>(kCsrRows, (int64_t)(0.85 * kCsrCap / tmax(avg, 1.0))));
     if (indptr64) {
         if (smem > 48 * 1024)
             IDS_CUDA_TRY(cudaFuncSetAttribute(cs_csr_bucket_kernel<int64_t>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cs_csr_bucket_kernel<int64_t><<<grid, kCsrThreads, smem, st>>>(
             static_cast<const int64_t*>(indptr), indices, data, cols, row0, rows, restrict_rows,
-            order_signed, bstart, out_dim, nseg, out, stride, init);
+            order_signed, bstart, out_dim, nseg, out, stride, init, rpb);
     } else {
         if (smem > 48 * 1024)
             IDS_CUDA_TRY(cudaFuncSetAttribute(cs_csr_bucket_kernel<int32_t>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cs_csr_bucket_kernel<int32_t><<<grid, kCsrThreads, smem, st>>>(
             static_cast<const int32_t*>(indptr), indices, data, cols, row0, rows, restrict_rows,
-            order_signed, bstart, out_dim, nseg, out, stride, init);
+            order_signed, bstart, out_dim, nseg, out, stride, init, rpb);
     }
     IDS_LAUNCH_CHECK();
     if (nseg > 1) {

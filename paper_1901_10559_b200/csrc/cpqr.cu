@@ -953,7 +953,8 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
     }
     // v lives in shared memory unless the sketch is very tall
     const int64_t mpad = ceil_div(rows, (int64_t)kSeg) * kSeg;
-    const bool vsmem = (size_t)(mpad + 2 * k) * sizeof(double) <= 160 * 1024;
+    bool vsmem = (size_t)(mpad + 2 * k) * sizeof(double) <= 160 * 1024;
+    if (const char* e = getenv("IDS_CPQR_VSMEM")) vsmem = vsmem && atoi(e) != 0;  // experiments
     const size_t smem = (size_t)((vsmem ? mpad : 0) + 2 * k) * sizeof(double);
     if (smem > 200 * 1024) {
         ids_set_last_error("cpqr: rank too large for the shared-memory z buffer");

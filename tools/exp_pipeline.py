@@ -22,3 +22,25 @@ for depth, cap in ((1, 32), (2, 32), (2, 16), (3, 16), (2, 24), (1, 48), (4, 8))
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / 10)
     print(f"depth {depth} cap {cap:3d}: {best * 1e3:7.0f} us per trial", flush=True)
+
+# main-stream work alone: one pre-drawn operator reused for every trial
+from paper_1901_10559_b200.matrix_id import device_matrix_id
+import paper_1901_10559_b200 as ids
+fixed = ids.CountSketchOp(I, 100, seed=7, surjective=True)
+fixed.bucket_index()
+def no_hash_trials(n):
+    outs = []
+    for _ in range(n):
+        y = torch.empty((R, 100), dtype=torch.float64, device="cuda")
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        fixed.sketch_into(op, y, flags=1, nonfinite=flag)
+        outs.append(device_matrix_id(y, 100, R, 20).packed())
+    return torch.stack(outs).cpu()
+no_hash_trials(3)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+no_hash_trials(10)
+e1.record()
+torch.cuda.synchronize()
+print(f"no hash (fixed operator): {e0.elapsed_time(e1) / 10 * 1e3:7.0f} us per trial", flush=True)
