@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
                 if (lane == 0) g.zpart[b * k + q] = s;
             }
         }
+        stamp(8);
         // GEMV W_j = Y[kk:, j]^T v in units of (column j, kSeg-row segment s),
         // two units per warp at a time (2 x 16 independent loads per lane);
         // partial dots go to W[s * n + j] and are summed in fixed order in S3.
@@ -292,10 +293,15 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             const int64_t WN = g.small ? kWarps : G * kWarps;
             for (int64_t u = wi; u < U; u += 2 * WN) {
                 double y1[kSegLoads], y2[kSegLoads];
-                const int64_t j1 = cA + u / ns, sg1 = s0 + u % ns;
+                // odd steps walk the units backwards: the tail of the previous
+                // pass is still in L2 when Y does not fit there
+                const bool rev = !g.small && (kk & 1);
+                const int64_t ua = rev ? U - 1 - u : u;
+                const int64_t j1 = cA + ua / ns, sg1 = s0 + ua % ns;
                 const int64_t u2 = u + WN;
                 const bool h2 = u2 < U;
-                const int64_t j2 = h2 ? cA + u2 / ns : j1, sg2 = h2 ? s0 + u2 % ns : sg1;
+                const int64_t ub = rev ? U - 1 - u2 : u2;
+                const int64_t j2 = h2 ? cA + ub / ns : j1, sg2 = h2 ? s0 + ub % ns : sg1;
                 const bool a1 = g.pos[j1] > kk, a2 = h2 && g.pos[j2] > kk;
                 const double* p1 = g.Y + j1 * ldy;
                 const double* p2 = g.Y + j2 * ldy;
@@ -953,8 +959,7 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
     }
     // v lives in shared memory unless the sketch is very tall
     const int64_t mpad = ceil_div(rows, (int64_t)kSeg) * kSeg;
-    bool vsmem = (size_t)(mpad + 2 * k) * sizeof(double) <= 160 * 1024;
-    if (const char* e = getenv("IDS_CPQR_VSMEM")) vsmem = vsmem && atoi(e) != 0;  // experiments
+    const bool vsmem = (size_t)(mpad + 2 * k) * sizeof(double) <= 160 * 1024;
     const size_t smem = (size_t)((vsmem ? mpad : 0) + 2 * k) * sizeof(double);
     if (smem > 200 * 1024) {
         ids_set_last_error("cpqr: rank too large for the shared-memory z buffer");
