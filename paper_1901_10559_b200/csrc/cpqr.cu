@@ -242,29 +242,30 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
                 for (int64_t r = threadIdx.x; r < mpad; r += kThreads)
                     vsm[r] = (r < kk || r >= m) ? 0.0 : (r == kk) ? 1.0 : vsm[r] * scal;
             } else {
-                // a[] already holds zeros above kk and in the padding; eight
-                // independent loads per thread per pass (mpad is a multiple of 512)
-                for (int64_t r0v = 8 * threadIdx.x - threadIdx.x % 8 * 7; r0v < mpad;
-                     r0v += 8 * kThreads) {
-                    double t[8];
+                // a[] already holds zeros above kk and in the padding; 32
+                // independent coalesced loads per thread per pass
+                for (int64_t rb = 0; rb < mpad; rb += 32 * kThreads) {
+                    double t[32];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) t[u] = g.a[r0v + 8 * u];
+                    for (int u = 0; u < 32; ++u) {
+                        const int64_t r = rb + u * kThreads + threadIdx.x;
+                        t[u] = r < mpad ? g.a[r] : 0.0;
+                    }
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int64_t r = r0v + 8 * u;
-                        vsm[r] = (r == kk) ? 1.0 : t[u] * scal;
+                    for (int u = 0; u < 32; ++u) {
+                        const int64_t r = rb + u * kThreads + threadIdx.x;
+                        if (r < mpad) vsm[r] = (r == kk) ? 1.0 : t[u] * scal;
                     }
                 }
             }
             __syncthreads();
         }
-        if (b == 0) {
-            for (int64_t r = threadIdx.x; r < m; r += kThreads)
-                g.V[kk * m + r] = r < kk ? 0.0 : vval(r);
-            if (threadIdx.x == 0) {
-                g.tau[kk] = tau;
-                g.beta[kk] = beta;
-            }
+        // every CTA stores its own rows of V[:, kk] (identical values everywhere)
+        for (int64_t r = r0 + threadIdx.x; r < r1; r += kThreads)
+            g.V[kk * m + r] = r < kk ? 0.0 : vval(r);
+        if (b == 0 && threadIdx.x == 0) {
+            g.tau[kk] = tau;
+            g.beta[kk] = beta;
         }
         if (threadIdx.x == 0 && cs >= c0 && cs < c1) g.Rcol[cs * k + kk] = beta;
         // z_q = V[:, q]^T v: whole columns (small) or owned-row partials
@@ -343,22 +344,15 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         }
         if (threadIdx.x == 0) s_nflag = 0;
         __syncthreads();
-        // one thread per owned remaining column (F is q-major: coalesced)
-        for (int64_t j = c0 + threadIdx.x; j < c1; j += kThreads) {
+        stamp(9);
+        // few owned columns: one warp per column (lanes split the segment
+        // partials and the F dot products, lane 0 finishes the column); many
+        // (short sketches): one thread per column
+        const bool warp_cols = c1 - c0 <= 2 * kWarps;
+        for (int64_t j = c0 + threadIdx.x; !warp_cols && j < c1; j += kThreads) {
             if (g.pos[j] <= kk) continue;
-            double wj = 0.0;  // fixed-order sum of the segment partials
-            {
-                const int64_t nseg = mpad / kSeg;
-                int64_t sg = kk / kSeg;
-                for (; sg + 8 <= nseg; sg += 8) {
-                    double t[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) t[u] = g.W[(sg + u) * n + j];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) wj += t[u];
-                }
-                for (; sg < nseg; ++sg) wj += g.W[sg * n + j];
-            }
+            double wj = 0.0;
+            for (int64_t sg = kk / kSeg; sg < mpad / kSeg; ++sg) wj += g.W[sg * n + j];
             double f = sub_dot(wj, g.F + j, n, zsh, 1, kk);
             double rk = sub_dot(g.Y[j * ldy + kk], g.F + j, n, vrow, 1, kk);
             f *= tau;
@@ -373,6 +367,36 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
                 const double temp2 = temp * ratio * ratio;
                 if (temp2 <= tol3z) flagged[atomicAdd(&s_nflag, 1)] = j;
                 else g.vn1[j] = vn1 * sqrt(temp);
+            }
+        }
+        for (int64_t j = c0 + wid; warp_cols && j < c1; j += kWarps) {
+            if (g.pos[j] <= kk) continue;
+            const double ykk = lane == 0 ? g.Y[j * ldy + kk] : 0.0;
+            const double vn1 = lane == 0 ? g.vn1[j] : 0.0;
+            const double vn2 = lane == 0 ? g.vn2[j] : 1.0;
+            double wj = 0.0, fz = 0.0, fv = 0.0;
+            for (int64_t sg = kk / kSeg + lane; sg < mpad / kSeg; sg += 32) wj += g.W[sg * n + j];
+            for (int64_t q = lane; q < kk; q += 32) {
+                const double fq = g.F[q * n + j];
+                fz = fma(fq, zsh[q], fz);
+                fv = fma(fq, vrow[q], fv);
+            }
+            wj = warp_sum(wj);
+            fz = warp_sum(fz);
+            fv = warp_sum(fv);
+            if (lane == 0) {
+                const double f = (wj - fz) * tau;
+                g.F[kk * n + j] = f;
+                const double rk = (ykk - fv) - f;  // V[kk, kk] = 1
+                g.Rcol[j * k + kk] = rk;
+                if (kk < m - 1 && vn1 != 0.0) {
+                    double temp = fabs(rk) / vn1;
+                    temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+                    const double ratio = vn1 / vn2;
+                    const double temp2 = temp * ratio * ratio;
+                    if (temp2 <= tol3z) flagged[atomicAdd(&s_nflag, 1)] = j;
+                    else g.vn1[j] = vn1 * sqrt(temp);
+                }
             }
         }
         __syncthreads();

@@ -40,14 +40,23 @@ __device__ __forceinline__ double dlapy2(double x, double y) {
 __device__ ArgMax reduce_partials_warp(const ArgMax* __restrict__ part, int64_t G) {
     const int lane = threadIdx.x & 31;
     ArgMax best{-1.0, INT64_MAX, -1, -1};
-    for (int64_t i = lane; i < G; i += 32) {
-        const ArgMax o = part[i];
-        if (better(o.val, o.pos, best.val, best.pos)) {
-            best.val = o.val;
-            best.pos = o.pos;
-            best.col = o.col;
+    for (int64_t i0 = 0; i0 < G; i0 += 128) {  // four candidates per lane in flight
+        ArgMax o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + lane + 32 * u;
+            if (i < G) o[u] = part[i];
+            else o[u] = ArgMax{-1.0, INT64_MAX, -1, -1};
         }
-        if (o.col_at_next >= 0) best.col_at_next = o.col_at_next;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (better(o[u].val, o[u].pos, best.val, best.pos)) {
+                best.val = o[u].val;
+                best.pos = o[u].pos;
+                best.col = o[u].col;
+            }
+            if (o[u].col_at_next >= 0) best.col_at_next = o[u].col_at_next;
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         ArgMax ot;
@@ -66,20 +75,46 @@ __device__ ArgMax reduce_partials_warp(const ArgMax* __restrict__ part, int64_t 
 }
 
 // Fixed-order sum of G partials strided by `stride`, by one warp (all lanes
-// get the result); identical in every CTA.
+// get the result); identical in every CTA.  Eight loads per lane in flight.
 __device__ __forceinline__ double warp_sum_partials(const double* __restrict__ p, int64_t G,
                                                     int64_t stride) {
     const int lane = threadIdx.x & 31;
     double s = 0.0;
-    for (int64_t i = lane; i < G; i += 32) s += p[i * stride];
+    for (int64_t i0 = 0; i0 < G; i0 += 256) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = i0 + lane + 32 * u;
+            t[u] = i < G ? p[i * stride] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += t[u];
+    }
     return warp_sum(s);
 }
 
-// y - sum_q a[q*lda] * b[q*ldb] for q < n, four independent chains.
+// y - sum_q a[q*lda] * b[q*ldb] for q < n: eight loads of each operand in
+// flight, four independent chains.
 __device__ __forceinline__ double sub_dot(double y, const double* __restrict__ a, int64_t lda,
                                           const double* __restrict__ b, int64_t ldb, int64_t n) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int64_t q = 0;
+    for (; q + 8 <= n; q += 8) {
+        double x[8], w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            x[u] = a[(q + u) * lda];
+            w[u] = b[(q + u) * ldb];
+        }
+        s0 = fma(x[0], w[0], s0);
+        s1 = fma(x[1], w[1], s1);
+        s2 = fma(x[2], w[2], s2);
+        s3 = fma(x[3], w[3], s3);
+        s0 = fma(x[4], w[4], s0);
+        s1 = fma(x[5], w[5], s1);
+        s2 = fma(x[6], w[6], s2);
+        s3 = fma(x[7], w[7], s3);
+    }
     for (; q + 4 <= n; q += 4) {
         s0 = fma(a[q * lda], b[q * ldb], s0);
         s1 = fma(a[(q + 1) * lda], b[(q + 1) * ldb], s1);

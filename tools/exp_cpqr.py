@@ -9,8 +9,8 @@ from paper_1901_10559_b200.linalg import device_cpqr
 
 lib = _native.load()
 lib.ids_debug_cpqr_timing.argtypes = [ctypes.c_void_p]
-NAMES = ["pivot col", "sync norm", "gemv", "sync gemv", "F/R/downdate",
-         "recompute", "argmax", "sync step", "hh+z"]
+NAMES = ["pivot col", "sync norm", "gemv", "sync gemv", "F/R columns",
+         "recompute", "argmax", "sync step", "hh+z", "z-reduce"]
 
 
 def near_dup(m, n, base, pert, seed):
