@@ -41,7 +41,7 @@ struct CpqrArgs {
     const double* Y;
     int64_t m, n, ldy, k;
     int small;  // m small: pivot column and z computed redundantly by every CTA
-    int vsmem;  // Householder vector kept in shared memory (else read from a)
+    int64_t vwin;  // doubles of v kept in shared memory (all of it when small)
     double rank_tol;
     int32_t* perm;
     double* Rtop;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double vsm[];  // v (m), z (k), V[kk, :kk] (k)
     const int64_t mpad = (g.m + kSeg - 1) / kSeg * kSeg;  // v padded with zeros
-    double* zsh = vsm + (g.vsmem ? mpad : 0);
+    double* zsh = vsm + g.vwin;
     double* vrow = zsh + g.k;
     __shared__ int s_nflag;
     __shared__ double s_red0;
@@ -231,38 +231,39 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             tau = (beta - alpha) / beta;
             scal = 1.0 / (alpha - beta);
         }
-        // v: in shared memory (vsm), or for very tall sketches read on the fly
-        // as a[r] * scal from the distributed pivot column (identical values)
-        const bool vs = g.vsmem;
-        auto vval = [&](int64_t r) -> double {
-            return vs ? vsm[r] : (r == kk ? 1.0 : g.a[r] * scal);
-        };
-        if (vs) {  // v with zeros above row kk and in the padding
-            if (g.small) {
-                for (int64_t r = threadIdx.x; r < mpad; r += kThreads)
-                    vsm[r] = (r < kk || r >= m) ? 0.0 : (r == kk) ? 1.0 : vsm[r] * scal;
-            } else {
-                // a[] already holds zeros above kk and in the padding; 32
-                // independent coalesced loads per thread per pass
-                for (int64_t rb = 0; rb < mpad; rb += 32 * kThreads) {
-                    double t[32];
+        // v = V[:, kk]: zero above kk, 1 at kk, a[r] * scal below (a[] holds
+        // zeros above kk and in the padding).  Small sketches keep all of v
+        // in shared memory; tall ones only the window of rows their GEMV
+        // units touch, and read single entries from a[] elsewhere.
+        auto vglob = [&](int64_t r) -> double { return r == kk ? 1.0 : g.a[r] * scal; };
+        const int64_t nseg = (m + kSeg - 1) / kSeg, s0 = kk / kSeg, ns = nseg - s0;
+        // tall: this CTA's contiguous range of units u = (sg - s0) * n + j
+        const int64_t Ut = ns * n;
+        const int64_t ub0 = g.small ? 0 : Ut * b / G, ub1 = g.small ? 0 : Ut * (b + 1) / G;
+        const int64_t vlo = g.small ? 0 : (s0 + ub0 / n) * kSeg;
+        const int64_t vhi = g.small ? mpad : (ub1 > ub0 ? (s0 + (ub1 - 1) / n + 1) * kSeg : vlo);
+        if (g.small) {
+            for (int64_t r = threadIdx.x; r < mpad; r += kThreads)
+                vsm[r] = (r < kk || r >= m) ? 0.0 : (r == kk) ? 1.0 : vsm[r] * scal;
+        } else {
+            for (int64_t rb = vlo; rb < vhi; rb += 8 * kThreads) {  // 8 loads in flight
+                double t[8];
 #pragma unroll
-                    for (int u = 0; u < 32; ++u) {
-                        const int64_t r = rb + u * kThreads + threadIdx.x;
-                        t[u] = r < mpad ? g.a[r] : 0.0;
-                    }
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t r = rb + u * kThreads + threadIdx.x;
+                    t[u] = r < vhi ? g.a[r] : 0.0;
+                }
 #pragma unroll
-                    for (int u = 0; u < 32; ++u) {
-                        const int64_t r = rb + u * kThreads + threadIdx.x;
-                        if (r < mpad) vsm[r] = (r == kk) ? 1.0 : t[u] * scal;
-                    }
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t r = rb + u * kThreads + threadIdx.x;
+                    if (r < vhi) vsm[r - vlo] = (r == kk) ? 1.0 : t[u] * scal;
                 }
             }
-            __syncthreads();
         }
+        __syncthreads();
         // every CTA stores its own rows of V[:, kk] (identical values everywhere)
         for (int64_t r = r0 + threadIdx.x; r < r1; r += kThreads)
-            g.V[kk * m + r] = r < kk ? 0.0 : vval(r);
+            g.V[kk * m + r] = r < kk ? 0.0 : (g.small ? vsm[r] : vglob(r));
         if (b == 0 && threadIdx.x == 0) {
             g.tau[kk] = tau;
             g.beta[kk] = beta;
@@ -271,55 +272,83 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         // z_q = V[:, q]^T v: whole columns (small) or owned-row partials
         for (int64_t q = wid; q < kk; q += kWarps) {
             if (g.small) {
-                const double s = warp_sum(lane_dot(g.V + q * m, vsm, kk, m));
-                if (lane == 0) zsh[q] = s;
+                const double sz = warp_sum(lane_dot(g.V + q * m, vsm, kk, m));
+                if (lane == 0) zsh[q] = sz;
             } else {
-                double s = 0.0;
-                for (int64_t r = tmax(r0, kk) + lane; r < r1; r += 32)
-                    s = fma(g.V[q * m + r], vval(r), s);
-                s = warp_sum(s);
-                if (lane == 0) g.zpart[b * k + q] = s;
+                double sz = 0.0;  // eight rows per lane in flight
+                for (int64_t rb = tmax(r0, kk); rb < r1; rb += 256) {
+                    double t[8], vv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t r = rb + lane + 32 * u;
+                        const bool ok = r < r1;
+                        t[u] = ok ? g.V[q * m + r] : 0.0;
+                        vv[u] = ok ? vglob(r) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) sz = fma(t[u], vv[u], sz);
+                }
+                sz = warp_sum(sz);
+                if (lane == 0) g.zpart[b * k + q] = sz;
             }
         }
         stamp(8);
-        // GEMV W_j = Y[kk:, j]^T v in units of (column j, kSeg-row segment s),
+        // GEMV W_j = Y[kk:, j]^T v in units of (column j, kSeg-row segment),
         // two units per warp at a time (2 x 16 independent loads per lane);
-        // partial dots go to W[s * n + j] and are summed in fixed order in S3.
-        // Small sketches: this CTA's columns and warps; tall: the whole grid.
+        // partial dots go to W[sg * n + j] and are summed in fixed order in S3.
+        // Small sketches: this CTA's columns; tall: this CTA's unit range,
+        // walked backwards on odd steps (the tail of the previous pass is
+        // still in L2 when Y does not fit there).
         {
-            const int64_t nseg = (m + kSeg - 1) / kSeg, s0 = kk / kSeg, ns = nseg - s0;
-            const int64_t cA = g.small ? c0 : 0, cB = g.small ? c1 : n;
-            const int64_t U = (cB - cA) * ns;
-            const int64_t wi = g.small ? wid : b * kWarps + wid;
-            const int64_t WN = g.small ? kWarps : G * kWarps;
-            for (int64_t u = wi; u < U; u += 2 * WN) {
-                double y1[kSegLoads], y2[kSegLoads];
-                // odd steps walk the units backwards: the tail of the previous
-                // pass is still in L2 when Y does not fit there
-                const bool rev = !g.small && (kk & 1);
-                const int64_t ua = rev ? U - 1 - u : u;
-                const int64_t j1 = cA + ua / ns, sg1 = s0 + ua % ns;
-                const int64_t u2 = u + WN;
-                const bool h2 = u2 < U;
-                const int64_t ub = rev ? U - 1 - u2 : u2;
-                const int64_t j2 = h2 ? cA + ub / ns : j1, sg2 = h2 ? s0 + ub % ns : sg1;
+            const int64_t cnt = g.small ? (c1 - c0) * ns : ub1 - ub0;
+            const bool rev = !g.small && (kk & 1);
+            const bool full = (m % kSeg) == 0;  // no clamping needed
+            for (int64_t li = wid; li < cnt; li += 2 * kWarps) {
+                int64_t j1, sg1, j2, sg2;
+                const bool h2 = li + kWarps < cnt;
+                if (g.small) {
+                    j1 = c0 + li / ns;
+                    sg1 = s0 + li % ns;
+                    const int64_t l2 = h2 ? li + kWarps : li;
+                    j2 = c0 + l2 / ns;
+                    sg2 = s0 + l2 % ns;
+                } else {
+                    const uint32_t nn = (uint32_t)n;
+                    const uint32_t ua = (uint32_t)(rev ? ub1 - 1 - li : ub0 + li);
+                    const uint32_t l2 = (uint32_t)(h2 ? li + kWarps : li);
+                    const uint32_t ub = (uint32_t)(rev ? ub1 - 1 - l2 : ub0 + l2);
+                    j1 = ua % nn;
+                    sg1 = s0 + ua / nn;
+                    j2 = ub % nn;
+                    sg2 = s0 + ub / nn;
+                }
                 const bool a1 = g.pos[j1] > kk, a2 = h2 && g.pos[j2] > kk;
                 const double* p1 = g.Y + j1 * ldy;
                 const double* p2 = g.Y + j2 * ldy;
-                // branch-free: clamped rows (v is zero there and above kk)
                 const int64_t b1 = sg1 * kSeg + lane, b2 = sg2 * kSeg + lane;
+                double y1[kSegLoads], y2[kSegLoads];
+                if (full) {
 #pragma unroll
-                for (int t = 0; t < kSegLoads; ++t) {
-                    y1[t] = p1[tmin(b1 + 32 * t, m - 1)];
-                    y2[t] = p2[tmin(b2 + 32 * t, m - 1)];
+                    for (int t = 0; t < kSegLoads; ++t) {
+                        y1[t] = p1[b1 + 32 * t];
+                        y2[t] = p2[b2 + 32 * t];
+                    }
+                } else {  // clamped rows (v is zero there)
+#pragma unroll
+                    for (int t = 0; t < kSegLoads; ++t) {
+                        y1[t] = p1[tmin(b1 + 32 * t, m - 1)];
+                        y2[t] = p2[tmin(b2 + 32 * t, m - 1)];
+                    }
                 }
+                const double* v1 = vsm + (b1 - vlo);
+                const double* v2 = vsm + (b2 - vlo);
                 double s1 = 0.0, s2 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
                 for (int t = 0; t < kSegLoads; t += 2) {
-                    s1 = fma(y1[t], vval(b1 + 32 * t), s1);
-                    t1 = fma(y1[t + 1], vval(b1 + 32 * t + 32), t1);
-                    s2 = fma(y2[t], vval(b2 + 32 * t), s2);
-                    t2 = fma(y2[t + 1], vval(b2 + 32 * t + 32), t2);
+                    s1 = fma(y1[t], v1[32 * t], s1);
+                    t1 = fma(y1[t + 1], v1[32 * t + 32], t1);
+                    s2 = fma(y2[t], v2[32 * t], s2);
+                    t2 = fma(y2[t + 1], v2[32 * t + 32], t2);
                 }
                 const double w1 = warp_sum(s1 + t1), w2 = warp_sum(s2 + t2);
                 if (lane == 0) {
@@ -410,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             double s = 0.0;
             for (int64_t r = kk + 1 + lane; r < m; r += 32) {
                 double v = sub_dot(y[r], g.V + r, m, g.F + j, n, kk);
-                v = fma(-vval(r), g.F[kk * n + j], v);
+                v = fma(-(g.small ? vsm[r] : vglob(r)), g.F[kk * n + j], v);
                 s = fma(v, v, s);
             }
             s = warp_sum(s);
@@ -451,7 +480,6 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
 // exchanged through distributed shared memory (double-buffered by step
 // parity), the pivot column and its F row are read from the owner CTA's
 // shared memory, and every CTA builds the Householder vector itself.
-constexpr int kClusterMax = 16;
 
 struct ClusterArgs {
     const double* Y;
@@ -981,10 +1009,15 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
             return IDS_OK;
         }
     }
-    // v lives in shared memory unless the sketch is very tall
+    // shared memory: v (whole, short sketches) or the window of v rows this
+    // CTA's GEMV units touch (tall sketches), then z and row kk of V
     const int64_t mpad = ceil_div(rows, (int64_t)kSeg) * kSeg;
-    const bool vsmem = (size_t)(mpad + 2 * k) * sizeof(double) <= 160 * 1024;
-    const size_t smem = (size_t)((vsmem ? mpad : 0) + 2 * k) * sizeof(double);
+    const bool small = rows <= 1024;
+    const int G = (int)tmin<int64_t>(
+        grid_size(rows, cols, (size_t)((small ? mpad : 0) + 2 * k) * sizeof(double)), kMaxG);
+    const int64_t nseg = mpad / kSeg;
+    const int64_t vwin = small ? mpad : (ceil_div(nseg * cols, G) / cols + 2) * kSeg;
+    const size_t smem = (size_t)(vwin + 2 * k) * sizeof(double);
     if (smem > 200 * 1024) {
         ids_set_last_error("cpqr: rank too large for the shared-memory z buffer");
         return IDS_EINVAL;
@@ -992,7 +1025,6 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
     if (smem > 48 * 1024)
         IDS_CUDA_TRY(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
-    const int G = (int)tmin<int64_t>(grid_size(rows, cols, smem), kMaxG);
     CpqrArgs a{};
     a.Y = Y;
     a.m = rows;
@@ -1000,8 +1032,8 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
     a.ldy = ldy;
     a.k = k;
     a.rank_tol = rank_tol;
-    a.small = rows <= 1024 ? 1 : 0;
-    a.vsmem = vsmem ? 1 : 0;
+    a.small = small ? 1 : 0;
+    a.vwin = vwin;
     a.perm = perm;
     a.Rtop = Rtop;
     a.numerical_rank = numerical_rank;
