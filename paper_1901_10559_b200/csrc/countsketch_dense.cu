@@ -50,20 +50,6 @@ struct VecT<2> {
     }
 };
 
-template <>
-struct VecT<4> {
-    static __device__ __forceinline__ void load(const double* p, double* v) {
-        const double2 x = __ldcs(reinterpret_cast<const double2*>(p));
-        const double2 y = __ldcs(reinterpret_cast<const double2*>(p) + 1);
-        v[0] = x.x;
-        v[1] = x.y;
-        v[2] = y.x;
-        v[3] = y.y;
-    }
-};
-
-int g_dense_variant = 0;  // debug: 1 = <4,8>, 2 = <4,4> for 4-aligned rows
-
 // unit = ((l * nseg + seg) * nchunks + chunk); one warp per unit.
 template <int VEC, int UNR>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
@@ -332,21 +318,7 @@ extern "C" int ids_countsketch_dense_f64(const double* A, int64_t rows, int64_t 
     double* out = p.nseg > 1 ? part : Y;
     const int64_t seg_stride = out_dim * cols;
     const int init_from_out = (p.nseg == 1 && accumulate) ? 1 : 0;
-    if (layout == IDS_ROW_MAJOR && g_dense_variant && aligned2 && cols % 4 == 0 && ld % 4 == 0) {
-        const int restrict_rows = (row0 != 0 || rows != in_dim) ? 1 : 0;
-        const int nchunks = (int)ceil_div(cols, 128);
-        const int64_t units = out_dim * nchunks * p.nseg;
-        const unsigned grid = (unsigned)ceil_div(units, kWarpsPerBlock);
-        if (g_dense_variant == 1)
-            cs_rowmajor_kernel<4, 8><<<grid, kWarpsPerBlock * 32, 0, st>>>(
-                A, ld, cols, row0, rows, restrict_rows, order_signed, bstart, out_dim,
-                nchunks, p.nseg, out, seg_stride, init_from_out);
-        else
-            cs_rowmajor_kernel<4, 4><<<grid, kWarpsPerBlock * 32, 0, st>>>(
-                A, ld, cols, row0, rows, restrict_rows, order_signed, bstart, out_dim,
-                nchunks, p.nseg, out, seg_stride, init_from_out);
-        IDS_LAUNCH_CHECK();
-    } else if (layout == IDS_ROW_MAJOR) {
+    if (layout == IDS_ROW_MAJOR) {
         const int restrict_rows = (row0 != 0 || rows != in_dim) ? 1 : 0;
         const unsigned grid = (unsigned)ceil_div(p.units, kWarpsPerBlock);
         if (p.vec == 2)
@@ -404,6 +376,3 @@ extern "C" int ids_dense_has_nonfinite(const double* A, int64_t rows, int64_t co
     IDS_LAUNCH_CHECK();
     return IDS_OK;
 }
-
-// Debug hook: dense row-major kernel variant (0 default).
-extern "C" void ids_debug_dense_variant(int v) { g_dense_variant = v; }
