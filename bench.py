@@ -214,6 +214,66 @@ def config_of(args, w, world):
             "parallelism": f"rows{world}", "l2": "A (>126 MB) larger than L2, no flush"}
 
 
+def secondary_configs(torch, dev, steps=3):
+    """Live device timings (CUDA events, after warm-up) of one full ID at the
+    other BASELINE.json configs, on seeded synthetic inputs of their shapes
+    built on the device: C3 CSR 1e7 x 1e4 with 1e8 nonzeros,
+    C4 / C5 CP tensors with near-duplicate terms.  Reported beside the
+    headline, not part of it."""
+    import paper_1901_10559_b200 as ids
+    from paper_1901_10559_b200._inputs import SparseOperand
+    from paper_1901_10559_b200.matrix_id import countsketch_device, device_matrix_id
+
+    def timed(fn):
+        for s in range(2):
+            fn(10_000 + s)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in range(steps):
+            fn(20_000 + s)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    out = {}
+    g = torch.Generator(device=dev).manual_seed(3)
+    I, R, per, K, L = 10_000_000, 10_000, 10, 20, 200
+    indptr = torch.arange(0, I + 1, dtype=torch.int64, device=dev) * per
+    idx = torch.randint(0, R, (I, per), generator=g, device=dev).sort(dim=1).values
+    idx = idx.to(torch.int32).reshape(-1)
+    data = torch.randn(I * per, generator=g, device=dev, dtype=torch.float64)
+    csr = SparseOperand("csr", indptr, idx, data, I, R, I * per)
+    ms = timed(lambda s: countsketch_device(csr, K, L, seed=s)[0].to_host("countsketch"))
+    out["C3"] = {"id_ms": ms, "shape": "CSR 1e7 x 1e4, nnz 1e8 (10 per row), K=20, L=200",
+                 "algorithmic_bytes": int(I * per * 12 + (I + 1) * 8)}
+    del indptr, idx, data, csr
+    for name, N, In, R, base, pert, K, L in (("C4", 3, 1000, 1000, 10, 1e-3, 10, 4096),
+                                             ("C5", 4, 10_000, 2000, 20, 1e-4, 20, 16384)):
+        g = torch.Generator(device=dev).manual_seed(4 if name == "C4" else 5)
+        bases = torch.randint(0, base, (R,), generator=g, device=dev)
+        bases[:base] = torch.arange(base, device=dev)
+        facs = []
+        for _ in range(N):
+            f = torch.randn(In, R, generator=g, device=dev, dtype=torch.float64)
+            f[:, :base] /= torch.linalg.vector_norm(f[:, :base], dim=0)
+            f = f[:, bases] + pert * torch.randn(In, R, generator=g, device=dev,
+                                                 dtype=torch.float64)
+            f /= torch.linalg.vector_norm(f, dim=0)
+            facs.append(f.t().contiguous().t())  # column-major I_n x R
+        w = torch.rand(R, generator=g, device=dev, dtype=torch.float64) * 0.5 + 0.5
+
+        def step(s, facs=facs, w=w, N=N, In=In, R=R, K=K, L=L):
+            y = ids.TensorSketchOp([In] * N, L, seed=s).apply_device(facs, w)
+            return device_matrix_id(y, L, R, K).to_host("tensorsketch")
+
+        out[name] = {"id_ms": timed(step),
+                     "shape": f"CP N={N}, I_n={In}, R={R}, K={K}, L={L}, near-duplicate terms",
+                     "algorithmic_bytes": int(N * In * R * 8)}
+        del facs
+    return out
+
+
 # ----------------------------------------------------------------- GPU -----
 def main():
     args = parse()
