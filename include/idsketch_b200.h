@@ -262,6 +262,20 @@ int ids_dcpqr_step_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy
 int ids_dcpqr_results_f64(int64_t rows, int64_t ncols, int64_t k, int64_t* pos, double* R,
                           double* beta, void* workspace, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Matrix Market input (replaces scipy.io.mmread behind
+ * mmio.py:23-28 and cp_tensor.py:346-361).  Host-side, multi-threaded parse.
+ * ids_mm_info: size line and kind[3] = {format (0 coordinate, 1 array),
+ *   field (0 real, 1 integer, 2 pattern, 3 complex), symmetry (0 general,
+ *   1 symmetric, 2 skew-symmetric, 3 hermitian)}; entries = stored entries.
+ * ids_mm_read: the stored entries in file order -- coordinate: 0-based
+ *   row/col and the value (1.0 for pattern, real part for complex); array:
+ *   values only (column-major, symmetric storage unexpanded).  Host pointers.
+ * ------------------------------------------------------------------------- */
+int ids_mm_info(const char* path, int64_t* rows, int64_t* cols, int64_t* entries, int32_t* kind);
+int ids_mm_read(const char* path, int nthreads, int64_t* row, int64_t* col, double* val,
+                int64_t capacity, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,6 +35,13 @@ from .matrix_id import (
     matrix_id,
     matrix_sketch,
 )
+from .mmio import (
+    load_cp_dir,
+    read_matrix_market,
+    read_matrix_market_device,
+    save_cp_dir,
+    write_matrix_market,
+)
 from .sketch import CountSketchOp, TensorSketchOp
 
 __version__ = "0.1.0"
@@ -59,10 +66,15 @@ __all__ = [
     "est_spectral_norm",
     "gram_hadamard",
     "id_residual_operator",
+    "load_cp_dir",
     "matrix_id",
     "matrix_operator",
     "matrix_sketch",
+    "read_matrix_market",
+    "read_matrix_market_device",
+    "save_cp_dir",
     "tensor_id_from_sketch",
     "tensorsketch_id",
     "triangular_solve",
+    "write_matrix_market",
 ]
