@@ -136,6 +136,8 @@ def sparse_operand(a):
 
 
 def matrix_operand(a, name="a"):
+    if isinstance(a, (DenseOperand, SparseOperand)):
+        return a
     if sp.issparse(a):
         return sparse_operand(a)
     return dense_operand(a, name)

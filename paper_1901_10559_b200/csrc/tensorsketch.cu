@@ -49,6 +49,7 @@ struct TsArgs {
     double2* spec_glob;   // per-CTA running spectrum (N2 + 1 bins) when not in smem
     int spec_in_smem;
     int stage_cap;        // staged CountSketch entries (shared memory) per round
+    int y_vec;            // Y 16-byte aligned: paired output stores
     int64_t* tlog;        // debug: per-phase ns accumulated by CTA 0 (NULL: off)
 };
 
@@ -534,7 +535,18 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
         const double wr = g.weights ? g.weights[r] : 1.0;
         double* y = g.Y + r * (int64_t)L;
         double nrm = 0.0;
-        if (!g.linear) {
+        if (!g.linear && g.y_vec) {
+            // y[2m], y[2m+1] from z[m]: one 16-byte streaming store per pair
+            // (L even, Y 16-byte aligned)
+            double2* y2 = reinterpret_cast<double2*>(y);
+            for (int mm = t; mm < L / 2; mm += T) {
+                const double2 z = buf[pad<PS>(mm)];
+                const double v0 = z.x * scale * wr, v1 = -z.y * scale * wr;
+                __stcs(y2 + mm, make_double2(v0, v1));
+                nrm = fma(v0, v0, nrm);
+                nrm = fma(v1, v1, nrm);
+            }
+        } else if (!g.linear) {
             for (int j = t; j < L; j += T) {
                 const double2 z = buf[pad<PS>(j >> 1)];
                 const double v = ((j & 1) ? -z.y : z.x) * scale * wr;
@@ -668,6 +680,7 @@ extern "C" int ids_tensorsketch_f64(int n_modes, const double* const* factors, c
     a.spec_glob = specg;
     a.spec_in_smem = p.spec_in_smem;
     a.stage_cap = p.stage_cap;
+    a.y_vec = (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && out_dim % 2 == 0;
     a.tlog = g_ts_tlog;
     if (colnorm2) IDS_CUDA_TRY(cudaMemsetAsync(colnorm2, 0, sizeof(double) * ncols, st));
     auto kern = p.ept == 16 ? tensorsketch_kernel<16> : tensorsketch_kernel<8>;

@@ -248,7 +248,7 @@ class CountSketchOp:
     def apply(self, a):
         """Sketch `a` (sparse or dense, in_dim rows); returns a dense array
         (sketch.py:116-122).  CUDA-tensor input returns a CUDA tensor."""
-        if not sp.issparse(a):
+        if not sp.issparse(a) and not isinstance(a, (DenseOperand, SparseOperand)):
             _check_rows(a, self.in_dim, "CountSketch")
         elif a.shape[0] != self.in_dim:
             raise ValueError(f"CountSketch expects {self.in_dim} input rows, got {a.shape[0]}")

@@ -170,3 +170,27 @@ def test_residual_operator_matches_explicit_residual():
         true = np.linalg.norm(resid, 2)
         assert est <= true + 1e-10 and est >= true / 2.0
         assert relerr_fro(np.array([est]), np.array([true])) <= 0.5
+
+
+# ---------------------------------------------------------------- I/O --------
+def test_matrix_market_to_device_feeds_the_path(tmp_path):
+    from scipy.io import mmwrite
+
+    rng = np.random.default_rng(24)
+    a = sp.random_array((4000, 150), density=0.03, rng=rng, format="csc")
+    p = tmp_path / "a.mtx"
+    mmwrite(p, a, precision=17)
+    host = ids.read_matrix_market(p)
+    dev = ids.read_matrix_market_device(p)
+    assert dev.kind == "csr" and dev.shape == (4000, 150)
+    op = ids.CountSketchOp(4000, 30, seed=7, surjective=True)
+    assert np.array_equal(op.apply(dev), op.apply(host))  # both ordered: scipy's sums
+    d1 = ids.countsketch_id(host, 10, 30, seed=7)
+    d2 = ids.countsketch_id(dev, 10, 30, seed=7)
+    assert np.array_equal(d1.cols, d2.cols) and np.array_equal(d1.coeffs, d2.coeffs)
+    w = oracle.countsketch_id(host, 10, 30, seed=7)
+    assert np.array_equal(d1.cols, w.cols)
+    x = rng.standard_normal((60, 7))
+    mmwrite(p, x, precision=17)
+    t = ids.read_matrix_market_device(p)
+    assert t.is_cuda and np.array_equal(t.cpu().numpy(), x)
