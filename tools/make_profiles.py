@@ -84,11 +84,14 @@ for cfg, what in (("c2", "C2 countsketch_id, dense 1e6 x 2000, K=20, L=100"),
         launches(src, os.path.join(PROF, f"{rnd}_step_launches_{cfg}.txt"),
                  f"{what}: tools/prof_step.py (warm-up call + one step)")
 for rep, name, title in (("ev_rowmajor.ncu-rep", "cs_rowmajor", "cs_rowmajor_kernel<2,8>, C2 sketch"),
-                         ("full_tensorsketch_kernel.ncu-rep", "tensorsketch_c5",
+                         ("full_tensorsketch_c5.ncu-rep", "tensorsketch_c5",
                           "tensorsketch_kernel<16>, C5 (N=4, I=1e4, R=2000, L=16384)"),
-                         ("full_cs_csr_bucket.ncu-rep", "cs_csr_bucket", "cs_csr_bucket_kernel, C3"),
-                         ("full_cpqr_kernel.ncu-rep", "cpqr_kernel", "cpqr_kernel (tall sketch)"),
-                         ("full_fy_phaseb.ncu-rep", "fy_phaseb", "fy_phaseb_kernel, I=1e6")):
+                         ("full_cpqr_c5.ncu-rep", "cpqr_c5", "cpqr_kernel, C5 sketch 16384 x 2000, k=20"),
+                         ("full_cs_csr_bucket.ncu-rep", "cs_csr_bucket",
+                          "cs_csr_bucket_kernel, C3 (CSR 1e7 x 1e4, nnz 1e8, L=200)"),
+                         ("full_fy_phaseb.ncu-rep", "fy_phaseb", "fy_phaseb_kernel, hash I=1e6, L=100"),
+                         ("full_cpqr_cluster.ncu-rep", "cpqr_cluster",
+                          "cpqr_cluster_kernel, C2 sketch 100 x 2000, k=20")):
     p = os.path.join(OUT, rep)
     if os.path.exists(p):
         full(p, os.path.join(PROF, f"{rnd}_{name}_ncu_full.txt"), title)
