@@ -151,13 +151,23 @@ __device__ __forceinline__ void dft<16>(double2* v) {
     dft16(v);
 }
 
+// Staged entry q lives at sidx(q): within each 256-entry block the [thread][8]
+// layout is transposed to [8][thread], so a warp's staging stores (8
+// consecutive entries per thread) hit 32 distinct banks.
+__device__ __forceinline__ int sidx(int q) { return (q & ~255) | ((q & 7) << 5) | ((q >> 3) & 31); }
+
+__device__ __forceinline__ int fpad(int f) { return f + (f >> 3) + (f >> 6); }
+constexpr int kFineSlots = 128 + 16 + 2;
+
 // exp(-2 pi i m / M) from two small shared-memory tables:
-// coarse[m >> 7] * fine[m & 127]  (M a power of two).
+// coarse[m >> 7] * fine[m & 127]  (M a power of two).  The fine table is
+// padded (fpad) so that the strided index patterns of the passes hit
+// distinct shared-memory banks.
 struct Twiddle {
     const double2* coarse;
     const double2* fine;
     __device__ __forceinline__ double2 operator()(int m) const {
-        return cmul(coarse[m >> 7], fine[m & 127]);
+        return cmul(coarse[m >> 7], fine[fpad(m & 127)]);
     }
 };
 
@@ -240,7 +250,8 @@ __device__ void stockham_pass16(double2* buf, int N2, int Ns, int M, const Twidd
         const int k = j % Ns;
         if (Ns > 1 && k != 0) {
             const int m1 = k * (M / (Ns * 16));
-            const double2 w1 = tw(m1), w2 = tw(2 * m1), w4 = tw(4 * m1), w8 = tw(8 * m1);
+            const double2 w1 = tw(m1);
+            const double2 w2 = cmul(w1, w1), w4 = cmul(w2, w2), w8 = cmul(w4, w4);
             v[1] = cmul(v[1], w1);
             v[2] = cmul(v[2], w2);
             v[4] = cmul(v[4], w4);
@@ -310,7 +321,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     constexpr int PS = EPT >= 16 ? 4 : 3;
     extern __shared__ double2 buf[];
     __shared__ double2 tw_coarse[kMaxHalf * 2 / 128 + 1];
-    __shared__ double2 tw_fine[128];
+    __shared__ double2 tw_fine[kFineSlots];
     __shared__ const double* s_fac[kMaxModes];
     __shared__ const int32_t* s_ord[kMaxModes];
     __shared__ const int32_t* s_key[kMaxModes];
@@ -334,7 +345,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     for (int m = t; m < 128; m += T) {
         double sn, cs;
         sincospi(2.0 * (double)m / (double)M, &sn, &cs);
-        tw_fine[m] = make_double2(cs, -sn);
+        tw_fine[fpad(m)] = make_double2(cs, -sn);
     }
     for (int q = t; q * 128 < M; q += T) {
         double sn, cs;
@@ -416,8 +427,8 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
                             if (gb + u < ns) {
-                                st_key[gb + u] = kq[u];
-                                st_val[gb + u] = x[u];
+                                st_key[sidx(gb + u)] = kq[u];
+                                st_val[sidx(gb + u)] = x[u];
                             } else {
                                 kq[u] = INT_MIN;  // past the staged block
                             }
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                     // in increasing row order (its registers, then the following
                     // threads' entries from shared memory)
                     if (gb < cn) {
-                        int32_t cur = gb > 0 ? st_key[gb - 1] : s_prevkey;
+                        int32_t cur = gb > 0 ? st_key[sidx(gb - 1)] : s_prevkey;
                         bool own = false;
                         double acc = 0.0;
 #pragma unroll
@@ -444,7 +455,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                         }
                         if (own) {  // the last run may continue past this thread
                             int q = gb + 8;
-                            while (q < ns && st_key[q] == cur) acc += st_val[q++];
+                            while (q < ns && st_key[sidx(q)] == cur) acc += st_val[sidx(q++)];
                             if (q == ns) {  // ... and past the look-ahead (rare)
                                 for (int kg = c0 + q; kg < In && __ldg(key + kg) == cur; ++kg) {
                                     const int32_t e = __ldg(ord + kg);
