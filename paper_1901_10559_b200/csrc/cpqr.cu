@@ -540,9 +540,9 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
 
     // load the Y slice ROW-major (Ys[r * ncl + jj]: a thread per column walks
     // rows conflict-free), norms, positions
-    for (int64_t e = threadIdx.x; e < (int64_t)nc * m; e += kThreads) {
-        const int64_t jj = e / m, r = e % m;
-        S.Ys[r * g.ncl + jj] = g.Y[(c0 + jj) * g.ldy + r];
+    for (int jj = wid; jj < nc; jj += kWarps) {  // a warp per column, coalesced rows
+        const double* ycol = g.Y + (c0 + jj) * g.ldy;
+        for (int64_t r = lane; r < m; r += 32) S.Ys[r * g.ncl + jj] = ycol[r];
     }
     __syncthreads();
     for (int jj = threadIdx.x; jj < nc; jj += kThreads) {
@@ -646,7 +646,9 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_cluster_kernel(ClusterArgs g
         }
         stamp(0);
         // ---- pivot column from the owner's shared memory, Householder ----
-        int owner = 0;
+        // owner of column cs: the largest b with n * b / CS <= cs (one division)
+        int owner = (int)tmin<int64_t>(CS - 1, (cs * CS) / n);
+        while (owner > 0 && n * owner / CS > cs) --owner;
         while (owner + 1 < CS && n * (owner + 1) / CS <= cs) ++owner;
         const int64_t oc0 = n * owner / CS;
         {   // copy the pivot column and its F row from the owner (one remote read each)
