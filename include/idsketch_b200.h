@@ -167,6 +167,12 @@ int ids_tensorsketch_f64(int n_modes, const double* const* factors, const int64_
                          const int32_t* const* sorted_bucket, int64_t out_dim,
                          const double* weights, double* Y, double* colnorm2, void* workspace,
                          size_t ws_bytes, void* stream);
+/* 1 when ids_tensorsketch_f64 handles (n_modes, out_dim) in its fused
+ * one-CTA-per-term kernel (transform half-length <= 8192: power-of-two
+ * out_dim <= 16384, or n_modes * (out_dim - 1) + 1 <= 16384 otherwise).
+ * Larger sketches take the per-mode CountSketch + batched FFT route of the
+ * Python layer. */
+int ids_tensorsketch_fused_ok(int n_modes, int64_t out_dim);
 
 /* ---------------------------------------------------------------------------
  * Truncated column-pivoted Householder QR (k steps).  Replaces linalg.py:97-102

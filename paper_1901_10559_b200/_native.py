@@ -57,6 +57,7 @@ SIGNATURES = {
          _c_p, _c_i64, _c_p, _c_int, _c_int, _c_p, _c_p, _c_sz, _c_p],
     ),
     "ids_tensorsketch_workspace_bytes": (_c_sz, [_c_int, _c_p, _c_i64, _c_i64]),
+    "ids_tensorsketch_fused_ok": (_c_int, [_c_int, _c_i64]),
     "ids_tensorsketch_f64": (
         _c_int,
         [_c_int, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz,

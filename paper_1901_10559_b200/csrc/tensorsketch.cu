@@ -630,6 +630,11 @@ TsPlan plan_ts(int n_modes, int64_t L) {
 // `buf` (device int64[8]); NULL disables.
 extern "C" void ids_debug_ts_timing(int64_t* buf) { g_ts_tlog = buf; }
 
+extern "C" int ids_tensorsketch_fused_ok(int n_modes, int64_t out_dim) {
+    if (n_modes < 1 || n_modes > kMaxModes || out_dim < 1) return 0;
+    return plan_ts(n_modes, out_dim).N2 <= kMaxHalf ? 1 : 0;
+}
+
 extern "C" size_t ids_tensorsketch_workspace_bytes(int n_modes, const int64_t* dims,
                                                    int64_t ncols, int64_t out_dim) {
     (void)dims;

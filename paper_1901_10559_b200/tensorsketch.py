@@ -65,6 +65,8 @@ def tensorsketch_device(op, factors, weights=None):
     dev_f = [factor_to_device(f) for f in factors]
     n = len(dev_f)
     L = op.out_dim
+    if not query("ids_tensorsketch_fused_ok", n, L):
+        return _tensorsketch_spectral(op, dev_f, w, ncols, L)
     idx = [m._bucket_index() for m in op.mode_ops]
     fac_p = (ctypes.c_void_p * n)(*[_device.ptr(t) for t in dev_f])
     ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _, _ in idx])
@@ -82,4 +84,24 @@ def tensorsketch_device(op, factors, weights=None):
         _device.ptr(w), _device.ptr(y), None, _device.ptr(ws), nbytes, _device.stream_ptr(),
     )
     # dev_f may be freed now: the caching allocator reuses memory in stream order
+    return y
+
+
+def _tensorsketch_spectral(op, dev_f, w, ncols, L):
+    """Transforms longer than the fused kernel holds in shared memory
+    (sketch.py:170-186 step by step): each mode's CountSketch S_n A_n with the
+    dense kernel (bit-exact, scipy's order), then length-L rfft / irfft
+    through cuFFT with the spectra multiplied left to right, weights applied
+    after the inverse -- the reference's own sequence of operations."""
+    from ._inputs import dense_operand
+    from ._native import IDS_FLAG_ORDERED
+
+    spec = None
+    for mode, f in zip(op.mode_ops, dev_f):  # f: (R, I_n) == col-major I_n x R
+        y = mode.apply_device(dense_operand(f.t()), flags=IDS_FLAG_ORDERED)
+        s = torch.fft.rfft(y, n=L, dim=1)
+        spec = s if spec is None else spec.mul_(s)
+    y = torch.fft.irfft(spec, n=L, dim=1).contiguous()
+    if w is not None:
+        y.mul_(w[:, None])
     return y

@@ -189,3 +189,19 @@ def test_reduced_preserves_sparsity_pattern():
             got = reduced_f.toarray()[:, t] != 0
             want = orig_f.toarray()[:, col] != 0
             assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dims,L", [([30, 20, 10, 8], 5000), ([12, 11], 32768), ([9, 9, 9], 16385)])
+def test_long_transforms_beyond_the_fused_kernel(dims, L):
+    """Sketch lengths whose transform exceeds the fused kernel's shared memory
+    take the per-mode CountSketch + cuFFT route; same result as pocketfft."""
+    from paper_1901_10559_b200._native import query
+
+    assert not query("ids_tensorsketch_fused_ok", len(dims), L)
+    rng = np.random.default_rng(L)
+    factors = [rng.standard_normal((d, 5)) for d in dims]
+    lam = rng.random(5) + 0.5
+    op = ids.TensorSketchOp(dims, L, seed=9)
+    want = oracle.OracleTensorSketch(dims, L, seed=9).apply(factors, lam)
+    assert relerr_fro(op.apply(factors, lam), want) <= 1e-12
+    assert query("ids_tensorsketch_fused_ok", 4, 16384) and query("ids_tensorsketch_fused_ok", 3, 3000)
