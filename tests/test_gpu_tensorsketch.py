@@ -191,10 +191,12 @@ def test_reduced_preserves_sparsity_pattern():
             assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("dims,L", [([30, 20, 10, 8], 5000), ([12, 11], 32768), ([9, 9, 9], 16385)])
+@pytest.mark.parametrize("dims,L", [([30, 20, 10, 8], 5000), ([12, 11], 32768), ([9, 9, 9], 16385),
+                                    ([2] * 9, 16)])
 def test_long_transforms_beyond_the_fused_kernel(dims, L):
     """Sketch lengths whose transform exceeds the fused kernel's shared memory
-    take the per-mode CountSketch + cuFFT route; same result as pocketfft."""
+    (and more than 8 modes) take the per-mode CountSketch + cuFFT route; same
+    result as pocketfft."""
     from paper_1901_10559_b200._native import query
 
     assert not query("ids_tensorsketch_fused_ok", len(dims), L)
