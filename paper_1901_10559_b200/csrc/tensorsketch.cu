@@ -76,6 +76,9 @@ template <int R>
 __device__ __forceinline__ void dft(double2* v);
 
 template <>
+__device__ __forceinline__ void dft<1>(double2*) {}  // length-1 transforms (N2 = 1)
+
+template <>
 __device__ __forceinline__ void dft<2>(double2* v) {
     const double2 a = v[0], b = v[1];
     v[0] = cadd(a, b);
@@ -285,8 +288,10 @@ __device__ void stockham_pass16(double2* buf, int N2, int Ns, int M, const Twidd
 
 // 8 points per thread: radix-8 passes (+ one radix-4/2).  16 points per thread
 // (N2 = 8192, the longest transform): radix-16 passes in registers + radix-2.
+// Every Stockham pass but the last; returns the stride Ns of the last pass
+// (its radix is N2 / Ns).
 template <int EPT>
-__device__ __forceinline__ void fft_forward(double2* buf, int N2, int M, const Twiddle tw) {
+__device__ __forceinline__ int fft_head(double2* buf, int N2, int M, const Twiddle tw) {
     constexpr int PS = EPT >= 16 ? 4 : 3;
     int Ns = 1;
     if constexpr (EPT >= 16) {
@@ -300,11 +305,120 @@ __device__ __forceinline__ void fft_forward(double2* buf, int N2, int M, const T
             Ns *= 8;
         }
     }
-    const int rem = N2 / Ns;  // the last pass, in place
-    if (rem == 16) stockham_last<16, PS>(buf, N2, M, tw);
-    else if (rem == 8) stockham_last<8, PS>(buf, N2, M, tw);
-    else if (rem == 4) stockham_last<4, PS>(buf, N2, M, tw);
-    else if (rem == 2) stockham_last<2, PS>(buf, N2, M, tw);
+    return Ns;
+}
+
+// One butterfly of the last (in-place) pass: outputs X[j + r * Ns].
+template <int R, int PS>
+__device__ __forceinline__ void last_butterfly(const double2* buf, int N2, int M, const Twiddle tw,
+                                               int j, double2* u) {
+    const int Ns = N2 / R;
+#pragma unroll
+    for (int r = 0; r < R; ++r) u[r] = buf[pad<PS>(j + r * Ns)];
+    if (Ns > 1 && j != 0) {
+        const double2 w1 = tw(j * (M / N2));
+        double2 w = w1;
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+            u[r] = cmul(u[r], w);
+            if (r + 1 < R) w = cmul(w, w1);
+        }
+    }
+    dft<R>(u);
+}
+
+// The last FFT pass fused with the real-spectrum untangle and the product
+// into the running spectrum S.  Untangle pair (p, N2 - p) is complete in the
+// butterflies j and Ns - j, so one thread takes both (no shared-memory round
+// trip, no barrier); every slot it reads is cleared for the next mode.
+template <int R, int PS>
+__device__ void last_pass_untangle(double2* buf, int N2, int M, const Twiddle tw,
+                                   double2* spec, bool first_mode) {
+    const int Ns = N2 / R;
+    // item i takes butterflies i and Ns - i (item 0: the self-paired 0 and Ns / 2)
+    const int items = Ns > 1 ? Ns / 2 : 1;
+    for (int i = threadIdx.x; i < items; i += blockDim.x) {
+        const int j = i, j2 = i == 0 ? Ns / 2 : Ns - i;
+        const bool two = j2 != j;
+        double2 a[R], c[R];
+        last_butterfly<R, PS>(buf, N2, M, tw, j, a);
+        if (two) last_butterfly<R, PS>(buf, N2, M, tw, j2, c);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            buf[pad<PS>(j + r * Ns)] = make_double2(0.0, 0.0);
+            if (two) buf[pad<PS>(j2 + r * Ns)] = make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // outputs of butterfly j (h = 0) and j2 (h = 1)
+            if (h == 1 && !two) break;
+            const int jj = h == 0 ? j : j2;
+            const bool self = jj == 0 || 2 * jj == Ns;  // partner in the same butterfly
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int p = r * Ns + jj;
+                if (p > N2 / 2) continue;  // the pair is handled from its lower index
+                const double2 zk = h == 0 ? a[r] : c[r];
+                double2 zm;
+                if (jj == 0) zm = h == 0 ? a[(R - r) % R] : c[(R - r) % R];
+                else if (self) zm = h == 0 ? a[R - r - 1] : c[R - r - 1];
+                else zm = h == 0 ? c[R - r - 1] : a[R - r - 1];
+                const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+                const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // zk - conj(zm)
+                const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);   // d * (-i/2)
+                const double2 wo = cmul(tw(p), o);
+                const double2 xlo = cadd(e, wo);
+                const double2 xhi = conj2(csub(e, wo));
+                if (first_mode) {
+                    spec[p] = xlo;
+                    if (N2 - p != p) spec[N2 - p] = xhi;
+                } else {
+                    spec[p] = cmul(spec[p], xlo);
+                    if (N2 - p != p) spec[N2 - p] = cmul(spec[N2 - p], xhi);
+                }
+            }
+        }
+    }
+}
+
+// Real-spectrum untangle of the finished transform, multiplied into S (each
+// slot is read by exactly one pair and cleared for the next mode).
+template <int PS>
+__device__ void untangle_pairs(double2* buf, int N2, const Twiddle tw, double2* spec,
+                               bool first_mode) {
+    const int T = blockDim.x, npairs = N2 / 2 + 1;
+    for (int p0 = threadIdx.x; p0 < npairs; p0 += 4 * T) {
+        double2 sk[4], sm[4];
+        if (!first_mode) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // independent spectrum loads first
+                const int p = min(p0 + u * T, npairs - 1);
+                sk[u] = spec[p];
+                sm[u] = spec[N2 - p];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int p = p0 + u * T;
+            if (p >= npairs) break;
+            const double2 zk = buf[pad<PS>(p % N2)];
+            const double2 zm = buf[pad<PS>((N2 - p) % N2)];
+            buf[pad<PS>(p % N2)] = make_double2(0.0, 0.0);
+            buf[pad<PS>((N2 - p) % N2)] = make_double2(0.0, 0.0);
+            const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+            const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // zk - conj(zm)
+            const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);   // d * (-i/2)
+            const double2 wo = cmul(tw(p), o);
+            const double2 xlo = cadd(e, wo);
+            const double2 xhi = conj2(csub(e, wo));
+            if (first_mode) {
+                spec[p] = xlo;
+                if (N2 - p != p) spec[N2 - p] = xhi;
+            } else {
+                spec[p] = cmul(sk[u], xlo);
+                if (N2 - p != p) spec[N2 - p] = cmul(sm[u], xhi);
+            }
+        }
+    }
 }
 
 __global__ void twiddle_kernel(double2* tw, int64_t M) {
@@ -498,47 +612,31 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
             }
             __syncthreads();
             stamp(3);
-            fft_forward<EPT>(buf, N2, M, tw);
+            // one call site for the FFT passes (all but the last)
+            const int rem = N2 / fft_head<EPT>(buf, N2, M, tw);
             stamp(4);
             if (n < g.n_modes) {
-                // ---- untangle the real spectrum, multiply into S ----
-                for (int p0 = t; p0 < npairs; p0 += 4 * T) {
-                    double2 sk[4], sm[4];
-                    if (n > 0) {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {  // independent spectrum loads first
-                            const int p = min(p0 + u * T, npairs - 1);
-                            sk[u] = spec[p];
-                            sm[u] = spec[N2 - p];
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int p = p0 + u * T;
-                        if (p >= npairs) break;
-                        const double2 zk = buf[pad<PS>(p % N2)];
-                        const double2 zm = buf[pad<PS>((N2 - p) % N2)];
-                        // each slot is read by exactly one pair: clear it for the
-                        // next mode's CountSketch (the inverse overwrites it anyway)
-                        buf[pad<PS>(p % N2)] = make_double2(0.0, 0.0);
-                        buf[pad<PS>((N2 - p) % N2)] = make_double2(0.0, 0.0);
-                        const double2 e = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
-                        const double2 d = make_double2(zk.x - zm.x, zk.y + zm.y);  // zk - conj(zm)
-                        const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);   // d * (-i/2)
-                        const double2 wo = cmul(tw(p), o);
-                        const double2 xlo = cadd(e, wo);
-                        const double2 xhi = conj2(csub(e, wo));
-                        if (n == 0) {
-                            spec[p] = xlo;
-                            if (N2 - p != p) spec[N2 - p] = xhi;
-                        } else {
-                            spec[p] = cmul(sk[u], xlo);
-                            if (N2 - p != p) spec[N2 - p] = cmul(sm[u], xhi);
-                        }
-                    }
+                // ---- last pass + untangle + product into S, fused ----
+                if constexpr (EPT >= 16) {  // N2 = 8192 = 16^3 * 2
+                    last_pass_untangle<2, PS>(buf, N2, M, tw, spec, n == 0);
+                } else {  // shorter transforms: plain last pass, then the untangle
+                    if (rem == 2) stockham_last<2, PS>(buf, N2, M, tw);
+                    else if (rem == 4) stockham_last<4, PS>(buf, N2, M, tw);
+                    else if (rem == 8) stockham_last<8, PS>(buf, N2, M, tw);
+                    else stockham_last<1, PS>(buf, N2, M, tw);
+                    untangle_pairs<PS>(buf, N2, tw, spec, n == 0);
                 }
                 __syncthreads();
                 stamp(5);
+            } else {  // inverse: plain last pass, then the output below
+                if constexpr (EPT >= 16) {
+                    stockham_last<2, PS>(buf, N2, M, tw);
+                } else {
+                    if (rem == 2) stockham_last<2, PS>(buf, N2, M, tw);
+                    else if (rem == 4) stockham_last<4, PS>(buf, N2, M, tw);
+                    else if (rem == 8) stockham_last<8, PS>(buf, N2, M, tw);
+                    else stockham_last<1, PS>(buf, N2, M, tw);
+                }
             }
         }
         // y[2m] = Re z[m], y[2m+1] = Im z[m], z = conj(FFT(conj Z)) / N2
