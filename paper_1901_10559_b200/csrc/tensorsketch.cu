@@ -380,6 +380,31 @@ __device__ void last_pass_untangle(double2* buf, int N2, int M, const Twiddle tw
     }
 }
 
+// Inverse transform: the last (radix-2) pass fused with the output.  Butterfly
+// j yields z[j] and z[j + N2/2]; y[2m], y[2m+1] = Re z[m], -Im z[m] (scaled)
+// leave as 16-byte streaming stores, and the slots are cleared for the next
+// column.  Returns this thread's share of the column's squared norm.
+template <int PS>
+__device__ double last_pass_output(double2* buf, int N2, int M, const Twiddle tw, double2* y2,
+                                   double scale, double wr) {
+    const int Ns = N2 / 2;
+    double nrm = 0.0;
+    for (int j = threadIdx.x; j < Ns; j += blockDim.x) {
+        double2 u[2];
+        last_butterfly<2, PS>(buf, N2, M, tw, j, u);
+        buf[pad<PS>(j)] = make_double2(0.0, 0.0);
+        buf[pad<PS>(j + Ns)] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double v0 = u[h].x * scale * wr, v1 = -u[h].y * scale * wr;
+            __stcs(y2 + j + h * Ns, make_double2(v0, v1));
+            nrm = fma(v0, v0, nrm);
+            nrm = fma(v1, v1, nrm);
+        }
+    }
+    return nrm;
+}
+
 // Real-spectrum untangle of the finished transform, multiplied into S (each
 // slot is read by exactly one pair and cleared for the next mode).
 template <int PS>
@@ -486,6 +511,8 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
             tprev = tn;
         }
     };
+    bool out_done = false;  // the previous column's fused output cleared the buffer
+    double out_nrm = 0.0;
     for (int64_t r = blockIdx.x; r < g.ncols; r += gridDim.x) {
         // passes 0..N-1: forward transform of mode n's CountSketch, product into S;
         // pass N: inverse transform of S (one inlined FFT for all passes)
@@ -498,7 +525,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 const int32_t* ord = s_ord[n];
                 const int32_t* key = s_key[n];
                 const int In = s_dim[n];
-                if (n == 0)  // later modes find the buffer zeroed by the untangle
+                if (n == 0 && !out_done)  // else zeroed by the untangle / fused output
                     for (int l = t; l < N2; l += T) buf[pad<PS>(l)] = make_double2(0.0, 0.0);
                 stamp(0);
                 for (int c0 = 0; c0 < In; c0 += stage_heads) {
@@ -630,7 +657,14 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 stamp(5);
             } else {  // inverse: plain last pass, then the output below
                 if constexpr (EPT >= 16) {
-                    stockham_last<2, PS>(buf, N2, M, tw);
+                    if (!g.linear && g.y_vec) {  // last pass fused with the output
+                        out_nrm = last_pass_output<PS>(buf, N2, M, tw,
+                                                       reinterpret_cast<double2*>(g.Y + r * (int64_t)L),
+                                                       1.0 / (double)N2, g.weights ? g.weights[r] : 1.0);
+                        out_done = true;
+                    } else {
+                        stockham_last<2, PS>(buf, N2, M, tw);
+                    }
                 } else {
                     if (rem == 2) stockham_last<2, PS>(buf, N2, M, tw);
                     else if (rem == 4) stockham_last<4, PS>(buf, N2, M, tw);
@@ -643,8 +677,10 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
         const double scale = 1.0 / (double)N2;
         const double wr = g.weights ? g.weights[r] : 1.0;
         double* y = g.Y + r * (int64_t)L;
-        double nrm = 0.0;
-        if (!g.linear && g.y_vec) {
+        double nrm = out_nrm;
+        if (out_done) {
+            // written by the fused last pass; the buffer is already clear
+        } else if (!g.linear && g.y_vec) {
             // y[2m], y[2m+1] from z[m]: one 16-byte streaming store per pair
             // (L even, Y 16-byte aligned)
             double2* y2 = reinterpret_cast<double2*>(y);
@@ -678,6 +714,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
             for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
             if ((t & 31) == 0) atomicAdd(g.colnorm2 + r, nrm);
         }
+        out_nrm = 0.0;
         __syncthreads();
         stamp(6);
     }
