@@ -15,6 +15,7 @@ all-reduce.  A (16 GB) is larger than L2 (126 MB), so no flush is needed.
 """
 
 import argparse
+import datetime
 import json
 import os
 import subprocess
@@ -107,7 +108,7 @@ class Clocks:
         if not enabled:
             return
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
@@ -118,7 +119,9 @@ class Clocks:
         except Exception:
             self.proc = None
 
-    def stop(self, gpu_index):
+    def stop(self, gpu_index, window=None):
+        """Median SM clock, max clock and throttle reasons of the samples taken
+        inside `window` (wall-clock seconds, time.time()) when given."""
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -128,7 +131,17 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9 or not f[0].isdigit() or int(f[0]) != gpu_index:
+            if len(f) < 10:
+                continue
+            if window is not None:
+                try:
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if not window[0] <= ts <= window[1]:
+                    continue
+            f = f[1:]
+            if not f[0].isdigit() or int(f[0]) != gpu_index:
                 continue
             try:
                 sm.append(float(f[1]))
@@ -275,6 +288,15 @@ def secondary_configs(torch, dev, steps=3):
 
 
 # ----------------------------------------------------------------- GPU -----
+def prime_nvml():
+    """One nvidia-smi call at start-up: the driver/NVML initialization it can
+    trigger lands long before anything is timed."""
+    try:
+        subprocess.run(["nvidia-smi", "-q", "-d", "CLOCK"], capture_output=True, timeout=120)
+    except Exception:
+        pass
+
+
 def main():
     args = parse()
     w = dict(WORKLOADS[args.workload])
@@ -286,6 +308,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args, w, rank, world)
 
+    if local == 0:
+        prime_nvml()
     import torch
     import torch.distributed as dist
 
@@ -338,12 +362,22 @@ def main():
     from paper_1901_10559_b200.distributed import countsketch_id_sharded_trials
 
     # ---- device-resident steps (value): K trials queued back to back ----
+    # warm-up: at least as many trials as one timed batch, so the allocator
+    # already holds every buffer a batch needs (no cudaMalloc while timed)
     countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
-                                  seeds=list(range(args.warmup)))
+                                  seeds=list(range(max(args.warmup, args.steps))))
+    torch.cuda.synchronize()
+    # the clock sampler runs under load: started here (its start-up lands in an
+    # idle second), then untimed trials for about a second before and after
+    # the timed batch; only samples from that busy window are reported
+    clocks = Clocks(rank == 0)
+    time.sleep(1.0)
+    busy0 = time.time()
+    while time.time() - busy0 < 1.0:
+        countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
+                                      seeds=list(range(args.steps)))
     torch.cuda.synchronize()
     barrier()
-    clocks = Clocks(rank == 0)
-    time.sleep(1.5)  # let nvidia-smi/NVML initialize before the timed region
     n0 = lib.ids_launch_count()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -357,11 +391,16 @@ def main():
     barrier()
     launches = (lib.ids_launch_count() - n0) // max(args.steps, 1)
     ms = start.elapsed_time(stop) / args.steps
+    busy1 = time.time()
+    while time.time() - busy1 < 1.0:
+        countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
+                                      seeds=list(range(args.steps)))
+    torch.cuda.synchronize()
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    clk = clocks.stop(local)
+    clk = clocks.stop(local, window=(busy0, time.time()))
 
     # ---- dominant kernel alone: the sketch (roofline) ----
     op = ids.CountSketchOp(w["rows"], w["L"], seed=5, surjective=True)

@@ -19,8 +19,7 @@
 //     time, then by one warp once i < 65536;
 //   * the Fisher-Yates swaps themselves are applied in parallel: the value
 //     that lands at position i is found by chasing "first later swap that
-//     targeted this position" links (see fy_final_kernel); the swaps are
-//     grouped by target with one stable radix sort, O(I) work.
+//     targeted this position" links (see fy_final_kernel), O(I) work.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -661,27 +660,25 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
 //   final[i]   = incoming(i) if j[i] == i;
 //              = incoming(min{s in S_{j[i]} : s > i}) if that exists,
 //              = slots[j[i]] otherwise;     final[0] = incoming(0).
-// Group the swaps by target: key = j[s] (or n for a no-op swap j[s] == s),
-// value = s; a stable radix sort then lists each S_p in increasing s.
-__global__ void fy_keys_kernel(const int32_t* __restrict__ j, int64_t n, int32_t* __restrict__ keys,
-                               int32_t* __restrict__ vals) {
+__global__ void fy_count_kernel(const int32_t* __restrict__ j, int64_t n, int32_t* first,
+                                int32_t* gcount) {
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; s < n;
          s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t p = j[s];
-        keys[s - 1] = p < s ? p : (int32_t)n;
-        vals[s - 1] = (int32_t)s;
+        if (p < s) {
+            atomicMin(&first[p], (int32_t)s);
+            atomicAdd(&gcount[p], 1);
+        }
     }
 }
 
-// first[p] = min S_p (group heads); pos_of[s] = rank of swap s in the sorted list
-__global__ void fy_heads_kernel(const int32_t* __restrict__ sk, const int32_t* __restrict__ sv,
-                                int64_t m, int64_t n, int32_t* __restrict__ first,
-                                int32_t* __restrict__ pos_of) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t p = sk[k];
-        pos_of[sv[k]] = (int32_t)k;
-        if (p < n && (k == 0 || sk[k - 1] != p)) first[p] = sv[k];
+__global__ void fy_scatter_kernel(const int32_t* __restrict__ j, int64_t n,
+                                  const int32_t* __restrict__ goff, int32_t* cursor,
+                                  int32_t* members) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; s < n;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = j[s];
+        if (p < s) members[goff[p] + atomicAdd(&cursor[p], 1)] = (int32_t)s;
     }
 }
 
@@ -702,19 +699,25 @@ __device__ __forceinline__ int32_t incoming(int32_t s, const int32_t* __restrict
 __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_t L,
                                 const int32_t* __restrict__ tail,
                                 const int32_t* __restrict__ first,
-                                const int32_t* __restrict__ sk, const int32_t* __restrict__ sv,
-                                const int32_t* __restrict__ pos_of, int32_t* bucket) {
-    const int64_t m = n - 1;
+                                const int32_t* __restrict__ goff,
+                                const int32_t* __restrict__ members, int32_t* bucket) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t out;
-        const int32_t p = i == 0 ? 0 : j[i];
-        if (i == 0 || p == i) {
-            out = incoming((int32_t)i, first, L, tail);
-        } else {  // the next swap after i that targets p: i's successor in S_p
-            const int64_t k = pos_of[i] + 1;
-            const int32_t best = (k < m && sk[k] == p) ? sv[k] : kNone;
-            out = best == kNone ? slot_value(p, L, tail) : incoming(best, first, L, tail);
+        if (i == 0) {
+            out = incoming(0, first, L, tail);
+        } else {
+            const int32_t p = j[i];
+            if (p == i) {
+                out = incoming((int32_t)i, first, L, tail);
+            } else {
+                int32_t best = kNone;
+                for (int32_t k = goff[p], e = goff[p + 1]; k < e; ++k) {
+                    const int32_t m = members[k];
+                    if (m > i && m < best) best = m;
+                }
+                out = best == kNone ? slot_value(p, L, tail) : incoming(best, first, L, tail);
+            }
         }
         bucket[i] = out;
     }
@@ -755,19 +758,17 @@ HashPlan make_plan(int64_t I, int64_t L, int surj) {
     p.scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, p.scan_bytes, (int64_t*)nullptr, (int64_t*)nullptr,
                                   (int)p.nblk);
-    p.scan2_bytes = 0;  // radix sort of the swaps by target
-    if (surj && I > 1)
-        cub::DeviceRadixSort::SortPairs(nullptr, p.scan2_bytes, (const int32_t*)nullptr,
-                                        (int32_t*)nullptr, (const int32_t*)nullptr,
-                                        (int32_t*)nullptr, (int)(I - 1));
+    p.scan2_bytes = 0;
+    if (surj)
+        cub::DeviceScan::ExclusiveSum(nullptr, p.scan2_bytes, (int32_t*)nullptr,
+                                      (int32_t*)nullptr, (int)(I + 1));
     return p;
 }
 
 template <class W>
 void carve(W& ws, const HashPlan& p, int64_t** blk_cnt, int64_t** blk_off, int64_t** scal,
            void** scan_tmp, int32_t** tail, uint32_t** draws, int32_t** jarr, int32_t** first,
-           int32_t** keys, int32_t** vals, int32_t** skeys, int32_t** svals, int32_t** pos_of,
-           FyState** fst, FyChunk** chunks,
+           int32_t** gcount, int32_t** goff, int32_t** members, FyState** fst, FyChunk** chunks,
            int64_t** starts) {
     *blk_cnt = ws.template take<int64_t>(p.nblk);
     *blk_off = ws.template take<int64_t>(p.nblk);
@@ -779,11 +780,9 @@ void carve(W& ws, const HashPlan& p, int64_t** blk_cnt, int64_t** blk_off, int64
         *draws = ws.template take<uint32_t>(p.nbuf);
         *jarr = ws.template take<int32_t>(p.I + 1);
         *first = ws.template take<int32_t>(p.I + 1);
-        *keys = ws.template take<int32_t>(p.I + 1);
-        *vals = ws.template take<int32_t>(p.I + 1);
-        *skeys = ws.template take<int32_t>(p.I + 1);
-        *svals = ws.template take<int32_t>(p.I + 1);
-        *pos_of = ws.template take<int32_t>(p.I + 1);
+        *gcount = ws.template take<int32_t>(p.I + 1);
+        *goff = ws.template take<int32_t>(p.I + 1);
+        *members = ws.template take<int32_t>(p.I + 1);
         *fst = ws.template take<FyState>(1);
         *chunks = ws.template take<FyChunk>(p.max_chunks);
         *starts = ws.template take<int64_t>(p.max_chunks + 1);
@@ -807,12 +806,12 @@ extern "C" size_t ids_hash_workspace_bytes(int64_t in_dim, int64_t out_dim, int 
     NullCarve nc;
     int64_t *a, *b, *c;
     void* d;
-    int32_t *e, *g, *h, *i2, *j2, *k2, *l2, *m2;
+    int32_t *e, *g, *h, *i2, *j2, *k2;
     uint32_t* f;
     FyState* fs;
     FyChunk* fc;
     int64_t* sts;
-    carve(nc, p, &a, &b, &c, &d, &e, &f, &g, &h, &i2, &j2, &k2, &l2, &m2, &fs, &fc, &sts);
+    carve(nc, p, &a, &b, &c, &d, &e, &f, &g, &h, &i2, &j2, &k2, &fs, &fc, &sts);
     return nc.off + 256;
 }
 
@@ -834,14 +833,14 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
     WsCarve ws(workspace, ws_bytes);
     int64_t *blk_cnt, *blk_off, *scal;
     void* scan_tmp;
-    int32_t *tail = nullptr, *jarr = nullptr, *first = nullptr, *keys = nullptr,
-            *vals = nullptr, *skeys = nullptr, *svals = nullptr, *pos_of = nullptr;
+    int32_t *tail = nullptr, *jarr = nullptr, *first = nullptr, *gcount = nullptr,
+            *goff = nullptr, *members = nullptr;
     uint32_t* draws = nullptr;
     FyState* fst = nullptr;
     FyChunk* chunks = nullptr;
     int64_t* starts = nullptr;
-    carve(ws, p, &blk_cnt, &blk_off, &scal, &scan_tmp, &tail, &draws, &jarr, &first, &keys,
-          &vals, &skeys, &svals, &pos_of, &fst, &chunks, &starts);
+    carve(ws, p, &blk_cnt, &blk_off, &scal, &scan_tmp, &tail, &draws, &jarr, &first, &gcount,
+          &goff, &members, &fst, &chunks, &starts);
     if (!ws.ok()) {
         ids_set_last_error("hash: workspace too small");
         return IDS_EWORKSPACE;
@@ -900,18 +899,18 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
         if (I > 1) {
             fill_i32_kernel<<<1024, 256, 0, st>>>(first, I, kNone);
             IDS_LAUNCH_CHECK();
+            IDS_CUDA_TRY(cudaMemsetAsync(gcount, 0, sizeof(int32_t) * (I + 1), st));
             const unsigned grid = (unsigned)tmin<int64_t>(ceil_div(I, 256), 148 * 16);
-            fy_keys_kernel<<<grid, 256, 0, st>>>(jarr, I, keys, vals);
+            fy_count_kernel<<<grid, 256, 0, st>>>(jarr, I, first, gcount);
             IDS_LAUNCH_CHECK();
-            int bits = 1;
-            while ((1LL << bits) <= I) ++bits;  // keys in [0, I]
             size_t sb = p.scan2_bytes;
-            IDS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(scan_tmp, sb, keys, skeys, vals, svals,
-                                                         (int)(I - 1), 0, bits, st));
-            fy_heads_kernel<<<grid, 256, 0, st>>>(skeys, svals, I - 1, I, first, pos_of);
+            IDS_CUDA_TRY(
+                cub::DeviceScan::ExclusiveSum(scan_tmp, sb, gcount, goff, (int)(I + 1), st));
+            IDS_CUDA_TRY(cudaMemsetAsync(gcount, 0, sizeof(int32_t) * (I + 1), st));
+            fy_scatter_kernel<<<grid, 256, 0, st>>>(jarr, I, goff, gcount, members);
             IDS_LAUNCH_CHECK();
-            fy_final_kernel<<<grid, 256, 0, st>>>(jarr, I, out_dim, tail, first, skeys, svals,
-                                                   pos_of, bucket);
+            fy_final_kernel<<<grid, 256, 0, st>>>(jarr, I, out_dim, tail, first, goff,
+                                                   members, bucket);
             IDS_LAUNCH_CHECK();
         } else {
             fill_i32_kernel<<<1, 32, 0, st>>>(bucket, 1, 0);
