@@ -1,0 +1,85 @@
+"""Boundary shapes and input kinds of the matrix path against the oracle."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+
+from conftest import relerr_fro
+
+pytestmark = pytest.mark.gpu
+
+ids = pytest.importorskip("paper_1901_10559_b200")
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+
+def _same_id(d, w):
+    assert np.array_equal(d.cols, w.cols)
+    assert relerr_fro(d.coeffs, w.coeffs) <= 1e-10
+    assert d.numerical_rank == w.numerical_rank and d.rank_deficient == w.rank_deficient
+
+
+@pytest.mark.parametrize("rows,cols,k,L", [(50, 1, 1, 1), (12, 30, 5, 5), (21, 9, 3, 20),
+                                           (2, 3, 1, 1), (300, 40, 40, 41)])
+def test_boundary_shapes(rows, cols, k, L):
+    rng = np.random.default_rng(rows * 100 + cols)
+    a = rng.standard_normal((rows, cols))
+    for surj in (True, False):
+        d = ids.countsketch_id(a, k, L, seed=rows, surjective=surj)
+        w = oracle.countsketch_id(a, k, L, seed=rows, surjective=surj)
+        assert np.array_equal(d.cols[:w.numerical_rank], w.cols[:w.numerical_rank])
+        if not w.rank_deficient:
+            _same_id(d, w)
+
+
+def test_input_kinds_agree():
+    rng = np.random.default_rng(50)
+    base = rng.standard_normal((400, 8)) @ rng.standard_normal((8, 60))
+    want = oracle.countsketch_id(base, 8, 24, seed=2)
+    kinds = {
+        "C": base,
+        "F": np.asfortranarray(base),
+        "strided numpy view": np.hstack([base, base])[:, :60],
+        "float32": base.astype(np.float32),
+        "int": np.round(base * 1000).astype(np.int64),
+        "cuda": torch.from_numpy(base).cuda(),
+        "cuda padded rows": torch.nn.functional.pad(torch.from_numpy(base), (0, 5)).cuda()[:, :60],
+        "cuda transposed": torch.from_numpy(np.ascontiguousarray(base.T)).cuda().t(),
+        "cuda padded columns": torch.nn.functional.pad(
+            torch.from_numpy(np.ascontiguousarray(base.T)), (0, 7)).cuda()[:, :400].t(),
+    }
+    for name, a in kinds.items():
+        d = ids.countsketch_id(a, 8, 24, seed=2)
+        if name in ("float32", "int"):
+            w = oracle.countsketch_id(np.asarray(a, dtype=np.float64), 8, 24, seed=2)
+            _same_id(d, w)
+        else:
+            _same_id(d, want)
+    # sparse formats: CSR (int32 and int64 indptr), CSC, COO with duplicates
+    s = sp.random_array((500, 70), density=0.05, rng=rng, format="csr")
+    w = oracle.countsketch_id(sp.csc_array(s), 6, 20, seed=3)
+    s64 = sp.csr_array((s.data, s.indices.astype(np.int64), s.indptr.astype(np.int64)), shape=s.shape)
+    coo = s.tocoo()
+    dup = sp.coo_array((np.concatenate([coo.data / 2, coo.data / 2]),
+                        (np.concatenate([coo.row, coo.row]), np.concatenate([coo.col, coo.col]))),
+                       shape=s.shape)
+    for a in (s, s64, sp.csc_array(s), dup):
+        _same_id(ids.countsketch_id(a, 6, 20, seed=3), w)
+
+
+def test_argument_errors():
+    a = np.ones((10, 4))
+    for bad in (dict(rank=0), dict(rank=5), dict(rank=2, sketch_dim=1), dict(rank=2, sketch_dim=10)):
+        with pytest.raises(ValueError):
+            ids.countsketch_id(a, **bad)
+    with pytest.raises(ValueError):
+        ids.countsketch_id(np.ones(10), 1)
+    with pytest.raises(ValueError):
+        ids.countsketch_id(np.ones((0, 3)), 1)
+    bad = sp.eye_array(10, 3, format="csr") * 1.0
+    bad.data[0] = np.inf
+    with pytest.raises(ValueError):
+        ids.countsketch_id(bad, 1, 2)
