@@ -504,7 +504,8 @@ def main():
             "config": config_of(args, w, world),
             "id_seconds": single_ms * 1e-3,
             "trials": "K trials (seeds) of the same A queued back to back, one host sync at "
-                      "the end; each trial draws its own hash on the device",
+                      "the end; each trial draws its own hash on the device, on a side stream "
+                      "beside the previous trial's sketch (sketch.pipelined_operators)",
             "phases_ms": {"hash_and_index": hash_ms, "sketch": sk_ms, "cpqr_and_coeffs": id_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
