@@ -6,7 +6,7 @@ import paper_1901_10559_b200 as ids
 from paper_1901_10559_b200 import _native
 
 lib = _native.load()
-lib.ids_set_phaseb_grid_cap.argtypes = [ctypes.c_int]
+lib.ids_set_hash_grid_cap.argtypes = [ctypes.c_int]
 I, L = 10**6, 100
 
 
@@ -15,7 +15,7 @@ def one(seed):
 
 
 for cap in (0, 148, 74, 37, 18):
-    lib.ids_set_phaseb_grid_cap(cap)
+    lib.ids_set_hash_grid_cap(cap)
     one(1)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -26,7 +26,7 @@ for cap in (0, 148, 74, 37, 18):
     torch.cuda.synchronize()
     print(f"cap {cap:4d}: {e0.elapsed_time(e1) / 5 * 1e3:8.1f} us per hash+index")
 for K, cap in ((10, 29), (10, 18), (5, 59), (4, 74)):
-    lib.ids_set_phaseb_grid_cap(cap)
+    lib.ids_set_hash_grid_cap(cap)
     streams = [torch.cuda.Stream() for _ in range(K)]
     for rep in range(2):
         torch.cuda.synchronize()
@@ -43,4 +43,4 @@ for K, cap in ((10, 29), (10, 18), (5, 59), (4, 74)):
         torch.cuda.synchronize()
     print(f"K={K} streams cap {cap}: {e0.elapsed_time(e1) * 1e3:8.1f} us total, "
           f"{e0.elapsed_time(e1) / K * 1e3:8.1f} us per hash")
-lib.ids_set_phaseb_grid_cap(0)
+lib.ids_set_hash_grid_cap(0)
