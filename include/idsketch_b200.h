@@ -43,7 +43,10 @@ enum {
 enum { IDS_ROW_MAJOR = 0, IDS_COL_MAJOR = 1 };
 
 /* flags for the CountSketch kernels */
-enum { IDS_FLAG_ORDERED = 1 /* force scipy's summation order (bit-exact Y) */ };
+enum {
+    IDS_FLAG_ORDERED = 1,       /* force scipy's summation order (bit-exact Y) */
+    IDS_FLAG_DETERMINISTIC = 2  /* sparse: fixed (segmented) summation order, run-to-run identical */
+};
 
 const char* ids_last_error(void);
 int ids_version(void);
@@ -137,6 +140,12 @@ int ids_values_has_nonfinite(const double* v, int64_t n, int32_t* flag, void* st
  *   indptr: int64[rows+1] (indptr64 = 1) or int32[rows+1] (indptr64 = 0),
  *   indices int32[nnz] (column ids < cols), data double[nnz].  Duplicate
  *   entries are summed in storage order, explicit zeros are harmless.
+ *   flags: IDS_FLAG_ORDERED -> one pass per bucket in scipy's order (Y
+ *   bit-identical to the reference); IDS_FLAG_DETERMINISTIC -> bucket
+ *   segments combined in a fixed order (run-to-run identical); neither ->
+ *   one streaming pass over A with fp64 reductions into an L2-resident Y
+ *   (fastest; summation order, hence the last bits of Y, not fixed).
+ *   order_signed/bstart are only read by the first two modes.
  * ------------------------------------------------------------------------- */
 size_t ids_countsketch_csr_workspace_bytes(int64_t rows, int64_t cols, int64_t nnz,
                                            int64_t out_dim);

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libidsketch_b200.so")
 IDS_OK, IDS_EINVAL, IDS_ENONFINITE, IDS_ESINGULAR, IDS_ECUDA, IDS_EWORKSPACE, IDS_ERETRY = range(7)
 IDS_ROW_MAJOR, IDS_COL_MAJOR = 0, 1
 IDS_FLAG_ORDERED = 1
+IDS_FLAG_DETERMINISTIC = 2
 
 _c_i64, _c_u64, _c_int, _c_dbl = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double
 _c_sz, _c_p = ctypes.c_size_t, ctypes.c_void_p

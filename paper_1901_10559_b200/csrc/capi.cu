@@ -1,4 +1,5 @@
 // Error reporting and version of the C ABI (include/idsketch_b200.h).
+#include <stdio.h>
 #include <string.h>
 
 #include <atomic>
@@ -10,6 +11,12 @@ static thread_local char g_last_error[512] = "";
 void ids_set_last_error(const char* msg) {
     strncpy(g_last_error, msg ? msg : "", sizeof(g_last_error) - 1);
     g_last_error[sizeof(g_last_error) - 1] = '\0';
+}
+
+void ids_set_cuda_error(cudaError_t e, const char* file, int line) {
+    const char* base = strrchr(file, '/');
+    snprintf(g_last_error, sizeof(g_last_error), "%s (%s:%d)", cudaGetErrorString(e),
+             base ? base + 1 : file, line);
 }
 
 extern "C" const char* ids_last_error(void) { return g_last_error; }

@@ -10,7 +10,7 @@
     do {                                                     \
         cudaError_t _e = (expr);                             \
         if (_e != cudaSuccess) {                             \
-            ids_set_last_error(cudaGetErrorString(_e));      \
+            ids_set_cuda_error(_e, __FILE__, __LINE__);      \
             return IDS_ECUDA;                                \
         }                                                    \
     } while (0)
@@ -20,12 +20,13 @@
         ids_count_launch();                                  \
         cudaError_t _e = cudaGetLastError();                 \
         if (_e != cudaSuccess) {                             \
-            ids_set_last_error(cudaGetErrorString(_e));      \
+            ids_set_cuda_error(_e, __FILE__, __LINE__);      \
             return IDS_ECUDA;                                \
         }                                                    \
     } while (0)
 
 void ids_set_last_error(const char* msg);
+void ids_set_cuda_error(cudaError_t e, const char* file, int line);
 void ids_count_launch();
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }

@@ -332,7 +332,7 @@ extern "C" int ids_countsketch_dense_f64(const double* A, int64_t rows, int64_t 
         IDS_LAUNCH_CHECK();
     } else {
         const unsigned grid = (unsigned)ceil_div(p.units, p.wpb);
-        if (p.smem > 48 * 1024) {
+        if (p.smem > 40 * 1024) {
             if (p.nc == 2)
                 IDS_CUDA_TRY(cudaFuncSetAttribute(cs_colmajor_kernel<2, 4>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1024,7 +1024,7 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
         ids_set_last_error("cpqr: rank too large for the shared-memory z buffer");
         return IDS_EINVAL;
     }
-    if (smem > 48 * 1024)
+    if (smem > 40 * 1024)
         IDS_CUDA_TRY(cudaFuncSetAttribute(cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
     CpqrArgs a{};

@@ -835,7 +835,7 @@ extern "C" int ids_tensorsketch_f64(int n_modes, const double* const* factors, c
     a.tlog = g_ts_tlog;
     if (colnorm2) IDS_CUDA_TRY(cudaMemsetAsync(colnorm2, 0, sizeof(double) * ncols, st));
     auto kern = p.ept == 16 ? tensorsketch_kernel<16> : tensorsketch_kernel<8>;
-    if (p.smem > 48 * 1024)
+    if (p.smem > 40 * 1024)
         IDS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)p.smem));
     int dev = 0, sms = 148, per_sm = 1;

@@ -17,12 +17,15 @@ import torch
 
 from . import _device
 from ._inputs import DenseOperand, SparseOperand, matrix_operand
-from ._native import IDS_ERETRY, IDS_FLAG_ORDERED, call, load, query
+from ._native import IDS_ERETRY, IDS_FLAG_DETERMINISTIC, IDS_FLAG_ORDERED, call, load, query
 
 _MAX_MATERIALIZE = 50_000_000  # sketch.py:30
-# Above this many nonzeros the CSR kernel splits each bucket into row segments
-# (fixed-order partial sums): deterministic run to run and within ~1e-16 of
-# scipy, but no longer bit-identical to its sequential order.
+# Up to this many nonzeros an ordered request keeps scipy's summation order
+# (one bucket-gather pass per bucket: Y bit-identical).  Above it the CSR
+# sketch streams A once and reduces into an L2-resident Y (equal to scipy's Y
+# up to summation-order rounding, ~1e-16 relative), or -- under
+# torch.use_deterministic_algorithms -- splits each bucket into row segments
+# combined in a fixed order (run-to-run identical).
 ORDERED_SPARSE_MAX_NNZ = 1 << 24
 
 
@@ -217,9 +220,14 @@ class CountSketchOp:
                 self.out_dim, _device.ptr(y), int(accumulate), nf, _device.ptr(ws), nbytes, st,
             )
         elif isinstance(operand, SparseOperand):
-            order, bstart = self.bucket_index()
-            if operand.nnz > ORDERED_SPARSE_MAX_NNZ:
-                flags &= ~IDS_FLAG_ORDERED  # segmented: deterministic, not bit-for-bit scipy
+            if operand.nnz > ORDERED_SPARSE_MAX_NNZ and flags & IDS_FLAG_ORDERED:
+                flags &= ~IDS_FLAG_ORDERED
+            if torch.are_deterministic_algorithms_enabled():
+                flags |= IDS_FLAG_DETERMINISTIC
+            if flags & (IDS_FLAG_ORDERED | IDS_FLAG_DETERMINISTIC):
+                order, bstart = self.bucket_index()
+            else:  # streaming pass: no bucket index needed
+                order = bstart = None
             nbytes = query(
                 "ids_countsketch_csr_workspace_bytes", operand.rows, operand.cols, operand.nnz,
                 self.out_dim,

@@ -32,7 +32,10 @@ def timed(fn, label, reps=3):
     return out
 
 
-timed(lambda: op.sketch_into(csr, y, flags=0), "CSR bucket kernel (segmented)")
+timed(lambda: op.sketch_into(csr, y, flags=2), "CSR bucket kernel (segmented)")
+y_seg = y.clone()
+timed(lambda: op.sketch_into(csr, y, flags=0), "CSR streaming kernel (L2 reductions)", reps=10)
+print("max |diff| stream vs segmented:", float((y - y_seg).abs().max()), flush=True)
 y_csr = y.clone()
 t = timed(lambda: _transpose(indptr, idx, data, I, R, I * per), "device transpose CSR->CSC")
 csc = SparseOperand("csc", t[0], t[1][: I * per], t[2][: I * per], I, R, I * per)
