@@ -32,6 +32,8 @@ METRICS = [
     "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
     "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "lts__t_sectors_srcunit_tex_op_red.sum",
+    "lts__t_sectors_srcunit_tex_op_red_lookup_hit.sum",
 ]
 
 
@@ -87,6 +89,8 @@ for rep, name, title in (("ev_rowmajor.ncu-rep", "cs_rowmajor", "cs_rowmajor_ker
                          ("full_tensorsketch_c5.ncu-rep", "tensorsketch_c5",
                           "tensorsketch_kernel<16>, C5 (N=4, I=1e4, R=2000, L=16384)"),
                          ("full_cpqr_c5.ncu-rep", "cpqr_c5", "cpqr_kernel, C5 sketch 16384 x 2000, k=20"),
+                         ("full_cs_csr_stream.ncu-rep", "cs_csr_stream",
+                          "cs_csr_stream_kernel, C3 (CSR 1e7 x 1e4, nnz 1e8, L=200)"),
                          ("full_cs_csr_bucket.ncu-rep", "cs_csr_bucket",
                           "cs_csr_bucket_kernel, C3 (CSR 1e7 x 1e4, nnz 1e8, L=200)"),
                          ("full_fy_phaseb.ncu-rep", "fy_phaseb", "fy_phaseb_kernel, hash I=1e6, L=100"),
