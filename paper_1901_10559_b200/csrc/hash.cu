@@ -114,12 +114,18 @@ __global__ void __launch_bounds__(kGenThreads) lemire_count_kernel(Seed sd, int6
     if (threadIdx.x == 0) blk_cnt[blockIdx.x] = tot;
 }
 
-// Pass 2: write the first n_acc accepted values; record draws consumed.
+// Pass 2: write the first n_acc accepted values; record draws consumed.  The
+// block's accepted values form one contiguous output range: they are staged
+// in shared memory (padded by one word per 32 against bank conflicts) and
+// written with coalesced stores.
+__device__ __forceinline__ int pad32(int x) { return x + (x >> 5); }
+
 __global__ void __launch_bounds__(kGenThreads) lemire_write_kernel(
     Seed sd, int64_t n_cand, uint32_t L, uint32_t thresh, const int64_t* blk_off,
     int64_t n_acc, int32_t* out, int64_t* consumed) {
     typedef cub::BlockScan<int, kGenThreads> BS;
     __shared__ typename BS::TempStorage tmp;
+    __shared__ int32_t stage[kGenThreads * kChunk + kGenThreads * kChunk / 32];
     const int64_t d0 = ((int64_t)blockIdx.x * kGenThreads + threadIdx.x) * kChunk;
     const int n = d0 < n_cand ? (int)tmin<int64_t>(kChunk, n_cand - d0) : 0;
     int cnt = 0;
@@ -131,19 +137,25 @@ __global__ void __launch_bounds__(kGenThreads) lemire_write_kernel(
             cnt += lemire_accept(ds.next(), L, thresh, &v) ? 1 : 0;
         }
     }
-    int pre;
-    BS(tmp).ExclusiveSum(cnt, pre);
-    int64_t o = blk_off[blockIdx.x] + pre;
-    if (n == 0 || o >= n_acc) return;
-    ds.init(sd.state(), sd.inc(), (uint64_t)d0);
-    for (int t = 0; t < n && o < n_acc; ++t) {
-        uint32_t v;
-        if (lemire_accept(ds.next(), L, thresh, &v)) {
-            out[o] = (int32_t)v;
-            if (o == n_acc - 1) *consumed = d0 + t + 1;
-            ++o;
+    int pre, tot;
+    BS(tmp).ExclusiveSum(cnt, pre, tot);
+    const int64_t ob = blk_off[blockIdx.x];
+    if (ob >= n_acc) return;  // whole block past the last needed value
+    if (n > 0 && ob + pre < n_acc) {
+        ds.init(sd.state(), sd.inc(), (uint64_t)d0);
+        int k = pre;
+        for (int t = 0; t < n && ob + k < n_acc; ++t) {
+            uint32_t v;
+            if (lemire_accept(ds.next(), L, thresh, &v)) {
+                stage[pad32(k)] = (int32_t)v;
+                if (ob + k == n_acc - 1) *consumed = d0 + t + 1;
+                ++k;
+            }
         }
     }
+    __syncthreads();
+    const int m = (int)tmin<int64_t>(tot, n_acc - ob);
+    for (int k = threadIdx.x; k < m; k += kGenThreads) out[ob + k] = stage[pad32(k)];
 }
 
 __global__ void fill_i32_kernel(int32_t* p, int64_t n, int32_t v) {
@@ -166,12 +178,26 @@ __global__ void __launch_bounds__(kGenThreads) raw_draws_kernel(Seed sd, const i
     DrawStream ds;
     ds.init(sd.state(), sd.inc(), (uint64_t)(base + d0));
     const int cnt = (int)tmin<int64_t>(kChunk, n - d0);
-    for (int t = 0; t < cnt; ++t) out[d0 + t] = ds.next();
+    if (cnt == kChunk) {  // a thread's 32 draws are 128 aligned bytes: 16-byte stores
+        uint4* o = reinterpret_cast<uint4*>(out + d0);
+#pragma unroll
+        for (int q = 0; q < kChunk / 4; ++q) {
+            uint4 v;
+            v.x = ds.next();
+            v.y = ds.next();
+            v.z = ds.next();
+            v.w = ds.next();
+            o[q] = v;
+        }
+    } else {
+        for (int t = 0; t < cnt; ++t) out[d0 + t] = ds.next();
+    }
 }
 
 // Signs: integers(0, 2) is Lemire with threshold 0 -> top bit of the draw.
 __global__ void __launch_bounds__(kGenThreads) sign_kernel(Seed sd, const int64_t* off,
-                                                           int n_off, int64_t n, int8_t* sign) {
+                                                           int n_off, int64_t n, int8_t* sign,
+                                                           int vec) {
     int64_t base = 0;
     for (int k = 0; k < n_off; ++k) base += off[k];
     const int64_t d0 = ((int64_t)blockIdx.x * kGenThreads + threadIdx.x) * kChunk;
@@ -179,7 +205,21 @@ __global__ void __launch_bounds__(kGenThreads) sign_kernel(Seed sd, const int64_
     DrawStream ds;
     ds.init(sd.state(), sd.inc(), (uint64_t)(base + d0));
     const int cnt = (int)tmin<int64_t>(kChunk, n - d0);
-    for (int t = 0; t < cnt; ++t) sign[d0 + t] = (ds.next() >> 31) ? (int8_t)1 : (int8_t)-1;
+    if (vec && cnt == kChunk) {  // 32 signs = 32 aligned bytes: two 16-byte stores
+        uint32_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) x |= ((ds.next() >> 31) ? 0x01u : 0xffu) << (8 * b);
+            w[q] = x;
+        }
+        uint4* o = reinterpret_cast<uint4*>(sign + d0);
+        o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+        for (int t = 0; t < cnt; ++t) sign[d0 + t] = (ds.next() >> 31) ? (int8_t)1 : (int8_t)-1;
+    }
 }
 
 __device__ __forceinline__ uint32_t mask_of(uint32_t i) { return 0xFFFFFFFFu >> __clz(i); }
@@ -203,6 +243,8 @@ struct FyState {
 // it walks its own 8 draws exactly from the now exact start.  Optionally
 // writes j[i] for accepted draws and records "near misses" (rejections with
 // gap v - i in [1, w], in draw order) for the speculative chunks.
+constexpr int kWalkAhead = 3;
+
 struct WalkOut {
     int64_t i, pos;
     int nev;
@@ -213,19 +255,25 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
                              int32_t* __restrict__ ev, int evmax) {
     const int ln = threadIdx.x & 31;
     int nev = 0;
-    uint32_t xn[8];  // next window, loaded one window ahead
+    // windows are loaded kWalkAhead windows ahead (the walk of one window is
+    // much shorter than a load's latency, even from L2)
+    uint32_t xn[kWalkAhead][8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int64_t p = pos + 8 * ln + q;
-        xn[q] = p < limit ? __ldg(g + p) : 0u;
-    }
+    for (int d = 0; d < kWalkAhead; ++d)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t p = pos + 256 * d + 8 * ln + q;
+            xn[d][q] = p < limit ? __ldg(g + p) : 0u;
+        }
     while (i > i_stop && pos < limit) {
         uint32_t x[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            x[q] = xn[q];
-            const int64_t p = pos + 256 + 8 * ln + q;
-            xn[q] = p < limit ? __ldg(g + p) : 0u;
+            x[q] = xn[0][q];
+#pragma unroll
+            for (int d = 0; d + 1 < kWalkAhead; ++d) xn[d][q] = xn[d + 1][q];
+            const int64_t p = pos + 256 * kWalkAhead + 8 * ln + q;
+            xn[kWalkAhead - 1][q] = p < limit ? __ldg(g + p) : 0u;
         }
         int b = 0;
         int64_t ib = i;
@@ -921,7 +969,8 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
     // ---- signs ----
     {
         const unsigned gb = (unsigned)ceil_div(in_dim, (int64_t)kGenThreads * kChunk);
-        sign_kernel<<<gb, kGenThreads, 0, st>>>(sd, d, 2, in_dim, sign);
+        const int vec = (reinterpret_cast<uintptr_t>(sign) & 15) == 0;
+        sign_kernel<<<gb, kGenThreads, 0, st>>>(sd, d, 2, in_dim, sign, vec);
         IDS_LAUNCH_CHECK();
         set_i64_kernel<<<1, 1, 0, st>>>(d + 2, in_dim);
         IDS_LAUNCH_CHECK();

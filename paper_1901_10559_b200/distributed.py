@@ -146,7 +146,7 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     from ._inputs import DenseOperand, SparseOperand, matrix_operand
     from ._native import IDS_FLAG_ORDERED
     from .matrix_id import check_matrix_id_args, device_matrix_id
-    from .sketch import pipelined_operators
+    from .sketch import id_stream, pipelined_operators
 
     world, _ = _world(group)
     operand = a_local if isinstance(a_local, (DenseOperand, SparseOperand)) else \
@@ -159,8 +159,11 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     L = check_matrix_id_args(_Shape, rank, sketch_dim, "countsketch")
     seeds = list(seeds)
     outs, flags = [], []
+    main = torch.cuda.current_stream()
+    side = id_stream()
     # each trial's hash is drawn on a side stream while the previous trial
-    # sketches (sketch.pipelined_operators)
+    # sketches (sketch.pipelined_operators); each trial's ID runs on a
+    # high-priority stream beside the next trial's sketch
     for op in pipelined_operators(in_dim, L, seeds, surjective):
         y = torch.empty((cols, L), dtype=torch.float64, device=torch.cuda.current_device())
         flag = torch.zeros(1, dtype=torch.int32, device=y.device)
@@ -168,8 +171,13 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
                        nonfinite=flag)
         if world > 1:
             dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
-        outs.append(device_matrix_id(y, L, cols, rank, rank_tol).packed())
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            outs.append(device_matrix_id(y, L, cols, rank, rank_tol).packed())
+        y.record_stream(side)
+        outs[-1].record_stream(main)
         flags.append(flag)
+    main.wait_stream(side)
     if flags:
         bad = torch.stack(flags).max()
         if world > 1:

@@ -332,8 +332,8 @@ class TensorSketchOp:
 
 
 _SIDE_STREAMS = {}
-PIPELINE_DEPTH = 1     # draws in flight ahead of the trial being computed
-PIPELINE_GRID_CAP = 32  # phase-B CTAs per background draw
+PIPELINE_DEPTH = 2     # draws in flight ahead of the trial being computed
+PIPELINE_GRID_CAP = 16  # phase-B CTAs per background draw
 
 
 def _side_streams(dev, n):
@@ -341,6 +341,21 @@ def _side_streams(dev, n):
     while len(pool) < n:
         pool.append(torch.cuda.Stream(device=dev))
     return pool[:n]
+
+
+_ID_STREAMS = {}
+
+
+def id_stream(dev=None):
+    """High-priority side stream for the small per-trial ID (CPQR + P): its
+    CTAs are dispatched as soon as any SM has room, so the ID of trial t runs
+    beside the HBM-bound sketch of trial t + 1 instead of after it."""
+    dev = dev or _device.device()
+    st = _ID_STREAMS.get(dev.index)
+    if st is None:
+        lo, hi = torch.cuda.Stream.priority_range()
+        st = _ID_STREAMS[dev.index] = torch.cuda.Stream(device=dev, priority=min(lo, hi))
+    return st
 
 
 def pipelined_operators(in_dim, out_dim, seeds, surjective=False, depth=None, grid_cap=None):
@@ -352,10 +367,12 @@ def pipelined_operators(in_dim, out_dim, seeds, surjective=False, depth=None, gr
     (whose sketch the caller then enqueues on the current stream), the draws
     of operators up to i + depth are enqueued on side streams with their
     resolution grid capped (ids_set_hash_grid_cap), so they run beside the
-    one-wave, HBM-bound sketch kernel instead of after it: measured on B200
-    at I = 1e6, the sketch keeps its speed (2.50 vs 2.48 ms) while a draw
-    completes under it.  The current stream waits for each draw before its
-    operator is used.
+    one-wave, HBM-bound sketch kernel instead of after it.  The current
+    stream waits for each draw before its operator is used.  Measured on B200
+    at configs[1] (I = 1e6, 10 trials, tools/exp_pipeline.py): 2.79 ms per
+    trial at depth 2 / 16 CTAs, against 2.54 ms for the sketch + ID alone;
+    depth 1 leaves the cooperative resolution waiting for room beside the
+    sketch (3.6 ms), deeper pipelines add more concurrent draws than help.
     """
     seeds = list(seeds)
     if not seeds:

@@ -21,3 +21,15 @@ for I in (10**6, 10**7):
     for k in range(n):
         print(f"  tag {tags[k]:5d}  t={(ts[k]-t0)/1e3:9.1f} us  (+{(ts[k]-prev)/1e3:7.1f})")
         prev = ts[k]
+
+# whole hash (draws + Fisher-Yates + signs + bucket index), device time
+for I, L in ((10**6, 100), (10**7, 200)):
+    ts = []
+    for s in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ids.CountSketchOp(I, L, seed=10 + s, surjective=True)._bucket_index()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(f"hash I={I}: median {sorted(ts[1:])[2] * 1e3:.0f} us", flush=True)

@@ -9,11 +9,12 @@ from paper_1901_10559_b200.distributed import countsketch_id_sharded_trials
 I, R = 1_000_000, 2000
 a = torch.randn(I, R, dtype=torch.float64, device="cuda")
 op = dense_operand(a)
-for depth, cap in ((1, 32), (2, 32), (2, 16), (3, 16), (2, 24), (1, 48), (4, 8)):
+countsketch_id_sharded_trials(op, 0, I, 20, 100, seeds=list(range(12)))
+for depth, cap in ((2, 16), (2, 24), (2, 32), (3, 24), (2, 16)):
     sketch.PIPELINE_DEPTH, sketch.PIPELINE_GRID_CAP = depth, cap
     countsketch_id_sharded_trials(op, 0, I, 20, 100, seeds=list(range(4)))
     torch.cuda.synchronize()
-    best = 1e9
+    best, allr = 1e9, []
     for rep in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -21,7 +22,8 @@ for depth, cap in ((1, 32), (2, 32), (2, 16), (3, 16), (2, 24), (1, 48), (4, 8))
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / 10)
-    print(f"depth {depth} cap {cap:3d}: {best * 1e3:7.0f} us per trial", flush=True)
+        allr.append(round(e0.elapsed_time(e1) / 10 * 1e3))
+    print(f"depth {depth} cap {cap:3d}: {best * 1e3:7.0f} us per trial {allr}", flush=True)
 
 # main-stream work alone: one pre-drawn operator reused for every trial
 from paper_1901_10559_b200.matrix_id import device_matrix_id
@@ -44,3 +46,36 @@ no_hash_trials(10)
 e1.record()
 torch.cuda.synchronize()
 print(f"no hash (fixed operator): {e0.elapsed_time(e1) / 10 * 1e3:7.0f} us per trial", flush=True)
+
+# sketch alone, and CPQR moved to a high-priority side stream
+def sketch_only(n):
+    y = torch.empty((R, 100), dtype=torch.float64, device="cuda")
+    for _ in range(n):
+        fixed.sketch_into(op, y, flags=1)
+    return y
+
+side = torch.cuda.Stream(priority=-1)
+def side_cpqr_trials(n):
+    outs = []
+    main = torch.cuda.current_stream()
+    for _ in range(n):
+        y = torch.empty((R, 100), dtype=torch.float64, device="cuda")
+        fixed.sketch_into(op, y, flags=1)
+        ev = torch.cuda.Event()
+        ev.record()
+        with torch.cuda.stream(side):
+            side.wait_event(ev)
+            outs.append(device_matrix_id(y, 100, R, 20).packed())
+            y.record_stream(side)
+    main.wait_stream(side)
+    return torch.stack(outs).cpu()
+
+for name, fn in (("sketch only", sketch_only), ("cpqr on side stream", side_cpqr_trials)):
+    fn(3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fn(10)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"{name}: {e0.elapsed_time(e1) / 10 * 1e3:7.0f} us per trial", flush=True)
