@@ -322,10 +322,19 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # IDS_BENCH_ONE_DEVICE=1 (test hook): every rank on cuda:0 over gloo, which
+    # stages collectives through the host -- exercises the multi-rank code
+    # path on a one-GPU box; its timings mean nothing
+    one_dev = os.environ.get("IDS_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     import paper_1901_10559_b200 as ids
     from paper_1901_10559_b200 import _native
@@ -450,6 +459,10 @@ def main():
             traffic = json.load(open(tpath)).get(args.workload)
         except Exception:
             traffic = None
+    if traffic is not None and world > 1:
+        # the capture is of the whole-matrix launch (one GPU): scale to this
+        # rank's row block by the measured traffic / algorithmic-bytes ratio
+        traffic = traffic * bytes_local / bytes_total
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
