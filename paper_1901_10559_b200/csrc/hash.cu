@@ -522,18 +522,31 @@ __device__ void chunk_work(const uint32_t* __restrict__ g, int64_t nbuf, int64_t
             }
         }
         out.ne = over ? -1 : nf;
-        for (int e = nf; e < kEvMax; ++e) out.ev[e] = 0;
+        for (int e = nf; e < kEvMax; ++e) out.ev[e] = 0x7fffffff;  // never <= d
         __syncwarp();
     }
     if (ln == 0) ch[c] = out;
 }
 
-// One block (thread 0 walks, the block stages summaries in shared memory):
+// One block (warp 0 walks, the block stages summaries in shared memory):
 // resolves the chunks in order from the exact epoch start; stops at the first
 // chunk whose start leaves its window (the exact walk continues from there).
+// Summaries arrive in batches of kStitchBatch through two shared buffers: the
+// next batch is copied (cp.async) while warp 0 resolves the current one.
 constexpr int kStitchBatch = 64;
+
+__device__ __forceinline__ void stage_batch(FyChunk* dst, const FyChunk* __restrict__ src, int cnt) {
+    const int words = (int)(cnt * sizeof(FyChunk) / 16);
+    const char* s = reinterpret_cast<const char*>(src);
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    for (int w = threadIdx.x; w < words; w += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d + 16 * w), "l"(s + 16 * w)
+                     : "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 __device__ void stitch_block(FyState* st, const FyChunk* __restrict__ ch, int64_t nchunks,
-                             int64_t T, int64_t* __restrict__ starts, FyChunk* sm) {
+                             int64_t T, int64_t* __restrict__ starts, FyChunk* sm2) {
     __shared__ int64_t s_S, s_done;
     __shared__ int s_ok;
     const int64_t pos0 = st->pos;
@@ -543,15 +556,21 @@ __device__ void stitch_block(FyState* st, const FyChunk* __restrict__ ch, int64_
         s_done = 0;
         starts[-1] = pos0;
     }
-    for (int64_t c0 = 0; c0 < nchunks; c0 += kStitchBatch) {
+    const int64_t nb = (nchunks + kStitchBatch - 1) / kStitchBatch;
+    if (nb > 0) stage_batch(sm2, ch, (int)tmin<int64_t>(kStitchBatch, nchunks));
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t c0 = b * kStitchBatch;
         const int cnt = (int)tmin<int64_t>(kStitchBatch, nchunks - c0);
+        FyChunk* sm = sm2 + (b & 1) * kStitchBatch;
+        if (b + 1 < nb) {
+            stage_batch(sm2 + ((b + 1) & 1) * kStitchBatch, ch + c0 + kStitchBatch,
+                        (int)tmin<int64_t>(kStitchBatch, nchunks - c0 - kStitchBatch));
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
         __syncthreads();
         if (!s_ok) break;
-        const int words = (int)(cnt * sizeof(FyChunk) / sizeof(int4));
-        const int4* src = reinterpret_cast<const int4*>(ch + c0);
-        int4* dst = reinterpret_cast<int4*>(sm);
-        for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
-        __syncthreads();
         if (threadIdx.x < 32) {  // warp 0: lane e holds flat e; one ballot per chunk
             const int ln = threadIdx.x;
             int64_t S = s_S;
@@ -582,7 +601,9 @@ __device__ void stitch_block(FyState* st, const FyChunk* __restrict__ ch, int64_
                 s_done += l;
             }
         }
+        __syncthreads();  // this buffer is refilled two batches on
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
         st->i = s_S;
@@ -619,7 +640,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         }
     };
     __shared__ int32_t evs[kPbThreads / 32][kEvMax];
-    __shared__ FyChunk sm[kStitchBatch];
+    __shared__ FyChunk sm[2 * kStitchBatch];
     const int wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * (kPbThreads / 32) + wib;
     const int64_t nw = (int64_t)gridDim.x * (kPbThreads / 32);

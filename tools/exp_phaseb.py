@@ -6,8 +6,11 @@ from paper_1901_10559_b200 import _native
 lib = _native.load()
 buf = torch.zeros(512, dtype=torch.int64, device="cuda")
 lib.ids_debug_phaseb_timing.argtypes = [ctypes.c_void_p]
+cap = int(os.environ.get("CAP", "0"))
+lib.ids_set_hash_grid_cap(cap)
 for I in (10**6, 10**7):
     ids.CountSketchOp(I, 100, seed=1, surjective=True)._bucket_index()
+    buf.zero_()
     lib.ids_debug_phaseb_timing(buf.data_ptr())
     ids.CountSketchOp(I, 100, seed=2, surjective=True)._bucket_index()
     torch.cuda.synchronize()
