@@ -176,6 +176,27 @@ int ids_tensorsketch_f64(int n_modes, const double* const* factors, const int64_
                          const int32_t* const* sorted_bucket, int64_t out_dim,
                          const double* weights, double* Y, double* colnorm2, void* workspace,
                          size_t ws_bytes, void* stream);
+/* Scatter plan of one mode (built once per mode hash, reused for every
+ * ids_tensorsketch_planned_f64 call): each row's (bucket, sign) code and its
+ * rank among the rows of its bucket.  With it the fused kernel reads factor
+ * columns contiguously instead of gathering rows in bucket order; the
+ * per-bucket sums keep scipy's row order (bit-identical CountSketch).
+ * plan: 16-byte aligned device buffer of ids_ts_mode_plan_bytes(dim) bytes;
+ * bstart: the bucket index's int64[out_dim + 1] starts. */
+size_t ids_ts_mode_plan_bytes(int64_t dim);
+int ids_ts_mode_plan(const int32_t* order_signed, const int32_t* sorted_bucket,
+                     const int64_t* bstart, int64_t dim, int64_t out_dim, void* plan,
+                     size_t plan_bytes, void* stream);
+/* ids_tensorsketch_f64 with per-mode scatter plans (host array of device
+ * pointers; an entry may be NULL, and a plan whose collisions exceed the
+ * kernel's staging falls back to the gather path for that mode). */
+int ids_tensorsketch_planned_f64(int n_modes, const double* const* factors, const int64_t* dims,
+                                 const int64_t* lds, int64_t ncols,
+                                 const int32_t* const* order_signed,
+                                 const int32_t* const* sorted_bucket, const void* const* plans,
+                                 int64_t out_dim, const double* weights, double* Y,
+                                 double* colnorm2, void* workspace, size_t ws_bytes,
+                                 void* stream);
 /* 1 when ids_tensorsketch_f64 handles (n_modes, out_dim) in its fused
  * one-CTA-per-term kernel (transform half-length <= 8192: power-of-two
  * out_dim <= 16384, or n_modes * (out_dim - 1) + 1 <= 16384 otherwise).

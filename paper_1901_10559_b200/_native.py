@@ -64,6 +64,13 @@ SIGNATURES = {
         [_c_int, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz,
          _c_p],
     ),
+    "ids_ts_mode_plan_bytes": (_c_sz, [_c_i64]),
+    "ids_ts_mode_plan": (_c_int, [_c_p, _c_p, _c_p, _c_i64, _c_i64, _c_p, _c_sz, _c_p]),
+    "ids_tensorsketch_planned_f64": (
+        _c_int,
+        [_c_int, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p,
+         _c_sz, _c_p],
+    ),
     "ids_cpqr_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_i64]),
     "ids_cpqr_trunc_f64": (
         _c_int,

@@ -33,6 +33,88 @@ constexpr int kMaxModes = 8;
 constexpr int kMaxHalf = 8192;  // largest half-length transform kept in shared memory
 constexpr int kStageExt = 64;   // look-ahead entries staged past a stage's last head
 
+// Per-mode scatter plan (ids_ts_mode_plan).  When a mode's rows spread over
+// the buckets with few collisions (I_n < L at the tensor configs), its
+// CountSketch is applied by reading the factor column CONTIGUOUSLY: each
+// row's first-in-bucket entry (rank 0, in row order) is stored straight into
+// the FFT buffer, later entries are parked in shared memory and added in
+// rank order, one barrier per rank -- every bucket still sums its rows in
+// increasing row order (scipy's), with no gathers from the factor column.
+constexpr int kMaxPhase = 32;  // ranks beyond this: the gather path
+struct TsModePlanHdr {
+    int32_t valid, maxr, nstash, pad;
+    int32_t hist[64];
+    int32_t cursor[64];
+    int32_t off[kMaxPhase + 4];  // stash slots of rank r: [off[r], off[r + 1]), r >= 1 (+2 pad)
+};
+static_assert(sizeof(TsModePlanHdr) % 16 == 0, "plan header keeps the arrays aligned");
+
+__host__ __device__ __forceinline__ int64_t ts_plan_stride(int64_t dim) { return (dim + 3) & ~int64_t(3); }
+__host__ __device__ __forceinline__ int32_t* ts_plan_code(const TsModePlanHdr* h) {
+    return reinterpret_cast<int32_t*>(const_cast<TsModePlanHdr*>(h) + 1);
+}
+
+// Bulk prefetch of [p, p + bytes) into L2 (TMA; 16-byte granules).
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+    for (uintptr_t a = a0; a < a1; a += 65536) {
+        const uint32_t n = (uint32_t)(a1 - a < 65536 ? a1 - a : 65536);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+    }
+}
+
+__global__ void ts_plan_rank_kernel(const int32_t* __restrict__ order,
+                                    const int32_t* __restrict__ keys,
+                                    const int64_t* __restrict__ bstart, int64_t dim,
+                                    TsModePlanHdr* hdr, int32_t* __restrict__ code,
+                                    int32_t* __restrict__ rank) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < dim;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t e = order[q], b = keys[q];
+        const int32_t row = dec_row(e);
+        const int32_t r = (int32_t)(q - bstart[b]);
+        code[row] = e >= 0 ? b : ~b;
+        rank[row] = r;
+        if (r >= 1) atomicAdd(&hdr->hist[r < 63 ? r : 63], 1);
+    }
+}
+
+__global__ void ts_plan_offsets_kernel(TsModePlanHdr* hdr) {
+    if (threadIdx.x != 0) return;
+    int maxr = 0;
+    for (int r = 1; r < 64; ++r)
+        if (hdr->hist[r] > 0) maxr = r;
+    hdr->maxr = maxr;
+    hdr->valid = maxr <= kMaxPhase && hdr->hist[63] == 0;
+    int acc = 0;
+    hdr->off[0] = 0;
+    for (int r = 1; r <= kMaxPhase + 1; ++r) {
+        hdr->off[r] = acc;
+        if (r <= kMaxPhase) acc += hdr->hist[r];
+    }
+    hdr->nstash = acc;
+}
+
+__global__ void ts_plan_slot_kernel(TsModePlanHdr* hdr, int64_t dim,
+                                    const int32_t* __restrict__ code, int32_t* __restrict__ slot,
+                                    int32_t* __restrict__ stash_code) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < dim;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = slot[i];  // holds the rank on entry
+        if (r == 0) {
+            slot[i] = -1;
+        } else if (r <= kMaxPhase) {
+            // any order inside a rank: its entries hit distinct buckets
+            const int32_t sl = hdr->off[r] + atomicAdd(&hdr->cursor[r], 1);
+            slot[i] = sl;
+            stash_code[sl] = code[i];
+        } else {
+            slot[i] = -2;  // plan invalid; never read
+        }
+    }
+}
+
 struct TsArgs {
     int n_modes;
     const double* factors[kMaxModes];
@@ -51,6 +133,7 @@ struct TsArgs {
     int stage_cap;        // staged CountSketch entries (shared memory) per round
     int y_vec;            // Y 16-byte aligned: paired output stores
     int64_t* tlog;        // debug: per-phase ns accumulated by CTA 0 (NULL: off)
+    const TsModePlanHdr* plan[kMaxModes];  // scatter plan of mode n, or NULL
 };
 
 __device__ __forceinline__ int64_t gtimer() {
@@ -467,6 +550,8 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     __shared__ int64_t s_ld[kMaxModes];
     __shared__ int s_dim[kMaxModes];
     __shared__ int32_t s_prevkey;
+    __shared__ int s_pvalid[kMaxModes], s_pmaxr[kMaxModes];
+    __shared__ int32_t s_poff[kMaxModes][kMaxPhase + 2];
     double* dbuf = reinterpret_cast<double*>(buf);
     const int T = blockDim.x, t = threadIdx.x;
     const int N2 = (int)g.N2, M = (int)g.M;
@@ -479,7 +564,15 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
             s_key[q] = g.keys[q];
             s_ld[q] = g.lds[q];
             s_dim[q] = (int)g.dims[q];
+            const TsModePlanHdr* h = q < g.n_modes ? g.plan[q] : nullptr;
+            s_pvalid[q] = h && h->valid && h->nstash <= g.stage_cap;
+            s_pmaxr[q] = h ? h->maxr : 0;
         }
+    }
+    for (int i = t; i < kMaxModes * (kMaxPhase + 2); i += T) {
+        const int q = i / (kMaxPhase + 2), r = i % (kMaxPhase + 2);
+        const TsModePlanHdr* h = q < g.n_modes ? g.plan[q] : nullptr;
+        s_poff[q][r] = h ? h->off[r] : 0;
     }
     for (int m = t; m < 128; m += T) {
         double sn, cs;
@@ -528,7 +621,59 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 if (n == 0 && !out_done)  // else zeroed by the untangle / fused output
                     for (int l = t; l < N2; l += T) buf[pad<PS>(l)] = make_double2(0.0, 0.0);
                 stamp(0);
-                for (int c0 = 0; c0 < In; c0 += stage_heads) {
+                if (s_pvalid[n]) {
+                    // scatter plan: the column is read contiguously; rank-0 rows
+                    // store into the (zeroed) buffer, later rows are parked in
+                    // the staging area and added rank by rank
+                    const TsModePlanHdr* ph = g.plan[n];
+                    const int32_t* pcode = ts_plan_code(ph);
+                    const int32_t* pslot = pcode + ts_plan_stride(In);
+                    if (t == 0) {  // the next (mode, column) factor column into L2
+                        int nn = n + 1;
+                        int64_t rn = r;
+                        if (nn == g.n_modes) {
+                            nn = 0;
+                            rn = r + gridDim.x;
+                        }
+                        if (rn < g.ncols) l2_prefetch(s_fac[nn] + rn * s_ld[nn], (size_t)s_dim[nn] * 8);
+                    }
+                    __syncthreads();  // zeroing (n == 0) before the stores
+                    for (int i0 = t; i0 < In; i0 += 4 * T) {
+                        double v[4];
+                        int32_t c[4], sl[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = min(i0 + u * T, In - 1);
+                            v[u] = __ldcs(col + i);
+                            c[u] = __ldg(pcode + i);
+                            sl[u] = __ldg(pslot + i);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (i0 + u * T < In) {
+                                const double sv = c[u] >= 0 ? v[u] : -v[u];
+                                const int h = dec_row(c[u]);
+                                if (sl[u] < 0) {
+                                    dbuf[2 * pad<PS>(h >> 1) + (h & 1)] = 0.0 + sv;
+                                } else {
+                                    st_val[sl[u]] = sv;
+                                    st_key[sl[u]] = h;
+                                }
+                            }
+                        }
+                    }
+                    __syncthreads();
+                    stamp(1);
+                    for (int rr = 1; rr <= s_pmaxr[n]; ++rr) {
+                        for (int q = s_poff[n][rr] + t; q < s_poff[n][rr + 1]; q += T) {
+                            const int h = st_key[q];
+                            dbuf[2 * pad<PS>(h >> 1) + (h & 1)] += st_val[q];
+                        }
+                        __syncthreads();
+                    }
+                    stamp(2);
+                }
+                for (int c0 = 0; c0 < In && !s_pvalid[n]; c0 += stage_heads) {
                     // stage entries [c0, c0 + ns): the heads below cn and a
                     // look-ahead; thread t owns the 8 consecutive entries
                     // [8t, 8t + 8) (one round: ns <= 8T), loaded with eight
@@ -779,12 +924,53 @@ extern "C" size_t ids_tensorsketch_workspace_bytes(int n_modes, const int64_t* d
     return (size_t)p.M * sizeof(double2) + 148 * 2 * (size_t)(p.N2 + 1) * sizeof(double2) + 1024;
 }
 
+extern "C" size_t ids_ts_mode_plan_bytes(int64_t dim) {
+    if (dim < 1) return 0;
+    return sizeof(TsModePlanHdr) + 3 * (size_t)ts_plan_stride(dim) * sizeof(int32_t);
+}
+
+extern "C" int ids_ts_mode_plan(const int32_t* order_signed, const int32_t* sorted_bucket,
+                                const int64_t* bstart, int64_t dim, int64_t out_dim, void* plan,
+                                size_t plan_bytes, void* stream) {
+    if (dim < 1 || out_dim < 1 || dim > 0x7fffffffLL || !plan ||
+        plan_bytes < ids_ts_mode_plan_bytes(dim) || (reinterpret_cast<uintptr_t>(plan) & 15)) {
+        ids_set_last_error("ts mode plan: bad arguments");
+        return IDS_EINVAL;
+    }
+    cudaStream_t st = as_stream(stream);
+    TsModePlanHdr* hdr = static_cast<TsModePlanHdr*>(plan);
+    int32_t* code = ts_plan_code(hdr);
+    int32_t* slot = code + ts_plan_stride(dim);
+    int32_t* stash = slot + ts_plan_stride(dim);
+    IDS_CUDA_TRY(cudaMemsetAsync(hdr, 0, sizeof(TsModePlanHdr), st));
+    const unsigned g = (unsigned)tmin<int64_t>(ceil_div(dim, 256), 148 * 8);
+    ts_plan_rank_kernel<<<g, 256, 0, st>>>(order_signed, sorted_bucket, bstart, dim, hdr, code, slot);
+    IDS_LAUNCH_CHECK();
+    ts_plan_offsets_kernel<<<1, 32, 0, st>>>(hdr);
+    IDS_LAUNCH_CHECK();
+    ts_plan_slot_kernel<<<g, 256, 0, st>>>(hdr, dim, code, slot, stash);
+    IDS_LAUNCH_CHECK();
+    return IDS_OK;
+}
+
 extern "C" int ids_tensorsketch_f64(int n_modes, const double* const* factors, const int64_t* dims,
                                     const int64_t* lds, int64_t ncols,
                                     const int32_t* const* order_signed,
                                     const int32_t* const* sorted_bucket, int64_t out_dim,
                                     const double* weights, double* Y, double* colnorm2,
                                     void* workspace, size_t ws_bytes, void* stream) {
+    return ids_tensorsketch_planned_f64(n_modes, factors, dims, lds, ncols, order_signed,
+                                        sorted_bucket, nullptr, out_dim, weights, Y, colnorm2,
+                                        workspace, ws_bytes, stream);
+}
+
+extern "C" int ids_tensorsketch_planned_f64(int n_modes, const double* const* factors,
+                                            const int64_t* dims, const int64_t* lds,
+                                            int64_t ncols, const int32_t* const* order_signed,
+                                            const int32_t* const* sorted_bucket,
+                                            const void* const* plans, int64_t out_dim,
+                                            const double* weights, double* Y, double* colnorm2,
+                                            void* workspace, size_t ws_bytes, void* stream) {
     if (n_modes < 1 || n_modes > kMaxModes || ncols < 0 || out_dim < 1) {
         ids_set_last_error("tensorsketch: need 1..8 modes and out_dim >= 1");
         return IDS_EINVAL;
@@ -818,6 +1004,7 @@ extern "C" int ids_tensorsketch_f64(int n_modes, const double* const* factors, c
         a.order[n] = order_signed[n];
         a.keys[n] = sorted_bucket[n];
         a.dims[n] = dims[n];
+        a.plan[n] = plans ? static_cast<const TsModePlanHdr*>(plans[n]) : nullptr;
     }
     a.ncols = ncols;
     a.L = out_dim;

@@ -187,6 +187,21 @@ class CountSketchOp:
             self._index = (order, bstart, keys)
         return self._index
 
+    def _ts_plan(self):
+        """Scatter plan of this operator as one TensorSketch mode (per-row
+        bucket/sign code and rank within its bucket), built on the device
+        once and cached (ids_ts_mode_plan)."""
+        if getattr(self, "_plan", None) is None:
+            order, bstart, keys = self._bucket_index()
+            nbytes = query("ids_ts_mode_plan_bytes", self.in_dim)
+            plan = _device.workspace(nbytes)
+            call(
+                "ids_ts_mode_plan", _device.ptr(order), _device.ptr(keys), _device.ptr(bstart),
+                self.in_dim, self.out_dim, _device.ptr(plan), nbytes, _device.stream_ptr(),
+            )
+            self._plan = plan
+        return self._plan
+
     def sketch_into(self, operand, y, row0=0, accumulate=False, flags=0, nonfinite=None):
         """Y (+)= S[:, row0:row0+rows] @ operand on the current stream.
 

@@ -68,6 +68,7 @@ def tensorsketch_device(op, factors, weights=None):
     if not query("ids_tensorsketch_fused_ok", n, L):
         return _tensorsketch_spectral(op, dev_f, w, ncols, L)
     idx = [m._bucket_index() for m in op.mode_ops]
+    plans = (ctypes.c_void_p * n)(*[_device.ptr(m._ts_plan()) for m in op.mode_ops])
     fac_p = (ctypes.c_void_p * n)(*[_device.ptr(t) for t in dev_f])
     ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _, _ in idx])
     key_p = (ctypes.c_void_p * n)(*[_device.ptr(k) for _, _, k in idx])
@@ -79,8 +80,9 @@ def tensorsketch_device(op, factors, weights=None):
     nbytes = query("ids_tensorsketch_workspace_bytes", n, ctypes.addressof(dims), ncols, L)
     ws = _device.workspace(nbytes)
     call(
-        "ids_tensorsketch_f64", n, ctypes.addressof(fac_p), ctypes.addressof(dims),
-        ctypes.addressof(lds), ncols, ctypes.addressof(ord_p), ctypes.addressof(key_p), L,
+        "ids_tensorsketch_planned_f64", n, ctypes.addressof(fac_p), ctypes.addressof(dims),
+        ctypes.addressof(lds), ncols, ctypes.addressof(ord_p), ctypes.addressof(key_p),
+        ctypes.addressof(plans), L,
         _device.ptr(w), _device.ptr(y), None, _device.ptr(ws), nbytes, _device.stream_ptr(),
     )
     # dev_f may be freed now: the caching allocator reuses memory in stream order

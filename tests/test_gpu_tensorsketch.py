@@ -207,3 +207,80 @@ def test_long_transforms_beyond_the_fused_kernel(dims, L):
     want = oracle.OracleTensorSketch(dims, L, seed=9).apply(factors, lam)
     assert relerr_fro(op.apply(factors, lam), want) <= 1e-12
     assert query("ids_tensorsketch_fused_ok", 4, 16384) and query("ids_tensorsketch_fused_ok", 3, 3000)
+
+
+# ---- scatter plans (contiguous factor-column reads) vs the gather path ----
+def _ts_both(op, factors, weights):
+    """Y through the planned kernel and through the plain (gather) entry on
+    the same operator and device factors; both (R, L) CUDA tensors."""
+    import ctypes
+
+    from paper_1901_10559_b200 import _device
+    from paper_1901_10559_b200._native import call, query
+    from paper_1901_10559_b200.tensorsketch import factor_to_device, tensorsketch_device
+
+    y_plan = tensorsketch_device(op, factors, weights)
+    dev_f = [factor_to_device(f) for f in factors]
+    n, L, ncols = len(dev_f), op.out_dim, factors[0].shape[1]
+    idx = [m._bucket_index() for m in op.mode_ops]
+    fac_p = (ctypes.c_void_p * n)(*[_device.ptr(t) for t in dev_f])
+    ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _, _ in idx])
+    key_p = (ctypes.c_void_p * n)(*[_device.ptr(k) for _, _, k in idx])
+    dims = (ctypes.c_int64 * n)(*[int(d) for d in op.mode_dims])
+    lds = (ctypes.c_int64 * n)(*[int(t.shape[1]) for t in dev_f])
+    w = torch.from_numpy(np.asarray(weights, np.float64)).cuda()
+    y = torch.empty((ncols, L), dtype=torch.float64, device="cuda")
+    nbytes = query("ids_tensorsketch_workspace_bytes", n, ctypes.addressof(dims), ncols, L)
+    ws = _device.workspace(nbytes)
+    call("ids_tensorsketch_f64", n, ctypes.addressof(fac_p), ctypes.addressof(dims),
+         ctypes.addressof(lds), ncols, ctypes.addressof(ord_p), ctypes.addressof(key_p), L,
+         _device.ptr(w), _device.ptr(y), None, _device.ptr(ws), nbytes, _device.stream_ptr())
+    return y_plan, y
+
+
+@pytest.mark.parametrize("dims,L,r", [
+    ([10_000] * 4, 16384, 40),      # C5 modes: ~29% of rows collide
+    ([1000] * 3, 4096, 50),         # C4 modes
+    ([4097, 333, 5], 64, 7),        # heavy collisions: plan falls back for mode 0
+    ([1, 2, 3], 8, 3),              # tiny dims
+    ([777, 1001], 1000, 9),         # non-power-of-two L (zero-padded transform)
+])
+def test_scatter_plan_matches_gather_path_bit_for_bit(dims, L, r):
+    rng = np.random.default_rng(sum(dims) + L)
+    factors = [rng.standard_normal((d, r)) for d in dims]
+    weights = rng.random(r) + 0.5
+    op = ids.TensorSketchOp(dims, L, seed=3)
+    y_plan, y_gather = _ts_both(op, factors, weights)
+    assert torch.equal(y_plan, y_gather)
+    want = oracle.tensorsketch_apply(
+        oracle.OracleTensorSketch(dims, L, seed=3).mode_ops, L, factors, weights)
+    assert relerr_fro(y_plan.t().cpu().numpy(), want) <= 1e-12
+
+
+def test_scatter_plan_ranks_and_slots():
+    """The plan's per-row code/rank layout against numpy: rank = position
+    among the rows of the same bucket in increasing row order; every row
+    with rank >= 1 owns one stash slot inside its rank's range."""
+    from paper_1901_10559_b200 import _device  # noqa: F401
+
+    op = ids.CountSketchOp(5000, 3000, seed=11)
+    plan = op._ts_plan().cpu().numpy().view(np.int32)
+    hdr = plan[:168]
+    valid, maxr, nstash = hdr[0], hdr[1], hdr[2]
+    off = hdr[4 + 64 + 64:]
+    stride = (5000 + 3) & ~3
+    code = plan[168:168 + 5000]
+    slot = plan[168 + stride:168 + stride + 5000]
+    b = op.bucket
+    assert np.array_equal(np.where(code >= 0, code, ~code), b)
+    assert np.array_equal(code >= 0, op.sign > 0)
+    rank = np.zeros(5000, np.int64)
+    seen = {}
+    for i in range(5000):
+        rank[i] = seen.get(b[i], 0)
+        seen[b[i]] = rank[i] + 1
+    assert valid == 1 and maxr == rank.max() and nstash == (rank >= 1).sum()
+    assert np.all(slot[rank == 0] == -1)
+    for rr in range(1, maxr + 1):
+        s = np.sort(slot[rank == rr])
+        assert np.array_equal(s, np.arange(off[rr], off[rr + 1]))
