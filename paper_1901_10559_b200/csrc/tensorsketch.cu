@@ -41,6 +41,7 @@ constexpr int kStageExt = 64;   // look-ahead entries staged past a stage's last
 // rank order, one barrier per rank -- every bucket still sums its rows in
 // increasing row order (scipy's), with no gathers from the factor column.
 constexpr int kMaxPhase = 32;  // ranks beyond this: the gather path
+constexpr int kScatterUnroll = 4;  // factor-column loads in flight per thread (8 measured no faster)
 struct TsModePlanHdr {
     int32_t valid, maxr, nstash, pad;
     int32_t hist[64];
@@ -638,18 +639,18 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                         if (rn < g.ncols) l2_prefetch(s_fac[nn] + rn * s_ld[nn], (size_t)s_dim[nn] * 8);
                     }
                     __syncthreads();  // zeroing (n == 0) before the stores
-                    for (int i0 = t; i0 < In; i0 += 4 * T) {
-                        double v[4];
-                        int32_t c[4], sl[4];
+                    for (int i0 = t; i0 < In; i0 += kScatterUnroll * T) {
+                        double v[kScatterUnroll];
+                        int32_t c[kScatterUnroll], sl[kScatterUnroll];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < kScatterUnroll; ++u) {
                             const int i = min(i0 + u * T, In - 1);
                             v[u] = __ldcs(col + i);
                             c[u] = __ldg(pcode + i);
                             sl[u] = __ldg(pslot + i);
                         }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < kScatterUnroll; ++u) {
                             if (i0 + u * T < In) {
                                 const double sv = c[u] >= 0 ? v[u] : -v[u];
                                 const int h = dec_row(c[u]);
