@@ -15,7 +15,7 @@ run_full() {  # $1 kernel regex, $2 report name, $3.. prof_step args
 }
 run_full tensorsketch_kernel tensorsketch_c5 --tensor 4,10000,2000,16384,20
 run_full cpqr_kernel cpqr_c5 --tensor 4,10000,2000,16384,20
-run_full cs_csr_bucket cs_csr_bucket --csr 10000000,10000,100000000,200,20
+run_full cs_csr_stream cs_csr_stream --csr 10000000,10000,100000000,200,20
 run_full fy_phaseb fy_phaseb
 run_full cpqr_cluster cpqr_cluster
 echo round profiles done
