@@ -251,32 +251,42 @@ struct WalkOut {
 };
 
 __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_t limit,
-                             int64_t i, int64_t i_stop, int32_t* __restrict__ jout, int64_t w,
-                             int32_t* __restrict__ ev, int evmax) {
+                             int64_t i64, int64_t i_stop64, int32_t* __restrict__ jout,
+                             int64_t w64, int32_t* __restrict__ ev, int evmax) {
+    // i < 2^31 (in_dim is limited to 2^31 - 2): the chain state and all the
+    // per-draw arithmetic run in 32 bits; only draw positions are 64-bit
     const int ln = threadIdx.x & 31;
+    int32_t i = (int32_t)i64;
+    const int32_t i_stop = (int32_t)i_stop64;
+    const int32_t w = (int32_t)tmin<int64_t>(w64, 0x7fffffff);
     int nev = 0;
     // windows are loaded kWalkAhead windows ahead (the walk of one window is
     // much shorter than a load's latency, even from L2)
     uint32_t xn[kWalkAhead][8];
+    {
+        const int64_t rem = limit - pos;
 #pragma unroll
-    for (int d = 0; d < kWalkAhead; ++d)
+        for (int d = 0; d < kWalkAhead; ++d)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int64_t p = pos + 256 * d + 8 * ln + q;
-            xn[d][q] = p < limit ? __ldg(g + p) : 0u;
-        }
+            for (int q = 0; q < 8; ++q) {
+                const int o = 256 * d + 8 * ln + q;
+                xn[d][q] = o < rem ? __ldg(g + pos + o) : 0u;
+            }
+    }
     while (i > i_stop && pos < limit) {
+        const int64_t rem = limit - pos;
+        const int nval = rem < 256 ? (int)rem : 256;  // valid draws in this window
         uint32_t x[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             x[q] = xn[0][q];
 #pragma unroll
             for (int d = 0; d + 1 < kWalkAhead; ++d) xn[d][q] = xn[d + 1][q];
-            const int64_t p = pos + 256 * kWalkAhead + 8 * ln + q;
-            xn[kWalkAhead - 1][q] = p < limit ? __ldg(g + p) : 0u;
+            const int o = 256 * kWalkAhead + 8 * ln + q;
+            xn[kWalkAhead - 1][q] = o < rem ? __ldg(g + pos + o) : 0u;
         }
         int b = 0;
-        int64_t ib = i;
+        int32_t ib = i;
         bool stop = false;
         int64_t pos_final = 0;
         while (b < 32) {
@@ -284,17 +294,16 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
             int a = 0;
             bool amb = false;
             if (ln >= b) {
-                const int64_t umax = 8 * (ln - b);
+                const int32_t umax = 8 * (ln - b);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     if (!amb) {
-                        const int64_t hi = ib - a, lo = hi - umax;
-                        const int64_t p = pos + 8 * ln + q;
-                        if (p >= limit || lo <= i_stop || lo < 1 ||
+                        const int32_t hi = ib - a, lo = hi - umax;
+                        if (8 * ln + q >= nval || lo <= i_stop || lo < 1 ||
                             mask_of((uint32_t)lo) != mask_of((uint32_t)hi)) {
                             amb = true;
                         } else {
-                            const int64_t v = (int64_t)(x[q] & mask_of((uint32_t)hi));
+                            const int32_t v = (int32_t)(x[q] & mask_of((uint32_t)hi));
                             if (v <= lo) ++a;
                             else if (v <= hi) amb = true;
                         }
@@ -312,7 +321,7 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
             }
             const int total = __shfl_sync(0xffffffffu, incl, 31);
             // -- exact walk of lanes [b, ls]
-            int64_t ii = ib - (incl - cnt);
+            int32_t ii = ib - (incl - cnt);
             int endq = 8;
             int ne = 0;
             int32_t gaps[8];  // gaps[q] (statically indexed): near miss at draw q, or 0
@@ -321,16 +330,15 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
                 for (int q = 0; q < 8; ++q) {
                     gaps[q] = 0;
                     if (endq == 8) {
-                        const int64_t p = pos + 8 * ln + q;
-                        if (p >= limit || ii <= i_stop) {
+                        if (8 * ln + q >= nval || ii <= i_stop) {
                             endq = q;
                         } else {
-                            const int64_t v = (int64_t)(x[q] & mask_of((uint32_t)ii));
+                            const int32_t v = (int32_t)(x[q] & mask_of((uint32_t)ii));
                             if (v <= ii) {
-                                if (jout) jout[ii] = (int32_t)v;
+                                if (jout) jout[ii] = v;
                                 --ii;
                             } else if (v - ii <= w) {
-                                gaps[q] = (int32_t)(v - ii);
+                                gaps[q] = v - ii;
                                 ++ne;
                             }
                         }
