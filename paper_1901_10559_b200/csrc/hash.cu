@@ -620,10 +620,10 @@ __device__ void stitch_block(FyState* st, const FyChunk* __restrict__ ch, int64_
     }
 }
 
-__device__ __forceinline__ int64_t band_chunk_dev(int k) {
-    const double want = 2.3 * exp2(0.5 * k);
+__device__ __forceinline__ int64_t band_chunk_dev(int k, double mul, int64_t tmax) {
+    const double want = mul * exp2(0.5 * k);
     int64_t T = 256;
-    while (T < want && T < 4096) T <<= 1;
+    while (T < want && T < tmax) T <<= 1;
     return T;
 }
 
@@ -635,7 +635,7 @@ constexpr int kPbThreads = 128;
 __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
     const uint32_t* __restrict__ g, int64_t nbuf, int64_t n, int32_t* __restrict__ jout,
     FyState* st, FyChunk* __restrict__ ch, int64_t* __restrict__ starts, int64_t max_chunks,
-    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog) {
+    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max) {
     cg::grid_group grid = cg::this_grid();
     int tl = 0;  // optional stage timestamps (globaltimer, ns) written by block 0
     auto stamp = [&](int tag) {
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         const int64_t lo_band = 1LL << k;
         const int64_t i0 = tmin<int64_t>(2 * lo_band - 1, n - 1);
         if (i0 < lo_band) continue;
-        const int64_t T1 = band_chunk_dev(k);
+        const int64_t T1 = band_chunk_dev(k, tmul, t1max);
         const double draws1 = (double)(2 * lo_band) * log((double)(i0 + 1) / (double)lo_band);
         const int64_t rem_i = (int64_t)(3.0 * sqrt(draws1) + 16.0) + T1 + 64;
         const int64_t T2 = tmax<int64_t>(256, T1 / 8);
@@ -802,6 +802,8 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_
 
 int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel
 int g_fy_grid_cap = 0;         // >0: cap on the phase-B grid (CTAs)
+double g_fy_tmul = 1.6;        // chunk length of band k: pow2 >= tmul * 2^(k/2) (swept: 0.575..4.6)
+int64_t g_fy_tmax = 4096;      // ... capped here
 
 struct HashPlan {
     int64_t I, L;
@@ -967,8 +969,10 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
             int64_t* cons = d + 1;
             int64_t* stat = d + 3;
             int64_t* tlog = g_fy_tlog;
+            double tmul = g_fy_tmul;
+            int64_t tmax = g_fy_tmax;
             void* args[] = {&dr, &nbuf, &nI, &jarr, &fst, &chunks, &sts, &mc, &kmin, &cons, &stat,
-                            &tlog};
+                            &tlog, &tmul, &tmax};
             IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fy_phaseb_kernel, dim3(G),
                                                      dim3(kPbThreads), args, 0, st));
             ids_count_launch();
@@ -1005,6 +1009,12 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
         IDS_LAUNCH_CHECK();
     }
     return IDS_OK;
+}
+
+// Tuning hook (experiments): chunk-length rule of the speculative epochs.
+extern "C" void ids_debug_phaseb_chunks(double mul, int64_t tmax) {
+    g_fy_tmul = mul > 0 ? mul : 1.6;
+    g_fy_tmax = tmax >= 256 ? tmax : 4096;
 }
 
 // Debug hook: record phase-B stage timestamps into `buf` (device int64[512])

@@ -36,3 +36,21 @@ for I, L in ((10**6, 100), (10**7, 200)):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     print(f"hash I={I}: median {sorted(ts[1:])[2] * 1e3:.0f} us", flush=True)
+
+# chunk-length rule sweep (ids_debug_phaseb_chunks)
+lib.ids_debug_phaseb_chunks.argtypes = [ctypes.c_double, ctypes.c_int64]
+for mul, tmax in ((2.3, 4096), (1.15, 4096), (1.15, 8192), (0.8, 4096), (0.575, 4096), (1.6, 4096), (1.6, 8192)):
+    lib.ids_debug_phaseb_chunks(mul, tmax)
+    out = []
+    for I, L in ((10**6, 100), (10**7, 200)):
+        ts = []
+        for s in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            op = ids.CountSketchOp(I, L, seed=40 + s, surjective=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out.append(f"I={I}: {sorted(ts)[2] * 1e3:.0f} us")
+    print(f"mul {mul} tmax {tmax}: " + ", ".join(out), flush=True)
+lib.ids_debug_phaseb_chunks(0, 0)
