@@ -525,9 +525,14 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_of(args, w, world),
             "id_seconds": single_ms * 1e-3,
-            "trials": "K trials (seeds) of the same A queued back to back, one host sync at "
-                      "the end; each trial draws its own hash on the device, on a side stream "
-                      "beside the previous trial's sketch (sketch.pipelined_operators)",
+            "trials": ("K trials (seeds) of the same A queued back to back, one host sync at "
+                       "the end; each trial's hash is drawn on the device on a side stream "
+                       "beside the earlier trials' sketches (sketch.pipelined_operators)"
+                       if world == 1 else
+                       "K trials (seeds) of the same row-sharded A queued back to back, one "
+                       "host sync at the end; trial t's hash is drawn by rank t mod N and "
+                       "broadcast (distributed.trial_sharded_operators), each rank sketches "
+                       "its rows, one all-reduce of the sketch per trial"),
             "phases_ms": {"hash_and_index": hash_ms, "sketch": sk_ms, "cpqr_and_coeffs": id_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -137,6 +137,56 @@ def countsketch_id_sharded(a_local, row0, in_dim, rank, sketch_dim=None, seed=No
     return backend.matrix_id(y, sketch_dim, cols, rank, rank_tol, "countsketch")
 
 
+def trial_sharded_operators(in_dim, out_dim, seeds, surjective=False, group=None):
+    """CountSketchOps for a sequence of trials on every rank of `group`, each
+    hash drawn by ONE rank: trial t by rank t % world, all of a rank's draws
+    enqueued up front on side streams, then, trial by trial, one broadcast of
+    the packed (bucket, sign, draw counters) buffer -- 5 bytes per row -- from
+    its owner.  The Fisher-Yates resolution of a draw is a sequential chain
+    that does not shrink with the row shard, so drawing every trial on every
+    rank would cost each rank the whole job's draws; split, each rank pays
+    for about K / world of them.  Every rank yields bit-identical operators."""
+    from . import _device
+    from ._native import load
+    from .sketch import PIPELINE_GRID_CAP, CountSketchOp, _side_streams
+
+    world, me = _world(group)
+    seeds = list(seeds)
+    mine = [t for t in range(len(seeds)) if t % world == me]
+    dev = _device.device()
+    main = torch.cuda.current_stream()
+    sides = _side_streams(dev, max(1, min(len(mine), 4)))
+    lib = load()
+    cap = max(PIPELINE_GRID_CAP, 148 // max(1, min(len(mine), 4)))
+    drawn = {}
+    for n, t in enumerate(mine):
+        st = sides[n % len(sides)]
+        lib.ids_set_hash_grid_cap(cap)
+        try:
+            with torch.cuda.stream(st):
+                op = CountSketchOp(in_dim, out_dim, seed=seeds[t], surjective=surjective)
+                buf = op.packed()
+                ev = torch.cuda.Event()
+                ev.record()
+        finally:
+            lib.ids_set_hash_grid_cap(0)
+        drawn[t] = (buf, ev)
+    nbytes = CountSketchOp._packed_layout(in_dim)[2]
+    for t in range(len(seeds)):
+        owner = t % world
+        if owner == me:
+            buf, ev = drawn.pop(t)
+            main.wait_event(ev)
+            buf.record_stream(main)
+        else:
+            buf = _device.empty(nbytes, torch.uint8)
+        src = dist.get_global_rank(group, owner) if group is not None else owner
+        dist.broadcast(buf, src=src, group=group)
+        op = CountSketchOp._from_packed(buf, in_dim, out_dim, surjective)
+        op._bucket_index()
+        yield op
+
+
 def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, seeds=(0,),
                                   rank_tol=1e-12, surjective=True, group=None):
     """countsketch_id_sharded for several seeds, fully queued on the device:
@@ -161,10 +211,13 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     outs, flags = [], []
     main = torch.cuda.current_stream()
     side = id_stream()
-    # each trial's hash is drawn on a side stream while the previous trial
-    # sketches (sketch.pipelined_operators); each trial's ID runs on a
-    # high-priority stream beside the next trial's sketch
-    for op in pipelined_operators(in_dim, L, seeds, surjective):
+    # one rank: each trial's hash is drawn on a side stream while the previous
+    # trial sketches (sketch.pipelined_operators); several ranks: the trials'
+    # hashes are split over the ranks and broadcast (trial_sharded_operators).
+    # Each trial's ID runs on a high-priority stream beside the next sketch.
+    ops = (pipelined_operators(in_dim, L, seeds, surjective) if world == 1
+           else trial_sharded_operators(in_dim, L, seeds, surjective, group))
+    for op in ops:
         y = torch.empty((cols, L), dtype=torch.float64, device=torch.cuda.current_device())
         flag = torch.zeros(1, dtype=torch.int32, device=y.device)
         op.sketch_into(operand, y, row0=row0, accumulate=False, flags=IDS_FLAG_ORDERED,

@@ -120,6 +120,41 @@ class CountSketchOp:
         op._checked = True
         return op
 
+    # ---- packed form (one buffer per operator, for a collective) -----------
+    @staticmethod
+    def _packed_layout(in_dim):
+        """Byte offsets of (bucket int32, sign int8, draws int64[4]) in the
+        packed buffer, and its total size."""
+        b1 = 4 * in_dim
+        d0 = (b1 + in_dim + 15) // 16 * 16
+        return b1, d0, d0 + 32
+
+    def packed(self):
+        """bucket, sign and the draw counters in one device uint8 buffer."""
+        b1, d0, n = self._packed_layout(self.in_dim)
+        buf = _device.empty(n, torch.uint8)
+        buf[:b1].view(torch.int32).copy_(self._bucket_d)
+        buf[b1:b1 + self.in_dim].view(torch.int8).copy_(self._sign_d)
+        if self._draws is not None:
+            buf[d0:].view(torch.int64).copy_(self._draws)
+        else:
+            buf[d0:].zero_()
+        return buf
+
+    @classmethod
+    def _from_packed(cls, buf, in_dim, out_dim, surjective):
+        """Operator over a packed buffer (views, no copy): the hash drawn by
+        another rank and broadcast (distributed.countsketch_id_sharded_trials)."""
+        b1, d0, n = cls._packed_layout(in_dim)
+        op = cls.__new__(cls)
+        op.in_dim, op.out_dim, op.surjective = int(in_dim), int(out_dim), bool(surjective)
+        op._bucket_h = op._sign_h = op._index = None
+        op._bucket_d = buf[:b1].view(torch.int32)
+        op._sign_d = buf[b1:b1 + in_dim].view(torch.int8)
+        op._draws = buf[d0:n].view(torch.int64)
+        op._checked = False
+        return op
+
     def record_stream(self, stream):
         """Mark the operator's device arrays as used on `stream` (they may have
         been drawn on another stream, see pipelined_operators)."""

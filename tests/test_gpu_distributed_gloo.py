@@ -72,7 +72,18 @@ def _worker(rank, world, port, out):
         xl = SimpleNamespace(factors=[f[:, c0:c1] for f in x.factors], weights=x.weights[c0:c1],
                              mode_dims=x.mode_dims)
         td, nw = tensorsketch_id_sharded(xl, c0, R, x.weights, 5, 64, seed=8)
+        # trial-sharded hash draws: every rank gets every trial's hash, drawn by
+        # one owner rank and broadcast; compare with local draws bit for bit
+        from paper_1901_10559_b200.distributed import trial_sharded_operators
+        hashes_ok = []
+        for s_, op in zip([9, 10, 11, 12, 13],
+                          trial_sharded_operators(a.shape[0], 40, [9, 10, 11, 12, 13], True)):
+            local_op = ids.CountSketchOp(a.shape[0], 40, seed=s_, surjective=True)
+            hashes_ok.append(bool(np.array_equal(op.bucket, local_op.bucket)
+                                  and np.array_equal(op.sign, local_op.sign)
+                                  and op.draws == local_op.draws))
         out[rank] = {
+            "hashes_ok": hashes_ok,
             "cols": d.cols.tolist(), "coeffs": d.coeffs.tolist(),
             "trials": [(t.cols.tolist(), t.coeffs.tolist()) for t in trials],
             "raised": raised,
@@ -104,6 +115,7 @@ def test_row_and_term_sharding_on_device_kernels():
             assert relerr_fro(np.array(coeffs), single.coeffs) <= 1e-10
         assert o["raised"]  # an Inf on one rank raises on every rank
     assert out[0]["coeffs"] == out[1]["coeffs"]
+    assert out[0]["hashes_ok"] == [True] * 5 and out[1]["hashes_ok"] == [True] * 5
     rng = np.random.default_rng(42)
     R = 37
     fac = [rng.standard_normal((d_, R)) for d_ in (11, 9, 8)]
