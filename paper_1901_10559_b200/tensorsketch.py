@@ -40,6 +40,9 @@ def factor_to_device(f):
     return torch.from_numpy(np.ascontiguousarray(arr.T)).to(_device.device())
 
 
+SCATTER_MIN_DIM = 4096  # mode length from which the fused kernel uses a scatter plan
+
+
 def tensorsketch_device(op, factors, weights=None):
     """Y = TensorSketch(khatri_rao(factors)) diag(weights): CUDA (R, L) tensor."""
     if len(factors) != len(op.mode_ops):
@@ -68,7 +71,10 @@ def tensorsketch_device(op, factors, weights=None):
     if not query("ids_tensorsketch_fused_ok", n, L):
         return _tensorsketch_spectral(op, dev_f, w, ncols, L)
     idx = [m._bucket_index() for m in op.mode_ops]
-    plans = (ctypes.c_void_p * n)(*[_device.ptr(m._ts_plan()) for m in op.mode_ops])
+    # scatter plans pay off on long factor columns; short modes (C4: 1000
+    # rows) keep the gather path rather than pay the plan's launches per draw
+    plans = (ctypes.c_void_p * n)(*[_device.ptr(m._ts_plan()) if m.in_dim >= SCATTER_MIN_DIM
+                                    else None for m in op.mode_ops])
     fac_p = (ctypes.c_void_p * n)(*[_device.ptr(t) for t in dev_f])
     ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _, _ in idx])
     key_p = (ctypes.c_void_p * n)(*[_device.ptr(k) for _, _, k in idx])

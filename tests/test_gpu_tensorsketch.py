@@ -245,7 +245,10 @@ def _ts_both(op, factors, weights):
     ([1, 2, 3], 8, 3),              # tiny dims
     ([777, 1001], 1000, 9),         # non-power-of-two L (zero-padded transform)
 ])
-def test_scatter_plan_matches_gather_path_bit_for_bit(dims, L, r):
+def test_scatter_plan_matches_gather_path_bit_for_bit(dims, L, r, monkeypatch):
+    from paper_1901_10559_b200 import tensorsketch as tsmod
+
+    monkeypatch.setattr(tsmod, "SCATTER_MIN_DIM", 1)  # plans for every mode
     rng = np.random.default_rng(sum(dims) + L)
     factors = [rng.standard_normal((d, r)) for d in dims]
     weights = rng.random(r) + 0.5
