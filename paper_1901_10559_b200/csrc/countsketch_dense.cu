@@ -16,6 +16,9 @@
 //
 // Both paths are HBM-streaming kernels (algorithmic traffic = bytes of A);
 // tensor cores have nothing to do here.
+#include <limits.h>
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace {
@@ -189,6 +192,211 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
 }
 
+// ---- column-major tiled kernel (F-order A, the reference's as_dense layout) ----
+// Rows are cut into tiles of kTT.  A pre-pass (tile_slot_lists_kernel) sorts
+// each tile's rows ONCE by owner slot (bucket mod kSlots; stable, so every
+// slot's list is in increasing row order), packing (bucket, sign, tile row)
+// into one int32 per row.  The sketch kernel gives each CTA at most kCt
+// columns and a row segment (all rows when ordered); its 256 threads form
+// kSlots slots of kCt lanes, slot x owning the buckets l = x (mod kSlots).
+// Tile after tile -- A's column runs, the lists and the slot starts arriving
+// through a kCtStages-deep cp.async pipeline -- each slot walks its list and
+// every lane adds its column into acc[l][c], an accumulator no other slot
+// touches.  Each Y entry is therefore summed in increasing row order from
+// +0.0 (scipy's order, bit for bit) while A streams once at full width.
+constexpr int kCtThreads = 256;
+constexpr int kCt = 8;                       // columns per CTA (lanes per slot)
+constexpr int kSlots = kCtThreads / kCt;     // 32
+constexpr int kTT = 512;                     // rows per tile
+constexpr int kTTp = kTT + 2;                // padded column stride in shared memory
+constexpr int kStartsStride = 36;            // int32 slot starts per tile (kSlots + 1, 16-byte padded)
+constexpr int kCtStages = 3;
+
+__global__ void row_codes_kernel(const int32_t* __restrict__ bucket, const int8_t* __restrict__ sign,
+                                 int64_t row0, int64_t rows, int32_t* __restrict__ codes) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+         r += (int64_t)gridDim.x * blockDim.x)
+        codes[r] = enc_row(bucket[row0 + r], sign[row0 + r]);
+}
+
+// One CTA per tile: lists[tile][q] = (bucket << 10 | negative << 9 | row in
+// tile), grouped by slot in increasing row order; starts[tile][x] = first q
+// of slot x (x = 0..kSlots).
+__global__ void __launch_bounds__(kCtThreads) tile_slot_lists_kernel(
+    const int32_t* __restrict__ codes, int64_t rows, int32_t* __restrict__ lists,
+    int32_t* __restrict__ starts) {
+    constexpr int kRpt = kTT / kCtThreads, kGroups = kTT / 32, kWarps = kCtThreads / 32;
+    __shared__ int s_cnt[kGroups][kSlots + 1];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t rb = (int64_t)blockIdx.x * kTT;
+    const int n = (int)tmin<int64_t>(kTT, rows - rb);
+    const uint32_t lt = (1u << lane) - 1u;
+    int sl2[kRpt], rank2[kRpt], ent2[kRpt];
+#pragma unroll
+    for (int h = 0; h < kRpt; ++h) {
+        const int g = warp + kWarps * h, r = 32 * g + lane;
+        const int32_t e = r < n ? codes[rb + r] : INT_MIN;
+        const int sl = e == INT_MIN ? kSlots : (dec_row(e) % kSlots);
+        ent2[h] = (dec_row(e) << 10) | (e < 0 ? 512 : 0) | r;
+        const uint32_t peers = __match_any_sync(0xffffffffu, sl);
+        const int rank = __popc(peers & lt);
+        for (int x = lane; x <= kSlots; x += 32) s_cnt[g][x] = 0;
+        __syncwarp();
+        if (rank == 0) s_cnt[g][sl] = __popc(peers);
+        sl2[h] = sl;
+        rank2[h] = rank;
+    }
+    __syncthreads();
+    if (warp == 0) {  // lane = slot (kSlots == 32): bases per (group, slot), slot starts
+        int tot = 0;
+        for (int g = 0; g < kGroups; ++g) tot += s_cnt[g][lane];
+        int incl = tot;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        int run = incl - tot;
+        starts[blockIdx.x * (int64_t)kStartsStride + lane] = run;
+        if (lane == 31) {
+            starts[blockIdx.x * (int64_t)kStartsStride + kSlots] = incl;
+            for (int x = kSlots + 1; x < kStartsStride; ++x)
+                starts[blockIdx.x * (int64_t)kStartsStride + x] = incl;
+        }
+        for (int g = 0; g < kGroups; ++g) {
+            const int cg = s_cnt[g][lane];
+            s_cnt[g][lane] = run;
+            run += cg;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < kRpt; ++h) {
+        const int g = warp + kWarps * h;
+        if (sl2[h] < kSlots) lists[rb + s_cnt[g][sl2[h]] + rank2[h]] = ent2[h];
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr size_t kCtStageBytes =
+    (size_t)kCt * kTTp * sizeof(double) + kTT * sizeof(int32_t) + kStartsStride * sizeof(int32_t);
+
+size_t coltile_smem(int64_t L) { return (size_t)L * kCt * sizeof(double) + kCtStages * kCtStageBytes; }
+
+__global__ void __launch_bounds__(kCtThreads) cs_coltile_kernel(
+    const double* __restrict__ A, int64_t ld, int64_t rows, int64_t cols,
+    const int32_t* __restrict__ lists, const int32_t* __restrict__ starts, int64_t L,
+    int ngroups, int nseg, int vec16, double* __restrict__ out, int64_t seg_stride,
+    int init_from_out) {
+    extern __shared__ double sm[];
+    double* acc = sm;  // [L][kCt]
+    char* stages = reinterpret_cast<char*>(acc + L * kCt);
+    const int t = threadIdx.x;
+    const int group = blockIdx.x % ngroups, seg = blockIdx.x / ngroups;
+    // column groups of at most kCt columns, balanced (ngroups >= cols / kCt)
+    const int64_t c0 = cols * group / ngroups;
+    const int nc = (int)(cols * (group + 1) / ngroups - c0);
+    // segment rows: boundaries on tile multiples (tile bases stay aligned)
+    const int64_t ntl = (rows + kTT - 1) / kTT;
+    const int64_t tb = ntl * seg / nseg, te = ntl * (seg + 1) / nseg;
+    double* o = out + (int64_t)seg * seg_stride;
+    for (int64_t q = t; q < L * kCt; q += kCtThreads) {
+        const int64_t l = q / kCt, c = q % kCt;
+        acc[q] = (init_from_out && c < nc) ? o[(c0 + c) * L + l] : 0.0;
+    }
+    auto stage_tile = [&](int s) { return reinterpret_cast<double*>(stages + s * kCtStageBytes); };
+    auto stage_list = [&](int s) {
+        return reinterpret_cast<int32_t*>(stages + s * kCtStageBytes + (size_t)kCt * kTTp * sizeof(double));
+    };
+    auto stage_starts = [&](int s) { return stage_list(s) + kTT; };
+    // copy tile k (k = 0 .. te - tb - 1) into stage k % kCtStages
+    auto issue = [&](int64_t k) {
+        const int64_t tile = tb + k;
+        if (tile < te) {
+            const int64_t rb = tile * kTT;
+            const int n = (int)tmin<int64_t>(kTT, rows - rb);
+            const int s = (int)(k % kCtStages);
+            double* dst = stage_tile(s);
+            if (vec16 && n == kTT) {
+                for (int q = t; q < kCt * (kTT / 2); q += kCtThreads) {
+                    const int c = q / (kTT / 2), j = q % (kTT / 2);
+                    if (c < nc) cp_async16(dst + c * kTTp + 2 * j, A + (c0 + c) * ld + rb + 2 * j);
+                }
+            } else {
+                for (int q = t; q < kCt * kTT; q += kCtThreads) {
+                    const int c = q / kTT, j = q % kTT;
+                    if (c < nc && j < n) cp_async8(dst + c * kTTp + j, A + (c0 + c) * ld + rb + j);
+                }
+            }
+            int32_t* ldst = stage_list(s);
+            for (int q = t; q < kTT / 4 + kStartsStride / 4; q += kCtThreads) {
+                if (q < kTT / 4) cp_async16(ldst + 4 * q, lists + rb + 4 * q);
+                else cp_async16(stage_starts(s) + 4 * (q - kTT / 4),
+                                starts + tile * kStartsStride + 4 * (q - kTT / 4));
+            }
+        }
+        cp_commit();
+    };
+    for (int64_t k = 0; k < kCtStages - 1; ++k) issue(k);
+    const int slot = t / kCt, c = t % kCt;
+    for (int64_t k = 0; k < te - tb; ++k) {
+        issue(k + kCtStages - 1);
+        cp_wait<kCtStages - 1>();
+        __syncthreads();
+        const int s = (int)(k % kCtStages);
+        const double* tl = stage_tile(s);
+        const int32_t* lst = stage_list(s);
+        const int32_t* sts = stage_starts(s);
+        // every slot walks its own rows; its lanes own one column each.  Two
+        // rows per step: independent unless they share a bucket.
+        if (c < nc) {
+            const int q1 = sts[slot + 1];
+            int q = sts[slot];
+            for (; q + 1 < q1; q += 2) {
+                const int32_t e0 = lst[q], e1 = lst[q + 1];
+                const double v0 = tl[c * kTTp + (e0 & 511)], v1 = tl[c * kTTp + (e1 & 511)];
+                const int b0 = e0 >> 10, b1 = e1 >> 10;
+                double* p0 = acc + (int64_t)b0 * kCt + c;
+                double a0 = *p0;
+                a0 = (e0 & 512) ? a0 - v0 : a0 + v0;
+                if (b0 == b1) {
+                    a0 = (e1 & 512) ? a0 - v1 : a0 + v1;
+                    *p0 = a0;
+                } else {
+                    double* p1 = acc + (int64_t)b1 * kCt + c;
+                    const double a1 = *p1;
+                    *p0 = a0;
+                    *p1 = (e1 & 512) ? a1 - v1 : a1 + v1;
+                }
+            }
+            if (q < q1) {
+                const int32_t e0 = lst[q];
+                const double v0 = tl[c * kTTp + (e0 & 511)];
+                double* p0 = acc + (int64_t)(e0 >> 10) * kCt + c;
+                *p0 = (e0 & 512) ? *p0 - v0 : *p0 + v0;
+            }
+        }
+        __syncthreads();  // the stage is refilled by a later issue()
+    }
+    cp_wait<0>();
+    __syncthreads();
+    for (int64_t q = t; q < L * kCt; q += kCtThreads) {
+        const int64_t l = q % L, cc = q / L;  // consecutive threads: consecutive l (coalesced Y)
+        if (cc < nc) o[(c0 + cc) * L + l] = acc[l * kCt + cc];
+    }
+}
+
 // Y[e] = (accumulate ? Y[e] : 0) + sum_s part[s][e], s in order.
 __global__ void seg_reduce_kernel(const double* __restrict__ part, int nseg, int64_t n,
                                   int64_t seg_stride, double* __restrict__ Y, int accumulate) {
@@ -274,6 +482,28 @@ DensePlan plan_dense(int64_t rows, int64_t cols, int64_t L, int layout, int flag
     return p;
 }
 
+struct ColTilePlan {
+    bool use;
+    int ngroups, nseg;
+    int64_t ntiles;
+    size_t smem;
+};
+
+// The tiled kernel needs L x kCt accumulators beside the tile pipeline, and
+// packs buckets into 21 bits of a list entry.
+ColTilePlan plan_coltile(int64_t rows, int64_t cols, int64_t L, int flags) {
+    ColTilePlan p{};
+    p.smem = coltile_smem(L);
+    p.use = p.smem <= 200 * 1024 && L < (1 << 21);
+    p.ntiles = ceil_div(rows, kTT);
+    // whole waves of two CTAs per SM when the columns allow it
+    p.ngroups = (int)tmax<int64_t>(ceil_div(cols, kCt), tmin<int64_t>(cols, 2 * 148));
+    p.nseg = 1;
+    if (!(flags & IDS_FLAG_ORDERED) && p.ngroups < 2 * 148)
+        p.nseg = (int)tmax<int64_t>(1, tmin<int64_t>(ceil_div(2 * 148, p.ngroups), p.ntiles / 4));
+    return p;
+}
+
 }  // namespace
 
 extern "C" size_t ids_countsketch_dense_workspace_bytes(int64_t rows, int64_t cols,
@@ -283,6 +513,14 @@ extern "C" size_t ids_countsketch_dense_workspace_bytes(int64_t rows, int64_t co
     const DensePlan p1 = plan_dense(rows, cols, out_dim, layout, 0, false, rows);
     const int nseg = max(p.nseg, p1.nseg);
     WsCount c;
+    if (layout == IDS_COL_MAJOR && plan_coltile(rows, cols, out_dim, 0).use) {
+        const ColTilePlan q = plan_coltile(rows, cols, out_dim, 0);
+        c.take<double>((size_t)tmax(nseg, q.nseg) * out_dim * cols);
+        c.take<int32_t>((size_t)rows);
+        c.take<int32_t>((size_t)q.ntiles * kTT);
+        c.take<int32_t>((size_t)q.ntiles * kStartsStride);
+        return c.off + 256;
+    }
     c.take<double>((size_t)nseg * out_dim * cols);
     if (layout == IDS_COL_MAJOR && p.global_acc) c.take<double>((size_t)p.units * p.nc * out_dim);
     return c.off + 256;
@@ -302,6 +540,50 @@ extern "C" int ids_countsketch_dense_f64(const double* A, int64_t rows, int64_t 
         return IDS_EINVAL;
     }
     cudaStream_t st = as_stream(stream);
+    if (layout == IDS_COL_MAJOR) {
+        const ColTilePlan q = plan_coltile(rows, cols, out_dim, flags);
+        if (q.use) {
+            WsCarve ws(workspace, ws_bytes);
+            double* part = q.nseg > 1 ? ws.take<double>((size_t)q.nseg * out_dim * cols) : nullptr;
+            int32_t* codes = ws.take<int32_t>((size_t)rows);
+            int32_t* lists = ws.take<int32_t>((size_t)q.ntiles * kTT);
+            int32_t* starts = ws.take<int32_t>((size_t)q.ntiles * kStartsStride);
+            if (!ws.ok()) {
+                ids_set_last_error("dense countsketch: workspace too small");
+                return IDS_EWORKSPACE;
+            }
+            const int64_t seg_stride = out_dim * cols;
+            const unsigned gc = (unsigned)tmin<int64_t>(ceil_div(rows, 256), 148 * 8);
+            row_codes_kernel<<<gc, 256, 0, st>>>(bucket, sign, row0, rows, codes);
+            IDS_LAUNCH_CHECK();
+            tile_slot_lists_kernel<<<(unsigned)q.ntiles, kCtThreads, 0, st>>>(codes, rows, lists,
+                                                                              starts);
+            IDS_LAUNCH_CHECK();
+            const int vec16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (ld % 2 == 0);
+            double* out = q.nseg > 1 ? part : Y;
+            const int init = (q.nseg == 1 && accumulate) ? 1 : 0;
+            const unsigned grid = (unsigned)((int64_t)q.ngroups * q.nseg);
+            IDS_CUDA_TRY(cudaFuncSetAttribute(cs_coltile_kernel,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)q.smem));
+            cs_coltile_kernel<<<grid, kCtThreads, q.smem, st>>>(A, ld, rows, cols, lists, starts,
+                                                                out_dim, q.ngroups, q.nseg, vec16,
+                                                                out, seg_stride, init);
+            IDS_LAUNCH_CHECK();
+            if (q.nseg > 1) {
+                const unsigned g = (unsigned)tmin<int64_t>(ceil_div(seg_stride, 256), 148 * 8);
+                seg_reduce_kernel<<<g, 256, 0, st>>>(part, q.nseg, seg_stride, seg_stride, Y,
+                                                     accumulate);
+                IDS_LAUNCH_CHECK();
+            }
+            if (nonfinite) {
+                const unsigned g = (unsigned)tmin<int64_t>(ceil_div(seg_stride, 256), 148 * 4);
+                nonfinite_scan_kernel<<<g, 256, 0, st>>>(Y, seg_stride, nonfinite);
+                IDS_LAUNCH_CHECK();
+            }
+            return IDS_OK;
+        }
+    }
     const bool aligned2 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (ld % 2 == 0) &&
                           (cols % 2 == 0);
     const DensePlan p = plan_dense(rows, cols, out_dim, layout, flags, aligned2,
