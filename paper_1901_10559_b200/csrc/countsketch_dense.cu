@@ -329,10 +329,11 @@ __global__ void __launch_bounds__(kCtThreads) cs_coltile_kernel(
             const int s = (int)(k % kCtStages);
             double* dst = stage_tile(s);
             if (vec16 && n == kTT) {
-                for (int q = t; q < kCt * (kTT / 2); q += kCtThreads) {
-                    const int c = q / (kTT / 2), j = q % (kTT / 2);
-                    if (c < nc) cp_async16(dst + c * kTTp + 2 * j, A + (c0 + c) * ld + rb + 2 * j);
-                }
+                static_assert(kTT / 2 == kCtThreads, "one 16-byte copy per thread and column");
+                const double* src = A + c0 * ld + rb + 2 * t;
+#pragma unroll
+                for (int c = 0; c < kCt; ++c, src += ld)
+                    if (c < nc) cp_async16(dst + c * kTTp + 2 * t, src);
             } else {
                 for (int q = t; q < kCt * kTT; q += kCtThreads) {
                     const int c = q / kTT, j = q % kTT;
