@@ -18,4 +18,7 @@ run_full cpqr_kernel cpqr_c5 --tensor 4,10000,2000,16384,20
 run_full cs_csr_stream cs_csr_stream --csr 10000000,10000,100000000,200,20
 run_full fy_phaseb fy_phaseb
 run_full cpqr_cluster cpqr_cluster
+python tools/exp_fortran_one.py > gpurun_out/full_plain_coltile.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:cs_coltile -s 1 -c 1 \
+      -o gpurun_out/full_cs_coltile python tools/exp_fortran_one.py > gpurun_out/ncu_full_coltile.log 2>&1
 echo round profiles done

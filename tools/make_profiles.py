@@ -89,6 +89,8 @@ for rep, name, title in (("ev_rowmajor.ncu-rep", "cs_rowmajor", "cs_rowmajor_ker
                          ("full_tensorsketch_c5.ncu-rep", "tensorsketch_c5",
                           "tensorsketch_kernel<16>, C5 (N=4, I=1e4, R=2000, L=16384)"),
                          ("full_cpqr_c5.ncu-rep", "cpqr_c5", "cpqr_kernel, C5 sketch 16384 x 2000, k=20"),
+                         ("full_cs_coltile.ncu-rep", "cs_coltile",
+                          "cs_coltile_kernel, configs[1] shape in F order (1e6 x 2000, L=100)"),
                          ("full_cs_csr_stream.ncu-rep", "cs_csr_stream",
                           "cs_csr_stream_kernel, C3 (CSR 1e7 x 1e4, nnz 1e8, L=200)"),
                          ("full_cs_csr_bucket.ncu-rep", "cs_csr_bucket",
