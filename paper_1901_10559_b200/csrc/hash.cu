@@ -232,7 +232,34 @@ struct FyState {
     int64_t pos;   // next unconsumed draw (relative to the phase-B stream)
     int64_t i;     // current i
     int64_t done;  // number of chunks resolved by the last stitch
+    unsigned bar_count, bar_gen;  // grid barrier (zeroed before launch)
 };
+
+// Grid-wide barrier of the cooperative phase-B kernel: one thread per CTA
+// arrives on a counter and the waiters poll the generation word with a
+// nanosleep back-off, so the CTAs parked at a barrier leave the SMs (and the
+// L2 slice of the counter) to the few warps doing the serial stitch/walks.
+__device__ __forceinline__ void fy_grid_bar(FyState* st, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = &st->bar_gen;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(&st->bar_count, 1u) == nblocks - 1) {
+            st->bar_count = 0;
+            __threadfence();
+            atomicAdd(&st->bar_gen, 1u);
+        } else {
+            unsigned ns = 32;
+            while (*gen == g0) {
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
 
 // One warp walks the chain EXACTLY over draws [pos, limit) from a known i,
 // until i == i_stop: 256 draws per window, 8 consecutive draws per lane.
@@ -635,8 +662,12 @@ constexpr int kPbThreads = 128;
 __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
     const uint32_t* __restrict__ g, int64_t nbuf, int64_t n, int32_t* __restrict__ jout,
     FyState* st, FyChunk* __restrict__ ch, int64_t* __restrict__ starts, int64_t max_chunks,
-    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max) {
+    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max, int custom_bar) {
     cg::grid_group grid = cg::this_grid();
+    auto gsync = [&]() {
+        if (custom_bar) fy_grid_bar(st, gridDim.x);
+        else grid.sync();
+    };
     int tl = 0;  // optional stage timestamps (globaltimer, ns) written by block 0
     auto stamp = [&](int tag) {
         if (tlog && blockIdx.x == 0 && threadIdx.x == 0 && tl < 254) {
@@ -662,7 +693,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         st->i = n - 1;
         st->done = 0;
     }
-    grid.sync();
+    gsync();
     stamp(0);
     int top = 0;
     while ((2LL << top) <= n - 1) ++top;
@@ -683,11 +714,11 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
             const int64_t ei = st->i, ep = st->pos;
             for (int64_t c = gw; c < nch; c += nw) chunk_work(g, nbuf, ei, ep, lo_band, T, c, ch, evs[wib]);
             stamp(100 * k + 10 * e + 1);
-            grid.sync();
+            gsync();
             stamp(100 * k + 10 * e + 2);
             if (blockIdx.x == 0) stitch_block(st, ch, nch, T, starts, sm);
             stamp(100 * k + 10 * e + 3);
-            grid.sync();
+            gsync();
             stamp(100 * k + 10 * e + 4);
             const int64_t done = st->done;
             for (int64_t c = gw; c < done; c += nw) {
@@ -698,7 +729,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
             // stitch that rewrites `starts` is behind the next grid barrier
         }
         stamp(100 * k + 5);
-        grid.sync();  // exact re-runs may still write j; st is final for the walk
+        gsync();  // exact re-runs may still write j; st is final for the walk
         stamp(100 * k + 6);
         if (lead_warp) {
             const WalkOut r = lo_band < 16384
@@ -711,7 +742,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
             }
         }
         stamp(100 * k + 7);
-        grid.sync();
+        gsync();
     }
     stamp(9000);
     if (lead_warp) {
@@ -802,6 +833,7 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_
 
 int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel
 int g_fy_grid_cap = 0;         // >0: cap on the phase-B grid (CTAs)
+int g_fy_custom_bar = 1;       // 1: nanosleep grid barrier (measured ~10% faster than cg grid.sync)
 double g_fy_tmul = 1.6;        // chunk length of band k: pow2 >= tmul * 2^(k/2) (swept: 0.575..4.6)
 int64_t g_fy_tmax = 4096;      // ... capped here
 
@@ -969,10 +1001,12 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
             int64_t* cons = d + 1;
             int64_t* stat = d + 3;
             int64_t* tlog = g_fy_tlog;
+            int cbar = g_fy_custom_bar;
+            if (cbar) IDS_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(FyState), st));
             double tmul = g_fy_tmul;
             int64_t tmax = g_fy_tmax;
             void* args[] = {&dr, &nbuf, &nI, &jarr, &fst, &chunks, &sts, &mc, &kmin, &cons, &stat,
-                            &tlog, &tmul, &tmax};
+                            &tlog, &tmul, &tmax, &cbar};
             IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fy_phaseb_kernel, dim3(G),
                                                      dim3(kPbThreads), args, 0, st));
             ids_count_launch();
@@ -1012,6 +1046,8 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
 }
 
 // Tuning hook (experiments): chunk-length rule of the speculative epochs.
+extern "C" void ids_debug_fy_custom_bar(int v) { g_fy_custom_bar = v; }
+
 extern "C" void ids_debug_phaseb_chunks(double mul, int64_t tmax) {
     g_fy_tmul = mul > 0 ? mul : 1.6;
     g_fy_tmax = tmax >= 256 ? tmax : 4096;

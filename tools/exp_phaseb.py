@@ -54,3 +54,22 @@ for mul, tmax in ((2.3, 4096), (1.15, 4096), (1.15, 8192), (0.8, 4096), (0.575, 
         out.append(f"I={I}: {sorted(ts)[2] * 1e3:.0f} us")
     print(f"mul {mul} tmax {tmax}: " + ", ".join(out), flush=True)
 lib.ids_debug_phaseb_chunks(0, 0)
+
+# cooperative-groups grid.sync vs the nanosleep barrier (ids_debug_fy_custom_bar)
+lib.ids_debug_fy_custom_bar.argtypes = [ctypes.c_int]
+for cb in (0, 1, 0, 1):
+    lib.ids_debug_fy_custom_bar(cb)
+    out = []
+    for I, L in ((10**6, 100), (10**7, 200)):
+        ts = []
+        for s in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            op = ids.CountSketchOp(I, L, seed=70 + s, surjective=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ref = oracle_ok = None
+        out.append(f"I={I}: {sorted(ts)[2] * 1e3:.0f} us")
+    print(f"custom barrier {cb}: " + ", ".join(out), flush=True)
+lib.ids_debug_fy_custom_bar(1)
