@@ -232,34 +232,9 @@ struct FyState {
     int64_t pos;   // next unconsumed draw (relative to the phase-B stream)
     int64_t i;     // current i
     int64_t done;  // number of chunks resolved by the last stitch
-    unsigned bar_count, bar_gen;  // grid barrier (zeroed before launch)
+    unsigned bar_count, bar_gen;  // ids_grid_bar state (zeroed before launch)
 };
 
-// Grid-wide barrier of the cooperative phase-B kernel: one thread per CTA
-// arrives on a counter and the waiters poll the generation word with a
-// nanosleep back-off, so the CTAs parked at a barrier leave the SMs (and the
-// L2 slice of the counter) to the few warps doing the serial stitch/walks.
-__device__ __forceinline__ void fy_grid_bar(FyState* st, unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* gen = &st->bar_gen;
-        const unsigned g0 = *gen;
-        __threadfence();
-        if (atomicAdd(&st->bar_count, 1u) == nblocks - 1) {
-            st->bar_count = 0;
-            __threadfence();
-            atomicAdd(&st->bar_gen, 1u);
-        } else {
-            unsigned ns = 32;
-            while (*gen == g0) {
-                __nanosleep(ns);
-                if (ns < 256) ns <<= 1;
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
 
 // One warp walks the chain EXACTLY over draws [pos, limit) from a known i,
 // until i == i_stop: 256 draws per window, 8 consecutive draws per lane.
@@ -665,7 +640,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
     int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max, int custom_bar) {
     cg::grid_group grid = cg::this_grid();
     auto gsync = [&]() {
-        if (custom_bar) fy_grid_bar(st, gridDim.x);
+        if (custom_bar) ids_grid_bar(&st->bar_count, gridDim.x);
         else grid.sync();
     };
     int tl = 0;  // optional stage timestamps (globaltimer, ns) written by block 0
