@@ -157,7 +157,8 @@ def trial_sharded_operators(in_dim, out_dim, seeds, surjective=False, group=None
     main = torch.cuda.current_stream()
     sides = _side_streams(dev, max(1, min(len(mine), 4)))
     lib = load()
-    cap = max(PIPELINE_GRID_CAP, 148 // max(1, min(len(mine), 4)))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    cap = max(PIPELINE_GRID_CAP, sms // max(1, min(len(mine), 4)))
     drawn = {}
     for n, t in enumerate(mine):
         st = sides[n % len(sides)]
