@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
             const int64_t cnt = g.small ? (c1 - c0) * ns : ub1 - ub0;
             const bool rev = !g.small && (kk & 1);
             const bool full = (m % kSeg) == 0;  // no clamping needed
+            const int nl = (g.small && m < kSeg) ? (int)((m + 31) / 32) : kSegLoads;
             for (int64_t li = wid; li < cnt; li += 2 * kWarps) {
                 int64_t j1, sg1, j2, sg2;
                 const bool h2 = li + kWarps < cnt;
@@ -333,11 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
                         y1[t] = p1[b1 + 32 * t];
                         y2[t] = p2[b2 + 32 * t];
                     }
-                } else {  // clamped rows (v is zero there)
+                } else {  // clamped rows (v is zero there); a short sketch
+                          // (m < kSeg) loads only its nl row groups
 #pragma unroll
                     for (int t = 0; t < kSegLoads; ++t) {
-                        y1[t] = p1[tmin(b1 + 32 * t, m - 1)];
-                        y2[t] = p2[tmin(b2 + 32 * t, m - 1)];
+                        y1[t] = t < nl ? p1[tmin(b1 + 32 * t, m - 1)] : 0.0;
+                        y2[t] = t < nl ? p2[tmin(b2 + 32 * t, m - 1)] : 0.0;
                     }
                 }
                 const double* v1 = vsm + (b1 - vlo);
@@ -345,10 +347,14 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
                 double s1 = 0.0, s2 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
                 for (int t = 0; t < kSegLoads; t += 2) {
-                    s1 = fma(y1[t], v1[32 * t], s1);
-                    t1 = fma(y1[t + 1], v1[32 * t + 32], t1);
-                    s2 = fma(y2[t], v2[32 * t], s2);
-                    t2 = fma(y2[t + 1], v2[32 * t + 32], t2);
+                    if (t < nl) {
+                        s1 = fma(y1[t], v1[32 * t], s1);
+                        s2 = fma(y2[t], v2[32 * t], s2);
+                    }
+                    if (t + 1 < nl) {
+                        t1 = fma(y1[t + 1], v1[32 * t + 32], t1);
+                        t2 = fma(y2[t + 1], v2[32 * t + 32], t2);
+                    }
                 }
                 const double w1 = warp_sum(s1 + t1), w2 = warp_sum(s2 + t2);
                 if (lane == 0) {
