@@ -637,7 +637,7 @@ constexpr int kPbThreads = 128;
 __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
     const uint32_t* __restrict__ g, int64_t nbuf, int64_t n, int32_t* __restrict__ jout,
     FyState* st, FyChunk* __restrict__ ch, int64_t* __restrict__ starts, int64_t max_chunks,
-    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max, int custom_bar) {
+    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max, int custom_bar, double e2_min_draws) {
     cg::grid_group grid = cg::this_grid();
     auto gsync = [&]() {
         if (custom_bar) ids_grid_bar(&st->bar_count, gridDim.x);
@@ -686,6 +686,9 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
                                                       : (2 * rem_i) / T2 + 2,
                                               max_chunks);
             if (nch < 2) continue;
+            // the second (short-chunk) epoch only pays on long bands: on short
+            // ones the exact tail walk is cheaper than its barriers and stitch
+            if (e == 1 && draws1 < e2_min_draws) continue;
             const int64_t ei = st->i, ep = st->pos;
             for (int64_t c = gw; c < nch; c += nw) chunk_work(g, nbuf, ei, ep, lo_band, T, c, ch, evs[wib]);
             stamp(100 * k + 10 * e + 1);
@@ -808,6 +811,7 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_
 
 int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel
 int g_fy_grid_cap = 0;         // >0: cap on the phase-B grid (CTAs)
+double g_fy_e2_min = 65536.0;  // bands with fewer draws skip the second epoch (swept 0..1e30)
 int g_fy_custom_bar = 1;       // 1: nanosleep grid barrier (measured ~10% faster than cg grid.sync)
 double g_fy_tmul = 1.6;        // chunk length of band k: pow2 >= tmul * 2^(k/2) (swept: 0.575..4.6)
 int64_t g_fy_tmax = 4096;      // ... capped here
@@ -979,9 +983,10 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
             int cbar = g_fy_custom_bar;
             if (cbar) IDS_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(FyState), st));
             double tmul = g_fy_tmul;
+            double e2min = g_fy_e2_min;
             int64_t tmax = g_fy_tmax;
             void* args[] = {&dr, &nbuf, &nI, &jarr, &fst, &chunks, &sts, &mc, &kmin, &cons, &stat,
-                            &tlog, &tmul, &tmax, &cbar};
+                            &tlog, &tmul, &tmax, &cbar, &e2min};
             IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fy_phaseb_kernel, dim3(G),
                                                      dim3(kPbThreads), args, 0, st));
             ids_count_launch();
@@ -1022,6 +1027,8 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
 
 // Tuning hook (experiments): chunk-length rule of the speculative epochs.
 extern "C" void ids_debug_fy_custom_bar(int v) { g_fy_custom_bar = v; }
+
+extern "C" void ids_debug_fy_e2_min(double d) { g_fy_e2_min = d; }
 
 extern "C" void ids_debug_phaseb_chunks(double mul, int64_t tmax) {
     g_fy_tmul = mul > 0 ? mul : 1.6;

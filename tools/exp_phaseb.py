@@ -73,3 +73,21 @@ for cb in (0, 1, 0, 1):
         out.append(f"I={I}: {sorted(ts)[2] * 1e3:.0f} us")
     print(f"custom barrier {cb}: " + ", ".join(out), flush=True)
 lib.ids_debug_fy_custom_bar(1)
+
+# second-epoch threshold (ids_debug_fy_e2_min)
+lib.ids_debug_fy_e2_min.argtypes = [ctypes.c_double]
+for th in (0.0, 2.0**14, 2.0**16, 2.0**18, 2.0**20, 1e30, 0.0):
+    lib.ids_debug_fy_e2_min(th)
+    out = []
+    for I, L in ((10**6, 100), (10**7, 200)):
+        ts = []
+        for s in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            op = ids.CountSketchOp(I, L, seed=110 + s, surjective=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out.append(f"I={I}: {sorted(ts)[2] * 1e3:.0f} us")
+    print(f"e2 min draws {th:.3g}: " + ", ".join(out), flush=True)
+lib.ids_debug_fy_e2_min(65536.0)
