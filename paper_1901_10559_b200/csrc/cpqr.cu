@@ -849,6 +849,48 @@ __global__ void id_solve_kernel(const double* __restrict__ Rtop, int64_t k, int6
     }
 }
 
+// id_solve_kernel for k <= kSolveRegs: each thread's column of T lives in
+// registers and R11 in shared memory; the same operations in the same order
+// (bit-identical results), without a global read-modify-write per update.
+constexpr int kSolveRegs = 24;
+__global__ void __launch_bounds__(128) id_solve_reg_kernel(const double* __restrict__ Rtop,
+                                                           int64_t k, int64_t n, double rank_tol,
+                                                           const int32_t* __restrict__ numerical_rank,
+                                                           double* __restrict__ T) {
+    __shared__ double r11[kSolveRegs * kSolveRegs];
+    const int64_t nt = n - k;
+    const double lead = fabs(Rtop[0]);
+    const bool deficient = *numerical_rank < k;
+    const double floorv = rank_tol * lead;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+        const int q = e / (int)k, i = e % (int)k;
+        double d = Rtop[q * n + i];
+        if (q == i && deficient && fabs(d) < floorv) d = d < 0.0 ? -floorv : floorv;
+        r11[q * kSolveRegs + i] = d;
+    }
+    __syncthreads();
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nt;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        double tv[kSolveRegs];
+#pragma unroll
+        for (int q = 0; q < kSolveRegs; ++q) tv[q] = (q < k && lead != 0.0) ? Rtop[q * n + k + p] : 0.0;
+        if (lead != 0.0) {
+#pragma unroll
+            for (int q = kSolveRegs - 1; q >= 0; --q) {
+                if (q < k && tv[q] != 0.0) {
+                    const double tq = tv[q] / r11[q * kSolveRegs + q];
+                    tv[q] = tq;
+#pragma unroll
+                    for (int i = 0; i < q; ++i) tv[i] = fma(-tq, r11[i * kSolveRegs + q], tv[i]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kSolveRegs; ++q)
+            if (q < k) T[q * nt + p] = tv[q];
+    }
+}
+
 // P[q, perm[c]] = (c < k) ? (q == c) : T[q, c - k]   (row-major k x n)
 __global__ void id_scatter_kernel(const double* __restrict__ T, const int32_t* __restrict__ perm,
                                   int64_t k, int64_t n, double* __restrict__ P) {
@@ -1086,7 +1128,10 @@ extern "C" int ids_id_coeffs_f64(const double* Rtop, const int32_t* perm, int64_
     }
     if (nt > 0) {
         const unsigned g = (unsigned)tmin<int64_t>(ceil_div(nt, 128), 148 * 8);
-        id_solve_kernel<<<g, 128, 0, st>>>(Rtop, k, cols, rank_tol, numerical_rank, T);
+        if (k <= kSolveRegs)
+            id_solve_reg_kernel<<<g, 128, 0, st>>>(Rtop, k, cols, rank_tol, numerical_rank, T);
+        else
+            id_solve_kernel<<<g, 128, 0, st>>>(Rtop, k, cols, rank_tol, numerical_rank, T);
         IDS_LAUNCH_CHECK();
     }
     const unsigned g2 = (unsigned)tmin<int64_t>(ceil_div(k * cols, 256), 148 * 8);
