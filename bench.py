@@ -227,7 +227,7 @@ def config_of(args, w, world):
             "parallelism": f"rows{world}", "l2": "A (>126 MB) larger than L2, no flush"}
 
 
-def secondary_configs(torch, dev, steps=3):
+def secondary_configs(torch, dev, steps=6):
     """Live device timings (CUDA events, after warm-up) of one full ID at the
     other BASELINE.json configs, on seeded synthetic inputs of their shapes
     built on the device: C3 CSR 1e7 x 1e4 with 1e8 nonzeros,
