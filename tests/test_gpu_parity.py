@@ -64,6 +64,22 @@ def test_hash_draw_counts_match_oracle():
         assert np.array_equal(op.sign, o.sign)
 
 
+@pytest.mark.parametrize("I,L,seed,surj", [
+    (5000, 1_500_000_000, 21, False),      # ~30% of the Lemire draws rejected
+    (20_000, 2_000_000_001, 22, False),    # ~7% rejected
+    (6_000_001, 3_000_000, 23, True),      # surjective tail of 3e6 draws, ~5e-4 rejected
+    (70_000, 65_537, 24, True),
+])
+def test_hash_lemire_rejections_vs_oracle(I, L, seed, surj):
+    """Sketch sizes whose Lemire threshold is large, so the tail/bucket draws
+    are really rejected and compacted (numpy's integers(0, L) loop)."""
+    op = ids.CountSketchOp(I, L, seed=seed, surjective=surj)
+    o = oracle.OracleCountSketch(I, L, seed, surj)
+    assert op.draws == tuple(int(v) for v in o.draws), (I, L, seed, surj)
+    assert np.array_equal(op.bucket, o.bucket)
+    assert np.array_equal(op.sign, o.sign)
+
+
 def test_hash_random_shapes_vs_oracle():
     rng = np.random.default_rng(5)
     for _ in range(60):
