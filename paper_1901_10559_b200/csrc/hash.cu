@@ -93,10 +93,48 @@ __device__ __forceinline__ bool lemire_accept(uint32_t x, uint32_t L, uint32_t t
     return (uint32_t)m >= thresh;
 }
 
-// Pass 1 of the Lemire compaction: accepted draws per block.
+// Fast path of phase A: with the usual sketch sizes a Lemire rejection has
+// probability (2^32 mod L) / 2^32 (2e-8 for L = 200), so the first n_acc
+// draws are normally all accepted and land at their own index.  This pass
+// writes them so (16-byte stores) and raises *rejected if any draw is
+// rejected, in which case the two compaction passes below redo phase A.
+__global__ void __launch_bounds__(kGenThreads) lemire_fast_kernel(Seed sd, int64_t n_acc, uint32_t L,
+                                                                  uint32_t thresh, int32_t* out,
+                                                                  int64_t* consumed,
+                                                                  int32_t* rejected) {
+    const int64_t d0 = ((int64_t)blockIdx.x * kGenThreads + threadIdx.x) * kChunk;
+    if (d0 >= n_acc) return;
+    DrawStream ds;
+    ds.init(sd.state(), sd.inc(), (uint64_t)d0);
+    const int cnt = (int)tmin<int64_t>(kChunk, n_acc - d0);
+    bool rej = false;
+    if (cnt == kChunk && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        int4* o = reinterpret_cast<int4*>(out + d0);
+#pragma unroll
+        for (int q = 0; q < kChunk / 4; ++q) {
+            uint32_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rej |= !lemire_accept(ds.next(), L, thresh, &v[u]);
+            o[q] = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+        }
+    } else {
+        for (int t = 0; t < cnt; ++t) {
+            uint32_t v;
+            rej |= !lemire_accept(ds.next(), L, thresh, &v);
+            out[d0 + t] = (int32_t)v;
+        }
+    }
+    if (rej) atomicExch(rejected, 1);
+    if (d0 + cnt == n_acc) *consumed = n_acc;
+}
+
+// Pass 1 of the Lemire compaction: accepted draws per block (only when the
+// fast path saw a rejection).
 __global__ void __launch_bounds__(kGenThreads) lemire_count_kernel(Seed sd, int64_t n_cand,
                                                                    uint32_t L, uint32_t thresh,
-                                                                   int64_t* blk_cnt) {
+                                                                   int64_t* blk_cnt,
+                                                                   const int32_t* rejected) {
+    if (*rejected == 0) return;
     typedef cub::BlockReduce<int, kGenThreads> BR;
     __shared__ typename BR::TempStorage tmp;
     const int64_t d0 = ((int64_t)blockIdx.x * kGenThreads + threadIdx.x) * kChunk;
@@ -122,7 +160,8 @@ __device__ __forceinline__ int pad32(int x) { return x + (x >> 5); }
 
 __global__ void __launch_bounds__(kGenThreads) lemire_write_kernel(
     Seed sd, int64_t n_cand, uint32_t L, uint32_t thresh, const int64_t* blk_off,
-    int64_t n_acc, int32_t* out, int64_t* consumed) {
+    int64_t n_acc, int32_t* out, int64_t* consumed, const int32_t* rejected) {
+    if (*rejected == 0) return;
     typedef cub::BlockScan<int, kGenThreads> BS;
     __shared__ typename BS::TempStorage tmp;
     __shared__ int32_t stage[kGenThreads * kChunk + kGenThreads * kChunk / 32];
@@ -862,7 +901,7 @@ void carve(W& ws, const HashPlan& p, int64_t** blk_cnt, int64_t** blk_off, int64
            int64_t** starts) {
     *blk_cnt = ws.template take<int64_t>(p.nblk);
     *blk_off = ws.template take<int64_t>(p.nblk);
-    *scal = ws.template take<int64_t>(4);
+    *scal = ws.template take<int64_t>(6);  // [4], [5]: phase-A rejection flag (int32)
     *scan_tmp = ws.template take<char>(p.scan_bytes > p.scan2_bytes ? p.scan_bytes
                                                                       : p.scan2_bytes);
     if (p.surj) {
@@ -948,14 +987,20 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
             fill_i32_kernel<<<1024, 256, 0, st>>>(phaseA_out, p.n_acc, 0);
             IDS_LAUNCH_CHECK();
         } else {
+            int32_t* rejected = reinterpret_cast<int32_t*>(scal + 4);
+            IDS_CUDA_TRY(cudaMemsetAsync(rejected, 0, sizeof(int32_t), st));
+            const unsigned gf = (unsigned)ceil_div(p.n_acc, (int64_t)kGenThreads * kChunk);
+            lemire_fast_kernel<<<gf, kGenThreads, 0, st>>>(sd, p.n_acc, L, thresh, phaseA_out,
+                                                          d + 0, rejected);
+            IDS_LAUNCH_CHECK();
             lemire_count_kernel<<<(unsigned)p.nblk, kGenThreads, 0, st>>>(sd, p.n_cand, L,
-                                                                         thresh, blk_cnt);
+                                                                         thresh, blk_cnt, rejected);
             IDS_LAUNCH_CHECK();
             size_t sb = p.scan_bytes;
             IDS_CUDA_TRY(cub::DeviceScan::ExclusiveSum(scan_tmp, sb, blk_cnt, blk_off,
                                                        (int)p.nblk, st));
             lemire_write_kernel<<<(unsigned)p.nblk, kGenThreads, 0, st>>>(
-                sd, p.n_cand, L, thresh, blk_off, p.n_acc, phaseA_out, d + 0);
+                sd, p.n_cand, L, thresh, blk_off, p.n_acc, phaseA_out, d + 0, rejected);
             IDS_LAUNCH_CHECK();
         }
     }
