@@ -1,23 +1,38 @@
-"""Benchmark of the CountSketch matrix-ID hot path on B200.
+"""Benchmark of the CountSketch / TensorSketch ID hot path on B200.
 
-Workload (BASELINE.json configs[1], the largest single-GPU config): dense
-fp64 A of 1,000,000 x 2,000 with a rank-20 part and geometric tail
-0.9^(i-20) plus N(0, 1e-8) noise; K = 20, CountSketch rows L = 100,
-surjective hash.  One step = one countsketch_id of A: device hash draw
-(bit-exact numpy PCG64), bucket index, sketch, all-reduce (N > 1), k-step
-pivoted QR, triangular solve, and the j / P device->host copy.
+    python bench.py [--gpus N --steps K --warmup W] [--workload C2|C3|C4|C5]
+                    [--impl b200|reference]
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Workloads are BASELINE.json's configs, built on the device by
+``paper_1901_10559_b200.generators`` (seeded synthetic inputs of the stated
+shapes and value distributions -- the paper's SuiteSparse / FROSTT data is
+not available offline):
 
-Under torchrun (N > 1) the rows are split into N contiguous blocks (strong
-scaling: total work fixed) and the L x R sketch is summed with one NCCL
-all-reduce.  A (16 GB) is larger than L2 (126 MB), so no flush is needed.
+* C2 (default, the headline): dense fp64 1,000,000 x 2,000, K = 20, L = 100,
+  surjective CountSketch; rows sharded over the ranks, one all-reduce of the
+  L x R sketch per trial.
+* C3: CSR 1e7 x 1e4, ~1e8 nonzeros, planted latent rank-20 structure,
+  K = 20, L = 200; rows sharded.
+* C4 / C5: CP tensors (N = 3, I = 1e3, R = 1e3, L = 4096 / N = 4, I = 1e4,
+  R = 2e3, L = 16384) with near-duplicate terms; terms sharded, the ID by
+  the column-distributed truncated CPQR.
+
+One step = one full ID trial (hash draw, sketch, collective, pivoted QR,
+coefficients, j / P to the host) on device-resident input; `value` = the
+workload's algorithmic bytes (A, or the factor matrices, read once) per
+step time, whole job.  Total work is fixed as N grows ("strong").  The
+headline line also carries the other configs (`secondary_configs`), each
+with its own roofline, CPU baseline, parity and end-to-end numbers at N = 1.
+
+With --gpus N > 1 outside torchrun the script re-launches itself under
+``torch.distributed.run`` (one process per GPU, NCCL).
 """
 
 import argparse
 import datetime
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -26,13 +41,11 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
-WORKLOADS = {
-    # name: rows, cols, k, L, low rank, tail ratio, noise std
-    "C2": dict(rows=1_000_000, cols=2_000, k=20, L=100, lowrank=20, ratio=0.9, noise=1e-4),
-    "C1": dict(rows=10_000, cols=1_000, k=10, L=40, lowrank=10, ratio=10 ** -0.1, noise=0.0),
-}
-METRIC = "sketch HBM GB/s (fraction of B200 peak); matrix ID seconds"
+METRIC = "sketch HBM GB/s (fraction of B200 peak); matrix/tensor ID seconds at 1/2/4/8 GPU"
+CPU_SAMPLE_ROWS = 200_000  # C2's CPU legs run on this many leading rows of A
+FP64_PEAK_DATASHEET = 37.0  # TFLOP/s, B200 fp64 (non-tensor) datasheet figure
 
 
 def parse():
@@ -41,70 +54,184 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
-    p.add_argument("--rows", type=int, default=0, help="override rows (debug only)")
+    p.add_argument("--workload", default="C2", choices=["C2", "C3", "C4", "C5"])
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-rows", type=int, default=200_000)
-    p.add_argument("--no-secondary", action="store_true",
-                   help="skip the live timings of configs C3-C5")
+    p.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines / parity")
+    p.add_argument("--no-secondary", action="store_true", help="headline workload only")
+    p.add_argument("--cpu-rows", type=int, default=CPU_SAMPLE_ROWS)
     return p.parse_args()
 
 
-def peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+def maybe_spawn(args):
+    """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def cores():
     try:
-        with open(path) as fh:
-            m = json.load(fh)
-        return float(m["hbm_gbs"]), "measured"
+        return len(os.sched_getaffinity(0))
     except Exception:
-        return 6650.0, "fallback"
+        return os.cpu_count() or 1
 
 
-def sigma_of(w):
-    i = np.arange(1, w["cols"] + 1, dtype=np.float64)
-    return np.where(i <= w["lowrank"], 1.0, w["ratio"] ** (i - w["lowrank"]))
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-# ----------------------------------------------------------------- inputs --
-CHUNK = 125_000  # global rows per generator chunk (so A is identical for any N | 8)
+def relerr(got, want):
+    got, want = np.asarray(got, dtype=np.float64), np.asarray(want, dtype=np.float64)
+    den = np.linalg.norm(want)
+    return float(np.linalg.norm(got - want) / (den if den > 0 else 1.0))
 
 
-def make_rows_device(w, r0, r1, torch, dev):
-    """Rows [r0, r1) of A = U diag(sigma) V^T + noise, generated on the GPU.
+# ------------------------------------------------------- CPU reference -----
+class RefCPU:
+    """The reference's own CPU implementation of the path: the unmodified
+    ``idsketch`` package installed in baseline/_ref when present (kind
+    "reference"), else the oracle port (numpy/scipy/LAPACK restatement,
+    kind "port").  Each call runs the steps of countsketch_id /
+    tensorsketch_id (matrix_id.py:162-182, cp_tensor.py:266-276) and also
+    returns the sketch for the parity check."""
 
-    U's rows are N(0, 1/rows) (columns orthonormal up to O(1/sqrt(rows))),
-    V is the Q factor of a seeded 2000 x 2000 Gaussian, both seeded per fixed
-    global chunk so every rank builds the same global matrix."""
-    cols = w["cols"]
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234)
-    v = torch.linalg.qr(torch.randn(cols, cols, generator=g, device=dev, dtype=torch.float64))[0]
-    vs = (v * torch.from_numpy(sigma_of(w)).to(dev)).t().contiguous()  # diag(s) V^T
-    out = torch.empty((r1 - r0, cols), dtype=torch.float64, device=dev)
-    c = (r0 // CHUNK) * CHUNK
-    while c < r1:
-        c1 = min(c + CHUNK, w["rows"])
-        g.manual_seed(10_000 + c // CHUNK)
-        u = torch.randn(c1 - c, cols, generator=g, device=dev, dtype=torch.float64)
-        u /= float(np.sqrt(w["rows"]))
-        blk = u @ vs
-        if w["noise"] > 0:
-            blk += w["noise"] * torch.randn(c1 - c, cols, generator=g, device=dev,
-                                            dtype=torch.float64)
-        a, b = max(c, r0), min(c1, r1)
-        out[a - r0:b - r0] = blk[a - c:b - c]
-        del u, blk
-        c = c1
+    def __init__(self):
+        self.kind = "port"
+        try:
+            if os.path.isdir(os.path.join(REF_DIR, "idsketch")):
+                sys.path.insert(0, REF_DIR)
+                import idsketch  # noqa: F401
+
+                self.ref = idsketch
+                self.kind = "reference"
+        except Exception:
+            self.kind = "port"
+        if self.kind == "port":
+            import oracle
+
+            self.ref = oracle
+
+    def matrix(self, a, k, L, seed):
+        import scipy.sparse as sp
+
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            from idsketch.linalg import as_csc, as_dense
+            from idsketch.matrix_id import matrix_id, matrix_sketch
+
+            a2 = as_csc(a) if sp.issparse(a) else as_dense(a)
+            y = matrix_sketch(a2, "countsketch", L, seed=seed, surjective=True)
+            d = matrix_id(y, k)
+        else:
+            d = self.ref.countsketch_id(a, k, L, seed=seed)
+            y = d.sketch
+        dt = time.perf_counter() - t0
+        return {"s": dt, "cols": np.asarray(d.cols), "coeffs": np.asarray(d.coeffs), "y": y}
+
+    def tensor(self, weights, factors, k, L, seed):
+        if self.kind == "reference":
+            x = self.ref.CpTensor(weights, factors)
+            t0 = time.perf_counter()
+            op = self.ref.TensorSketchOp(x.mode_dims, L, seed=seed)
+            y = op.apply(x.factors, x.weights)
+            from idsketch.cp_tensor import tensor_id_from_sketch
+
+            res = tensor_id_from_sketch(x, y, k, "tensorsketch")
+            dt = time.perf_counter() - t0
+            return {"s": dt, "cols": res.cols, "coeffs": res.coeffs, "y": y,
+                    "new_weights": res.new_weights}
+        t0 = time.perf_counter()
+        d, nw = self.ref.tensorsketch_id(weights, factors, k, L, seed=seed)
+        dt = time.perf_counter() - t0
+        return {"s": dt, "cols": d.cols, "coeffs": d.coeffs, "y": d.sketch, "new_weights": nw}
+
+
+def host_sample_c2(rows, cols=2000, seed=7):
+    """Host-only stand-in for a row block of C2 (the reference arm must not
+    touch the product): rows of U are N(0, 1/1e6) (a 1e6-row orthonormal U's
+    rows up to O(1e-3)), the same sigma and noise as generators.dense_config."""
+    rng = np.random.default_rng(seed)
+    i = np.arange(1, cols + 1, dtype=np.float64)
+    sig = np.where(i <= 20, 1.0, 0.9 ** (i - 20))
+    v = np.linalg.qr(rng.standard_normal((cols, cols)))[0]
+    a = (rng.standard_normal((rows, cols)) / 1e3 * sig) @ v.T
+    a += 1e-4 * rng.standard_normal(a.shape)
+    return np.asfortranarray(a)
+
+
+def config_of(name, world, cpu_rows=CPU_SAMPLE_ROWS):
+    from_cfg = {
+        "C2": dict(shape="dense fp64 1000000x2000", k=20, L=100, parallelism=f"rows{world}",
+                   cpu_sample=f"{cpu_rows} leading rows (F order)"),
+        "C3": dict(shape="CSR fp64 10000000x10000, ~1e8 nnz, planted latent rank 20", k=20,
+                   L=200, parallelism=f"rows{world}", cpu_sample="full matrix"),
+        "C4": dict(shape="CP N=3 I_n=1000 R=1000 near-duplicate terms", k=10, L=4096,
+                   parallelism=f"terms{world}", cpu_sample="full tensor"),
+        "C5": dict(shape="CP N=4 I_n=10000 R=2000 near-duplicate terms", k=20, L=16384,
+                   parallelism=f"terms{world}", cpu_sample="full tensor"),
+    }[name]
+    kind = "countsketch_id surjective" if name in ("C2", "C3") else "tensorsketch_id"
+    out = {"workload": f"{name}: {from_cfg['shape']} {kind} K={from_cfg['k']} L={from_cfg['L']}"}
+    out.update(from_cfg)
+    out["l2"] = ("inputs larger than the 126 MB L2, no flush" if name != "C4" else
+                 "C4 factors (24 MB) fit in L2: steps run back to back, no flush "
+                 "(the reference config is that small)")
     return out
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation on this box's host
+    cores, rank 0 only, each step a bounded sample of the workload."""
+    if rank != 0:
+        return
+    ref = RefCPU()
+    name = args.workload
+    if name == "C2":
+        a = host_sample_c2(min(args.cpu_rows, 1_000_000))
+        nbytes = a.nbytes
+        run = lambda s: ref.matrix(a, 20, 100, s)  # noqa: E731
+        sample = f"{a.shape[0]} x {a.shape[1]} row sample of C2 ({nbytes / 1e9:.2f} GB), F order"
+    else:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"reference arm is timed on the headline workload C2 only (got {name})"}))
+        return
+    secs = []
+    for step in range(args.warmup + args.steps):
+        r = run(step)
+        if step >= args.warmup:
+            secs.append(r["s"])
+    sec = float(np.median(secs))
+    gbs = nbytes / sec / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(name, world, args.cpu_rows),
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores(), "kind": ref.kind,
+                         "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------- clocks --
 class Clocks:
+    """nvidia-smi sampler (100 ms) around the timed region."""
+
     def __init__(self, enabled):
         self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
-        self.t0 = time.time()
         if not enabled:
             return
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
@@ -120,8 +247,6 @@ class Clocks:
             self.proc = None
 
     def stop(self, gpu_index, window=None):
-        """Median SM clock, max clock and throttle reasons of the samples taken
-        inside `window` (wall-clock seconds, time.time()) when given."""
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -157,165 +282,391 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ----------------------------------------------------------------- CPU -----
-def cpu_sample_matrix(w, rows):
-    """A row sample of the workload built the same way (host numpy)."""
-    rng = np.random.default_rng(7)
-    cols = w["cols"]
-    v = np.linalg.qr(rng.standard_normal((cols, cols)))[0]
-    u = rng.standard_normal((rows, cols)) / np.sqrt(w["rows"])
-    a = (u * sigma_of(w)) @ v.T
-    if w["noise"] > 0:
-        a += w["noise"] * rng.standard_normal(a.shape)
-    # F order, as BASELINE.md section 2 prescribes for the reference (no extra copy
-    # in as_dense, linalg.py:29)
-    return np.asfortranarray(a)
-
-
-def cpu_sample_gbs(w, rows, seed=0, a=None):
-    """The oracle port (reference algorithm on numpy/scipy/LAPACK) on a
-    bounded row sample of the workload; returns (GB/s, seconds, rows)."""
-    import oracle
-
-    if a is None:
-        a = cpu_sample_matrix(w, rows)
-    t0 = time.perf_counter()
-    oracle.countsketch_id(a, w["k"], w["L"], seed=seed)
-    dt = time.perf_counter() - t0
-    return a.nbytes / dt / 1e9, dt, a.shape[0]
-
-
-def cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
-
-
-def run_reference(args, w, rank, world):
-    if rank != 0:
-        return
-    rows = min(args.cpu_rows, w["rows"])
-    a = cpu_sample_matrix(w, rows)
-    vals = []
-    for step in range(args.warmup + args.steps):
-        gbs, dt, _ = cpu_sample_gbs(w, rows, seed=step, a=a)
-        if step >= args.warmup:
-            vals.append((gbs, dt))
-    gb = float(np.median([v[0] for v in vals]))
-    sec = float(np.median([v[1] for v in vals]))
-    sample = (f"{rows} x {w['cols']} row sample of {args.workload} "
-              f"({rows * w['cols'] * 8 / 1e9:.2f} GB), full countsketch_id")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": gb, "unit": "GB/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_of(args, w, world),
-        "cpu_baseline": {"value": gb, "unit": "GB/s", "cores": cores(), "kind": "port",
-                         "sample": sample},
-        "e2e": {"value": gb, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def config_of(args, w, world):
-    rows = args.rows or w["rows"]
-    return {"workload": f"{args.workload}: dense fp64 {rows}x{w['cols']} countsketch_id "
-                        f"K={w['k']} L={w['L']} surjective",
-            "rows": rows, "cols": w["cols"], "rank": w["k"], "sketch_dim": w["L"],
-            "parallelism": f"rows{world}", "l2": "A (>126 MB) larger than L2, no flush"}
-
-
-def secondary_configs(torch, dev, steps=6):
-    """Live device timings (CUDA events, after warm-up) of one full ID at the
-    other BASELINE.json configs, on seeded synthetic inputs of their shapes
-    built on the device: C3 CSR 1e7 x 1e4 with 1e8 nonzeros,
-    C4 / C5 CP tensors with near-duplicate terms.  Reported beside the
-    headline, not part of it."""
-    import paper_1901_10559_b200 as ids
-    from paper_1901_10559_b200._inputs import SparseOperand
-    from paper_1901_10559_b200.matrix_id import countsketch_device, device_matrix_id
-
-    def timed(fn):
-        for s in range(2):
-            fn(10_000 + s)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for s in range(steps):
-            fn(20_000 + s)
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / steps
-
-    out = {}
-    g = torch.Generator(device=dev).manual_seed(3)
-    I, R, per, K, L = 10_000_000, 10_000, 10, 20, 200
-    indptr = torch.arange(0, I + 1, dtype=torch.int64, device=dev) * per
-    idx = torch.randint(0, R, (I, per), generator=g, device=dev).sort(dim=1).values
-    idx = idx.to(torch.int32).reshape(-1)
-    data = torch.randn(I * per, generator=g, device=dev, dtype=torch.float64)
-    csr = SparseOperand("csr", indptr, idx, data, I, R, I * per)
-    ms = timed(lambda s: countsketch_device(csr, K, L, seed=s)[0].to_host("countsketch"))
-    nbytes = int(I * per * 12 + (I + 1) * 8)
-    # the sketch kernel alone (hash drawn once, outside the clock)
-    op = ids.CountSketchOp(I, L, seed=1, surjective=True)
-    y = torch.empty((R, L), dtype=torch.float64, device=dev)
-    sk_ms = timed(lambda s: op.sketch_into(csr, y, flags=0))
-    out["C3"] = {"id_ms": ms, "shape": "CSR 1e7 x 1e4, nnz 1e8 (10 per row), K=20, L=200",
-                 "algorithmic_bytes": nbytes,
-                 "sketch": {"kernel": "cs_csr_stream_kernel", "ms": sk_ms,
-                            "achieved_gbs": nbytes / sk_ms / 1e6,
-                            "bound": "L2 fp64 reductions (one per nonzero)"}}
-    del op, y
-    del indptr, idx, data, csr
-    for name, N, In, R, base, pert, K, L in (("C4", 3, 1000, 1000, 10, 1e-3, 10, 4096),
-                                             ("C5", 4, 10_000, 2000, 20, 1e-4, 20, 16384)):
-        g = torch.Generator(device=dev).manual_seed(4 if name == "C4" else 5)
-        bases = torch.randint(0, base, (R,), generator=g, device=dev)
-        bases[:base] = torch.arange(base, device=dev)
-        facs = []
-        for _ in range(N):
-            f = torch.randn(In, R, generator=g, device=dev, dtype=torch.float64)
-            f[:, :base] /= torch.linalg.vector_norm(f[:, :base], dim=0)
-            f = f[:, bases] + pert * torch.randn(In, R, generator=g, device=dev,
-                                                 dtype=torch.float64)
-            f /= torch.linalg.vector_norm(f, dim=0)
-            facs.append(f.t().contiguous().t())  # column-major I_n x R
-        w = torch.rand(R, generator=g, device=dev, dtype=torch.float64) * 0.5 + 0.5
-
-        def step(s, facs=facs, w=w, N=N, In=In, R=R, K=K, L=L):
-            y = ids.TensorSketchOp([In] * N, L, seed=s).apply_device(facs, w)
-            return device_matrix_id(y, L, R, K).to_host("tensorsketch")
-
-        out[name] = {"id_ms": timed(step),
-                     "shape": f"CP N={N}, I_n={In}, R={R}, K={K}, L={L}, near-duplicate terms",
-                     "algorithmic_bytes": int(N * In * R * 8)}
-        del facs
-    return out
-
-
-# ----------------------------------------------------------------- GPU -----
 def prime_nvml():
-    """One nvidia-smi call at start-up: the driver/NVML initialization it can
-    trigger lands long before anything is timed."""
     try:
         subprocess.run(["nvidia-smi", "-q", "-d", "CLOCK"], capture_output=True, timeout=120)
     except Exception:
         pass
 
 
+# -------------------------------------------------------------- workloads --
+class Ctx:
+    """Per-process device / collective context."""
+
+    def __init__(self, torch, dist, dev, rank, world):
+        self.torch, self.dist, self.dev, self.rank, self.world = torch, dist, dev, rank, world
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max_over_ranks(self, v):
+        if self.world == 1:
+            return float(v)
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(self, v):
+        if self.world == 1:
+            return float(v)
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def events(self, fn, reps):
+        """Average device time (ms) of fn() over reps calls, CUDA events on the
+        current stream, synchronized on both sides."""
+        torch = self.torch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for i in range(reps):
+            fn(i)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+
+class MatrixWorkload:
+    """C2 (dense) / C3 (CSR): rows [r0, r1) of A on this rank."""
+
+    def __init__(self, ctx, name):
+        from paper_1901_10559_b200 import generators as G
+        from paper_1901_10559_b200._inputs import dense_operand
+        from paper_1901_10559_b200.distributed import row_block
+
+        self.ctx, self.name = ctx, name
+        cfg = G.CONFIGS[name]
+        self.rows, self.cols, self.k, self.L = cfg["rows"], cfg["cols"], cfg["k"], cfg["L"]
+        self.r0, self.r1 = row_block(self.rows, ctx.world, ctx.rank)
+        if cfg["kind"] == "dense":
+            self.operand = dense_operand(G.dense_config(name, row_range=(self.r0, self.r1)))
+            self.bytes_local = (self.r1 - self.r0) * self.cols * 8
+            self.kernel_name = "cs_rowmajor_kernel"
+        else:
+            self.operand = G.csr_config(name, row_range=(self.r0, self.r1))
+            ptr_b = self.operand.indptr.element_size()
+            self.bytes_local = self.operand.nnz * 12 + (self.r1 - self.r0 + 1) * ptr_b
+            self.kernel_name = "cs_csr_stream_kernel"
+        ctx.torch.cuda.synchronize()
+        self.bytes_total = int(ctx.sum_over_ranks(self.bytes_local))
+
+    def bytes_note(self):
+        if self.name == "C2":
+            return "8 B per element of A (1e6 x 2000 fp64)"
+        return "12 B per nonzero (fp64 value + int32 column) + 4 B per row pointer"
+
+    def trials(self, seeds):
+        from paper_1901_10559_b200.distributed import countsketch_id_sharded_trials
+
+        return countsketch_id_sharded_trials(self.operand, self.r0, self.rows, self.k, self.L,
+                                             seeds=list(seeds))
+
+    def single(self, seed):
+        from paper_1901_10559_b200.distributed import countsketch_id_sharded
+
+        return countsketch_id_sharded(self.operand, self.r0, self.rows, self.k, self.L,
+                                      seed=seed)
+
+    def kernel(self, reps):
+        """The sketch kernel alone: (ms per launch, bytes per launch, extra)."""
+        import paper_1901_10559_b200 as ids
+
+        torch = self.ctx.torch
+        op = ids.CountSketchOp(self.rows, self.L, seed=5, surjective=True)
+        op.bucket_index()
+        y = torch.empty((self.cols, self.L), dtype=torch.float64, device=self.ctx.dev)
+        flags = 1 if self.name == "C2" else 0
+        for _ in range(2):
+            op.sketch_into(self.operand, y, row0=self.r0, flags=flags)
+        ms = self.ctx.events(lambda i: op.sketch_into(self.operand, y, row0=self.r0,
+                                                      flags=flags), reps)
+        from paper_1901_10559_b200.matrix_id import device_matrix_id
+
+        id_ms = self.ctx.events(lambda i: device_matrix_id(y, self.L, self.cols, self.k), reps)
+        hash_ms = self.ctx.events(lambda i: ids.CountSketchOp(
+            self.rows, self.L, seed=100 + i, surjective=True).bucket_index(), reps)
+        return ms, self.bytes_local, {"cpqr_and_coeffs": id_ms, "hash_and_index": hash_ms}
+
+    def host_copy(self):
+        """This rank's block in host memory (pinned for dense)."""
+        torch = self.ctx.torch
+        if self.operand.kind == "dense":
+            h = torch.empty((self.r1 - self.r0, self.cols), dtype=torch.float64, pin_memory=True)
+            h.copy_(self.operand.t)
+            return h, int(h.numel() * 8)
+        from paper_1901_10559_b200.generators import operand_to_scipy
+
+        m = operand_to_scipy(self.operand)
+        return m, int(m.data.nbytes + m.indices.nbytes + m.indptr.nbytes)
+
+    def e2e_call(self, host, seed):
+        import paper_1901_10559_b200 as ids
+        from paper_1901_10559_b200.distributed import countsketch_id_sharded
+
+        if self.ctx.world == 1:  # the call a user makes
+            return ids.countsketch_id(host, self.k, self.L, seed=seed)
+        return countsketch_id_sharded(host, self.r0, self.rows, self.k, self.L, seed=seed)
+
+    def cpu_and_parity(self, ref, cpu_rows, seed=11):
+        """The reference on the host (C2: leading rows, C3: the full matrix)
+        and the product on the same input and seed."""
+        import paper_1901_10559_b200 as ids
+
+        if self.name == "C2":
+            rows = min(cpu_rows, self.rows)
+            a = np.asfortranarray(self.operand.t[:rows].cpu().numpy())
+            sample = f"{rows} x {self.cols} leading rows of C2 ({a.nbytes / 1e9:.2f} GB), F order"
+            nbytes = a.nbytes
+        else:
+            from paper_1901_10559_b200.generators import operand_to_scipy
+
+            a = operand_to_scipy(self.operand)
+            rows = self.rows
+            sample = f"full C3 matrix ({a.nnz} nonzeros)"
+            nbytes = self.bytes_local
+        r = ref.matrix(a, self.k, self.L, seed)
+        d = ids.countsketch_id(a, self.k, self.L, seed=seed)
+        y = ids.CountSketchOp(rows, self.L, seed=seed, surjective=True).apply(a)
+        cpu = {"value": nbytes / r["s"] / 1e9, "unit": "GB/s", "cores": cores(),
+               "kind": ref.kind, "seconds": r["s"],
+               "sample": sample + ", full countsketch_id (as_dense/as_csc, S@A, dgeqp3, dtrtrs)"}
+        parity = {"input": sample, "seed": seed,
+                  "cols_equal": bool(np.array_equal(d.cols, r["cols"])),
+                  "P_relerr": relerr(d.coeffs, r["coeffs"]),
+                  "Y_relerr": relerr(y, r["y"]),
+                  "Y_bit_exact": bool(np.array_equal(y, r["y"])),
+                  "against": ref.kind}
+        return cpu, parity
+
+
+class TensorWorkload:
+    """C4 / C5: terms [c0, c1) of the CP tensor on this rank."""
+
+    def __init__(self, ctx, name):
+        from paper_1901_10559_b200 import generators as G
+        from paper_1901_10559_b200.distributed import row_block
+
+        self.ctx, self.name = ctx, name
+        cfg = G.CONFIGS[name]
+        self.N, self.I, self.R, self.k, self.L = (cfg["modes"], cfg["dim"], cfg["terms"],
+                                                  cfg["k"], cfg["L"])
+        self.c0, self.c1 = row_block(self.R, ctx.world, ctx.rank)
+        w, facs = G.cp_config(name)
+        self.w_all = w.cpu().numpy()
+        self.w_local = w[self.c0:self.c1].contiguous()
+        self.f_local = [f[:, self.c0:self.c1] for f in facs]  # column-major views
+        self.full = (w, facs) if ctx.world == 1 else None
+        self.bytes_local = self.N * self.I * (self.c1 - self.c0) * 8
+        self.bytes_total = self.N * self.I * self.R * 8
+        self.flops_local = (self.N + 1) * (self.c1 - self.c0) * 2.5 * self.L * np.log2(self.L)
+        self.kernel_name = "tensorsketch_kernel"
+
+        class _X:
+            factors = self.f_local
+            weights = self.w_local
+            mode_dims = tuple([self.I] * self.N)
+
+        self.x_local = _X
+
+    def bytes_note(self):
+        return (f"8 B per factor entry ({self.N} x {self.I} x {self.R} fp64); fp64 FFT work "
+                f"(N+1) x R x 2.5 L log2 L flops")
+
+    def trials(self, seeds):
+        from paper_1901_10559_b200.distributed import tensorsketch_id_sharded
+
+        return [tensorsketch_id_sharded(self.x_local, self.c0, self.R, self.w_all, self.k,
+                                        self.L, seed=s) for s in seeds]
+
+    def single(self, seed):
+        return self.trials([seed])[0]
+
+    def kernel(self, reps):
+        import paper_1901_10559_b200 as ids
+        from paper_1901_10559_b200.matrix_id import device_matrix_id
+
+        op = ids.TensorSketchOp([self.I] * self.N, self.L, seed=5)
+        y = op.apply_device(self.f_local, self.w_local)
+        ms = self.ctx.events(lambda i: op.apply_device(self.f_local, self.w_local), reps)
+        n_loc = self.c1 - self.c0
+        id_ms = self.ctx.events(lambda i: device_matrix_id(y, self.L, n_loc, self.k), reps)
+        return ms, self.bytes_local, {"cpqr_and_coeffs_local_block": id_ms,
+                                      "flops_per_launch": self.flops_local,
+                                      "y_write_bytes": n_loc * self.L * 8}
+
+    def host_copy(self):
+        import paper_1901_10559_b200 as ids
+
+        w = self.w_local.cpu().numpy()
+        facs = [f.cpu().numpy() for f in self.f_local]  # F order (I_n x R)
+        return ids.CpTensor(w, facs), int(sum(f.nbytes for f in facs) + w.nbytes)
+
+    def e2e_call(self, host, seed):
+        import paper_1901_10559_b200 as ids
+        from paper_1901_10559_b200.distributed import tensorsketch_id_sharded
+
+        if self.ctx.world == 1:
+            return ids.tensorsketch_id(host, self.k, self.L, seed=seed)
+        return tensorsketch_id_sharded(host, self.c0, self.R, self.w_all, self.k, self.L,
+                                       seed=seed)
+
+    def cpu_and_parity(self, ref, cpu_rows, seed=11):
+        import paper_1901_10559_b200 as ids
+
+        w, facs = self.full
+        wh = w.cpu().numpy()
+        fh = [f.cpu().numpy() for f in facs]
+        r = ref.tensor(wh, fh, self.k, self.L, seed)
+        x = ids.CpTensor(wh, fh)
+        res = ids.tensorsketch_id(x, self.k, self.L, seed=seed)
+        y = ids.TensorSketchOp(x.mode_dims, self.L, seed=seed).apply(x.factors, x.weights)
+        sample = f"full {self.name} tensor ({self.bytes_total / 1e6:.0f} MB of factors)"
+        cpu = {"value": self.bytes_total / r["s"] / 1e9, "unit": "GB/s", "cores": cores(),
+               "kind": ref.kind, "seconds": r["s"],
+               "sample": sample + ", full tensorsketch_id (CountSketch, pocketfft, dgeqp3)"}
+        parity = {"input": sample, "seed": seed,
+                  "cols_equal": bool(np.array_equal(res.cols, r["cols"])),
+                  "P_relerr": relerr(res.coeffs, r["coeffs"]),
+                  "Y_relerr": relerr(y, r["y"]),
+                  "new_weights_relerr": relerr(res.new_weights, r["new_weights"]),
+                  "against": ref.kind}
+        return cpu, parity
+
+
+def make_workload(ctx, name):
+    return MatrixWorkload(ctx, name) if name in ("C2", "C3") else TensorWorkload(ctx, name)
+
+
+def fp64_peak(ctx):
+    """Measured fp64 FMA throughput (TFLOP/s) of this GPU, from the library's
+    DFMA probe; datasheet figure when the probe is unavailable."""
+    try:
+        from paper_1901_10559_b200 import _native
+
+        lib = _native.load()
+        v = float(lib.ids_probe_fp64_tflops(ctx.torch.cuda.current_stream().cuda_stream))
+        if v > 0:
+            return v, "measured (ids_probe_fp64_tflops: DFMA chains on every SM)"
+    except Exception:
+        pass
+    return FP64_PEAK_DATASHEET, "datasheet"
+
+
+def measure(ctx, wl, steps, warmup, args, headline):
+    """Time one workload: trials (value), single-call latency, the dominant
+    kernel alone (roofline), end to end from host buffers; CPU baseline and
+    parity at N = 1 on rank 0."""
+    torch = ctx.torch
+    from paper_1901_10559_b200 import _native
+
+    lib = _native.load()
+    # single-call latency (one ID, nothing overlapped): the "ID seconds"
+    for s in range(2):
+        wl.single(s)
+    ctx.barrier()
+    t_single = []
+    for s in range(3):
+        t_single.append(ctx.events(lambda i, s=s: wl.single(100 + s), 1))
+    single_ms = ctx.max_over_ranks(float(np.median(t_single)))
+
+    # device-resident trials (value); warm-up sized to one timed batch
+    wl.trials(range(max(warmup, steps)))
+    torch.cuda.synchronize()
+    clocks = busy0 = None
+    if headline:
+        clocks = Clocks(ctx.rank == 0)
+        time.sleep(1.0)
+        busy0 = time.time()
+        while time.time() - busy0 < 1.0:
+            wl.trials(range(steps))
+        torch.cuda.synchronize()
+    ctx.barrier()
+    n0 = lib.ids_launch_count()
+    ms = ctx.events(lambda i: wl.trials([1000 + s for s in range(steps)]), 1) / steps
+    launches = (lib.ids_launch_count() - n0) // max(steps, 1)
+    ms = ctx.max_over_ranks(ms)
+    clk = None
+    if headline:
+        busy1 = time.time()
+        while time.time() - busy1 < 1.0:
+            wl.trials(range(steps))
+        torch.cuda.synchronize()
+        clk = clocks.stop(torch.cuda.current_device(), window=(busy0, time.time()))
+
+    # dominant kernel alone
+    k_ms, k_bytes, extra = wl.kernel(max(3, steps))
+    peak, peak_kind = peaks()
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic_of(wl.name, k_bytes),
+            "kernel": wl.kernel_name, "peak_kind": peak_kind, "bytes_per_launch": k_bytes,
+            "bytes_note": wl.bytes_note(), "kernel_ms": k_ms}
+    if "flops_per_launch" in extra:
+        fpk, fkind = fp64_peak(ctx)
+        tf = extra["flops_per_launch"] / (k_ms * 1e-3) / 1e12
+        roof["fp64"] = {"achieved": tf, "peak": fpk, "unit": "TFLOP/s", "frac": tf / fpk,
+                        "peak_kind": fkind, "flops_per_launch": extra["flops_per_launch"]}
+    if wl.name == "C3":
+        roof["ceiling"] = ("one fp64 L2 reduction per nonzero: measured scattered-RED peak "
+                           "222 G/s (profiles/r01_l2_red_peak.txt) bounds 1e8 nonzeros at "
+                           ">= 0.45 ms")
+
+    # end to end through the public API from host buffers
+    e2e = None
+    if not args.no_e2e:
+        host, h2d = wl.host_copy()
+        d = wl.e2e_call(host, 1)
+        ctx.barrier()
+        reps = max(1, min(steps, 3))
+        t0 = time.perf_counter()
+        e_ms = ctx.max_over_ranks(ctx.events(lambda i: wl.e2e_call(host, 2000 + i), reps) / 1)
+        res = d[0] if isinstance(d, tuple) else d
+        d2h = int(res.coeffs.nbytes + res.cols.nbytes)
+        e2e = {"value": wl.bytes_total / (e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(ctx.sum_over_ranks(h2d)),
+               "d2h_bytes_per_step": d2h * ctx.world, "ms_per_step": e_ms,
+               "wall_s": time.perf_counter() - t0}
+        del host
+
+    cpu = parity = None
+    if ctx.world == 1 and not args.no_cpu:
+        cpu, parity = wl.cpu_and_parity(RefCPU(), args.cpu_rows)
+
+    out = {"value": wl.bytes_total / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+           "id_seconds": single_ms * 1e-3, "phases_ms": dict(
+               {"sketch_kernel": k_ms}, **{k: v for k, v in extra.items() if k.endswith("ms")
+                                           or "cpqr" in k or "hash" in k}),
+           "roofline": roof, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+           "gpu_launches": int(launches), "config": config_of(wl.name, ctx.world, args.cpu_rows)}
+    if clk is not None:
+        out["clocks"] = clk
+    return out
+
+
+def traffic_of(name, nbytes):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    full capture (profiles/traffic.json), scaled to this rank's share."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        v = t.get(name)
+        if v is None:
+            return None
+        full = t.get(name + "_bytes")
+        return float(v) * (nbytes / full if full else 1.0)
+    except Exception:
+        return None
+
+
 def main():
     args = parse()
-    w = dict(WORKLOADS[args.workload])
-    if args.rows:
-        w["rows"] = args.rows
+    maybe_spawn(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        return run_reference(args, w, rank, world)
+        return run_reference(args, rank, world)
 
     if local == 0:
         prime_nvml()
@@ -335,213 +686,40 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
+    ctx = Ctx(torch, dist, dev, rank, world)
 
-    import paper_1901_10559_b200 as ids
     from paper_1901_10559_b200 import _native
-    from paper_1901_10559_b200._inputs import dense_operand
-    from paper_1901_10559_b200.distributed import countsketch_id_sharded, row_block
-    from paper_1901_10559_b200.matrix_id import device_matrix_id
 
-    lib = _native.load()
-    r0, r1 = row_block(w["rows"], world, rank)
-    a_dev = make_rows_device(w, r0, r1, torch, dev)
-    torch.cuda.synchronize()
-    operand = dense_operand(a_dev)
-    bytes_local = a_dev.numel() * 8
-    bytes_total = w["rows"] * w["cols"] * 8
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    from paper_1901_10559_b200.distributed import DeviceBackend
-
-    backend = DeviceBackend()
-
-    def step(seed):
-        return countsketch_id_sharded(operand, r0, w["rows"], w["k"], w["L"], seed=seed,
-                                      backend=backend)
-
-    # ---- single-call latency (no cross-trial overlap): the ID seconds ----
-    for s in range(2):
-        step(s)
-    torch.cuda.synchronize()
-    barrier()
-    t_single = []
-    for s in range(3):
-        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e_a.record()
-        step(100 + s)
-        e_b.record()
-        torch.cuda.synchronize()
-        t_single.append(e_a.elapsed_time(e_b))
-    single_ms = float(np.median(t_single))
-
-    from paper_1901_10559_b200.distributed import countsketch_id_sharded_trials
-
-    # ---- device-resident steps (value): K trials queued back to back ----
-    # warm-up: at least as many trials as one timed batch, so the allocator
-    # already holds every buffer a batch needs (no cudaMalloc while timed)
-    countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
-                                  seeds=list(range(max(args.warmup, args.steps))))
-    torch.cuda.synchronize()
-    # the clock sampler runs under load: started here (its start-up lands in an
-    # idle second), then untimed trials for about a second before and after
-    # the timed batch; only samples from that busy window are reported
-    clocks = Clocks(rank == 0)
-    time.sleep(1.0)
-    busy0 = time.time()
-    while time.time() - busy0 < 1.0:
-        countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
-                                      seeds=list(range(args.steps)))
-    torch.cuda.synchronize()
-    barrier()
-    n0 = lib.ids_launch_count()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    barrier()
-    start.record()
-    ds = countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
-                                       seeds=[1000 + s for s in range(args.steps)])
-    d = ds[-1]
-    stop.record()
-    torch.cuda.synchronize()
-    barrier()
-    launches = (lib.ids_launch_count() - n0) // max(args.steps, 1)
-    ms = start.elapsed_time(stop) / args.steps
-    busy1 = time.time()
-    while time.time() - busy1 < 1.0:
-        countsketch_id_sharded_trials(operand, r0, w["rows"], w["k"], w["L"],
-                                      seeds=list(range(args.steps)))
-    torch.cuda.synchronize()
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    clk = clocks.stop(local, window=(busy0, time.time()))
-
-    # ---- dominant kernel alone: the sketch (roofline) ----
-    op = ids.CountSketchOp(w["rows"], w["L"], seed=5, surjective=True)
-    y = torch.empty((w["cols"], w["L"]), dtype=torch.float64, device=dev)
-    op.bucket_index()
-    for _ in range(2):
-        op.sketch_into(operand, y, row0=r0, flags=1)
-    torch.cuda.synchronize()
-    reps = max(3, args.steps)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        op.sketch_into(operand, y, row0=r0, flags=1)
-    e1.record()
-    torch.cuda.synchronize()
-    sk_ms = e0.elapsed_time(e1) / reps
-    # CPQR + coefficients alone (ID seconds without the sketch)
-    e0.record()
-    for _ in range(reps):
-        device_matrix_id(y, w["L"], w["cols"], w["k"])
-    e1.record()
-    torch.cuda.synchronize()
-    id_ms = e0.elapsed_time(e1) / reps
-    # hash draw alone
-    e0.record()
-    for s in range(reps):
-        ids.CountSketchOp(w["rows"], w["L"], seed=s, surjective=True).bucket_index()
-    e1.record()
-    torch.cuda.synchronize()
-    hash_ms = e0.elapsed_time(e1) / reps
-
-    peak, peak_kind = peaks()
-    achieved = bytes_local / (sk_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.workload)
-        except Exception:
-            traffic = None
-    if traffic is not None and world > 1:
-        # the capture is of the whole-matrix launch (one GPU): scale to this
-        # rank's row block by the measured traffic / algorithmic-bytes ratio
-        traffic = traffic * bytes_local / bytes_total
-
-    # ---- end to end through the public API with host buffers ----
-    e2e = None
-    if not args.no_e2e:
-        try:
-            host = torch.empty((r1 - r0, w["cols"]), dtype=torch.float64, pin_memory=True)
-            host.copy_(a_dev, non_blocking=False)
-            del_dev = True
-        except RuntimeError:
-            host, del_dev = None, False
-        if host is not None:
-            def api(seed):
-                if world == 1:  # the call a user makes
-                    return ids.countsketch_id(host, w["k"], w["L"], seed=seed)
-                return countsketch_id_sharded(host, r0, w["rows"], w["k"], w["L"], seed=seed)
-
-            d = api(1)
-            torch.cuda.synchronize()
-            barrier()
-            t0 = time.perf_counter()
-            e0.record()
-            nsteps = max(1, min(args.steps, 3))
-            for s in range(nsteps):
-                d = api(2000 + s)
-            e1.record()
-            torch.cuda.synchronize()
-            e2e_ms = e0.elapsed_time(e1) / nsteps
-            if world > 1:
-                t = torch.tensor([e2e_ms], device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                e2e_ms = float(t.item())
-            e2e = {"value": bytes_total / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
-                   "h2d_bytes_per_step": bytes_total,
-                   "d2h_bytes_per_step": int(d.coeffs.nbytes + d.cols.nbytes) * world,
-                   "ms_per_step": e2e_ms, "wall_s": time.perf_counter() - t0}
-            del host
-            _ = del_dev
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        gbs, dt, rows = cpu_sample_gbs(w, min(args.cpu_rows, w["rows"]))
-        cpu = {"value": gbs, "unit": "GB/s", "cores": cores(), "kind": "port",
-               "sample": f"{rows} x {w['cols']} row sample of {args.workload}, full "
-                         f"countsketch_id in {dt:.2f} s (scipy S@A single-threaded, "
-                         f"LAPACK dgeqp3 multithreaded)"}
+    _native.load()
+    wl = make_workload(ctx, args.workload)
+    head = measure(ctx, wl, args.steps, args.warmup, args, headline=True)
+    del wl
+    torch.cuda.empty_cache()
 
     secondary = None
-    if rank == 0 and world == 1 and not args.no_secondary:
-        del a_dev, operand
-        torch.cuda.empty_cache()
-        secondary = secondary_configs(torch, dev)
+    if not args.no_secondary:
+        secondary = {}
+        for name in ("C2", "C3", "C4", "C5"):
+            if name == args.workload:
+                continue
+            w2 = make_workload(ctx, name)
+            secondary[name] = measure(ctx, w2, 6, 3, args, headline=False)
+            del w2
+            torch.cuda.empty_cache()
 
     if rank == 0:
         line = {
-            "metric": METRIC,
-            "value": bytes_total / (ms * 1e-3) / 1e9,
-            "unit": "GB/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_of(args, w, world),
-            "id_seconds": single_ms * 1e-3,
-            "trials": ("K trials (seeds) of the same A queued back to back, one host sync at "
-                       "the end; each trial's hash is drawn on the device on a side stream "
-                       "beside the earlier trials' sketches (sketch.pipelined_operators)"
-                       if world == 1 else
-                       "K trials (seeds) of the same row-sharded A queued back to back, one "
-                       "host sync at the end; trial t's hash is drawn by rank t mod N and "
-                       "broadcast (distributed.trial_sharded_operators), each rank sketches "
-                       "its rows, one all-reduce of the sketch per trial"),
-            "phases_ms": {"hash_and_index": hash_ms, "sketch": sk_ms, "cpqr_and_coeffs": id_ms},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "cs_rowmajor_kernel", "peak_kind": peak_kind,
-                         "bytes_per_launch": bytes_local},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "clocks": clk,
+            "metric": METRIC, "value": head["value"], "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, paper_1901_10559_b200.generators)",
+            "config": head["config"], "id_seconds": head["id_seconds"],
+            "trials": ("K trials (seeds) of the same input queued back to back, one host sync "
+                       "at the end (matrices); hash draws pipelined on side streams (N = 1) or "
+                       "split over the ranks and broadcast (N > 1)"),
+            "phases_ms": head["phases_ms"], "roofline": head["roofline"],
+            "cpu_baseline": head["cpu_baseline"], "parity": head["parity"], "e2e": head["e2e"],
+            "gpu_launches": head["gpu_launches"], "clocks": head.get("clocks"),
             "secondary_configs": secondary,
         }
         print(json.dumps(line), flush=True)

@@ -52,6 +52,11 @@ const char* ids_last_error(void);
 int ids_version(void);
 /* Diagnostic: number of kernels this library has launched so far (process-wide). */
 int64_t ids_launch_count(void);
+/* Diagnostic: sustained fp64 FMA throughput of the current device in TFLOP/s
+ * (DFMA chains on every SM, timed with CUDA events; synchronizes `stream`).
+ * The fp64 roof bench.py reports for the TensorSketch FFT work; not on the
+ * sketch / ID path.  Returns a negative value on failure. */
+double ids_probe_fp64_tflops(void* stream);
 
 /* ---------------------------------------------------------------------------
  * Hash generation.  Replaces sketch.py:77-84 (CountSketchOp.__init__):

@@ -27,6 +27,7 @@ SIGNATURES = {
     "ids_last_error": (ctypes.c_char_p, []),
     "ids_version": (_c_int, []),
     "ids_launch_count": (_c_i64, []),
+    "ids_probe_fp64_tflops": (_c_dbl, [_c_p]),
     "ids_hash_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_int]),
     "ids_countsketch_hash": (
         _c_int,

@@ -104,6 +104,31 @@ def _world(group):
     return dist.get_world_size(group), dist.get_rank(group)
 
 
+def _global_rank(group, r):
+    """Global rank of group-local rank r (dist.broadcast's src is global)."""
+    return dist.get_global_rank(group, r) if group is not None else r
+
+
+def _coll_device(group):
+    """Device for collective buffers: CUDA under NCCL, host under gloo."""
+    backend = dist.get_backend(group)
+    if "nccl" in str(backend).lower() and torch.cuda.is_available():
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def _agreed_entropy(group):
+    """Fresh OS entropy (seed=None, sketch.py:77) agreed on by every rank:
+    group-local rank 0 draws, everyone receives it."""
+    ent = np.random.SeedSequence().entropy % (2**63)
+    world, _ = _world(group)
+    if world == 1:
+        return int(ent)
+    t = torch.tensor([ent], dtype=torch.int64, device=_coll_device(group))
+    dist.broadcast(t, src=_global_rank(group, 0), group=group)
+    return int(t.item())
+
+
 def countsketch_id_sharded(a_local, row0, in_dim, rank, sketch_dim=None, seed=None,
                            rank_tol=1e-12, surjective=True, group=None, backend=None):
     """countsketch_id of the global matrix whose rows [row0, row0 + rows) are
@@ -120,10 +145,7 @@ def countsketch_id_sharded(a_local, row0, in_dim, rank, sketch_dim=None, seed=No
     sketch_dim = check_matrix_id_args(_Shape, rank, sketch_dim, "countsketch")
     if seed is None:
         # every rank must draw the same hash: agree on fresh entropy first
-        ent = torch.tensor([np.random.SeedSequence().entropy % (2**63)], dtype=torch.int64)
-        if world > 1:
-            dist.broadcast(ent, src=0, group=group)
-        seed = int(ent.item())
+        seed = _agreed_entropy(group)
     y, flag, operand = backend.matrix_sketch(a_local, row0, in_dim, sketch_dim, seed, surjective)
     if world > 1:
         dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
@@ -181,7 +203,7 @@ def trial_sharded_operators(in_dim, out_dim, seeds, surjective=False, group=None
             buf.record_stream(main)
         else:
             buf = _device.empty(nbytes, torch.uint8)
-        src = dist.get_global_rank(group, owner) if group is not None else owner
+        src = _global_rank(group, owner)
         dist.broadcast(buf, src=src, group=group)
         op = CountSketchOp._from_packed(buf, in_dim, out_dim, surjective)
         op._bucket_index()
@@ -267,10 +289,7 @@ def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketc
 
     sketch_dim = check_tensor_id_args(_X, rank, sketch_dim, "tensorsketch")
     if seed is None:
-        ent = torch.tensor([np.random.SeedSequence().entropy % (2**63)], dtype=torch.int64)
-        if world > 1:
-            dist.broadcast(ent, src=0, group=group)
-        seed = int(ent.item())
+        seed = _agreed_entropy(group)
     y_local = backend.tensor_sketch(x_local.factors, x_local.weights, x_local.mode_dims,
                                     sketch_dim, seed)
     if world > 1 and cpqr == "columns":
@@ -397,6 +416,10 @@ def cpqr_columns_sharded(y_local, col0, total_cols, rank, rank_tol=1e-12, group=
     backend = backend or DeviceBackend()
     world, me = _world(group)
     blocks = [row_block(total_cols, world, r) for r in range(world)]
+    if (col0, col0 + int(y_local.shape[0])) != blocks[me]:
+        # the owner lookup and the all-gather sizes assume the row_block split
+        raise ValueError(f"rank {me} holds columns [{col0}, {col0 + int(y_local.shape[0])}) "
+                         f"but the split of {total_cols} over {world} ranks gives {blocks[me]}")
     shard = backend.cpqr_shard(y_local, col0, rank)
 
     def gather(cands):
@@ -410,7 +433,7 @@ def cpqr_columns_sharded(y_local, col0, total_cols, rank, rank_tol=1e-12, group=
     def broadcast(a_list, cs):
         if world > 1:
             owner = next(r for r, (b0, b1) in enumerate(blocks) if b0 <= cs < b1)
-            dist.broadcast(a_list[0], src=owner, group=group)
+            dist.broadcast(a_list[0], src=_global_rank(group, owner), group=group)
 
     dcpqr_steps([shard], rank, gather, broadcast)
     pos, r, beta = shard.results()
