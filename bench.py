@@ -475,13 +475,16 @@ class TensorWorkload:
                 f"(N+1) x R x 2.5 L log2 L flops")
 
     def trials(self, seeds):
-        from paper_1901_10559_b200.distributed import tensorsketch_id_sharded
+        from paper_1901_10559_b200.distributed import tensorsketch_id_sharded_trials
 
-        return [tensorsketch_id_sharded(self.x_local, self.c0, self.R, self.w_all, self.k,
-                                        self.L, seed=s) for s in seeds]
+        return tensorsketch_id_sharded_trials(self.x_local, self.c0, self.R, self.w_all,
+                                              self.k, self.L, seeds=list(seeds))
 
     def single(self, seed):
-        return self.trials([seed])[0]
+        from paper_1901_10559_b200.distributed import tensorsketch_id_sharded
+
+        return tensorsketch_id_sharded(self.x_local, self.c0, self.R, self.w_all, self.k,
+                                       self.L, seed=seed)
 
     def kernel(self, reps):
         import paper_1901_10559_b200 as ids

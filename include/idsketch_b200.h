@@ -302,6 +302,22 @@ int ids_dcpqr_step_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy
                        void* workspace, size_t ws_bytes, void* stream);
 int ids_dcpqr_results_f64(int64_t rows, int64_t ncols, int64_t k, int64_t* pos, double* R,
                           double* beta, void* workspace, size_t ws_bytes, void* stream);
+/* Device-driven step (no host round trip per step): gather every rank's cand
+ * into cands (device double[4 * nshards], shard order) and
+ *   ids_dcpqr_select_f64  -> piv (device int64[3]: pivot column, its position,
+ *                            column at position kk) -- the same rule as above;
+ *   ids_dcpqr_pivot_dev_f64 -> a: the owner's residual pivot column, -0.0 on
+ *                            every other rank, so an all-reduce(SUM) of a
+ *                            over the ranks is the owner's column bit for bit;
+ *   ids_dcpqr_step_dev_f64 -> as ids_dcpqr_step_f64 with the pivot from piv. */
+int ids_dcpqr_select_f64(const double* cands, int64_t nshards, int64_t kk, int64_t* piv,
+                         void* stream);
+int ids_dcpqr_pivot_dev_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy, int64_t k,
+                            int64_t col0, int64_t kk, const int64_t* piv, double* a,
+                            void* workspace, size_t ws_bytes, void* stream);
+int ids_dcpqr_step_dev_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy, int64_t k,
+                           int64_t col0, int64_t kk, const int64_t* piv, const double* a,
+                           double* cand, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Matrix Market input (replaces scipy.io.mmread behind

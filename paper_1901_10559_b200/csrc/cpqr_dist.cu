@@ -144,18 +144,60 @@ __global__ void __launch_bounds__(kT) dc_candidate_kernel(int64_t n, int64_t col
     }
 }
 
-// position swap (CTA 0) and, on the owner, the residual pivot column
+// Global pivot from the gathered per-shard candidates (shard order, 4
+// doubles each: value, position, column, column at position kk): largest
+// value, ties to the lowest position; all-NaN norms keep position kk.  The
+// device twin of distributed.pick_pivot -- piv = (c*, p*, column at kk).
+__global__ void dc_select_kernel(const double* __restrict__ cands, int64_t nshards, int64_t kk,
+                                 int64_t* __restrict__ piv) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    bool have = false;
+    double bv = 0.0;
+    int64_t bp = 0, bc = -1, ck = -1;
+    for (int64_t q = 0; q < nshards; ++q) {
+        const double val = cands[4 * q], pos = cands[4 * q + 1];
+        const double col = cands[4 * q + 2], nxt = cands[4 * q + 3];
+        if (nxt >= 0.0) ck = (int64_t)nxt;
+        if (col < 0.0) continue;
+        if (!have || val > bv || (val == bv && (int64_t)pos < bp)) {
+            have = true;
+            bv = val;
+            bp = (int64_t)pos;
+            bc = (int64_t)col;
+        }
+    }
+    piv[0] = have ? bc : ck;
+    piv[1] = have ? bp : kk;
+    piv[2] = ck;
+}
+
+// position swap (CTA 0) and, on the owner, the residual pivot column.  With
+// piv (device) the pivot comes from dc_select_kernel and the non-owners fill
+// a with -0.0, the identity of IEEE addition: an all-reduce(SUM) of a over
+// the ranks then reproduces the owner's column bit for bit.
 __global__ void __launch_bounds__(kT) dc_pivot_kernel(const double* __restrict__ Y, int64_t m,
                                                       int64_t n, int64_t ldy, int64_t k,
                                                       int64_t col0, int64_t kk, int64_t cs,
-                                                      int64_t ps, int64_t ck, DState s,
+                                                      int64_t ps, int64_t ck,
+                                                      const int64_t* __restrict__ piv, DState s,
                                                       double* __restrict__ a) {
+    if (piv) {
+        cs = piv[0];
+        ps = piv[1];
+        ck = piv[2];
+    }
     const int64_t csl = cs - col0, ckl = ck - col0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (ckl >= 0 && ckl < n && ck != cs) s.pos[ckl] = ps;
         if (csl >= 0 && csl < n) s.pos[csl] = kk;
     }
-    if (csl < 0 || csl >= n) return;
+    if (csl < 0 || csl >= n) {
+        if (piv)
+            for (int64_t r = (int64_t)blockIdx.x * kT + threadIdx.x; r < m;
+                 r += (int64_t)gridDim.x * kT)
+                a[r] = -0.0;
+        return;
+    }
     const int64_t mpad = ceil_div_dev(m);
     const double* ycol = Y + csl * ldy;
     for (int64_t r = (int64_t)blockIdx.x * kT + threadIdx.x; r < m; r += (int64_t)gridDim.x * kT)
@@ -165,9 +207,12 @@ __global__ void __launch_bounds__(kT) dc_pivot_kernel(const double* __restrict__
 // Householder vector v = V[:, kk] from the broadcast pivot column (one CTA,
 // identical arithmetic on every rank); the owner records R[kk, c*] = beta
 __global__ void __launch_bounds__(1024) dc_householder_kernel(int64_t m, int64_t n, int64_t col0,
-                                                              int64_t kk, int64_t cs, DState s,
+                                                              int64_t kk, int64_t cs,
+                                                              const int64_t* __restrict__ piv,
+                                                              DState s,
                                                               const double* __restrict__ a) {
     __shared__ double red[32];
+    if (piv) cs = piv[0];
     const int64_t mpad = ceil_div_dev(m);
     double ss = 0.0;
     for (int64_t r = kk + 1 + threadIdx.x; r < m; r += blockDim.x) ss = fma(a[r], a[r], ss);
@@ -350,14 +395,14 @@ extern "C" int ids_dcpqr_pivot_f64(const double* Y, int64_t rows, int64_t ncols,
     }
     const unsigned g = (unsigned)tmax<int64_t>(1, tmin<int64_t>(ceil_div(rows, kT), sm_count()));
     dc_pivot_kernel<<<g, kT, 0, as_stream(stream)>>>(Y, rows, ncols, ldy, k, col0, kk, cs, ps, ck,
-                                                     s, a);
+                                                     nullptr, s, a);
     IDS_LAUNCH_CHECK();
     return IDS_OK;
 }
 
-extern "C" int ids_dcpqr_step_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy,
-                                  int64_t k, int64_t col0, int64_t kk, int64_t cs, const double* a,
-                                  double* cand, void* workspace, size_t ws_bytes, void* stream) {
+static int dcpqr_step(const double* Y, int64_t rows, int64_t ncols, int64_t ldy, int64_t k,
+                      int64_t col0, int64_t kk, int64_t cs, const int64_t* piv, const double* a,
+                      double* cand, void* workspace, size_t ws_bytes, void* stream) {
     if (bad_args(rows, ncols, ldy, k) || kk < 0 || kk >= k) {
         ids_set_last_error("dcpqr: bad arguments");
         return IDS_EINVAL;
@@ -370,7 +415,7 @@ extern "C" int ids_dcpqr_step_f64(const double* Y, int64_t rows, int64_t ncols, 
     }
     cudaStream_t st = as_stream(stream);
     const int sms = sm_count();
-    dc_householder_kernel<<<1, 1024, 0, st>>>(rows, ncols, col0, kk, cs, s, a);
+    dc_householder_kernel<<<1, 1024, 0, st>>>(rows, ncols, col0, kk, cs, piv, s, a);
     IDS_LAUNCH_CHECK();
     if (kk > 0) {
         dc_z_kernel<<<(unsigned)kk, kT, 0, st>>>(rows, kk, s);
@@ -391,6 +436,56 @@ extern "C" int ids_dcpqr_step_f64(const double* Y, int64_t rows, int64_t ncols, 
     dc_candidate_kernel<<<1, kT, 0, st>>>(ncols, col0, kk + 1, s, cand);
     IDS_LAUNCH_CHECK();
     return IDS_OK;
+}
+
+extern "C" int ids_dcpqr_step_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy,
+                                  int64_t k, int64_t col0, int64_t kk, int64_t cs, const double* a,
+                                  double* cand, void* workspace, size_t ws_bytes, void* stream) {
+    return dcpqr_step(Y, rows, ncols, ldy, k, col0, kk, cs, nullptr, a, cand, workspace, ws_bytes,
+                      stream);
+}
+
+extern "C" int ids_dcpqr_select_f64(const double* cands, int64_t nshards, int64_t kk, int64_t* piv,
+                                    void* stream) {
+    if (nshards < 1 || kk < 0) {
+        ids_set_last_error("dcpqr: bad arguments");
+        return IDS_EINVAL;
+    }
+    dc_select_kernel<<<1, 32, 0, as_stream(stream)>>>(cands, nshards, kk, piv);
+    IDS_LAUNCH_CHECK();
+    return IDS_OK;
+}
+
+extern "C" int ids_dcpqr_pivot_dev_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy,
+                                       int64_t k, int64_t col0, int64_t kk, const int64_t* piv,
+                                       double* a, void* workspace, size_t ws_bytes, void* stream) {
+    if (bad_args(rows, ncols, ldy, k) || kk < 0 || kk >= k || !piv) {
+        ids_set_last_error("dcpqr: bad arguments");
+        return IDS_EINVAL;
+    }
+    WsCarve ws(workspace, ws_bytes);
+    const DState s = carve(ws, rows, ncols, k);
+    if (!ws.ok()) {
+        ids_set_last_error("dcpqr: workspace too small");
+        return IDS_EWORKSPACE;
+    }
+    const unsigned g = (unsigned)tmax<int64_t>(1, tmin<int64_t>(ceil_div(rows, kT), sm_count()));
+    dc_pivot_kernel<<<g, kT, 0, as_stream(stream)>>>(Y, rows, ncols, ldy, k, col0, kk, -1, kk, -1,
+                                                     piv, s, a);
+    IDS_LAUNCH_CHECK();
+    return IDS_OK;
+}
+
+extern "C" int ids_dcpqr_step_dev_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy,
+                                      int64_t k, int64_t col0, int64_t kk, const int64_t* piv,
+                                      const double* a, double* cand, void* workspace,
+                                      size_t ws_bytes, void* stream) {
+    if (!piv) {
+        ids_set_last_error("dcpqr: bad arguments");
+        return IDS_EINVAL;
+    }
+    return dcpqr_step(Y, rows, ncols, ldy, k, col0, kk, -1, piv, a, cand, workspace, ws_bytes,
+                      stream);
 }
 
 extern "C" int ids_dcpqr_results_f64(int64_t rows, int64_t ncols, int64_t k, int64_t* pos,

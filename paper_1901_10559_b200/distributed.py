@@ -313,6 +313,46 @@ def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketc
     return d, new_weights
 
 
+def tensorsketch_id_sharded_trials(x_local, col0, total_terms, all_weights, rank,
+                                   sketch_dim=None, seeds=(0,), rank_tol=1e-12, group=None):
+    """tensorsketch_id_sharded for several seeds, fully queued on the device
+    (the tensor twin of countsketch_id_sharded_trials): each trial's mode
+    hashes, TensorSketch block and ID (single-GPU CPQR at one rank, the
+    device-driven column-distributed CPQR beyond) are enqueued back to back
+    and the host synchronizes once, on one packed copy of every trial's
+    (j, P).  Returns [(InterpolativeDecomposition, new_weights)], identical
+    on every rank and to separate tensorsketch_id calls."""
+    from .cp_tensor import check_tensor_id_args
+    from .matrix_id import DeviceId, device_matrix_id
+    from .sketch import TensorSketchOp
+
+    world, me = _world(group)
+
+    class _X:
+        rank = total_terms
+        total_entries = int(np.prod(x_local.mode_dims))
+
+    L = check_tensor_id_args(_X, rank, sketch_dim, "tensorsketch")
+    blocks = [row_block(total_terms, world, r) for r in range(world)]
+    outs = []
+    for s in seeds:
+        y = TensorSketchOp(x_local.mode_dims, L, seed=s).apply_device(x_local.factors,
+                                                                     x_local.weights)
+        if world == 1:
+            d = device_matrix_id(y, L, total_terms, rank, rank_tol)
+        else:
+            d = _dcpqr_device(DeviceCpqrShard(y, col0, rank), blocks, total_terms, rank,
+                              rank_tol, group)
+        outs.append(d.packed())
+    host = torch.stack(outs).cpu().numpy() if outs else []
+    weights = np.asarray(all_weights, dtype=np.float64)
+    res = []
+    for v in host:
+        d = DeviceId.unpack(v, rank, total_terms, "tensorsketch")
+        res.append((d, weights[d.cols] * d.coeffs.sum(axis=1)))
+    return res
+
+
 # ---- column-distributed truncated CPQR (SURVEY.md 8f-2) ---------------------
 class DeviceCpqrShard:
     """This rank's column block of an L x R sketch for the column-distributed
@@ -350,6 +390,32 @@ class DeviceCpqrShard:
         self._call("ids_dcpqr_step_f64", d.ptr(self.y), self.m, self.n, self.m, self.k,
                    self.col0, kk, cs, d.ptr(a), d.ptr(self.cand), d.ptr(self.ws), self.nbytes,
                    d.stream_ptr())
+
+    # device-driven steps (ids_dcpqr_select / pivot_dev / step_dev): the pivot
+    # never visits the host
+    device_steps = True
+
+    def select(self, cands, kk):
+        """piv (device int64[3]) from the gathered candidates (device, shard order)."""
+        d = self._d
+        if not hasattr(self, "piv"):
+            self.piv = d.empty(3, torch.int64)
+        self._call("ids_dcpqr_select_f64", d.ptr(cands), int(cands.numel() // 4), kk,
+                   d.ptr(self.piv), d.stream_ptr())
+        return self.piv
+
+    def pivot_dev(self, kk, piv):
+        d = self._d
+        self._call("ids_dcpqr_pivot_dev_f64", d.ptr(self.y), self.m, self.n, self.m, self.k,
+                   self.col0, kk, d.ptr(piv), d.ptr(self.a), d.ptr(self.ws), self.nbytes,
+                   d.stream_ptr())
+        return self.a
+
+    def step_dev(self, kk, piv, a):
+        d = self._d
+        self._call("ids_dcpqr_step_dev_f64", d.ptr(self.y), self.m, self.n, self.m, self.k,
+                   self.col0, kk, d.ptr(piv), d.ptr(a), d.ptr(self.cand), d.ptr(self.ws),
+                   self.nbytes, d.stream_ptr())
 
     def results(self):
         d = self._d
@@ -408,6 +474,72 @@ def assemble_pivoted(pos_all, r_all, beta, k, rank_tol):
     return perm, rtop, nr
 
 
+def _gather_blocks(pos, r, blocks, rank, group):
+    """All-gather the per-rank positions and R rows (padded to the widest
+    block) into global column order."""
+    world = len(blocks)
+    width = max(b1 - b0 for b0, b1 in blocks)
+    pp = torch.zeros(width, dtype=torch.int64, device=pos.device)
+    rp = torch.zeros((rank, width), dtype=torch.float64, device=r.device)
+    pp[: pos.numel()] = pos
+    rp[:, : r.shape[1]] = r
+    pparts = [torch.empty_like(pp) for _ in range(world)]
+    rparts = [torch.empty_like(rp) for _ in range(world)]
+    dist.all_gather(pparts, pp, group=group)
+    dist.all_gather(rparts, rp, group=group)
+    sizes = [b1 - b0 for b0, b1 in blocks]
+    pos = torch.cat([p[:s] for p, s in zip(pparts, sizes)])
+    r = torch.cat([q[:, :s] for q, s in zip(rparts, sizes)], dim=1)
+    return pos, r
+
+
+def _dcpqr_device(shard, blocks, total_cols, rank, rank_tol, group):
+    """The column-distributed CPQR driven entirely on the device: per step
+    the candidates are gathered into a device tensor, the pivot is picked by
+    a kernel (ids_dcpqr_select_f64) and the pivot column is summed over the
+    ranks (the non-owners contribute -0.0, so the sum is the owner's column
+    bit for bit); the factors are assembled and P solved on the device.  No
+    host synchronization: returns a DeviceId (identical on every rank)."""
+    from . import _device
+    from ._native import call, query
+    from .matrix_id import DeviceId
+
+    world = len(blocks)
+    for kk in range(rank):
+        c = shard.cand.reshape(1, 4)
+        if world > 1:
+            parts = [torch.empty_like(c) for _ in range(world)]
+            dist.all_gather(parts, c, group=group)
+            c = torch.cat(parts)
+        piv = shard.select(c, kk)
+        a = shard.pivot_dev(kk, piv)
+        if world > 1:
+            dist.all_reduce(a, op=dist.ReduceOp.SUM, group=group)
+        shard.step_dev(kk, piv, a)
+    pos, r, beta = shard.results()
+    if world > 1:
+        pos, r = _gather_blocks(pos, r, blocks, rank, group)
+    # assemble_pivoted on the device: perm[pos] = column, Rtop[:, pos] = R
+    # rows (upper trapezoid), numerical rank from the diagonal beta
+    dev = pos.device
+    perm = torch.empty(total_cols, dtype=torch.int32, device=dev)
+    perm[pos] = torch.arange(total_cols, dtype=torch.int32, device=dev)
+    q = torch.arange(rank, device=dev)[:, None]
+    rtop = torch.zeros((rank, total_cols), dtype=torch.float64, device=dev)
+    rtop[:, pos] = torch.where(pos[None, :] >= q, r, torch.zeros((), dtype=r.dtype, device=dev))
+    lead = beta[0].abs()
+    nr = torch.where(lead != 0, (beta.abs() > rank_tol * lead).sum(), 0).to(torch.int32)
+    nr = nr.reshape(1)
+    p = _device.empty((rank, total_cols), torch.float64)
+    de = _device.empty(1, torch.int32)
+    nbytes = query("ids_id_coeffs_workspace_bytes", rank, total_cols)
+    ws = _device.workspace(nbytes)
+    call("ids_id_coeffs_f64", _device.ptr(rtop), _device.ptr(perm), rank, total_cols,
+         float(rank_tol), _device.ptr(nr), _device.ptr(p), _device.ptr(de), _device.ptr(ws),
+         nbytes, _device.stream_ptr())
+    return DeviceId(perm[:rank], p, nr, de, rank)
+
+
 def cpqr_columns_sharded(y_local, col0, total_cols, rank, rank_tol=1e-12, group=None,
                          backend=None):
     """ID of an L x R sketch whose columns [col0, col0 + R_local) live on this
@@ -435,21 +567,13 @@ def cpqr_columns_sharded(y_local, col0, total_cols, rank, rank_tol=1e-12, group=
             owner = next(r for r, (b0, b1) in enumerate(blocks) if b0 <= cs < b1)
             dist.broadcast(a_list[0], src=_global_rank(group, owner), group=group)
 
+    if getattr(shard, "device_steps", False):
+        return _dcpqr_device(shard, blocks, total_cols, rank, rank_tol, group).to_host(
+            "tensorsketch")
     dcpqr_steps([shard], rank, gather, broadcast)
     pos, r, beta = shard.results()
     if world > 1:
-        width = max(b1 - b0 for b0, b1 in blocks)
-        pp = torch.zeros(width, dtype=torch.int64, device=pos.device)
-        rp = torch.zeros((rank, width), dtype=torch.float64, device=r.device)
-        pp[: pos.numel()] = pos
-        rp[:, : r.shape[1]] = r
-        pparts = [torch.empty_like(pp) for _ in range(world)]
-        rparts = [torch.empty_like(rp) for _ in range(world)]
-        dist.all_gather(pparts, pp, group=group)
-        dist.all_gather(rparts, rp, group=group)
-        sizes = [b1 - b0 for b0, b1 in blocks]
-        pos = torch.cat([p[:s] for p, s in zip(pparts, sizes)])
-        r = torch.cat([q[:, :s] for q, s in zip(rparts, sizes)], dim=1)
+        pos, r = _gather_blocks(pos, r, blocks, rank, group)
     perm, rtop, nr = assemble_pivoted(pos.cpu().numpy(), r.cpu().numpy(), beta.cpu().numpy(),
                                       rank, rank_tol)
     return backend.coeffs_from_factors(rtop, perm, rank, total_cols, rank_tol, nr)

@@ -93,3 +93,46 @@ def test_zero_and_deficient_sketches():
     w = oracle.matrix_id(y, 12)
     assert nr == w.numerical_rank
     assert np.array_equal(perm[:nr], w.cols[:nr])
+
+
+def _run_local_shards_device(y, k, bounds):
+    """The device-driven loop of cpqr_columns_sharded with the collectives
+    replaced by local ops: cat of the candidates, a plain sum of the pivot
+    columns (non-owners contribute -0.0)."""
+    shards = [DeviceCpqrShard(torch.from_numpy(np.ascontiguousarray(y[:, a:b].T)).cuda(), a, k)
+              for a, b in zip(bounds[:-1], bounds[1:])]
+    for kk in range(k):
+        c = torch.cat([sh.cand.reshape(1, 4) for sh in shards])
+        pivs = [sh.select(c, kk) for sh in shards]
+        a_list = [sh.pivot_dev(kk, p) for sh, p in zip(shards, pivs)]
+        tot = a_list[0].clone()
+        for a in a_list[1:]:
+            tot += a
+        for sh, p in zip(shards, pivs):
+            sh.step_dev(kk, p, tot)
+    parts = [sh.results() for sh in shards]
+    pos = np.concatenate([p[0].cpu().numpy() for p in parts])
+    r = np.concatenate([p[1].cpu().numpy() for p in parts], axis=1)
+    return assemble_pivoted(pos, r, parts[0][2].cpu().numpy(), k, 1e-12)
+
+
+@pytest.mark.parametrize("bounds", [[0, 300, 600, 1000], [0, 1, 500, 999, 1000], [0, 1000]])
+def test_device_driven_steps_bit_identical(bounds):
+    """Pivot picked on the device + summed pivot column == the host-driven
+    steps (host pick + broadcast), bit for bit; pivots equal LAPACK's."""
+    y = _near_dup(np.random.default_rng(3), 4096, 1000, 10, 1e-3)
+    y[:, 17] = 0.0  # an exactly zero column (its +-0 entries must survive the sum)
+    k = 10
+    p1, r1, n1 = _run_local_shards(y, k, bounds)
+    p2, r2, n2 = _run_local_shards_device(y, k, bounds)
+    assert np.array_equal(p1, p2) and n1 == n2
+    assert np.array_equal(r1, r2)
+    assert np.array_equal(p2[:k], oracle.cpqr(y, k).perm[:k])
+
+
+def test_device_driven_zero_sketch():
+    y = np.zeros((64, 30))
+    p1, r1, n1 = _run_local_shards(y, 4, [0, 10, 30])
+    p2, r2, n2 = _run_local_shards_device(y, 4, [0, 10, 30])
+    assert np.array_equal(p1, p2) and n1 == n2 == 0
+    assert np.array_equal(np.signbit(r1), np.signbit(r2)) and np.array_equal(r1, r2)
