@@ -171,7 +171,8 @@ int ids_countsketch_csr_f64(const void* indptr, int indptr64, const int32_t* ind
  *   order_signed[n], sorted_bucket[n]: bucket index of mode n (out_dim
  *   buckets; see ids_bucket_index).
  *   weights: device double[ncols] or NULL.  Y: col-major out_dim x ncols.
- *   colnorm2 (may be NULL): ||Y[:,r]||^2 per column.
+ *   colnorm2 (may be NULL): ||Y[:,r]||^2 per column (fixed-order sum of the
+ *   written values: run-to-run identical), for ids_cpqr_trunc_norms_f64.
  * ------------------------------------------------------------------------- */
 size_t ids_tensorsketch_workspace_bytes(int n_modes, const int64_t* dims, int64_t ncols,
                                         int64_t out_dim);
@@ -225,6 +226,14 @@ int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, int64_t ldy,
                        int64_t k, double rank_tol, int32_t* perm, double* Rtop,
                        double* Q, int32_t* numerical_rank, void* workspace,
                        size_t ws_bytes, void* stream);
+/* ids_cpqr_trunc_f64 with the initial column norms supplied: colnorm2
+ * (device double[cols], may be NULL) holds ||Y[:,j]||^2, e.g. from the
+ * TensorSketch kernel's epilogue, so the factorization skips its own norm
+ * pass over Y (dgeqp3's initial dnrm2 loop, linalg.py:97). */
+int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t cols, int64_t ldy, int64_t k,
+                             double rank_tol, const double* colnorm2, int32_t* perm,
+                             double* Rtop, double* Q, int32_t* numerical_rank, void* workspace,
+                             size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * ID coefficients from the truncated factorization.  Replaces

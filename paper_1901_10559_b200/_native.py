@@ -77,6 +77,11 @@ SIGNATURES = {
         _c_int,
         [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p],
     ),
+    "ids_cpqr_trunc_norms_f64": (
+        _c_int,
+        [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz,
+         _c_p],
+    ),
     "ids_id_coeffs_workspace_bytes": (_c_sz, [_c_i64, _c_i64]),
     "ids_id_coeffs_f64": (
         _c_int,

@@ -201,8 +201,8 @@ def tensorsketch_device(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RA
     """Device half of tensorsketch_id: (DeviceId, sketch (R, L))."""
     sketch_dim = check_tensor_id_args(x, rank, sketch_dim, "tensorsketch")
     op = TensorSketchOp(x.mode_dims, sketch_dim, seed=seed)
-    y = op.apply_device(x.factors, x.weights)
-    return device_matrix_id(y, sketch_dim, x.rank, rank, rank_tol), y
+    y, nrm = op.apply_device(x.factors, x.weights, norms=True)
+    return device_matrix_id(y, sketch_dim, x.rank, rank, rank_tol, colnorm2=nrm), y
 
 
 def tensorsketch_id(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL):

@@ -42,6 +42,7 @@ struct CpqrArgs {
     int64_t m, n, ldy, k;
     int small;  // m small: pivot column and z computed redundantly by every CTA
     int64_t vwin;  // doubles of v kept in shared memory (all of it when small)
+    const double* colnorm2;  // optional ||Y[:,j]||^2 (skips the initial norm pass)
     double rank_tol;
     int32_t* perm;
     double* Rtop;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1) cpqr_kernel(CpqrArgs g) {
         for (int64_t r = m + threadIdx.x; r < mpad; r += kThreads) g.a[r] = 0.0;
     for (int64_t j = c0 + wid; j < c1; j += kWarps) {
         const double* y = g.Y + j * ldy;
-        const double s = warp_sum(lane_dot(y, y, 0, m));
+        const double s = g.colnorm2 ? g.colnorm2[j] : warp_sum(lane_dot(y, y, 0, m));
         if (lane == 0) {
             g.vn1[j] = sqrt(s);
             g.vn2[j] = sqrt(s);
@@ -980,6 +981,8 @@ int grid_size(int64_t m, int64_t n, size_t smem) {
 
 constexpr int64_t kMaxG = 148;
 
+
+
 int64_t* g_cpqr_tlog = nullptr;  // debug: per-phase timing of the cooperative kernel
 
 }  // namespace
@@ -999,6 +1002,15 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
                                   int64_t k, double rank_tol, int32_t* perm, double* Rtop,
                                   double* Q, int32_t* numerical_rank, void* workspace,
                                   size_t ws_bytes, void* stream) {
+    return ids_cpqr_trunc_norms_f64(Y, rows, cols, ldy, k, rank_tol, nullptr, perm, Rtop, Q,
+                                    numerical_rank, workspace, ws_bytes, stream);
+}
+
+extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t cols, int64_t ldy,
+                                        int64_t k, double rank_tol, const double* colnorm2,
+                                        int32_t* perm, double* Rtop, double* Q,
+                                        int32_t* numerical_rank, void* workspace,
+                                        size_t ws_bytes, void* stream) {
     if (rows < 1 || cols < 1 || k < 1 || k > rows || k > cols || ldy < rows || k > 64 * 1024) {
         ids_set_last_error("cpqr: bad arguments (need 1 <= k <= min(rows, cols))");
         return IDS_EINVAL;
@@ -1084,6 +1096,7 @@ extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, i
     a.rank_tol = rank_tol;
     a.small = small ? 1 : 0;
     a.vwin = vwin;
+    a.colnorm2 = colnorm2;
     a.perm = perm;
     a.Rtop = Rtop;
     a.numerical_rank = numerical_rank;

@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
     __shared__ int32_t s_prevkey;
     __shared__ int s_pvalid[kMaxModes], s_pmaxr[kMaxModes];
     __shared__ int32_t s_poff[kMaxModes][kMaxPhase + 2];
+    __shared__ double s_nrm[32];
     double* dbuf = reinterpret_cast<double*>(buf);
     const int T = blockDim.x, t = threadIdx.x;
     const int N2 = (int)g.N2, M = (int)g.M;
@@ -856,9 +857,15 @@ __global__ void __launch_bounds__(512, 1) tensorsketch_kernel(TsArgs g) {
                 nrm = fma(v, v, nrm);
             }
         }
-        if (g.colnorm2) {
+        if (g.colnorm2) {  // fixed-order block reduction: run-to-run identical
             for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-            if ((t & 31) == 0) atomicAdd(g.colnorm2 + r, nrm);
+            if ((t & 31) == 0) s_nrm[t >> 5] = nrm;
+            __syncthreads();
+            if (t == 0) {
+                double acc = 0.0;
+                for (int w = 0; w < (T >> 5); ++w) acc += s_nrm[w];
+                g.colnorm2[r] = acc;
+            }
         }
         out_nrm = 0.0;
         __syncthreads();
@@ -1021,7 +1028,6 @@ extern "C" int ids_tensorsketch_planned_f64(int n_modes, const double* const* fa
     a.stage_cap = p.stage_cap;
     a.y_vec = (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && out_dim % 2 == 0;
     a.tlog = g_ts_tlog;
-    if (colnorm2) IDS_CUDA_TRY(cudaMemsetAsync(colnorm2, 0, sizeof(double) * ncols, st));
     auto kern = p.ept == 16 ? tensorsketch_kernel<16> : tensorsketch_kernel<8>;
     if (p.smem > 40 * 1024)
         IDS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -336,10 +336,10 @@ def tensorsketch_id_sharded_trials(x_local, col0, total_terms, all_weights, rank
     blocks = [row_block(total_terms, world, r) for r in range(world)]
     outs = []
     for s in seeds:
-        y = TensorSketchOp(x_local.mode_dims, L, seed=s).apply_device(x_local.factors,
-                                                                     x_local.weights)
+        y, nrm = TensorSketchOp(x_local.mode_dims, L, seed=s).apply_device(
+            x_local.factors, x_local.weights, norms=True)
         if world == 1:
-            d = device_matrix_id(y, L, total_terms, rank, rank_tol)
+            d = device_matrix_id(y, L, total_terms, rank, rank_tol, colnorm2=nrm)
         else:
             d = _dcpqr_device(DeviceCpqrShard(y, col0, rank), blocks, total_terms, rank,
                               rank_tol, group)

@@ -73,9 +73,12 @@ class DeviceQr:
     q: torch.Tensor = None  # float64[k, rows] (col-major rows x k) or None
 
 
-def device_cpqr(y_cm, rows, cols, rank, rank_tol=DEFAULT_RANK_TOL, want_q=False, ld=None):
+def device_cpqr(y_cm, rows, cols, rank, rank_tol=DEFAULT_RANK_TOL, want_q=False, ld=None,
+                colnorm2=None):
     """Truncated CPQR of the col-major rows x cols matrix stored in y_cm
-    (CUDA float64, column j at y_cm[j*ld : j*ld + rows])."""
+    (CUDA float64, column j at y_cm[j*ld : j*ld + rows]).  colnorm2: optional
+    device ||Y[:, j]||^2 (the TensorSketch epilogue's), replacing the
+    factorization's own initial norm pass."""
     ld = rows if ld is None else ld
     perm = _device.empty(cols, torch.int32)
     rtop = _device.empty((rank, cols), torch.float64)
@@ -84,9 +87,9 @@ def device_cpqr(y_cm, rows, cols, rank, rank_tol=DEFAULT_RANK_TOL, want_q=False,
     nbytes = query("ids_cpqr_workspace_bytes", rows, cols, rank)
     ws = _device.workspace(nbytes)
     call(
-        "ids_cpqr_trunc_f64", _device.ptr(y_cm), rows, cols, ld, rank, float(rank_tol),
-        _device.ptr(perm), _device.ptr(rtop), _device.ptr(q), _device.ptr(nr),
-        _device.ptr(ws), nbytes, _device.stream_ptr(),
+        "ids_cpqr_trunc_norms_f64", _device.ptr(y_cm), rows, cols, ld, rank, float(rank_tol),
+        _device.ptr(colnorm2), _device.ptr(perm), _device.ptr(rtop), _device.ptr(q),
+        _device.ptr(nr), _device.ptr(ws), nbytes, _device.stream_ptr(),
     )
     return DeviceQr(perm, rtop, nr, q)
 

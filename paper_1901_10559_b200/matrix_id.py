@@ -94,10 +94,11 @@ class DeviceId:
                                           numerical_rank=nr, rank_deficient=de)
 
 
-def device_matrix_id(y_cm, rows, cols, rank, rank_tol=DEFAULT_RANK_TOL, ld=None):
+def device_matrix_id(y_cm, rows, cols, rank, rank_tol=DEFAULT_RANK_TOL, ld=None, colnorm2=None):
     """ID of the col-major rows x cols sketch in y_cm, on the device
-    (matrix_id.py:87-113 via cpqr + _coeffs_from_pivoted)."""
-    f = device_cpqr(y_cm, rows, cols, rank, rank_tol, want_q=False, ld=ld)
+    (matrix_id.py:87-113 via cpqr + _coeffs_from_pivoted).  colnorm2:
+    optional device squared column norms of the sketch (see device_cpqr)."""
+    f = device_cpqr(y_cm, rows, cols, rank, rank_tol, want_q=False, ld=ld, colnorm2=colnorm2)
     p = _device.empty((rank, cols), torch.float64)
     de = _device.empty(1, torch.int32)
     nbytes = query("ids_id_coeffs_workspace_bytes", rank, cols)

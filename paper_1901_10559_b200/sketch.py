@@ -343,12 +343,13 @@ class TensorSketchOp:
     def in_dim(self):
         return int(np.prod(self.mode_dims))
 
-    def apply_device(self, factors, weights=None):
+    def apply_device(self, factors, weights=None, norms=False):
         """Sketch of khatri_rao(factors) @ diag(weights) as a CUDA tensor of
-        shape (ncols, out_dim) (col-major L x R)."""
+        shape (ncols, out_dim) (col-major L x R); norms=True also returns the
+        squared column norms of the sketch (device, or None)."""
         from .tensorsketch import tensorsketch_device
 
-        return tensorsketch_device(self, factors, weights)
+        return tensorsketch_device(self, factors, weights, norms=norms)
 
     def apply(self, factors, weights=None):
         """sketch.py:156-186: numpy L x R for host factors."""

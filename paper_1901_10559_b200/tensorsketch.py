@@ -43,8 +43,11 @@ def factor_to_device(f):
 SCATTER_MIN_DIM = 4096  # mode length from which the fused kernel uses a scatter plan
 
 
-def tensorsketch_device(op, factors, weights=None):
-    """Y = TensorSketch(khatri_rao(factors)) diag(weights): CUDA (R, L) tensor."""
+def tensorsketch_device(op, factors, weights=None, norms=False):
+    """Y = TensorSketch(khatri_rao(factors)) diag(weights): CUDA (R, L) tensor.
+    norms=True returns (Y, colnorm2): the fused kernel's epilogue also writes
+    ||Y[:, r]||^2 (None on the long-sketch route), which the CPQR takes in
+    place of its own first pass over Y."""
     if len(factors) != len(op.mode_ops):
         raise ValueError(f"expected {len(op.mode_ops)} factors, got {len(factors)}")
     ncols = factors[0].shape[1]
@@ -69,7 +72,8 @@ def tensorsketch_device(op, factors, weights=None):
     n = len(dev_f)
     L = op.out_dim
     if not query("ids_tensorsketch_fused_ok", n, L):
-        return _tensorsketch_spectral(op, dev_f, w, ncols, L)
+        y = _tensorsketch_spectral(op, dev_f, w, ncols, L)
+        return (y, None) if norms else y
     idx = [m._bucket_index() for m in op.mode_ops]
     # scatter plans pay off on long factor columns; short modes (C4: 1000
     # rows) keep the gather path rather than pay the plan's launches per draw
@@ -81,18 +85,20 @@ def tensorsketch_device(op, factors, weights=None):
     dims = (ctypes.c_int64 * n)(*[int(d) for d in op.mode_dims])
     lds = (ctypes.c_int64 * n)(*[int(t.shape[1]) for t in dev_f])
     y = _device.empty((ncols, L), torch.float64)
+    nrm = _device.empty(max(ncols, 1), torch.float64)[:ncols] if norms else None
     if ncols == 0:
-        return y
+        return (y, nrm) if norms else y
     nbytes = query("ids_tensorsketch_workspace_bytes", n, ctypes.addressof(dims), ncols, L)
     ws = _device.workspace(nbytes)
     call(
         "ids_tensorsketch_planned_f64", n, ctypes.addressof(fac_p), ctypes.addressof(dims),
         ctypes.addressof(lds), ncols, ctypes.addressof(ord_p), ctypes.addressof(key_p),
         ctypes.addressof(plans), L,
-        _device.ptr(w), _device.ptr(y), None, _device.ptr(ws), nbytes, _device.stream_ptr(),
+        _device.ptr(w), _device.ptr(y), _device.ptr(nrm), _device.ptr(ws), nbytes,
+        _device.stream_ptr(),
     )
     # dev_f may be freed now: the caching allocator reuses memory in stream order
-    return y
+    return (y, nrm) if norms else y
 
 
 def _tensorsketch_spectral(op, dev_f, w, ncols, L):

@@ -287,3 +287,27 @@ def test_scatter_plan_ranks_and_slots():
     for rr in range(1, maxr + 1):
         s = np.sort(slot[rank == rr])
         assert np.array_equal(s, np.arange(off[rr], off[rr + 1]))
+
+
+def test_colnorm_epilogue_feeds_cpqr():
+    """The fused kernel's ||Y[:, r]||^2 epilogue (fixed-order: run-to-run
+    identical) equals the norms of the written sketch, and the CPQR that
+    takes it (ids_cpqr_trunc_norms_f64, no initial norm pass) picks the
+    same pivots and R as the one that computes its own (linalg.py:97)."""
+    from paper_1901_10559_b200.linalg import device_cpqr
+
+    rng = np.random.default_rng(21)
+    w, fac = _near_dup_cp(rng, [3000] * 3, 600, 12, 1e-3)
+    x = ids.CpTensor(w, fac)
+    op = ids.TensorSketchOp(x.mode_dims, 4096, seed=3)
+    y, nrm = op.apply_device(x.factors, x.weights, norms=True)
+    y2, nrm2 = op.apply_device(x.factors, x.weights, norms=True)
+    assert torch.equal(nrm, nrm2) and torch.equal(y, y2)
+    ref = (y * y).sum(dim=1)
+    assert float(((nrm - ref).abs() / ref).max()) <= 1e-13
+    a = device_cpqr(y, 4096, 600, 12)
+    b = device_cpqr(y, 4096, 600, 12, colnorm2=nrm)
+    assert torch.equal(a.perm[:12], b.perm[:12])
+    assert float((a.rtop - b.rtop).abs().max() / a.rtop.abs().max()) <= 1e-12
+    want = oracle.cpqr(y.t().cpu().numpy(), 12)
+    assert np.array_equal(b.perm[:12].cpu().numpy(), want.perm[:12])
