@@ -159,7 +159,7 @@ def countsketch_id_sharded(a_local, row0, in_dim, rank, sketch_dim=None, seed=No
     return backend.matrix_id(y, sketch_dim, cols, rank, rank_tol, "countsketch")
 
 
-def trial_sharded_operators(in_dim, out_dim, seeds, surjective=False, group=None):
+def trial_sharded_operators(in_dim, out_dim, seeds, surjective=False, group=None, index=True):
     """CountSketchOps for a sequence of trials on every rank of `group`, each
     hash drawn by ONE rank: trial t by rank t % world, all of a rank's draws
     enqueued up front on side streams, then, trial by trial, one broadcast of
@@ -206,16 +206,18 @@ def trial_sharded_operators(in_dim, out_dim, seeds, surjective=False, group=None
         src = _global_rank(group, owner)
         dist.broadcast(buf, src=src, group=group)
         op = CountSketchOp._from_packed(buf, in_dim, out_dim, surjective)
-        op._bucket_index()
+        if index:
+            op._bucket_index()
         yield op
 
 
 def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, seeds=(0,),
-                                  rank_tol=1e-12, surjective=True, group=None):
+                                  rank_tol=1e-12, surjective=True, group=None, **pipe):
     """countsketch_id_sharded for several seeds, fully queued on the device:
     hash, sketch, all-reduce and ID of every trial are enqueued back to back
     and the host synchronizes once at the end (non-finite input is checked
     then, for all trials at once).  Every rank returns the same list."""
+    from . import _device
     from ._inputs import DenseOperand, SparseOperand, matrix_operand
     from ._native import IDS_FLAG_ORDERED
     from .matrix_id import check_matrix_id_args, device_matrix_id
@@ -233,13 +235,20 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     seeds = list(seeds)
     outs, flags = [], []
     main = torch.cuda.current_stream()
-    side = id_stream()
+    side = id_stream() if pipe.pop("id_side", True) else main
     # one rank: each trial's hash is drawn on a side stream while the previous
     # trial sketches (sketch.pipelined_operators); several ranks: the trials'
     # hashes are split over the ranks and broadcast (trial_sharded_operators).
     # Each trial's ID runs on a high-priority stream beside the next sketch.
-    ops = (pipelined_operators(in_dim, L, seeds, surjective) if world == 1
-           else trial_sharded_operators(in_dim, L, seeds, surjective, group))
+    from .sketch import CountSketchOp
+
+    index = CountSketchOp.needs_index(operand, IDS_FLAG_ORDERED)
+    if isinstance(operand, SparseOperand):
+        # a sparse sketch is short next to its I-row hash draw: background
+        # draws run at full grid (tools/exp_trials.py: C3 4.25 vs 4.78 ms)
+        pipe.setdefault("grid_cap", 0)
+    ops = (pipelined_operators(in_dim, L, seeds, surjective, index=index, **pipe) if world == 1
+           else trial_sharded_operators(in_dim, L, seeds, surjective, group, index=index))
     for op in ops:
         y = torch.empty((cols, L), dtype=torch.float64, device=torch.cuda.current_device())
         flag = torch.zeros(1, dtype=torch.int32, device=y.device)
@@ -267,7 +276,8 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     packed = torch.stack(outs) if outs else None
     from .matrix_id import DeviceId
 
-    host = packed.cpu().numpy() if packed is not None else []  # one copy for all trials
+    # one pinned copy for all trials
+    host = _device.to_host(packed) if packed is not None else []
     return [DeviceId.unpack(v, rank, cols, "countsketch") for v in host]
 
 
@@ -322,6 +332,7 @@ def tensorsketch_id_sharded_trials(x_local, col0, total_terms, all_weights, rank
     and the host synchronizes once, on one packed copy of every trial's
     (j, P).  Returns [(InterpolativeDecomposition, new_weights)], identical
     on every rank and to separate tensorsketch_id calls."""
+    from . import _device
     from .cp_tensor import check_tensor_id_args
     from .matrix_id import DeviceId, device_matrix_id
     from .sketch import TensorSketchOp
@@ -344,7 +355,7 @@ def tensorsketch_id_sharded_trials(x_local, col0, total_terms, all_weights, rank
             d = _dcpqr_device(DeviceCpqrShard(y, col0, rank), blocks, total_terms, rank,
                               rank_tol, group)
         outs.append(d.packed())
-    host = torch.stack(outs).cpu().numpy() if outs else []
+    host = _device.to_host(torch.stack(outs)) if outs else []
     weights = np.asarray(all_weights, dtype=np.float64)
     res = []
     for v in host:

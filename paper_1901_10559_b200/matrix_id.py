@@ -68,28 +68,30 @@ class DeviceId:
     deficient: torch.Tensor  # int32[1]
     rank: int
 
-    def to_host(self, method):
-        cols = _device.to_host(self.cols).copy()
-        coeffs = _device.to_host(self.coeffs)
-        nr = _device.to_host(self.numerical_rank)
-        de = _device.to_host(self.deficient)
-        return InterpolativeDecomposition(
-            coeffs=coeffs, cols=cols, rank=self.rank, method=method,
-            numerical_rank=int(nr[0]), rank_deficient=bool(de[0]),
-        )
+    def to_host(self, method, flag=None):
+        """The decomposition on the host: one packed device->host copy.  With
+        flag (device int32[1], e.g. the sketch's non-finite flag) returns
+        (decomposition, bool(flag)) from the same copy."""
+        vec = _device.to_host(self.packed(flag))
+        d = self.unpack(vec[1:] if flag is not None else vec, self.rank,
+                        self.coeffs.shape[1], method)
+        return (d, bool(vec[0])) if flag is not None else d
 
-    def packed(self):
+    def packed(self, flag=None):
         """cols, numerical_rank, deficient and coeffs packed in one float64
-        device vector (indices are exact in float64), for one batched copy."""
-        head = torch.cat([self.cols.to(torch.float64), self.numerical_rank.to(torch.float64),
-                          self.deficient.to(torch.float64)])
-        return torch.cat([head, self.coeffs.reshape(-1)])
+        device vector (indices are exact in float64), for one batched copy;
+        flag (device int32[1]) is prepended when given."""
+        parts = [self.cols.to(torch.float64), self.numerical_rank.to(torch.float64),
+                 self.deficient.to(torch.float64), self.coeffs.reshape(-1)]
+        if flag is not None:
+            parts.insert(0, flag.to(torch.float64).reshape(1))
+        return torch.cat(parts)
 
     @staticmethod
     def unpack(vec, rank, ncols, method):
         cols = vec[:rank].astype(np.int32)
         nr, de = int(vec[rank]), bool(vec[rank + 1])
-        coeffs = vec[rank + 2:].reshape(rank, ncols).copy()
+        coeffs = vec[rank + 2:rank + 2 + rank * ncols].reshape(rank, ncols).copy()
         return InterpolativeDecomposition(coeffs=coeffs, cols=cols, rank=rank, method=method,
                                           numerical_rank=nr, rank_deficient=de)
 
@@ -177,16 +179,23 @@ def _raise_if_nonfinite(flag, operand):
 
 
 def countsketch_device(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL,
-                       surjective=True, flags=IDS_FLAG_ORDERED, check_finite=True):
-    """The device half of countsketch_id: returns (DeviceId, sketch (cols, L))."""
+                       surjective=True, flags=IDS_FLAG_ORDERED, check_finite=True,
+                       defer_check=False):
+    """The device half of countsketch_id: returns (DeviceId, sketch (cols, L)).
+    defer_check=True leaves the non-finite flag of the sketch on the device
+    (DeviceId.nonfinite, DeviceId.operand) for the caller to read with the
+    result -- no host synchronization before the ID is enqueued."""
     operand = a if isinstance(a, (DenseOperand, SparseOperand)) else matrix_operand(a)
     sketch_dim = check_matrix_id_args(operand, rank, sketch_dim, "countsketch")
     op = CountSketchOp(operand.rows, sketch_dim, seed=seed, surjective=surjective)
     nonfinite = _device.zeros(1, torch.int32) if check_finite else None
     y = op.apply_device(operand, flags=flags, nonfinite=nonfinite)
-    if check_finite:
+    if check_finite and not defer_check:
         _raise_if_nonfinite(nonfinite, operand)
-    return device_matrix_id(y, sketch_dim, operand.cols, rank, rank_tol), y
+    d = device_matrix_id(y, sketch_dim, operand.cols, rank, rank_tol)
+    if defer_check:
+        d.nonfinite, d.operand = nonfinite, operand
+    return d, y
 
 
 def countsketch_id_trials(a, rank, sketch_dim=None, seeds=(0,), rank_tol=DEFAULT_RANK_TOL,
@@ -210,8 +219,11 @@ def countsketch_id(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TO
     maps (the default) keep the sketch operator full rank.  Default
     sketch_dim is rank + 10.
     """
-    d, _ = countsketch_device(a, rank, sketch_dim, seed, rank_tol, surjective)
-    return d.to_host("countsketch")
+    d, _ = countsketch_device(a, rank, sketch_dim, seed, rank_tol, surjective, defer_check=True)
+    out, bad = d.to_host("countsketch", flag=d.nonfinite)
+    if bad:  # Y had a NaN / Inf: confirm on A itself (raises ValueError)
+        _raise_if_nonfinite(d.nonfinite, d.operand)
+    return out
 
 
 __all__ = [

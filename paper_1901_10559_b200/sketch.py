@@ -237,6 +237,21 @@ class CountSketchOp:
             self._plan = plan
         return self._plan
 
+    @staticmethod
+    def needs_index(operand, flags=0):
+        """Whether sketch_into(operand, flags=flags) reads the bucket index
+        (dense kernels and the ordered / deterministic CSR kernels do; CSC
+        and the streaming CSR kernel read bucket / sign directly)."""
+        if isinstance(operand, DenseOperand):
+            return True
+        if operand.fmt == "csc":
+            return False
+        if operand.nnz > ORDERED_SPARSE_MAX_NNZ and flags & IDS_FLAG_ORDERED:
+            flags &= ~IDS_FLAG_ORDERED
+        if torch.are_deterministic_algorithms_enabled():
+            flags |= IDS_FLAG_DETERMINISTIC
+        return bool(flags & (IDS_FLAG_ORDERED | IDS_FLAG_DETERMINISTIC))
+
     def sketch_into(self, operand, y, row0=0, accumulate=False, flags=0, nonfinite=None):
         """Y (+)= S[:, row0:row0+rows] @ operand on the current stream.
 
@@ -409,7 +424,8 @@ def id_stream(dev=None):
     return st
 
 
-def pipelined_operators(in_dim, out_dim, seeds, surjective=False, depth=None, grid_cap=None):
+def pipelined_operators(in_dim, out_dim, seeds, surjective=False, depth=None, grid_cap=None,
+                        index=True):
     """CountSketchOps (hash + bucket index) for a sequence of trials, each
     drawn while earlier trials compute.
 
@@ -424,18 +440,28 @@ def pipelined_operators(in_dim, out_dim, seeds, surjective=False, depth=None, gr
     trial at depth 2 / 16 CTAs, against 2.54 ms for the sketch + ID alone;
     depth 1 leaves the cooperative resolution waiting for room beside the
     sketch (3.6 ms), deeper pipelines add more concurrent draws than help.
+    index=False skips the bucket index (operands whose sketch kernel reads
+    bucket / sign directly: CSC, streaming CSR).
     """
     seeds = list(seeds)
     if not seeds:
         return
     depth = PIPELINE_DEPTH if depth is None else int(depth)
     grid_cap = PIPELINE_GRID_CAP if grid_cap is None else int(grid_cap)
+    if depth == 0:  # no look-ahead: every draw in order on the current stream
+        for sd in seeds:
+            op = CountSketchOp(in_dim, out_dim, seed=sd, surjective=surjective)
+            if index:
+                op._bucket_index()
+            yield op
+        return
     dev = _device.device()
     main = torch.cuda.current_stream()
     sides = _side_streams(dev, max(depth, 1))
     lib = load()
     first = CountSketchOp(in_dim, out_dim, seed=seeds[0], surjective=surjective)
-    first._bucket_index()
+    if index:
+        first._bucket_index()
     pending = [(first, None)]
     nxt = 1
     for i in range(len(seeds)):
@@ -444,7 +470,8 @@ def pipelined_operators(in_dim, out_dim, seeds, surjective=False, depth=None, gr
             try:
                 with torch.cuda.stream(sides[nxt % len(sides)]):
                     op = CountSketchOp(in_dim, out_dim, seed=seeds[nxt], surjective=surjective)
-                    op._bucket_index()
+                    if index:
+                        op._bucket_index()
                     ev = torch.cuda.Event()
                     ev.record()
             finally:

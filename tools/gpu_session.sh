@@ -1,11 +1,11 @@
 #!/bin/bash
 # One GPU session: build check, tests (optionally filtered), smoke, bench.
-#   PYTEST_ARGS="-k config" BENCH_ARGS="--steps 10 --warmup 3" tools/gpu_session.sh
+#   PYTEST_K="config or cpqr" BENCH_ARGS="--steps 10 --warmup 3" tools/gpu_session.sh
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 { nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv; nproc; free -g; } > gpurun_out/env.txt 2>&1
 if [ -z "$SKIP_TESTS" ]; then
-  timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1
+  timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 ${PYTEST_K:+-k "$PYTEST_K"} ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1
   echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
   echo "smoke exit $?" >> gpurun_out/smoke.log
