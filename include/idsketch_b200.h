@@ -74,6 +74,12 @@ int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                          int surjective, int32_t* bucket, int8_t* sign,
                          int64_t* draws_out, void* workspace, size_t ws_bytes,
                          void* stream);
+/* ids_countsketch_hash with (state_hi, state_lo, inc_hi, inc_lo) read from
+ * DEVICE memory (uint64[4]) when the kernels run: a CUDA graph that captured
+ * the draw replays it for a new seed after a 32-byte copy into seed_dev. */
+int ids_countsketch_hash_dev(const uint64_t* seed_dev, int64_t in_dim, int64_t out_dim,
+                             int surjective, int32_t* bucket, int8_t* sign, int64_t* draws_out,
+                             void* workspace, size_t ws_bytes, void* stream);
 /* Concurrency hint for ids_countsketch_hash: cap the Fisher-Yates resolution
  * grid at `ctas` CTAs (0 = whole GPU) so that several hash draws issued on
  * different streams (independent trials) run side by side.  Process-wide;

@@ -11,6 +11,7 @@ there is no CPU fallback.
 
 from .cp_tensor import (
     CpTensor,
+    TensorIdGraph,
     TensorIdResult,
     check_tensor_id_args,
     cp_diff_norm,
@@ -54,6 +55,7 @@ __all__ = [
     "NormEstimate",
     "PivotedQr",
     "SingularTriangleError",
+    "TensorIdGraph",
     "TensorIdResult",
     "TensorSketchOp",
     "check_matrix_id_args",

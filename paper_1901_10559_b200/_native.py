@@ -34,6 +34,9 @@ SIGNATURES = {
         [_c_u64, _c_u64, _c_u64, _c_u64, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_sz,
          _c_p],
     ),
+    "ids_countsketch_hash_dev": (
+        _c_int, [_c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]
+    ),
     "ids_bucket_index_workspace_bytes": (_c_sz, [_c_i64, _c_i64]),
     "ids_bucket_index": (
         _c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]

@@ -212,6 +212,112 @@ def tensorsketch_id(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_T
     return _assemble(x, d.to_host("tensorsketch"), "tensorsketch")
 
 
+class TensorIdGraph:
+    """tensorsketch_id of one device-resident CP tensor, captured once as a
+    CUDA graph and replayed per seed (B200 extension; the reference has no
+    counterpart -- its calls are host-bound numpy).
+
+    Every kernel of the path -- the N per-mode hash draws (reading their
+    PCG64 states from device memory, ids_countsketch_hash_dev), bucket
+    indexes, scatter plans, the fused TensorSketch, the truncated CPQR and
+    the coefficients -- is recorded once; a call writes the seed's per-mode
+    states into a pinned buffer, copies them over (N x 32 bytes), replays the
+    graph and reads (j, P) back in one packed copy.  Results are identical
+    to tensorsketch_id on the same tensor and seed (same kernels, same
+    order).
+
+    factors: CUDA float64 I_n x R column-major (tensor.t() of an (R, I_n)
+    contiguous tensor) -- normalized CP factors, as CpTensor stores them;
+    weights: CUDA float64 (R,); host_weights: the same weights on the host
+    (new_weights = weights[cols] * coeffs.sum(axis=1), cp_tensor.py:216, is
+    formed in numpy, bit-identical to the reference)."""
+
+    def __init__(self, factors, weights, rank, sketch_dim=None, rank_tol=DEFAULT_RANK_TOL,
+                 host_weights=None):
+        import torch
+
+        from . import _device
+
+        self.factors = list(factors)
+        self.weights = weights
+        self.mode_dims = tuple(int(f.shape[0]) for f in self.factors)
+        self.R = int(self.factors[0].shape[1])
+
+        class _X:
+            pass
+
+        _X.rank = self.R
+        _X.total_entries = int(np.prod(self.mode_dims))
+        self.L = check_tensor_id_args(_X, rank, sketch_dim, "tensorsketch")
+        self.k, self.rank_tol = int(rank), float(rank_tol)
+        self.host_weights = (np.asarray(host_weights, dtype=np.float64) if host_weights is not None
+                             else weights.detach().cpu().numpy())
+        n = len(self.mode_dims)
+        self.seed_host = torch.empty((n, 4), dtype=torch.int64, pin_memory=True)
+        self.seed_dev = _device.empty((n, 4), torch.int64)
+        self.seed_host.numpy()[:] = TensorSketchOp.mode_seed_states(n, 0)
+        self.seed_dev.copy_(self.seed_host)
+        self._body()  # eager run: lazy initialization outside the capture
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
+            self.out = self._body()
+        self.host_out = torch.empty(self.out.shape, dtype=self.out.dtype, pin_memory=True)
+
+    def _body(self):
+        op = TensorSketchOp(self.mode_dims, self.L, _seed_dev=self.seed_dev)
+        y, nrm = op.apply_device(self.factors, self.weights, norms=True)
+        return device_matrix_id(y, self.L, self.R, self.k, self.rank_tol, colnorm2=nrm).packed()
+
+    def device(self, seed):
+        """Replay for `seed`; the packed (cols, numerical rank, deficient, P)
+        device vector (valid until the next replay)."""
+        import torch
+
+        self.seed_host.numpy()[:] = TensorSketchOp.mode_seed_states(len(self.mode_dims), seed)
+        self.seed_dev.copy_(self.seed_host, non_blocking=True)
+        self.graph.replay()
+        return self.out
+
+    def trials(self, seeds):
+        """[(InterpolativeDecomposition, new_weights)] for several seeds: one
+        copy of every seed's states, the replays back to back (each result
+        copied aside on the device), one device->host copy at the end."""
+        import torch
+
+        from . import _device
+        from .matrix_id import DeviceId
+
+        seeds = list(seeds)
+        if not seeds:
+            return []
+        n = len(self.mode_dims)
+        st = torch.from_numpy(np.stack([TensorSketchOp.mode_seed_states(n, s) for s in seeds]))
+        st_dev = st.pin_memory().to(self.seed_dev.device, non_blocking=True)
+        outs = []
+        for t in range(len(seeds)):
+            self.seed_dev.copy_(st_dev[t])
+            self.graph.replay()
+            outs.append(self.out.clone())
+        host = _device.to_host(torch.stack(outs))
+        res = []
+        for v in host:
+            d = DeviceId.unpack(v, self.k, self.R, "tensorsketch")
+            res.append((d, self.host_weights[d.cols] * d.coeffs.sum(axis=1)))
+        return res
+
+    def __call__(self, seed):
+        """(InterpolativeDecomposition of the sketch, new_weights) for `seed`."""
+        import torch
+
+        from .matrix_id import DeviceId
+
+        self.host_out.copy_(self.device(seed), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        d = DeviceId.unpack(self.host_out.numpy(), self.k, self.R, "tensorsketch")
+        return d, self.host_weights[d.cols] * d.coeffs.sum(axis=1)
+
+
 # ---- error metric for tensor trials (SURVEY.md 8f-3) --------------------------
 def _gram_device(weights, factor_lists):
     """diag(w) (hadamard of factor Grams) diag(w) on the device (cp_tensor.py:
@@ -253,6 +359,7 @@ def cp_diff_norm(x, y):
 
 __all__ = [
     "CpTensor",
+    "TensorIdGraph",
     "TENSOR_METHODS",
     "TensorIdResult",
     "check_tensor_id_args",

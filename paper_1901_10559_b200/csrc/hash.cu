@@ -80,10 +80,18 @@ struct DrawStream {
     }
 };
 
+// PCG64 (state, inc) of a draw: by value, or read from device memory (dev
+// non-NULL: {state_hi, state_lo, inc_hi, inc_lo}) so that a captured CUDA
+// graph replays the draw for a new seed without re-recording its kernels.
 struct Seed {
     uint64_t s_hi, s_lo, i_hi, i_lo;
-    __device__ u128 state() const { return ((u128)s_hi << 64) | s_lo; }
-    __device__ u128 inc() const { return ((u128)i_hi << 64) | i_lo; }
+    const uint64_t* dev;
+    __device__ u128 state() const {
+        return dev ? ((u128)__ldg(dev) << 64) | __ldg(dev + 1) : ((u128)s_hi << 64) | s_lo;
+    }
+    __device__ u128 inc() const {
+        return dev ? ((u128)__ldg(dev + 2) << 64) | __ldg(dev + 3) : ((u128)i_hi << 64) | i_lo;
+    }
 };
 
 __device__ __forceinline__ bool lemire_accept(uint32_t x, uint32_t L, uint32_t thresh,
@@ -944,11 +952,36 @@ extern "C" size_t ids_hash_workspace_bytes(int64_t in_dim, int64_t out_dim, int 
     return nc.off + 256;
 }
 
+static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                            uint64_t inc_lo, const uint64_t* seed_dev, int64_t in_dim,
+                            int64_t out_dim, int surjective, int32_t* bucket, int8_t* sign,
+                            int64_t* draws_out, void* workspace, size_t ws_bytes, void* stream);
+
 extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                                     uint64_t inc_lo, int64_t in_dim, int64_t out_dim,
                                     int surjective, int32_t* bucket, int8_t* sign,
                                     int64_t* draws_out, void* workspace, size_t ws_bytes,
                                     void* stream) {
+    return countsketch_hash(state_hi, state_lo, inc_hi, inc_lo, nullptr, in_dim, out_dim,
+                            surjective, bucket, sign, draws_out, workspace, ws_bytes, stream);
+}
+
+extern "C" int ids_countsketch_hash_dev(const uint64_t* seed_dev, int64_t in_dim, int64_t out_dim,
+                                        int surjective, int32_t* bucket, int8_t* sign,
+                                        int64_t* draws_out, void* workspace, size_t ws_bytes,
+                                        void* stream) {
+    if (!seed_dev) {
+        ids_set_last_error("hash: seed_dev is NULL");
+        return IDS_EINVAL;
+    }
+    return countsketch_hash(0, 0, 0, 0, seed_dev, in_dim, out_dim, surjective, bucket, sign,
+                            draws_out, workspace, ws_bytes, stream);
+}
+
+static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                            uint64_t inc_lo, const uint64_t* seed_dev, int64_t in_dim,
+                            int64_t out_dim, int surjective, int32_t* bucket, int8_t* sign,
+                            int64_t* draws_out, void* workspace, size_t ws_bytes, void* stream) {
     if (in_dim < 1 || out_dim < 1 || out_dim > 0x7fffffffLL || in_dim > 0x7ffffffeLL) {
         ids_set_last_error("hash: dimensions out of range");
         return IDS_EINVAL;
@@ -976,7 +1009,7 @@ extern "C" int ids_countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64
     }
     int64_t* d = draws_out ? draws_out : scal;
     IDS_CUDA_TRY(cudaMemsetAsync(d, 0, 4 * sizeof(int64_t), st));
-    Seed sd{state_hi, state_lo, inc_hi, inc_lo};
+    Seed sd{state_hi, state_lo, inc_hi, inc_lo, seed_dev};
     const uint32_t L = (uint32_t)out_dim;
     const uint32_t thresh = L > 1 ? (uint32_t)(0u - L) % L : 0u;
     int32_t* phaseA_out = surjective ? tail : bucket;

@@ -68,7 +68,7 @@ class CountSketchOp:
     at least one input row.
     """
 
-    def __init__(self, in_dim, out_dim, seed=None, surjective=False):
+    def __init__(self, in_dim, out_dim, seed=None, surjective=False, _seed_dev=None):
         if in_dim < 1 or out_dim < 1:
             raise ValueError("dimensions must be positive")
         if surjective and out_dim > in_dim:
@@ -81,19 +81,24 @@ class CountSketchOp:
         self._bucket_h = None
         self._sign_h = None
         self._index = None
-        state, inc = seed_state(seed)
         self._bucket_d = _device.empty(self.in_dim, torch.int32)
         self._sign_d = _device.empty(self.in_dim, torch.int8)
         self._draws = _device.empty(4, torch.int64)
         nbytes = query("ids_hash_workspace_bytes", self.in_dim, self.out_dim, int(self.surjective))
         ws = _device.workspace(nbytes)
-        sh, sl = _split(state)
-        ih, il = _split(inc)
-        call(
-            "ids_countsketch_hash", sh, sl, ih, il, self.in_dim, self.out_dim,
-            int(self.surjective), _device.ptr(self._bucket_d), _device.ptr(self._sign_d),
-            _device.ptr(self._draws), _device.ptr(ws), nbytes, _device.stream_ptr(),
-        )
+        tail = (self.in_dim, self.out_dim, int(self.surjective), _device.ptr(self._bucket_d),
+                _device.ptr(self._sign_d), _device.ptr(self._draws), _device.ptr(ws), nbytes,
+                _device.stream_ptr())
+        if _seed_dev is not None:
+            # (state_hi, state_lo, inc_hi, inc_lo) read by the kernels from
+            # device memory: the draw can be captured in a CUDA graph once and
+            # replayed for any seed (cp_tensor.TensorIdGraph)
+            call("ids_countsketch_hash_dev", _device.ptr(_seed_dev), *tail)
+        else:
+            state, inc = seed_state(seed)
+            sh, sl = _split(state)
+            ih, il = _split(inc)
+            call("ids_countsketch_hash", sh, sl, ih, il, *tail)
         self._checked = False
 
     @classmethod
@@ -339,20 +344,37 @@ class TensorSketchOp:
     """CountSketch whose hash and sign factor across tensor modes
     (reference sketch.py:128-207)."""
 
-    def __init__(self, mode_dims, out_dim, seed=None):
+    def __init__(self, mode_dims, out_dim, seed=None, _seed_dev=None):
         mode_dims = [int(d) for d in mode_dims]
         if len(mode_dims) == 0:
             raise ValueError("need at least one mode")
         if any(d < 1 for d in mode_dims) or out_dim < 1:
             raise ValueError("dimensions must be positive")
-        entropy = _seed_entropy(seed)
         self.mode_dims = tuple(mode_dims)
         self.out_dim = int(out_dim)
+        if _seed_dev is not None:  # device (N, 4) PCG64 states (see mode_seed_states)
+            self.seed = None
+            self.mode_ops = [CountSketchOp(d, out_dim, _seed_dev=_seed_dev[n])
+                             for n, d in enumerate(mode_dims)]
+            return
+        entropy = _seed_entropy(seed)
         self.seed = entropy
         self.mode_ops = [
             CountSketchOp(d, out_dim, seed=np.random.SeedSequence([entropy, n]))
             for n, d in enumerate(mode_dims)
         ]
+
+    @staticmethod
+    def mode_seed_states(n_modes, seed):
+        """int64 (n_modes, 4) host array: the (state_hi, state_lo, inc_hi,
+        inc_lo) words of mode n's PCG64, seeded SeedSequence([entropy, n])
+        (reference sketch.py:143-150), as ids_countsketch_hash_dev reads them."""
+        entropy = _seed_entropy(seed)
+        out = np.empty((n_modes, 4), dtype=np.uint64)
+        for n in range(n_modes):
+            state, inc = seed_state(np.random.SeedSequence([entropy, n]))
+            out[n] = (*_split(state), *_split(inc))
+        return out.view(np.int64)
 
     @property
     def in_dim(self):
