@@ -31,7 +31,8 @@ def _fortran_dev(a, pad_rows=0):
 
 @pytest.mark.parametrize("rows,cols,L", [
     (512, 8, 37), (513, 8, 37), (1, 3, 1), (1000, 5, 128), (3000, 333, 100),
-    (5001, 17, 1000), (2049, 300, 7)])
+    (5001, 17, 1000), (2049, 300, 7), (4096, 64, 33), (10240, 20, 128), (2112, 9, 97),
+    (1538, 8, 64), (20480, 600, 100)])
 @pytest.mark.parametrize("pad", [0, 1])
 def test_fortran_ordered_bit_exact(rows, cols, L, pad):
     rng = np.random.default_rng(rows * 7 + cols + L)
