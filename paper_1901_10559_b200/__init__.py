@@ -43,7 +43,12 @@ from .mmio import (
     save_cp_dir,
     write_matrix_market,
 )
-from .sketch import CountSketchOp, TensorSketchOp
+from .sketch import (
+    CountSketchOp,
+    NondeterministicSketchWarning,
+    TensorSketchOp,
+    set_sparse_sketch_mode,
+)
 
 __version__ = "0.1.0"
 
@@ -52,6 +57,7 @@ __all__ = [
     "CpTensor",
     "DEFAULT_RANK_TOL",
     "InterpolativeDecomposition",
+    "NondeterministicSketchWarning",
     "NormEstimate",
     "PivotedQr",
     "SingularTriangleError",
@@ -75,6 +81,7 @@ __all__ = [
     "read_matrix_market",
     "read_matrix_market_device",
     "save_cp_dir",
+    "set_sparse_sketch_mode",
     "tensor_id_from_sketch",
     "tensorsketch_id",
     "triangular_solve",

@@ -904,8 +904,25 @@ __global__ void id_scatter_kernel(const double* __restrict__ T, const int32_t* _
     }
 }
 
-__global__ void deficient_kernel(const int32_t* nr, int64_t k, int32_t* deficient) {
-    *deficient = (*nr < k) ? 1 : 0;
+// Flags of the decomposition: bit 0 = numerically rank deficient; bit 1 =
+// the solve met an exactly zero R11 diagonal (lead != 0, cols > k and a zero
+// floor: rank_tol == 0 or rank_tol * |r00| underflowing), where the
+// reference's triangular_solve raises SingularTriangleError (linalg.py:141-144)
+// -- the first such index in bits 2.. .
+__global__ void deficient_kernel(const int32_t* nr, const double* __restrict__ Rtop, int64_t k,
+                                 int64_t cols, double rank_tol, int32_t* deficient) {
+    const bool def = *nr < k;
+    int32_t out = def ? 1 : 0;
+    const double lead = fabs(Rtop[0]);
+    const double floorv = rank_tol * lead;
+    if (lead != 0.0 && cols > k && !(def && floorv > 0.0)) {
+        for (int64_t q = 0; q < k; ++q)
+            if (Rtop[q * cols + q] == 0.0) {
+                out |= 2 | (int32_t)(q << 2);
+                break;
+            }
+    }
+    *deficient = out;
 }
 
 // Generic triangular solve r x = b (reference dtrsm loop order), one thread
@@ -1151,7 +1168,7 @@ extern "C" int ids_id_coeffs_f64(const double* Rtop, const int32_t* perm, int64_
     id_scatter_kernel<<<g2, 256, 0, st>>>(T, perm, k, cols, P);
     IDS_LAUNCH_CHECK();
     if (deficient) {
-        deficient_kernel<<<1, 1, 0, st>>>(numerical_rank, k, deficient);
+        deficient_kernel<<<1, 1, 0, st>>>(numerical_rank, Rtop, k, cols, rank_tol, deficient);
         IDS_LAUNCH_CHECK();
     }
     return IDS_OK;

@@ -142,7 +142,10 @@ __global__ void __launch_bounds__(kGenThreads) lemire_count_kernel(Seed sd, int6
                                                                    uint32_t L, uint32_t thresh,
                                                                    int64_t* blk_cnt,
                                                                    const int32_t* rejected) {
-    if (*rejected == 0) return;
+    if (*rejected == 0) {  // fast path: the scan still reads blk_cnt, keep it defined
+        if (threadIdx.x == 0) blk_cnt[blockIdx.x] = 0;
+        return;
+    }
     typedef cub::BlockReduce<int, kGenThreads> BR;
     __shared__ typename BR::TempStorage tmp;
     const int64_t d0 = ((int64_t)blockIdx.x * kGenThreads + threadIdx.x) * kChunk;

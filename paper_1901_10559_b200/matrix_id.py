@@ -20,6 +20,7 @@ from . import _device
 from ._inputs import DenseOperand, SparseOperand, matrix_operand
 from ._native import IDS_FLAG_ORDERED, call, query
 from .linalg import DEFAULT_RANK_TOL, _check_finite_device, _col_major_device, device_cpqr
+from .errors import SingularTriangleError
 from .sketch import CountSketchOp
 
 MATRIX_METHODS = ("deterministic", "countsketch")
@@ -90,7 +91,10 @@ class DeviceId:
     @staticmethod
     def unpack(vec, rank, ncols, method):
         cols = vec[:rank].astype(np.int32)
-        nr, de = int(vec[rank]), bool(vec[rank + 1])
+        nr, flags = int(vec[rank]), int(vec[rank + 1])
+        if flags & 2:  # an exactly zero R11 diagonal reached the solve
+            raise SingularTriangleError(f"zero diagonal entry at index {flags >> 2}")
+        de = bool(flags & 1)
         coeffs = vec[rank + 2:rank + 2 + rank * ncols].reshape(rank, ncols).copy()
         return InterpolativeDecomposition(coeffs=coeffs, cols=cols, rank=rank, method=method,
                                           numerical_rank=nr, rank_deficient=de)

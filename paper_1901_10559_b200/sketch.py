@@ -27,6 +27,58 @@ _MAX_MATERIALIZE = 50_000_000  # sketch.py:30
 # torch.use_deterministic_algorithms -- splits each bucket into row segments
 # combined in a fixed order (run-to-run identical).
 ORDERED_SPARSE_MAX_NNZ = 1 << 24
+_SPARSE_MODES = ("auto", "ordered", "deterministic", "stream")
+_sparse_mode = "auto"
+_warned_stream = False
+
+
+class NondeterministicSketchWarning(UserWarning):
+    """The streaming CSR sketch sums each Y entry in L2 reductions whose
+    order varies run to run (Y within ~1e-16 relative of scipy's)."""
+
+
+def set_sparse_sketch_mode(mode):
+    """Summation order of the CSR CountSketch (the reference's scipy S @ A is
+    sequential and deterministic, sketch.py:116-122):
+
+    * "auto" (default): scipy's order bit for bit up to ORDERED_SPARSE_MAX_NNZ
+      nonzeros, the streaming kernel above (fast, not run-to-run identical;
+      a NondeterministicSketchWarning is issued once), or fixed-order
+      segments under torch.use_deterministic_algorithms(True);
+    * "ordered": scipy's order at any size (bucket-gather kernel, slower);
+    * "deterministic": fixed-order segments at any size (run-to-run identical);
+    * "stream": the streaming kernel at any size (no warning).
+    Returns the previous mode."""
+    global _sparse_mode
+    if mode not in _SPARSE_MODES:
+        raise ValueError(f"mode must be one of {_SPARSE_MODES}, got {mode!r}")
+    prev, _sparse_mode = _sparse_mode, mode
+    return prev
+
+
+def _sparse_flags(operand, flags):
+    """CSR flags after the sparse sketch mode (see set_sparse_sketch_mode)."""
+    global _warned_stream
+    if _sparse_mode == "ordered":
+        return (flags | IDS_FLAG_ORDERED) & ~IDS_FLAG_DETERMINISTIC
+    if _sparse_mode == "deterministic":
+        return (flags | IDS_FLAG_DETERMINISTIC) & ~IDS_FLAG_ORDERED
+    if _sparse_mode == "stream":
+        return flags & ~(IDS_FLAG_ORDERED | IDS_FLAG_DETERMINISTIC)
+    if operand.nnz > ORDERED_SPARSE_MAX_NNZ and flags & IDS_FLAG_ORDERED:
+        flags &= ~IDS_FLAG_ORDERED
+    if torch.are_deterministic_algorithms_enabled():
+        flags |= IDS_FLAG_DETERMINISTIC
+    if not flags & (IDS_FLAG_ORDERED | IDS_FLAG_DETERMINISTIC) and not _warned_stream:
+        import warnings
+
+        _warned_stream = True
+        warnings.warn(
+            f"CSR input with {operand.nnz} nonzeros is sketched by the streaming kernel: Y "
+            "matches scipy's to rounding but is not run-to-run identical; use "
+            "set_sparse_sketch_mode('ordered' or 'deterministic') for a fixed order",
+            NondeterministicSketchWarning, stacklevel=4)
+    return flags
 
 
 def _seed_entropy(seed):
@@ -251,6 +303,10 @@ class CountSketchOp:
             return True
         if operand.fmt == "csc":
             return False
+        if _sparse_mode == "ordered" or _sparse_mode == "deterministic":
+            return True
+        if _sparse_mode == "stream":
+            return False
         if operand.nnz > ORDERED_SPARSE_MAX_NNZ and flags & IDS_FLAG_ORDERED:
             flags &= ~IDS_FLAG_ORDERED
         if torch.are_deterministic_algorithms_enabled():
@@ -290,10 +346,7 @@ class CountSketchOp:
                 self.out_dim, _device.ptr(y), int(accumulate), nf, _device.ptr(ws), nbytes, st,
             )
         elif isinstance(operand, SparseOperand):
-            if operand.nnz > ORDERED_SPARSE_MAX_NNZ and flags & IDS_FLAG_ORDERED:
-                flags &= ~IDS_FLAG_ORDERED
-            if torch.are_deterministic_algorithms_enabled():
-                flags |= IDS_FLAG_DETERMINISTIC
+            flags = _sparse_flags(operand, flags)
             if flags & (IDS_FLAG_ORDERED | IDS_FLAG_DETERMINISTIC):
                 order, bstart = self.bucket_index()
             else:  # streaming pass: no bucket index needed

@@ -191,3 +191,37 @@ def test_c3_shaped_id_streamed_matches_oracle_error():
     e_got = np.linalg.norm(ad - ad[:, d.cols] @ d.coeffs) / np.linalg.norm(ad)
     e_want = np.linalg.norm(ad - ad[:, w.cols] @ w.coeffs) / np.linalg.norm(ad)
     assert e_got <= max(1.01 * e_want, 1e-12)
+
+
+def test_sparse_sketch_modes_above_ordered_threshold():
+    """Above ORDERED_SPARSE_MAX_NNZ: "auto" streams (one warning), "ordered"
+    keeps scipy's order bit for bit, "deterministic" is run-to-run identical."""
+    import warnings
+
+    from paper_1901_10559_b200 import sketch as sk
+
+    rng = np.random.default_rng(44)
+    rows, cols, per = 2_000_000, 3000, 9  # 1.8e7 nonzeros > 2^24
+    idx = np.sort(rng.integers(0, cols, size=(rows, per)), axis=1).astype(np.int32)
+    a = sp.csr_array((rng.standard_normal(rows * per), idx.ravel(),
+                      np.arange(0, rows * per + 1, per)), shape=(rows, cols))
+    a.sum_duplicates()
+    op = ids.CountSketchOp(rows, 50, seed=9, surjective=True)
+    want = oracle.cs_apply(op.bucket, op.sign, 50, a)
+    operand = _operand(a)
+    prev = ids.set_sparse_sketch_mode("auto")
+    try:
+        sk._warned_stream = False
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            y = _sketch(op, operand, IDS_FLAG_ORDERED)
+            _sketch(op, operand, IDS_FLAG_ORDERED)
+        assert sum(issubclass(x.category, ids.NondeterministicSketchWarning) for x in w) == 1
+        assert relerr_fro(y, want) <= 1e-13
+        ids.set_sparse_sketch_mode("ordered")
+        assert np.array_equal(_sketch(op, operand, 0), want)
+        ids.set_sparse_sketch_mode("deterministic")
+        y1, y2 = _sketch(op, operand, 0), _sketch(op, operand, 0)
+        assert np.array_equal(y1, y2) and relerr_fro(y1, want) <= 1e-13
+    finally:
+        ids.set_sparse_sketch_mode(prev)

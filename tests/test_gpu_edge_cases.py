@@ -83,3 +83,16 @@ def test_argument_errors():
     bad.data[0] = np.inf
     with pytest.raises(ValueError):
         ids.countsketch_id(bad, 1, 2)
+
+
+def test_rank_tol_zero_singular_triangle_raises():
+    """rank_tol = 0 leaves an exactly zero R11 diagonal unfloored; the
+    reference's triangular_solve then raises SingularTriangleError
+    (matrix_id.py:68-80, linalg.py:141-144) -- so does the device solve."""
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((60, 3)) @ rng.standard_normal((3, 9))
+    a[:, 3:] = 0.0  # rank 3 with 6 exactly zero columns: pivots 4.. have zero norm
+    with pytest.raises(ids.SingularTriangleError, match="index 3"):
+        ids.matrix_id(a, 5, rank_tol=0.0)
+    d = ids.matrix_id(a, 5)  # default rank_tol floors the zero diagonal instead
+    assert d.rank_deficient and np.all(np.isfinite(d.coeffs))

@@ -105,3 +105,12 @@ def test_check_tensor_id_args():
         check_tensor_id_args(x, 2, 25, "tensorsketch")
     with pytest.raises(ValueError):
         check_tensor_id_args(x, 2, 1, "tensorsketch")
+
+
+def test_sparse_sketch_mode_validation():
+    import paper_1901_10559_b200 as ids
+
+    prev = ids.set_sparse_sketch_mode("stream")
+    assert ids.set_sparse_sketch_mode(prev) == "stream"
+    with pytest.raises(ValueError):
+        ids.set_sparse_sketch_mode("fast")
