@@ -1,0 +1,31 @@
+#!/bin/bash
+# Round evidence for profiles/ (each ncu run only after the same command has
+# exited 0 without ncu):
+#   * ncu launch list of the headline bench command;
+#   * per-config launch lists of one full ID (tools/prof_config.py);
+#   * --set full captures of each config's dominant kernels.
+# Then: python tools/make_profiles.py r02  (here, after the gpurun merge).
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+L="--metrics gpu__time_duration.sum --clock-control none --csv"
+B="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-secondary"
+$B > gpurun_out/pf_bench_plain.log 2>&1 && \
+  ncu $L --log-file gpurun_out/pf_launches_bench.csv $B > gpurun_out/pf_ncu_bench.log 2>&1
+for w in C2 C3 C4 C5; do
+  python tools/prof_config.py --workload $w > gpurun_out/pf_plain_$w.log 2>&1 && \
+    ncu $L --log-file gpurun_out/pf_launches_$w.csv python tools/prof_config.py --workload $w \
+      > gpurun_out/pf_ncu_$w.log 2>&1
+done
+full() {  # $1 kernel regex, $2 report name, $3.. prof_config args
+  local k=$1 name=$2; shift 2
+  ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+      -o gpurun_out/pf_full_$name python tools/prof_config.py "$@" > gpurun_out/pf_ncu_full_$name.log 2>&1
+}
+full cs_rowmajor cs_rowmajor --workload C2
+full cs_coltile cs_coltile --workload C2 --fortran
+full cs_csr_stream cs_csr_stream --workload C3
+full fy_phaseb fy_phaseb_c3 --workload C3
+full tensorsketch_kernel tensorsketch_c4 --workload C4
+full tensorsketch_kernel tensorsketch_c5 --workload C5
+full "cpqr_kernel" cpqr_c5 --workload C5
+echo profiles done

@@ -72,32 +72,49 @@ def full(rep, dst, title):
     print("wrote", dst)
 
 
-if os.path.exists(os.path.join(OUT, "ev_launches_bench.csv")):
-    shutil.copy(os.path.join(OUT, "ev_launches_bench.csv"), os.path.join(PROF, f"{rnd}_bench_launches.csv"))
-    launches(os.path.join(OUT, "ev_launches_bench.csv"), os.path.join(PROF, f"{rnd}_bench_launches_summary.txt"),
-             "python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e (whole process: data "
-             "generation, warm-up, timed trials, roofline and phase timers)")
-for cfg, what in (("c2", "C2 countsketch_id, dense 1e6 x 2000, K=20, L=100"),
-                  ("c3", "C3 countsketch_id, CSR 1e7 x 1e4, nnz 1e8, K=20, L=200"),
-                  ("c4", "C4 tensorsketch_id, N=3, I=1000, R=1000, K=10, L=4096"),
-                  ("c5", "C5 tensorsketch_id, N=4, I=1e4, R=2000, K=20, L=16384")):
-    src = os.path.join(OUT, f"launches_{cfg}.csv")
+if os.path.exists(os.path.join(OUT, "pf_launches_bench.csv")):
+    shutil.copy(os.path.join(OUT, "pf_launches_bench.csv"), os.path.join(PROF, f"{rnd}_bench_launches.csv"))
+    launches(os.path.join(OUT, "pf_launches_bench.csv"), os.path.join(PROF, f"{rnd}_bench_launches_summary.txt"),
+             "python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-secondary (whole process: "
+             "data generation, warm-up, timed trials, roofline and phase timers)")
+for cfg, what in (("C2", "C2 countsketch_id, dense 1e6 x 2000, K=20, L=100"),
+                  ("C3", "C3 countsketch_id, CSR 1e7 x 1e4, ~1e8 nnz, K=20, L=200"),
+                  ("C4", "C4 tensorsketch_id, N=3, I=1000, R=1000, K=10, L=4096"),
+                  ("C5", "C5 tensorsketch_id, N=4, I=1e4, R=2000, K=20, L=16384")):
+    src = os.path.join(OUT, f"pf_launches_{cfg}.csv")
     if os.path.exists(src):
-        launches(src, os.path.join(PROF, f"{rnd}_step_launches_{cfg}.txt"),
-                 f"{what}: tools/prof_step.py (warm-up call + one step)")
-for rep, name, title in (("ev_rowmajor.ncu-rep", "cs_rowmajor", "cs_rowmajor_kernel<2,8>, C2 sketch"),
-                         ("full_tensorsketch_c5.ncu-rep", "tensorsketch_c5",
-                          "tensorsketch_kernel<16>, C5 (N=4, I=1e4, R=2000, L=16384)"),
-                         ("full_cpqr_c5.ncu-rep", "cpqr_c5", "cpqr_kernel, C5 sketch 16384 x 2000, k=20"),
-                         ("full_cs_coltile.ncu-rep", "cs_coltile",
-                          "cs_coltile_kernel, configs[1] shape in F order (1e6 x 2000, L=100)"),
-                         ("full_cs_csr_stream.ncu-rep", "cs_csr_stream",
-                          "cs_csr_stream_kernel, C3 (CSR 1e7 x 1e4, nnz 1e8, L=200)"),
-                         ("full_cs_csr_bucket.ncu-rep", "cs_csr_bucket",
-                          "cs_csr_bucket_kernel, C3 (CSR 1e7 x 1e4, nnz 1e8, L=200)"),
-                         ("full_fy_phaseb.ncu-rep", "fy_phaseb", "fy_phaseb_kernel, hash I=1e6, L=100"),
-                         ("full_cpqr_cluster.ncu-rep", "cpqr_cluster",
-                          "cpqr_cluster_kernel, C2 sketch 100 x 2000, k=20")):
+        launches(src, os.path.join(PROF, f"{rnd}_step_launches_{cfg.lower()}.txt"),
+                 f"{what}: tools/prof_config.py --workload {cfg} (warm-up call + one call)")
+traffic = {}
+for rep, name, title, key in (
+        ("pf_full_cs_rowmajor.ncu-rep", "cs_rowmajor", "cs_rowmajor_kernel, C2 sketch (C order)", "C2"),
+        ("pf_full_cs_coltile.ncu-rep", "cs_coltile", "cs_coltile_kernel, C2 in F order", None),
+        ("pf_full_cs_csr_stream.ncu-rep", "cs_csr_stream", "cs_csr_stream_kernel, C3", "C3"),
+        ("pf_full_fy_phaseb_c3.ncu-rep", "fy_phaseb_c3", "fy_phaseb_kernel, C3 hash (I = 1e7)", None),
+        ("pf_full_tensorsketch_c4.ncu-rep", "tensorsketch_c4", "tensorsketch_kernel<8>, C4", "C4"),
+        ("pf_full_tensorsketch_c5.ncu-rep", "tensorsketch_c5", "tensorsketch_kernel<16>, C5", "C5"),
+        ("pf_full_cpqr_c5.ncu-rep", "cpqr_c5", "cpqr_kernel, C5 sketch 16384 x 2000, k = 20", None)):
     p = os.path.join(OUT, rep)
     if os.path.exists(p):
         full(p, os.path.join(PROF, f"{rnd}_{name}_ncu_full.txt"), title)
+        if key:
+            raw = list(csv.reader(run(["ncu", "-i", p, "--page", "raw", "--csv"]).splitlines()))
+            hdr, units, vals = raw[0], raw[1], raw[2]
+            tot = 0.0
+            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                i = hdr.index(m)
+                tot += float(vals[i]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1)
+            traffic[key] = tot
+if traffic:
+    import json
+
+    tp = os.path.join(PROF, "traffic.json")
+    t = json.load(open(tp)) if os.path.exists(tp) else {}
+    t.update(traffic)
+    t.update({"C2_bytes": 16_000_000_000, "C3_bytes": 1_239_938_912, "C4_bytes": 24_000_000,
+              "C5_bytes": 640_000_000})
+    t["_source"] = (f"profiles/{rnd}_*_ncu_full.txt: dram__bytes_read.sum + dram__bytes_write.sum "
+                    "of one launch of each config's dominant kernel; <name>_bytes = the "
+                    "algorithmic bytes of that launch")
+    json.dump(t, open(tp, "w"), indent=1)
+    print("wrote", tp, traffic)
