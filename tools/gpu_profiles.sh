@@ -13,12 +13,14 @@ $B > gpurun_out/pf_bench_plain.log 2>&1 && \
   ncu $L --log-file gpurun_out/pf_launches_bench.csv $B > gpurun_out/pf_ncu_bench.log 2>&1
 for w in C2 C3 C4 C5; do
   python tools/prof_config.py --workload $w > gpurun_out/pf_plain_$w.log 2>&1 && \
-    ncu $L --log-file gpurun_out/pf_launches_$w.csv python tools/prof_config.py --workload $w \
+    ncu $L --profile-from-start off --log-file gpurun_out/pf_launches_$w.csv \
+      python tools/prof_config.py --workload $w \
       > gpurun_out/pf_ncu_$w.log 2>&1
 done
 full() {  # $1 kernel regex, $2 report name, $3.. prof_config args
   local k=$1 name=$2; shift 2
-  ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+  ncu --set full --clock-control none --import-source on --profile-from-start off \
+      -k regex:$k -s 1 -c 1 \
       -o gpurun_out/pf_full_$name python tools/prof_config.py "$@" > gpurun_out/pf_ncu_full_$name.log 2>&1
 }
 full cs_rowmajor cs_rowmajor --workload C2

@@ -29,6 +29,8 @@ if cfg["kind"] in ("dense", "csr"):
 
     a = (dense_operand(G.dense_config(args.workload, layout="F" if args.fortran else "C"))
          if cfg["kind"] == "dense" else G.csr_config(args.workload))
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()  # ncu --profile-from-start off: the ID calls only
     for s in range(args.steps + 1):
         d, _ = countsketch_device(a, cfg["k"], cfg["L"], seed=s, defer_check=True)
         d.to_host("countsketch")
@@ -43,7 +45,10 @@ else:
         mode_dims = tuple([cfg["dim"]] * cfg["modes"])
 
     wh = w.cpu().numpy()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
     for s in range(args.steps + 1):
         tensorsketch_id_sharded(X, 0, cfg["terms"], wh, cfg["k"], cfg["L"], seed=s)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok", args.workload)
