@@ -28,3 +28,16 @@ static std::atomic<long long> g_launches{0};
 void ids_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 extern "C" int64_t ids_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int ids_sm_count() {
+    static int sms = [] {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            return 148;  // B200
+        }
+        return n;
+    }();
+    return sms;
+}

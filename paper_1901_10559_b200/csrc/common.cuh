@@ -31,6 +31,10 @@ void ids_count_launch();
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// SM count of the current device (148 on B200), queried once per process:
+// the planners size grids and per-CTA workspaces from it.
+int ids_sm_count();
+
 template <class T>
 __host__ __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
 template <class T>

@@ -440,8 +440,10 @@ struct DensePlan {
     size_t smem;
 };
 
-constexpr int64_t kTargetWarps = 148 * 16;
-constexpr int64_t kMinWarps = 148 * 8;
+// warps wanted for a whole-GPU row-major launch (16 per SM) and the floor
+// below which rows are split into segments (8 per SM)
+static inline int64_t target_warps() { return (int64_t)ids_sm_count() * 16; }
+static inline int64_t min_warps() { return (int64_t)ids_sm_count() * 8; }
 
 DensePlan plan_dense(int64_t rows, int64_t cols, int64_t L, int layout, int flags,
                      bool aligned2, int64_t bucket_rows) {
@@ -452,18 +454,18 @@ DensePlan plan_dense(int64_t rows, int64_t cols, int64_t L, int layout, int flag
         p.vec = aligned2 ? 2 : 1;
         p.nchunks = (int)ceil_div(cols, 32 * p.vec);
         p.units = L * p.nchunks;
-        if (!(flags & IDS_FLAG_ORDERED) && p.units < kMinWarps) {
-            int64_t ns = ceil_div(kTargetWarps, p.units);
+        if (!(flags & IDS_FLAG_ORDERED) && p.units < min_warps()) {
+            int64_t ns = ceil_div(target_warps(), p.units);
             const int64_t cap = tmax<int64_t>(1, bucket_rows / 256);
             p.nseg = (int)tmax<int64_t>(1, tmin<int64_t>(ns, cap));
         }
         p.units *= p.nseg;
     } else {
-        p.nc = cols >= 2 * kTargetWarps ? 2 : 1;
+        p.nc = cols >= 2 * target_warps() ? 2 : 1;
         p.ngroups = (int)ceil_div(cols, p.nc);
         p.units = p.ngroups;
-        if (!(flags & IDS_FLAG_ORDERED) && p.units < kMinWarps) {
-            int64_t ns = ceil_div(kTargetWarps, p.units);
+        if (!(flags & IDS_FLAG_ORDERED) && p.units < min_warps()) {
+            int64_t ns = ceil_div(target_warps(), p.units);
             const int64_t cap = tmax<int64_t>(1, rows / 1024);
             p.nseg = (int)tmax<int64_t>(1, tmin<int64_t>(ns, cap));
         }
@@ -498,10 +500,11 @@ ColTilePlan plan_coltile(int64_t rows, int64_t cols, int64_t L, int flags) {
     p.use = p.smem <= 200 * 1024 && L < (1 << 21);
     p.ntiles = ceil_div(rows, kTT);
     // whole waves of two CTAs per SM when the columns allow it
-    p.ngroups = (int)tmax<int64_t>(ceil_div(cols, kCt), tmin<int64_t>(cols, 2 * 148));
+    const int64_t wave = 2 * (int64_t)ids_sm_count();  // two CTAs per SM
+    p.ngroups = (int)tmax<int64_t>(ceil_div(cols, kCt), tmin<int64_t>(cols, wave));
     p.nseg = 1;
-    if (!(flags & IDS_FLAG_ORDERED) && p.ngroups < 2 * 148)
-        p.nseg = (int)tmax<int64_t>(1, tmin<int64_t>(ceil_div(2 * 148, p.ngroups), p.ntiles / 4));
+    if (!(flags & IDS_FLAG_ORDERED) && p.ngroups < wave)
+        p.nseg = (int)tmax<int64_t>(1, tmin<int64_t>(ceil_div(wave, p.ngroups), p.ntiles / 4));
     return p;
 }
 

@@ -929,7 +929,8 @@ extern "C" size_t ids_tensorsketch_workspace_bytes(int n_modes, const int64_t* d
     (void)ncols;
     if (n_modes < 1 || out_dim < 1) return 256;
     const TsPlan p = plan_ts(n_modes, out_dim);
-    return (size_t)p.M * sizeof(double2) + 148 * 2 * (size_t)(p.N2 + 1) * sizeof(double2) + 1024;
+    return (size_t)p.M * sizeof(double2) +
+           (size_t)ids_sm_count() * 2 * (size_t)(p.N2 + 1) * sizeof(double2) + 1024;
 }
 
 extern "C" size_t ids_ts_mode_plan_bytes(int64_t dim) {
@@ -997,7 +998,9 @@ extern "C" int ids_tensorsketch_planned_f64(int n_modes, const double* const* fa
     cudaStream_t st = as_stream(stream);
     WsCarve ws(workspace, ws_bytes);
     double2* tw = ws.take<double2>(p.M);
-    double2* specg = p.spec_in_smem ? nullptr : ws.take<double2>((size_t)148 * 2 * (p.N2 + 1));
+    // one running-spectrum slice per resident CTA (at most two per SM)
+    double2* specg = p.spec_in_smem ? nullptr
+                                    : ws.take<double2>((size_t)ids_sm_count() * 2 * (p.N2 + 1));
     if (!ws.ok()) {
         ids_set_last_error("tensorsketch: workspace too small");
         return IDS_EWORKSPACE;
@@ -1038,7 +1041,7 @@ extern "C" int ids_tensorsketch_planned_f64(int n_modes, const double* const* fa
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, p.threads, p.smem);
     if (per_sm < 1) per_sm = 1;
     int64_t cap = (int64_t)sms * per_sm;
-    if (!p.spec_in_smem) cap = tmin<int64_t>(cap, 148 * 2);
+    if (!p.spec_in_smem) cap = tmin<int64_t>(cap, (int64_t)ids_sm_count() * 2);
     const int64_t grid = tmin<int64_t>(ncols, cap);
     kern<<<(unsigned)grid, p.threads, p.smem, st>>>(a);
     IDS_LAUNCH_CHECK();

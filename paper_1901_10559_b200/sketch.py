@@ -92,11 +92,48 @@ def _seed_entropy(seed):
 
 def seed_state(seed):
     """The (state, inc) of the fresh PCG64 that ``np.random.default_rng(seed)``
-    builds (sketch.py:77): SeedSequence hashing is numpy's own host code."""
+    builds (sketch.py:77): SeedSequence hashing is numpy's own host code.  A
+    Generator seed (default_rng returns it as is) starts at its current state
+    (see _generator_state)."""
     if isinstance(seed, np.random.Generator):
-        raise TypeError("pass an int or SeedSequence seed (Generator state is not replayable)")
+        return _generator_state(seed)
     st = np.random.PCG64(seed).state["state"]
     return int(st["state"]), int(st["inc"])
+
+
+def _generator_state(gen):
+    """(state, inc) of a PCG64-backed Generator passed as seed.  The device
+    draws start at a 64-bit boundary, so a pending 32-bit half (left by an
+    odd number of earlier 32-bit draws) is not supported."""
+    bg = gen.bit_generator
+    if not isinstance(bg, np.random.PCG64):
+        raise TypeError(f"Generator seeds must use PCG64 (numpy's default), got "
+                        f"{type(bg).__name__}")
+    st = bg.state
+    if st["has_uint32"]:
+        raise ValueError("Generator holds a pending 32-bit half-draw; draw an even number of "
+                         "32-bit values first or pass an int / SeedSequence seed")
+    return int(st["state"]["state"]), int(st["state"]["inc"])
+
+
+def _advance_generator(gen, n32):
+    """Leave `gen` where numpy's own draws of n32 32-bit values would: past
+    ceil(n32 / 2) PCG64 outputs, the high half of the last one pending when
+    n32 is odd."""
+    bg = gen.bit_generator
+    n64 = (int(n32) + 1) // 2
+    if n64 == 0:
+        return
+    probe = np.random.PCG64()
+    probe.state = bg.state
+    probe.advance(n64 - 1)
+    last = int(probe.random_raw())
+    st = probe.state
+    if n32 % 2:
+        st["has_uint32"], st["uinteger"] = 1, last >> 32
+    else:
+        st["has_uint32"], st["uinteger"] = 0, 0
+    bg.state = st
 
 
 def _split(v):
@@ -152,6 +189,9 @@ class CountSketchOp:
             ih, il = _split(inc)
             call("ids_countsketch_hash", sh, sl, ih, il, *tail)
         self._checked = False
+        if isinstance(seed, np.random.Generator):
+            # default_rng(gen) draws from gen itself (sketch.py:77): advance it
+            _advance_generator(seed, sum(self.draws))
 
     @classmethod
     def from_arrays(cls, bucket, sign, out_dim=None):

@@ -96,3 +96,25 @@ def test_rank_tol_zero_singular_triangle_raises():
         ids.matrix_id(a, 5, rank_tol=0.0)
     d = ids.matrix_id(a, 5)  # default rank_tol floors the zero diagonal instead
     assert d.rank_deficient and np.all(np.isfinite(d.coeffs))
+
+
+@pytest.mark.parametrize("I,L,surj,pre", [(5000, 37, True, 0), (3001, 64, False, 2),
+                                          (999, 5, True, 3)])
+def test_generator_seed_draws_and_advances_like_numpy(I, L, surj, pre):
+    """default_rng(gen) draws from gen itself (reference sketch.py:77): same
+    bucket / sign as numpy's draws, and gen left where numpy leaves it."""
+    g1 = np.random.default_rng(1234)
+    g2 = np.random.default_rng(1234)
+    for g in (g1, g2):  # an even number of 32-bit draws already taken
+        g.integers(0, 7, size=2 * pre, dtype=np.int32)
+    rng = np.random.default_rng(g2)
+    if surj:
+        tail = rng.integers(0, L, size=I - L)
+        want_b = rng.permutation(np.concatenate([np.arange(L, dtype=np.int64), tail]))
+    else:
+        want_b = rng.integers(0, L, size=I)
+    want_s = rng.integers(0, 2, size=I).astype(np.float64) * 2.0 - 1.0
+    op = ids.CountSketchOp(I, L, seed=g1, surjective=surj)
+    assert np.array_equal(op.bucket, want_b) and np.array_equal(op.sign, want_s)
+    assert np.array_equal(g1.integers(0, 2**31, size=9), g2.integers(0, 2**31, size=9))
+    assert g1.bit_generator.state == g2.bit_generator.state
