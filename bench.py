@@ -602,6 +602,9 @@ def measure(ctx, wl, steps, warmup, args, headline):
     n0 = lib.ids_launch_count()
     ms = ctx.events(lambda i: wl.trials([1000 + s for s in range(steps)]), 1) / steps
     launches = (lib.ids_launch_count() - n0) // max(steps, 1)
+    if getattr(wl, "graph", None) is not None:
+        # graph replays launch the captured library kernels without host calls
+        launches += wl.graph.launches
     ms = ctx.max_over_ranks(ms)
     clk = None
     if headline:
@@ -646,9 +649,7 @@ def measure(ctx, wl, steps, warmup, args, headline):
                "wall_s": time.perf_counter() - t0}
         del host
 
-    cpu = parity = None
-    if ctx.world == 1 and not args.no_cpu:
-        cpu, parity = wl.cpu_and_parity(RefCPU(), args.cpu_rows)
+    cpu = parity = None  # filled by cpu_legs() after every GPU timing
 
     out = {"value": wl.bytes_total / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
            "id_seconds": single_ms * 1e-3, "phases_ms": dict(
@@ -659,6 +660,20 @@ def measure(ctx, wl, steps, warmup, args, headline):
     if clk is not None:
         out["clocks"] = clk
     return out
+
+
+def cpu_legs(ctx, wls, results, args):
+    """CPU baselines and parity, after every GPU timing of the run: the
+    reference's BLAS / scipy threads stay busy for a while after they
+    return, which would inflate the host-side launch times of anything
+    timed next."""
+    if ctx.world != 1 or args.no_cpu:
+        return
+    ref = RefCPU()
+    for name, wl in wls.items():
+        cpu, parity = wl.cpu_and_parity(ref, args.cpu_rows)
+        results[name]["cpu_baseline"] = cpu
+        results[name]["parity"] = parity
 
 
 def traffic_of(name, nbytes):
@@ -707,21 +722,21 @@ def main():
     from paper_1901_10559_b200 import _native
 
     _native.load()
-    wl = make_workload(ctx, args.workload)
-    head = measure(ctx, wl, args.steps, args.warmup, args, headline=True)
-    del wl
-    torch.cuda.empty_cache()
-
+    wls, results = {}, {}
+    wls[args.workload] = make_workload(ctx, args.workload)
+    head = results[args.workload] = measure(ctx, wls[args.workload], args.steps, args.warmup, args,
+                                            headline=True)
     secondary = None
     if not args.no_secondary:
         secondary = {}
         for name in ("C2", "C3", "C4", "C5"):
             if name == args.workload:
                 continue
-            w2 = make_workload(ctx, name)
-            secondary[name] = measure(ctx, w2, 6, 3, args, headline=False)
-            del w2
-            torch.cuda.empty_cache()
+            wls[name] = make_workload(ctx, name)
+            secondary[name] = results[name] = measure(ctx, wls[name], 6, 3, args, headline=False)
+    cpu_legs(ctx, wls, results, args)
+    del wls
+    torch.cuda.empty_cache()
 
     if rank == 0:
         line = {

@@ -260,8 +260,11 @@ class TensorIdGraph:
         self._body()  # eager run: lazy initialization outside the capture
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
+        lib = _device.lib()
+        n0 = lib.ids_launch_count()
         with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
             self.out = self._body()
+        self.launches = int(lib.ids_launch_count() - n0)  # library kernels per replay
         self.host_out = torch.empty(self.out.shape, dtype=self.out.dtype, pin_memory=True)
 
     def _body(self):
