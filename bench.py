@@ -384,6 +384,7 @@ class MatrixWorkload:
                                                       flags=flags), reps)
         from paper_1901_10559_b200.matrix_id import device_matrix_id
 
+        device_matrix_id(y, self.L, self.cols, self.k)
         id_ms = self.ctx.events(lambda i: device_matrix_id(y, self.L, self.cols, self.k), reps)
         hash_ms = self.ctx.events(lambda i: ids.CountSketchOp(
             self.rows, self.L, seed=100 + i, surjective=True).bucket_index(), reps)
@@ -507,6 +508,7 @@ class TensorWorkload:
         y = op.apply_device(self.f_local, self.w_local)
         ms = self.ctx.events(lambda i: op.apply_device(self.f_local, self.w_local), reps)
         n_loc = self.c1 - self.c0
+        device_matrix_id(y, self.L, n_loc, self.k)
         id_ms = self.ctx.events(lambda i: device_matrix_id(y, self.L, n_loc, self.k), reps)
         return ms, self.bytes_local, {"cpqr_and_coeffs_local_block": id_ms,
                                       "flops_per_launch": self.flops_local,
