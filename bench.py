@@ -37,6 +37,14 @@ import subprocess
 import sys
 import time
 
+_REF_ARM = "--impl=reference" in sys.argv or any(
+    a == "--impl" and b == "reference" for a, b in zip(sys.argv, sys.argv[1:]))
+if _REF_ARM and "TORCHELASTIC_RUN_ID" in os.environ and os.environ.get("OMP_NUM_THREADS") == "1":
+    # torch.distributed.run pins OMP_NUM_THREADS=1 in every rank; the
+    # reference arm's rank 0 is a CPU job that should use the host's cores
+    # (LAPACK / OpenBLAS read it when numpy loads, just below)
+    del os.environ["OMP_NUM_THREADS"]
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
