@@ -235,3 +235,35 @@ def test_column_distributed_cpqr_local_shards():
 
 if __name__ == "__main__":  # pragma: no cover
     pytest.main([__file__, "-q"])
+
+
+def _entropy_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1901_10559_b200.distributed import _agreed_entropy
+
+        sub = dist.new_group([1, 0][:world])  # a subgroup: src must be a GLOBAL rank
+        vals = [_agreed_entropy(None), _agreed_entropy(sub)]
+        # seed=None: every rank draws the same hash (fresh entropy agreed on)
+        rng = np.random.default_rng(3)
+        a = rng.standard_normal((500, 6)) @ rng.standard_normal((6, 40))
+        r0, r1 = row_block(500, world, rank)
+        d = countsketch_id_sharded(a[r0:r1], r0, 500, 6, 20, seed=None, backend=OracleBackend())
+        try:
+            cpqr_columns_sharded(torch.zeros((3, 20), dtype=torch.float64), 5, 40, 2,
+                                 backend=OracleBackend())
+            bad_split = False
+        except ValueError:
+            bad_split = True
+        out[rank] = (vals, d.cols.tolist(), bad_split)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_seed_none_agreement_and_split_check_gloo():
+    out = _run(_entropy_worker)
+    assert out[0][0] == out[1][0]  # same entropy on every rank, default and subgroup
+    assert out[0][1] == out[1][1]  # same hash -> same decomposition
+    assert out[0][2] and out[1][2]  # a column block off the row_block split is rejected
