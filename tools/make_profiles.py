@@ -1,12 +1,12 @@
 """Summaries for profiles/ from the ncu outputs of a gpurun (gpurun_out/).
 
-usage: python tools/make_profiles.py ROUND   (e.g. r01)
+usage: python tools/make_profiles.py ROUND   (e.g. r02), after tools/gpu_profiles.sh ran on the box
 
 Writes, when the inputs exist:
   profiles/ROUND_bench_launches.csv          ncu launch list of the bench command
   profiles/ROUND_bench_launches_summary.txt  per-kernel counts / mean / total
   profiles/ROUND_step_launches_cN.txt        one countsketch_id / tensorsketch_id
-                                             step per config (tools/prof_step.py)
+                                             call per config (tools/prof_config.py)
   profiles/ROUND_<kernel>_ncu_full.txt       key metrics + top stall lines of the
                                              --set full captures
 """
@@ -19,7 +19,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
-rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r02"
 
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
