@@ -68,21 +68,36 @@ def tensorsketch_device(op, factors, weights=None, norms=False):
             w = torch.from_numpy(wn).to(_device.device())
         if tuple(w.shape) != (ncols,):
             raise ValueError(f"weights must have length {ncols}, got {tuple(w.shape)}")
-    dev_f = [factor_to_device(f) for f in factors]
-    n = len(dev_f)
+    n = len(factors)
     L = op.out_dim
     if not query("ids_tensorsketch_fused_ok", n, L):
-        y = _tensorsketch_spectral(op, dev_f, w, ncols, L)
+        y = _tensorsketch_spectral(op, factors, w, ncols, L)
         return (y, None) if norms else y
-    idx = [m._bucket_index() for m in op.mode_ops]
+    # Sparse (CSC) factors are never densified: their mode's CountSketch is
+    # taken straight from the CSC arrays by the ordered CSC kernel (scipy's
+    # order, bit for bit), giving an L x R dense "factor" that the fused
+    # kernel then reads through the identity hash of length L -- the same
+    # values enter the same FFT as on the dense path (reference sketch.py:175,
+    # where scipy sketches the CSC factor directly).
+    mode_ops, dev_f = [], []
+    for m, f in zip(op.mode_ops, factors):
+        if sp.issparse(f):
+            from ._inputs import sparse_operand
+
+            dev_f.append(m.apply_device(sparse_operand(sp.csc_array(f, dtype=np.float64))))
+            mode_ops.append(_identity_op(L))
+        else:
+            dev_f.append(factor_to_device(f))
+            mode_ops.append(m)
+    idx = [m._bucket_index() for m in mode_ops]
     # scatter plans pay off on long factor columns; short modes (C4: 1000
     # rows) keep the gather path rather than pay the plan's launches per draw
     plans = (ctypes.c_void_p * n)(*[_device.ptr(m._ts_plan()) if m.in_dim >= SCATTER_MIN_DIM
-                                    else None for m in op.mode_ops])
+                                    else None for m in mode_ops])
     fac_p = (ctypes.c_void_p * n)(*[_device.ptr(t) for t in dev_f])
     ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _, _ in idx])
     key_p = (ctypes.c_void_p * n)(*[_device.ptr(k) for _, _, k in idx])
-    dims = (ctypes.c_int64 * n)(*[int(d) for d in op.mode_dims])
+    dims = (ctypes.c_int64 * n)(*[int(m.in_dim) for m in mode_ops])
     lds = (ctypes.c_int64 * n)(*[int(t.shape[1]) for t in dev_f])
     y = _device.empty((ncols, L), torch.float64)
     nrm = _device.empty(max(ncols, 1), torch.float64)[:ncols] if norms else None
@@ -101,18 +116,36 @@ def tensorsketch_device(op, factors, weights=None, norms=False):
     return (y, nrm) if norms else y
 
 
-def _tensorsketch_spectral(op, dev_f, w, ncols, L):
+_IDENTITY_OPS = {}
+
+
+def _identity_op(L):
+    """CountSketch with bucket = row and sign = +1 on L rows (cached per L and
+    device, with its bucket index and scatter plan)."""
+    key = (int(L), torch.cuda.current_device())
+    op = _IDENTITY_OPS.get(key)
+    if op is None:
+        from .sketch import CountSketchOp
+
+        op = _IDENTITY_OPS[key] = CountSketchOp.from_arrays(np.arange(L), np.ones(L), out_dim=L)
+    return op
+
+
+def _tensorsketch_spectral(op, factors, w, ncols, L):
     """Transforms longer than the fused kernel holds in shared memory
     (sketch.py:170-186 step by step): each mode's CountSketch S_n A_n with the
-    dense kernel (bit-exact, scipy's order), then length-L rfft / irfft
+    dense or CSC kernel (bit-exact, scipy's order), then length-L rfft / irfft
     through cuFFT with the spectra multiplied left to right, weights applied
     after the inverse -- the reference's own sequence of operations."""
-    from ._inputs import dense_operand
+    from ._inputs import dense_operand, sparse_operand
     from ._native import IDS_FLAG_ORDERED
 
     spec = None
-    for mode, f in zip(op.mode_ops, dev_f):  # f: (R, I_n) == col-major I_n x R
-        y = mode.apply_device(dense_operand(f.t()), flags=IDS_FLAG_ORDERED)
+    for mode, f in zip(op.mode_ops, factors):
+        if sp.issparse(f):  # CSC sketch straight from the sparse arrays
+            y = mode.apply_device(sparse_operand(sp.csc_array(f, dtype=np.float64)))
+        else:  # (R, I_n) == col-major I_n x R
+            y = mode.apply_device(dense_operand(factor_to_device(f).t()), flags=IDS_FLAG_ORDERED)
         s = torch.fft.rfft(y, n=L, dim=1)
         spec = s if spec is None else spec.mul_(s)
     y = torch.fft.irfft(spec, n=L, dim=1).contiguous()

@@ -311,3 +311,25 @@ def test_colnorm_epilogue_feeds_cpqr():
     assert float((a.rtop - b.rtop).abs().max() / a.rtop.abs().max()) <= 1e-12
     want = oracle.cpqr(y.t().cpu().numpy(), 12)
     assert np.array_equal(b.perm[:12].cpu().numpy(), want.perm[:12])
+
+
+@pytest.mark.parametrize("L", [64, 4096, 16384, 20000])
+def test_sparse_factors_native_path_matches_dense(L):
+    """CSC factors are CountSketched from their sparse arrays (never
+    densified): the sketch is bit-identical to the same factors passed dense
+    (fused kernel, L <= 16384) or agrees to rounding (spectral route), and
+    matches the oracle (reference sketch.py:175 sketches CSC directly)."""
+    rng = np.random.default_rng(L)
+    dims = [5000, 300, 7000]
+    fs = [sp.random_array((d, 12), density=0.02, rng=rng, format="csc") for d in dims]
+    fs[1] = fs[1].toarray()  # mixed: one dense mode
+    lam = rng.random(12) + 0.5
+    op = ids.TensorSketchOp(dims, L, seed=4)
+    y_sparse = op.apply(fs, lam)
+    y_dense = op.apply([f.toarray() if sp.issparse(f) else f for f in fs], lam)
+    if L <= 16384:
+        assert np.array_equal(y_sparse, y_dense)
+    else:
+        assert relerr_fro(y_sparse, y_dense) <= 1e-14
+    want = oracle.OracleTensorSketch(dims, L, seed=4).apply(fs, lam)
+    assert relerr_fro(y_sparse, want) <= 1e-12
