@@ -23,7 +23,33 @@ TENSOR_METHODS = ("tensorsketch",)
 _MAX_DENSE_ENTRIES = 50_000_000
 
 
+def _is_cuda(f):
+    import torch
+
+    return isinstance(f, torch.Tensor) and f.device.type == "cuda"
+
+
+def _fortran_cuda(t):
+    """CUDA float64 I x R tensor in column-major layout (a view of an
+    (R, I) contiguous tensor), the layout the TensorSketch kernel reads."""
+    import torch
+
+    t = t.to(torch.float64)
+    return t if t.t().is_contiguous() else t.t().contiguous().t()
+
+
 def _canon_factor(f, n):
+    if _is_cuda(f):  # device-resident factor (B200 extension): stays in HBM
+        import torch
+
+        if f.dim() != 2:
+            raise ValueError(f"factor {n} must be 2-D, got ndim={f.dim()}")
+        if f.numel() == 0:
+            raise ValueError(f"factor {n} must be nonempty")
+        out = _fortran_cuda(f)
+        if not bool(torch.isfinite(out).all()):
+            raise ValueError(f"factor {n} contains non-finite entries")
+        return out
     if sp.issparse(f):
         out = sp.csc_array(f, dtype=np.float64)
         out.sum_duplicates()
@@ -43,12 +69,20 @@ def _canon_factor(f, n):
 
 
 def _col_norms(f):
+    if _is_cuda(f):
+        import torch
+
+        return torch.linalg.vector_norm(f, dim=0).cpu().numpy()
     if sp.issparse(f):
         return np.sqrt(np.asarray(f.power(2).sum(axis=0)).ravel())
     return np.linalg.norm(f, axis=0)
 
 
 def _scaled(f, scale):
+    if _is_cuda(f):
+        import torch
+
+        return _fortran_cuda(f * torch.from_numpy(np.asarray(scale, np.float64)).to(f.device))
     if sp.issparse(f):
         out = sp.csc_array(f @ sp.diags_array(scale), dtype=np.float64)
         out.sum_duplicates()
@@ -60,6 +94,11 @@ def _scaled(f, scale):
 
 def _unit_columns(f, cols):
     """Replace zero columns by e_0 (cp_tensor.py:131-141)."""
+    if _is_cuda(f):
+        f = f.clone()
+        f[:, cols] = 0.0
+        f[0, cols] = 1.0
+        return _fortran_cuda(f)
     if sp.issparse(f):
         lil = f.tolil()
         for c in cols:
@@ -74,7 +113,9 @@ def _unit_columns(f, cols):
 
 class CpTensor:
     """CP tensor: nonnegative `weights` (R) and one unit-column factor per mode
-    (cp_tensor.py:41-95).  Norms and the sign that keeps weights nonnegative
+    (cp_tensor.py:41-95).  Factors may be numpy, scipy sparse, or (B200
+    extension) CUDA tensors, which are normalized on the device and stay in
+    HBM: tensorsketch_id then reads them without a host round trip.  Norms and the sign that keeps weights nonnegative
     (applied to mode 0) are folded into the weights; zero columns get weight 0
     and an arbitrary unit vector.  Columns already unit to 1e-12 are kept bit
     for bit, so selecting terms is an exact column-subset operation."""
@@ -131,16 +172,25 @@ class CpTensor:
 
     def select(self, cols, weights):
         """CP tensor built from the given term indices and new weights."""
-        return CpTensor(weights, [f[:, cols] for f in self.factors])
+        sel = []
+        for f in self.factors:
+            if _is_cuda(f):
+                import torch
+
+                sel.append(f[:, torch.as_tensor(np.asarray(cols, np.int64), device=f.device)])
+            else:
+                sel.append(f[:, cols])
+        return CpTensor(weights, sel)
 
     def to_dense(self, max_entries=_MAX_DENSE_ENTRIES):
         """Materialize the full tensor (testing and small problems only)."""
         if self.total_entries > max_entries:
             raise ValueError("tensor too large to densify")
         out = np.zeros(self.mode_dims)
+        host = [f.cpu().numpy() if _is_cuda(f) else f for f in self.factors]
         for r in range(self.rank):
             term = np.array(self.weights[r])
-            for f in self.factors:
+            for f in host:
                 col = f[:, [r]].toarray().ravel() if sp.issparse(f) else f[:, r]
                 term = np.multiply.outer(term, col)
             out += term

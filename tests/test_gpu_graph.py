@@ -50,3 +50,35 @@ def test_tensor_id_graph_trials():
         want = ids.tensorsketch_id(x, cfg["k"], cfg["L"], seed=s)
         assert np.array_equal(d.cols, want.cols) and np.array_equal(d.coeffs, want.coeffs)
         assert np.array_equal(nw, want.new_weights)
+
+
+def test_device_cp_tensor_matches_host():
+    """CpTensor over CUDA factors (normalized on the device, kept in HBM):
+    tensorsketch_id gives the host path's results (bit-identical for unit
+    columns, 1e-13 when the device rescales), the reduced tensor stays on the
+    device, and the sign fix / zero columns follow cp_tensor.py:52-95."""
+    rng = np.random.default_rng(8)
+    w, facs = G.cp_config("C4")
+    xh = ids.CpTensor(w.cpu().numpy(), [f.cpu().numpy() for f in facs])
+    xd = ids.CpTensor(w.cpu().numpy(), facs)
+    assert all(f.is_cuda and f.t().is_contiguous() for f in xd.factors)
+    a = ids.tensorsketch_id(xh, 10, 4096, seed=2)
+    b = ids.tensorsketch_id(xd, 10, 4096, seed=2)
+    assert np.array_equal(a.cols, b.cols) and np.array_equal(a.coeffs, b.coeffs)
+    assert np.array_equal(a.new_weights, b.new_weights)
+    assert b.reduced.factors[0].is_cuda
+    assert ids.cp_diff_norm(xd, b.reduced) == pytest.approx(ids.cp_diff_norm(xh, a.reduced),
+                                                            rel=1e-12)
+    # unnormalized columns, a negative weight, a zero column
+    fh = [rng.standard_normal((40, 6)) * 3.0 for _ in range(3)]
+    fh[1][:, 4] = 0.0
+    wh = np.array([1.0, -2.0, 0.5, 1.5, 1.0, 0.7])
+    xh = ids.CpTensor(wh, fh)
+    xd = ids.CpTensor(wh, [torch.from_numpy(f).cuda() for f in fh])
+    assert np.allclose(xd.weights, xh.weights, rtol=1e-14) and (xd.weights >= 0).all()
+    assert np.array_equal(xd.zero_columns, xh.zero_columns)
+    for u, v in zip(xd.factors, xh.factors):
+        assert np.allclose(u.cpu().numpy(), v, rtol=0, atol=1e-15)
+    ra, rb = ids.tensorsketch_id(xh, 3, 30, seed=1), ids.tensorsketch_id(xd, 3, 30, seed=1)
+    assert np.array_equal(ra.cols, rb.cols)
+    assert np.allclose(ra.coeffs, rb.coeffs, rtol=1e-12, atol=1e-13)
