@@ -333,6 +333,12 @@ int ids_dcpqr_pivot_dev_f64(const double* Y, int64_t rows, int64_t ncols, int64_
 int ids_dcpqr_step_dev_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy, int64_t k,
                            int64_t col0, int64_t kk, const int64_t* piv, const double* a,
                            double* cand, void* workspace, size_t ws_bytes, void* stream);
+/* ids_dcpqr_select_f64 + ids_dcpqr_pivot_dev_f64 in one launch (what
+ * distributed.py uses): the candidates in, piv and the pivot column out. */
+int ids_dcpqr_select_pivot_f64(const double* Y, int64_t rows, int64_t ncols, int64_t ldy,
+                               int64_t k, int64_t col0, int64_t kk, const double* cands,
+                               int64_t nshards, int64_t* piv, double* a, void* workspace,
+                               size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Matrix Market input (replaces scipy.io.mmread behind

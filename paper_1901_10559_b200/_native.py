@@ -120,6 +120,11 @@ SIGNATURES = {
         [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz,
          _c_p],
     ),
+    "ids_dcpqr_select_pivot_f64": (
+        _c_int,
+        [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p,
+         _c_sz, _c_p],
+    ),
     "ids_dcpqr_results_f64": (
         _c_int, [_c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]
     ),

@@ -335,12 +335,56 @@ __global__ void __launch_bounds__(kT) dc_recompute_kernel(const double* __restri
     }
 }
 
-int sm_count() {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms;
+// ---- fused device-driven steps (one launch each side of the pivot all-reduce) ----
+
+// Pivot selection (dc_select_kernel's rule, redundantly per CTA) fused with
+// the position swap and the residual pivot column (dc_pivot_kernel's with
+// -0.0 from non-owners); CTA 0 publishes piv for the fused step.
+__global__ void __launch_bounds__(kT) dc_select_pivot_kernel(
+    const double* __restrict__ Y, int64_t m, int64_t n, int64_t ldy, int64_t col0, int64_t kk,
+    const double* __restrict__ cands, int64_t nshards, int64_t* __restrict__ piv, DState s,
+    double* __restrict__ a) {
+    __shared__ int64_t sp[3];
+    if (threadIdx.x == 0) {
+        bool have = false;
+        double bv = 0.0;
+        int64_t bp = 0, bc = -1, ck = -1;
+        for (int64_t q = 0; q < nshards; ++q) {
+            const double val = cands[4 * q], pos = cands[4 * q + 1];
+            const double col = cands[4 * q + 2], nxt = cands[4 * q + 3];
+            if (nxt >= 0.0) ck = (int64_t)nxt;
+            if (col < 0.0) continue;
+            if (!have || val > bv || (val == bv && (int64_t)pos < bp)) {
+                have = true;
+                bv = val;
+                bp = (int64_t)pos;
+                bc = (int64_t)col;
+            }
+        }
+        sp[0] = have ? bc : ck;
+        sp[1] = have ? bp : kk;
+        sp[2] = ck;
+        if (blockIdx.x == 0) {
+            piv[0] = sp[0];
+            piv[1] = sp[1];
+            piv[2] = sp[2];
+        }
+    }
+    __syncthreads();
+    const int64_t cs = sp[0], ps = sp[1], ck = sp[2];
+    const int64_t csl = cs - col0, ckl = ck - col0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (ckl >= 0 && ckl < n && ck != cs) s.pos[ckl] = ps;
+        if (csl >= 0 && csl < n) s.pos[csl] = kk;
+    }
+    const int64_t mpad = ceil_div_dev(m);
+    const bool own = csl >= 0 && csl < n;
+    const double* ycol = own ? Y + csl * ldy : nullptr;
+    for (int64_t r = (int64_t)blockIdx.x * kT + threadIdx.x; r < m; r += (int64_t)gridDim.x * kT)
+        a[r] = !own ? -0.0 : (r < kk ? 0.0 : sub_dot(ycol[r], s.V + r, mpad, s.F + csl, n, kk));
 }
+
+int sm_count() { return ids_sm_count(); }
 
 bool bad_args(int64_t m, int64_t n, int64_t ldy, int64_t k) {
     return m < 1 || n < 0 || k < 1 || k > m || ldy < m;
@@ -486,6 +530,28 @@ extern "C" int ids_dcpqr_step_dev_f64(const double* Y, int64_t rows, int64_t nco
     }
     return dcpqr_step(Y, rows, ncols, ldy, k, col0, kk, -1, piv, a, cand, workspace, ws_bytes,
                       stream);
+}
+
+extern "C" int ids_dcpqr_select_pivot_f64(const double* Y, int64_t rows, int64_t ncols,
+                                          int64_t ldy, int64_t k, int64_t col0, int64_t kk,
+                                          const double* cands, int64_t nshards, int64_t* piv,
+                                          double* a, void* workspace, size_t ws_bytes,
+                                          void* stream) {
+    if (bad_args(rows, ncols, ldy, k) || kk < 0 || kk >= k || nshards < 1 || !piv) {
+        ids_set_last_error("dcpqr: bad arguments");
+        return IDS_EINVAL;
+    }
+    WsCarve ws(workspace, ws_bytes);
+    const DState s = carve(ws, rows, ncols, k);
+    if (!ws.ok()) {
+        ids_set_last_error("dcpqr: workspace too small");
+        return IDS_EWORKSPACE;
+    }
+    const unsigned g = (unsigned)tmax<int64_t>(1, tmin<int64_t>(ceil_div(rows, kT), sm_count()));
+    dc_select_pivot_kernel<<<g, kT, 0, as_stream(stream)>>>(Y, rows, ncols, ldy, col0, kk, cands,
+                                                            nshards, piv, s, a);
+    IDS_LAUNCH_CHECK();
+    return IDS_OK;
 }
 
 extern "C" int ids_dcpqr_results_f64(int64_t rows, int64_t ncols, int64_t k, int64_t* pos,

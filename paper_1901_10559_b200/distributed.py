@@ -428,6 +428,16 @@ class DeviceCpqrShard:
                    self.col0, kk, d.ptr(piv), d.ptr(a), d.ptr(self.cand), d.ptr(self.ws),
                    self.nbytes, d.stream_ptr())
 
+    def select_pivot(self, cands, kk):
+        """select + pivot_dev in one launch; returns (piv, a)."""
+        d = self._d
+        if not hasattr(self, "piv"):
+            self.piv = d.empty(3, torch.int64)
+        self._call("ids_dcpqr_select_pivot_f64", d.ptr(self.y), self.m, self.n, self.m, self.k,
+                   self.col0, kk, d.ptr(cands), int(cands.numel() // 4), d.ptr(self.piv),
+                   d.ptr(self.a), d.ptr(self.ws), self.nbytes, d.stream_ptr())
+        return self.piv, self.a
+
     def results(self):
         d = self._d
         pos = d.empty(max(self.n, 1), torch.int64)[: self.n]
@@ -516,14 +526,18 @@ def _dcpqr_device(shard, blocks, total_cols, rank, rank_tol, group):
     from .matrix_id import DeviceId
 
     world = len(blocks)
+    nccl = world > 1 and "nccl" in str(dist.get_backend(group)).lower()
+    gathered = torch.empty((world, 4), dtype=torch.float64, device=shard.cand.device)
     for kk in range(rank):
         c = shard.cand.reshape(1, 4)
-        if world > 1:
+        if nccl:
+            dist.all_gather_into_tensor(gathered, c, group=group)
+            c = gathered
+        elif world > 1:
             parts = [torch.empty_like(c) for _ in range(world)]
             dist.all_gather(parts, c, group=group)
             c = torch.cat(parts)
-        piv = shard.select(c, kk)
-        a = shard.pivot_dev(kk, piv)
+        piv, a = shard.select_pivot(c, kk)  # one launch
         if world > 1:
             dist.all_reduce(a, op=dist.ReduceOp.SUM, group=group)
         shard.step_dev(kk, piv, a)

@@ -136,3 +136,39 @@ def test_device_driven_zero_sketch():
     p2, r2, n2 = _run_local_shards_device(y, 4, [0, 10, 30])
     assert np.array_equal(p1, p2) and n1 == n2 == 0
     assert np.array_equal(np.signbit(r1), np.signbit(r2)) and np.array_equal(r1, r2)
+
+
+def _run_local_shards_fused(y, k, bounds):
+    """As _run_local_shards_device, with select + pivot in one launch
+    (ids_dcpqr_select_pivot_f64), as distributed.py drives it."""
+    shards = [DeviceCpqrShard(torch.from_numpy(np.ascontiguousarray(y[:, a:b].T)).cuda(), a, k)
+              for a, b in zip(bounds[:-1], bounds[1:])]
+    for kk in range(k):
+        c = torch.cat([sh.cand.reshape(1, 4) for sh in shards])
+        outs = [sh.select_pivot(c, kk) for sh in shards]
+        tot = outs[0][1].clone()
+        for _, a in outs[1:]:
+            tot += a
+        for sh, (p, _) in zip(shards, outs):
+            sh.step_dev(kk, p, tot)
+    parts = [sh.results() for sh in shards]
+    pos = np.concatenate([p[0].cpu().numpy() for p in parts])
+    r = np.concatenate([p[1].cpu().numpy() for p in parts], axis=1)
+    return assemble_pivoted(pos, r, parts[0][2].cpu().numpy(), k, 1e-12)
+
+
+@pytest.mark.parametrize("shape,bounds", [((4096, 1000), [0, 300, 600, 1000]),
+                                          ((4096, 1000), [0, 1, 500, 999, 1000]),
+                                          ((16384, 250), [0, 250]), ((700, 90), [0, 45, 90])])
+def test_fused_steps_bit_identical(shape, bounds):
+    """The fused select+pivot kernel reproduces the separate select and
+    pivot kernels bit for bit."""
+    m, n = shape
+    y = _near_dup(np.random.default_rng(m + n), m, n, 10, 1e-3)
+    y[:, 17] = 0.0
+    k = 10
+    p1, r1, n1 = _run_local_shards_device(y, k, bounds)
+    p2, r2, n2 = _run_local_shards_fused(y, k, bounds)
+    assert np.array_equal(p1, p2) and n1 == n2
+    assert np.array_equal(r1, r2)
+    assert np.array_equal(p2[:k], oracle.cpqr(y, k).perm[:k])

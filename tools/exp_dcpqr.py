@@ -1,4 +1,4 @@
-"""Column-distributed CPQR (device-driven) on one GPU: a full C5-shaped
+"""Column-distributed CPQR (device-driven, fused launches) on one GPU: a full C5-shaped
 sketch and a 1/8 column shard (what each of 8 ranks runs, minus the two
 collectives per step), host enqueue time vs device time, against the
 single-GPU cpqr_kernel."""
