@@ -13,9 +13,15 @@ this module adds the two partitionings SURVEY.md section 8(e) derives:
   the TensorSketch depends only on column r of each factor, so each rank
   sketches its block independently.  The ID then runs as a COLUMN-distributed
   truncated CPQR (``cpqr_columns_sharded``): per step one
-  all-gather of 4-double pivot candidates and one broadcast of the L-double
-  pivot column, so the L x R sketch (262 MB for configs[4]) is never
-  gathered; ``cpqr="gather"`` keeps the all-gather + redundant CPQR variant.
+  all-gather of 4-double pivot candidates into a device tensor, the pivot
+  picked by a kernel, and one all-reduce of the L-double pivot column (the
+  non-owners contribute -0.0), with no host synchronization; the L x R
+  sketch (262 MB for configs[4]) is never gathered.  ``cpqr="gather"`` keeps
+  the all-gather + redundant CPQR variant.  Trials of several seeds are
+  queued with one host synchronization (``*_sharded_trials``).
+
+``seed=None`` draws fresh entropy on the group's rank 0 and broadcasts it;
+every broadcast names the source by its global rank, so subgroups work.
 
 The arithmetic goes through a backend object so the partitioning and the
 collectives can be exercised on CPU with gloo (tests/test_distributed_gloo.py,
