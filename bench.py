@@ -399,16 +399,20 @@ class MatrixWorkload:
         return ms, self.bytes_local, {"cpqr_and_coeffs": id_ms, "hash_and_index": hash_ms}
 
     def host_copy(self):
-        """This rank's block in host memory (pinned for dense)."""
+        """This rank's block in pinned host memory: a pinned tensor (dense) or a
+        scipy CSR over pinned arrays (the contract's e2e input)."""
         torch = self.ctx.torch
         if self.operand.kind == "dense":
             h = torch.empty((self.r1 - self.r0, self.cols), dtype=torch.float64, pin_memory=True)
             h.copy_(self.operand.t)
             return h, int(h.numel() * 8)
-        from paper_1901_10559_b200.generators import operand_to_scipy
+        import scipy.sparse as sp
 
-        m = operand_to_scipy(self.operand)
-        return m, int(m.data.nbytes + m.indices.nbytes + m.indptr.nbytes)
+        parts = [pinned_copy(torch, t) for t in (self.operand.data, self.operand.indices,
+                                                 self.operand.indptr)]
+        m = sp.csr_array(tuple(p.numpy() for p in parts), shape=self.operand.shape)
+        m._pinned = parts  # keep the pinned buffers alive with the matrix
+        return m, int(sum(p.numel() * p.element_size() for p in parts))
 
     def e2e_call(self, host, seed):
         import paper_1901_10559_b200 as ids
@@ -523,11 +527,15 @@ class TensorWorkload:
                                       "y_write_bytes": n_loc * self.L * 8}
 
     def host_copy(self):
+        """The CP tensor over factors in pinned host memory (F order)."""
         import paper_1901_10559_b200 as ids
 
+        torch = self.ctx.torch
         w = self.w_local.cpu().numpy()
-        facs = [f.cpu().numpy() for f in self.f_local]  # F order (I_n x R)
-        return ids.CpTensor(w, facs), int(sum(f.nbytes for f in facs) + w.nbytes)
+        pins = [pinned_copy(torch, f.t()) for f in self.f_local]  # (R, I_n) contiguous
+        x = ids.CpTensor(w, [p.numpy().T for p in pins])  # I_n x R, F order, no copy
+        x._pinned = pins
+        return x, int(sum(p.numel() * 8 for p in pins) + w.nbytes)
 
     def e2e_call(self, host, seed):
         import paper_1901_10559_b200 as ids
@@ -559,6 +567,13 @@ class TensorWorkload:
                   "new_weights_relerr": relerr(res.new_weights, r["new_weights"]),
                   "against": ref.kind}
         return cpu, parity
+
+
+def pinned_copy(torch, t):
+    """A pinned host copy of device tensor t (same shape, contiguous)."""
+    h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h
 
 
 def make_workload(ctx, name):
