@@ -288,8 +288,14 @@ class TensorIdGraph:
 
         from . import _device
 
-        self.factors = list(factors)
-        self.weights = weights
+        import torch as _t
+
+        if not all(isinstance(f, _t.Tensor) and f.device.type == "cuda" for f in factors) or \
+                not (isinstance(weights, _t.Tensor) and weights.device.type == "cuda"):
+            raise ValueError("TensorIdGraph takes CUDA factors and weights (host inputs cannot "
+                             "be captured); use tensorsketch_id for host CP tensors")
+        self.factors = [_fortran_cuda(f) for f in factors]
+        self.weights = weights.to(_t.float64).contiguous()
         self.mode_dims = tuple(int(f.shape[0]) for f in self.factors)
         self.R = int(self.factors[0].shape[1])
 

@@ -82,3 +82,8 @@ def test_device_cp_tensor_matches_host():
     ra, rb = ids.tensorsketch_id(xh, 3, 30, seed=1), ids.tensorsketch_id(xd, 3, 30, seed=1)
     assert np.array_equal(ra.cols, rb.cols)
     assert np.allclose(ra.coeffs, rb.coeffs, rtol=1e-12, atol=1e-13)
+
+
+def test_tensor_id_graph_rejects_host_inputs():
+    with pytest.raises(ValueError):
+        ids.TensorIdGraph([np.ones((5, 3))] * 2, np.ones(3), 2, 8)
