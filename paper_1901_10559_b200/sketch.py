@@ -261,6 +261,8 @@ class CountSketchOp:
         if self._index is not None:
             for t in self._index:
                 t.record_stream(stream)
+        if getattr(self, "_plan", None) is not None:
+            self._plan.record_stream(stream)
 
     # ---- host views -------------------------------------------------------
     def _check_draws(self):
@@ -447,15 +449,12 @@ class TensorSketchOp:
         self.out_dim = int(out_dim)
         if _seed_dev is not None:  # device (N, 4) PCG64 states (see mode_seed_states)
             self.seed = None
-            self.mode_ops = [CountSketchOp(d, out_dim, _seed_dev=_seed_dev[n])
-                             for n, d in enumerate(mode_dims)]
-            return
-        entropy = _seed_entropy(seed)
-        self.seed = entropy
-        self.mode_ops = [
-            CountSketchOp(d, out_dim, seed=np.random.SeedSequence([entropy, n]))
-            for n, d in enumerate(mode_dims)
-        ]
+            kw = [dict(_seed_dev=_seed_dev[n]) for n in range(len(mode_dims))]
+        else:
+            entropy = _seed_entropy(seed)
+            self.seed = entropy
+            kw = [dict(seed=np.random.SeedSequence([entropy, n])) for n in range(len(mode_dims))]
+        self.mode_ops = _draw_modes(mode_dims, self.out_dim, kw)
 
     @staticmethod
     def mode_seed_states(n_modes, seed):
@@ -513,6 +512,37 @@ class TensorSketchOp:
 
 
 _SIDE_STREAMS = {}
+_MODE_STREAMS = {}
+
+
+def _draw_modes(mode_dims, out_dim, kw):
+    """The N per-mode CountSketchOps of a TensorSketchOp, each with its
+    bucket index and (long modes) scatter plan, drawn CONCURRENTLY on side
+    streams -- a dozen small kernels per mode that would otherwise run one
+    after another -- joined back into the current stream (also inside a
+    CUDA-graph capture, where they become parallel branches)."""
+    from .tensorsketch import SCATTER_MIN_DIM
+
+    if len(mode_dims) == 1 or not torch.cuda.is_available():
+        return [CountSketchOp(d, out_dim, **k) for d, k in zip(mode_dims, kw)]
+    dev = _device.device()
+    pool = _MODE_STREAMS.setdefault(dev.index, [])
+    while len(pool) < len(mode_dims):
+        pool.append(torch.cuda.Stream(device=dev))
+    main = torch.cuda.current_stream()
+    ops = []
+    for d, k, st in zip(mode_dims, kw, pool):
+        st.wait_stream(main)
+        with torch.cuda.stream(st):
+            op = CountSketchOp(d, out_dim, **k)
+            op._bucket_index()
+            if d >= SCATTER_MIN_DIM:
+                op._ts_plan()
+        ops.append(op)
+    for op, st in zip(ops, pool):
+        main.wait_stream(st)
+        op.record_stream(main)
+    return ops
 PIPELINE_DEPTH = 2     # draws in flight ahead of the trial being computed
 PIPELINE_GRID_CAP = 16  # phase-B CTAs per background draw
 
