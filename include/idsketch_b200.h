@@ -209,6 +209,24 @@ int ids_tensorsketch_planned_f64(int n_modes, const double* const* factors, cons
                                  int64_t out_dim, const double* weights, double* Y,
                                  double* colnorm2, void* workspace, size_t ws_bytes,
                                  void* stream);
+/* Split-spectrum TensorSketch (sm_100a clusters + tensor memory), the
+ * product path for out_dim in {4096, 8192, 16384} (C4, C5).  Same operation
+ * as ids_tensorsketch_f64 (reference sketch.py:156-186): a cluster of two
+ * CTAs per term column computes the even / odd bins of the half-length
+ * spectrum from a CountSketch folded at out_dim / 2, keeps its half of the
+ * running spectrum in TMEM, and the halves meet once, in the inverse.
+ * Per mode it reads a folded plan (ids_ts_split_plan, built from the hash's
+ * bucket int32[dim] and sign int8[dim]; ids_ts_split_plan_bytes(dim,
+ * out_dim) bytes, 16-byte aligned) instead of the bucket index.  Y must be
+ * 16-byte aligned; colnorm2 as for ids_tensorsketch_f64. */
+int ids_tensorsketch_split_ok(int n_modes, int64_t out_dim);
+size_t ids_ts_split_plan_bytes(int64_t dim, int64_t out_dim);
+int ids_ts_split_plan(const int32_t* bucket, const int8_t* sign, int64_t dim, int64_t out_dim,
+                      void* plan, size_t plan_bytes, void* stream);
+int ids_tensorsketch_split_f64(int n_modes, const double* const* factors, const int64_t* dims,
+                               const int64_t* lds, int64_t ncols, const void* const* plans,
+                               int64_t out_dim, const double* weights, double* Y,
+                               double* colnorm2, void* stream);
 /* 1 when ids_tensorsketch_f64 handles (n_modes, out_dim) in its fused
  * one-CTA-per-term kernel (transform half-length <= 8192: power-of-two
  * out_dim <= 16384, or n_modes * (out_dim - 1) + 1 <= 16384 otherwise).

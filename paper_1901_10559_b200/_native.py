@@ -75,6 +75,12 @@ SIGNATURES = {
         [_c_int, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p,
          _c_sz, _c_p],
     ),
+    "ids_tensorsketch_split_ok": (_c_int, [_c_int, _c_i64]),
+    "ids_ts_split_plan_bytes": (_c_sz, [_c_i64, _c_i64]),
+    "ids_ts_split_plan": (_c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_p, _c_sz, _c_p]),
+    "ids_tensorsketch_split_f64": (
+        _c_int, [_c_int, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p]
+    ),
     "ids_cpqr_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_i64]),
     "ids_cpqr_trunc_f64": (
         _c_int,

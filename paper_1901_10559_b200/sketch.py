@@ -261,8 +261,9 @@ class CountSketchOp:
         if self._index is not None:
             for t in self._index:
                 t.record_stream(stream)
-        if getattr(self, "_plan", None) is not None:
-            self._plan.record_stream(stream)
+        for name in ("_plan", "_split_plan"):
+            if getattr(self, name, None) is not None:
+                getattr(self, name).record_stream(stream)
 
     # ---- host views -------------------------------------------------------
     def _check_draws(self):
@@ -335,6 +336,21 @@ class CountSketchOp:
             )
             self._plan = plan
         return self._plan
+
+    def _ts_split_plan(self):
+        """Folded scatter plan of this operator as one mode of the
+        split-spectrum TensorSketch kernel (per-row slot b mod L/2, sign,
+        b >= L/2, rank inside its chunk; per-chunk largest rank), built on
+        the device from bucket / sign once and cached (ids_ts_split_plan)."""
+        if getattr(self, "_split_plan", None) is None:
+            nbytes = query("ids_ts_split_plan_bytes", self.in_dim, self.out_dim)
+            plan = _device.workspace(nbytes)
+            call(
+                "ids_ts_split_plan", _device.ptr(self._bucket_d), _device.ptr(self._sign_d),
+                self.in_dim, self.out_dim, _device.ptr(plan), nbytes, _device.stream_ptr(),
+            )
+            self._split_plan = plan
+        return self._split_plan
 
     @staticmethod
     def needs_index(operand, flags=0):
@@ -521,10 +537,11 @@ def _draw_modes(mode_dims, out_dim, kw):
     streams -- a dozen small kernels per mode that would otherwise run one
     after another -- joined back into the current stream (also inside a
     CUDA-graph capture, where they become parallel branches)."""
-    from .tensorsketch import SCATTER_MIN_DIM
+    from .tensorsketch import SCATTER_MIN_DIM, uses_split_kernel
 
     if len(mode_dims) == 1 or not torch.cuda.is_available():
         return [CountSketchOp(d, out_dim, **k) for d, k in zip(mode_dims, kw)]
+    split = uses_split_kernel(len(mode_dims), out_dim)
     dev = _device.device()
     pool = _MODE_STREAMS.setdefault(dev.index, [])
     while len(pool) < len(mode_dims):
@@ -535,9 +552,12 @@ def _draw_modes(mode_dims, out_dim, kw):
         st.wait_stream(main)
         with torch.cuda.stream(st):
             op = CountSketchOp(d, out_dim, **k)
-            op._bucket_index()
-            if d >= SCATTER_MIN_DIM:
-                op._ts_plan()
+            if split:  # the split kernel reads its folded plan only
+                op._ts_split_plan()
+            else:
+                op._bucket_index()
+                if d >= SCATTER_MIN_DIM:
+                    op._ts_plan()
         ops.append(op)
     for op, st in zip(ops, pool):
         main.wait_stream(st)

@@ -41,6 +41,13 @@ def factor_to_device(f):
 
 
 SCATTER_MIN_DIM = 4096  # mode length from which the fused kernel uses a scatter plan
+USE_SPLIT = True  # the split-spectrum kernel where it applies (tests flip it to compare)
+
+
+def uses_split_kernel(n_modes, out_dim):
+    """Whether (n_modes, L) runs on the split-spectrum cluster kernel
+    (ids_tensorsketch_split_f64: L in {4096, 8192, 16384}, <= 8 modes)."""
+    return USE_SPLIT and bool(query("ids_tensorsketch_split_ok", n_modes, out_dim))
 
 
 def tensorsketch_device(op, factors, weights=None, norms=False):
@@ -89,20 +96,28 @@ def tensorsketch_device(op, factors, weights=None, norms=False):
         else:
             dev_f.append(factor_to_device(f))
             mode_ops.append(m)
-    idx = [m._bucket_index() for m in mode_ops]
-    # scatter plans pay off on long factor columns; short modes (C4: 1000
-    # rows) keep the gather path rather than pay the plan's launches per draw
-    plans = (ctypes.c_void_p * n)(*[_device.ptr(m._ts_plan()) if m.in_dim >= SCATTER_MIN_DIM
-                                    else None for m in mode_ops])
     fac_p = (ctypes.c_void_p * n)(*[_device.ptr(t) for t in dev_f])
-    ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _, _ in idx])
-    key_p = (ctypes.c_void_p * n)(*[_device.ptr(k) for _, _, k in idx])
     dims = (ctypes.c_int64 * n)(*[int(m.in_dim) for m in mode_ops])
     lds = (ctypes.c_int64 * n)(*[int(t.shape[1]) for t in dev_f])
     y = _device.empty((ncols, L), torch.float64)
     nrm = _device.empty(max(ncols, 1), torch.float64)[:ncols] if norms else None
     if ncols == 0:
         return (y, nrm) if norms else y
+    if uses_split_kernel(n, L):
+        plans = (ctypes.c_void_p * n)(*[_device.ptr(m._ts_split_plan()) for m in mode_ops])
+        call(
+            "ids_tensorsketch_split_f64", n, ctypes.addressof(fac_p), ctypes.addressof(dims),
+            ctypes.addressof(lds), ncols, ctypes.addressof(plans), L, _device.ptr(w),
+            _device.ptr(y), _device.ptr(nrm), _device.stream_ptr(),
+        )
+        return (y, nrm) if norms else y
+    idx = [m._bucket_index() for m in mode_ops]
+    # scatter plans pay off on long factor columns; short modes (C4: 1000
+    # rows) keep the gather path rather than pay the plan's launches per draw
+    plans = (ctypes.c_void_p * n)(*[_device.ptr(m._ts_plan()) if m.in_dim >= SCATTER_MIN_DIM
+                                    else None for m in mode_ops])
+    ord_p = (ctypes.c_void_p * n)(*[_device.ptr(o) for o, _, _ in idx])
+    key_p = (ctypes.c_void_p * n)(*[_device.ptr(k) for _, _, k in idx])
     nbytes = query("ids_tensorsketch_workspace_bytes", n, ctypes.addressof(dims), ncols, L)
     ws = _device.workspace(nbytes)
     call(
