@@ -1000,6 +1000,580 @@ constexpr int64_t kMaxG = 148;
 
 
 
+
+// ---- tall sketches: column ownership, two barriers per step ----------------
+// For m > 1024 rows (C4: 4096 x 1000, C5: 16384 x 2000).  CTA b owns a
+// contiguous block of COLUMNS for the whole factorization and keeps the full
+// Householder vector v in shared memory, so the GEMV W_j = Y[:, j]^T v of
+// its columns, their F entries, row kk of R and the norm downdates all stay
+// on the CTA: no W partials cross CTAs.  Rows are split across CTAs only for
+// the pivot column's residual a = Y[:, p] - V F[p, :]^T, whose norm and
+// z~ = V^T a partials ride on the first barrier: the LAST CTA to arrive sums
+// them (fixed order) before releasing it; the second barrier likewise
+// reduces the argmax candidates to the next pivot.  A step is
+//   S1 residual rows -> [barrier A: norm, z~] -> S2 Householder, v into
+//   shared memory, GEMV, F / R / downdate, argmax -> [barrier B: pivot],
+// against three grid syncs and two all-CTA partial reductions before.
+constexpr int kTThreads = 512;
+constexpr int kTWarps = kTThreads / 32;
+constexpr int kSegT = 2048;   // GEMV unit: rows of one owned column
+constexpr int kSegTLoads = kSegT / 32 / 4;  // loads per lane per quarter unit (16)
+constexpr int kMaxOwn = 64;   // owned columns per CTA
+constexpr int kTallMaxK = 256;
+
+struct TallArgs {
+    const double* Y;
+    int64_t m, n, ldy, k;
+    const double* colnorm2;
+    double rank_tol;
+    int32_t* perm;
+    double* Rtop;
+    int32_t* numerical_rank;
+    double *F, *Rcol, *V, *tau, *beta, *a, *normpart, *zpart, *red;
+    int64_t* piv;
+    int64_t* flag_list;
+    ArgMax* amax;
+    unsigned* bar;
+    int64_t* tlog;
+    int pin_segs;  // leading 2048-row segments of each column kept in L2 (evict_last)
+};
+
+__device__ __forceinline__ double block_sum_t(double v, double* red) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < kTWarps; ++i) s += red[i];
+    return s;
+}
+
+// Grid barrier whose LAST arriving CTA runs `last()` (all its threads) before
+// releasing the others; bar[0] counts arrivals, bar[1] is the generation.
+template <class Fn>
+__device__ __forceinline__ void bar_last(unsigned* bar, unsigned nblocks, Fn&& last) {
+    __shared__ int s_last;
+    __shared__ unsigned s_gen;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_gen = *((volatile unsigned*)bar + 1);
+        __threadfence();
+        s_last = atomicAdd(bar, 1u) == nblocks - 1;
+        if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_last) {
+        last();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        }
+    } else if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        while (*gen == s_gen) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Grid barrier on a monotonic arrival counter: every CTA posts one release-add
+// and polls with acquire loads until the count reaches its target (number of
+// barriers passed x grid size) -- one posted reduction and one polling round
+// trip, no reset.  ctr must be zero at launch.
+__device__ __forceinline__ void grid_bar_count(unsigned* ctr, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+// y - sum_q a[q*lda] * b[q*ldb] with the b operand read through L2 (entries
+// written by other CTAs)
+__device__ __forceinline__ double sub_dot_cg(double y, const double* __restrict__ a, int64_t lda,
+                                             const double* b, int64_t ldb, int64_t n) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t q = 0;
+    for (; q + 4 <= n; q += 4) {
+        s0 = fma(a[q * lda], __ldcg(b + q * ldb), s0);
+        s1 = fma(a[(q + 1) * lda], __ldcg(b + (q + 1) * ldb), s1);
+        s2 = fma(a[(q + 2) * lda], __ldcg(b + (q + 2) * ldb), s2);
+        s3 = fma(a[(q + 3) * lda], __ldcg(b + (q + 3) * ldb), s3);
+    }
+    for (; q < n; ++q) s0 = fma(a[q * lda], __ldcg(b + q * ldb), s0);
+    return y - ((s0 + s1) + (s2 + s3));
+}
+
+static_assert(sizeof(ArgMax) == 32, "ArgMax is read as two 16-byte words");
+
+// reduce_partials_warp with the candidates read through L2 (written by the
+// other CTAs since this CTA last read them).
+__device__ ArgMax reduce_partials_warp_cg(const ArgMax* part, int64_t G) {
+    const int lane = threadIdx.x & 31;
+    ArgMax best{-1.0, INT64_MAX, -1, -1};
+    for (int64_t i0 = 0; i0 < G; i0 += 128) {
+        ArgMax o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + lane + 32 * u;
+            if (i < G) {
+                const double2* w = reinterpret_cast<const double2*>(part + i);
+                const double2 w0 = __ldcg(w), w1 = __ldcg(w + 1);
+                o[u] = ArgMax{w0.x, __double_as_longlong(w0.y), __double_as_longlong(w1.x),
+                              __double_as_longlong(w1.y)};
+            } else {
+                o[u] = ArgMax{-1.0, INT64_MAX, -1, -1};
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (better(o[u].val, o[u].pos, best.val, best.pos)) {
+                best.val = o[u].val;
+                best.pos = o[u].pos;
+                best.col = o[u].col;
+            }
+            if (o[u].col_at_next >= 0) best.col_at_next = o[u].col_at_next;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ArgMax ot;
+        ot.val = __shfl_xor_sync(0xffffffffu, best.val, o);
+        ot.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
+        ot.col = __shfl_xor_sync(0xffffffffu, best.col, o);
+        ot.col_at_next = __shfl_xor_sync(0xffffffffu, best.col_at_next, o);
+        if (better(ot.val, ot.pos, best.val, best.pos)) {
+            best.val = ot.val;
+            best.pos = ot.pos;
+            best.col = ot.col;
+        }
+        if (ot.col_at_next >= 0) best.col_at_next = ot.col_at_next;
+    }
+    return best;
+}
+
+// Fixed-order sum of G contiguous partials by one warp, read through L2.
+__device__ __forceinline__ double warp_sum_partials_cg(const double* p, int64_t G) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int64_t i0 = 0; i0 < G; i0 += 256) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = i0 + lane + 32 * u;
+            t[u] = i < G ? __ldcg(p + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += t[u];
+    }
+    return warp_sum(s);
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ int64_t ceil_div_d(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Y loads with an L2 eviction policy: the pinned segments of every column
+// (read again by each of the k GEMV passes) evict_last, the rest evict_first
+__device__ __forceinline__ double ld_pol(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+__global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
+    extern __shared__ double vsm[];
+    const int64_t m = g.m, n = g.n, k = g.k, ldy = g.ldy;
+    const int64_t mpad = (m + kSegT - 1) / kSegT * kSegT;
+    const int nsegT = (int)(mpad / kSegT);
+    const int G = gridDim.x, b = blockIdx.x;
+    const int64_t rmax = (m + G - 1) / G;
+    // shared memory: v | GEMV partials | z | row kk of V | F[cs, :] | owned
+    // columns' norms, Y[kk, j], F rows | owned rows of V | positions
+    double* part = vsm + mpad;                 // kMaxOwn x nsegT
+    double* zsh = part + kMaxOwn * nsegT;      // k
+    double* vrow = zsh + k;                    // k: V[kk, :kk]
+    double* fpiv = vrow + k;                   // k: F[cs, :kk]
+    double* svn1 = fpiv + k;                   // kMaxOwn
+    double* svn2 = svn1 + kMaxOwn;
+    double* sykk = svn2 + kMaxOwn;             // Y[kk, j] of the owned columns
+    double* fown = sykk + kMaxOwn;             // kMaxOwn x k: F[j, :] of the owned columns
+    double* vown = fown + kMaxOwn * k;         // rmax x k: V[r, :] of the owned rows
+    int64_t* spos = reinterpret_cast<int64_t*>(vown + rmax * k);
+    __shared__ double red[kTWarps];
+    __shared__ double zacc[kTThreads];  // a[r] of the owned rows below kk
+    __shared__ ArgMax wbest[kTWarps];
+    __shared__ int s_nflag;
+    __shared__ int64_t s_piv[3];
+    __shared__ double s_nrm;
+    __shared__ __align__(8) uint64_t s_mb;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t c0 = n * b / G, c1 = n * (b + 1) / G, nown = c1 - c0;
+    const int64_t r0 = m * b / G, r1 = m * (b + 1) / G, nrow = r1 - r0;
+    const double tol3z = sqrt(DBL_EPSILON);
+    int64_t* flagged = g.flag_list + c0;
+    unsigned nbar = 0;
+    uint64_t pol_keep, pol_stream;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+
+    auto local_argmax = [&](int64_t pmin, int64_t pnext) {  // warp 0 (nown <= 64)
+        if (wid != 0) return;
+        ArgMax best{-1.0, INT64_MAX, -1, -1};
+        for (int64_t jj = lane; jj < nown; jj += 32) {
+            const int64_t pj = spos[jj];
+            if (pj == pnext) best.col_at_next = c0 + jj;
+            if (pj >= pmin && better(svn1[jj], pj, best.val, best.pos)) {
+                best.val = svn1[jj];
+                best.pos = pj;
+                best.col = c0 + jj;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            ArgMax ot;
+            ot.val = __shfl_xor_sync(0xffffffffu, best.val, o);
+            ot.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
+            ot.col = __shfl_xor_sync(0xffffffffu, best.col, o);
+            ot.col_at_next = __shfl_xor_sync(0xffffffffu, best.col_at_next, o);
+            if (better(ot.val, ot.pos, best.val, best.pos)) {
+                best.val = ot.val;
+                best.pos = ot.pos;
+                best.col = ot.col;
+            }
+            if (ot.col_at_next >= 0) best.col_at_next = ot.col_at_next;
+        }
+        if (lane == 0) g.amax[b] = best;
+    };
+
+    // ---- prologue: zero v (its padding stays zero), owned columns' norms ----
+    for (int64_t r = threadIdx.x; r < mpad; r += kTThreads) vsm[r] = 0.0;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_mb)) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    for (int64_t jj = wid; jj < nown; jj += kTWarps) {
+        const int64_t j = c0 + jj;
+        const double* y = g.Y + j * ldy;
+        const double s2 = g.colnorm2 ? g.colnorm2[j] : warp_sum(lane_dot(y, y, 0, m));
+        if (lane == 0) {
+            svn1[jj] = sqrt(s2);
+            svn2[jj] = sqrt(s2);
+            spos[jj] = j;
+        }
+    }
+    __syncthreads();
+    local_argmax(0, 0);
+    grid_bar_count(g.bar, (unsigned)(++nbar * G));
+
+    // debug timing: phase durations of CTA 0, thread 0, kept in shared memory
+    // (a global read-modify-write per stamp would itself cost a round trip)
+    __shared__ int64_t s_tacc[16];
+    const bool tl = g.tlog && b == 0 && threadIdx.x == 0;
+    if (tl)
+        for (int i = 0; i < 16; ++i) s_tacc[i] = 0;
+    int64_t tprev = tl ? gtimer() : 0;
+    auto stamp = [&](int phase) {
+        if (tl) {
+            const int64_t t = gtimer();
+            s_tacc[phase] += t - tprev;
+            tprev = t;
+        }
+    };
+    for (int64_t kk = 0; kk < k; ++kk) {
+        // ---- S1: the pivot (every CTA reduces the candidates itself), row kk
+        // of V, positions, the pivot column's residual on the owned rows ----
+        if (wid == 0) {
+            const ArgMax r = reduce_partials_warp_cg(g.amax, G);
+            if (lane == 0) {
+                s_piv[0] = r.col;
+                s_piv[1] = r.pos;
+                s_piv[2] = r.col_at_next;
+            }
+        } else {
+            for (int64_t q = threadIdx.x - 32; q < kk; q += kTThreads - 32)
+                vrow[q] = __ldcg(g.V + q * m + kk);  // V[kk, q]
+        }
+        __syncthreads();
+        stamp(8);
+        int64_t cs = s_piv[0], ps = s_piv[1];
+        const int64_t ck = s_piv[2];
+        if (cs < 0) {  // every remaining norm is NaN (non-finite input): keep position kk
+            cs = ck;
+            ps = kk;
+        }
+        if (threadIdx.x == 0) {
+            if (ck >= c0 && ck < c1 && ck != cs) spos[ck - c0] = ps;
+            if (cs >= c0 && cs < c1) spos[cs - c0] = kk;
+        }
+        const int64_t rr = r0 + threadIdx.x;
+        const double yrr = (threadIdx.x < nrow && rr >= kk) ? __ldg(g.Y + cs * ldy + rr) : 0.0;
+        for (int64_t q = threadIdx.x; q < kk; q += kTThreads) fpiv[q] = __ldcg(g.F + q * n + cs);
+        __syncthreads();
+        stamp(9);
+        double av = 0.0;
+        if (threadIdx.x < nrow && rr >= kk) {  // a[r] = Y[r, cs] - V[r, :kk] F[cs, :kk]^T
+            const double* vr = vown + threadIdx.x * k;
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int64_t q = 0; q < kk; ++q) s4[q & 3] = fma(vr[q], fpiv[q], s4[q & 3]);
+            av = yrr - ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+        }
+        if (threadIdx.x < nrow) g.a[rr] = av;
+        const double ac = rr > kk ? av : 0.0;  // rows below kk enter the norm and z~
+        const double ss = block_sum_t(ac * ac, red);
+        if (threadIdx.x == 0) g.normpart[b] = ss;
+        stamp(10);
+        // z~_q partial = V[r0:r1, q]^T a over the owned rows (threads < nrow)
+        // (16 threads per q, rows strided by 16, a fixed shuffle tree)
+        if (threadIdx.x < nrow) zacc[threadIdx.x] = ac;
+        __syncthreads();
+        for (int64_t q0 = 0; q0 < kk; q0 += kTThreads / 16) {
+            const int64_t q = q0 + (threadIdx.x >> 4);
+            const int sub = threadIdx.x & 15;
+            double x = 0.0;
+            if (q < kk)
+                for (int64_t rl = sub; rl < nrow; rl += 16) x = fma(vown[rl * k + q], zacc[rl], x);
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if (q < kk && sub == 0) g.zpart[q * G + b] = x;
+        }
+        stamp(0);
+        grid_bar_count(g.bar, (unsigned)(++nbar * G));
+        stamp(1);
+
+        // ---- S2: a[] into shared memory by one bulk copy, ||a[kk+1:]|| (fixed-
+        // order sum of the partials), Householder, v = a * scal ----
+        if (threadIdx.x == 0) {
+            const uint32_t bytes = (uint32_t)(((m + 1) / 2) * 16);  // a[m] is a zero pad
+            asm volatile("fence.proxy.async;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&s_mb)),
+                         "r"(bytes)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(vsm)),
+                "l"(g.a), "r"(bytes), "r"(smem_addr(&s_mb))
+                : "memory");
+        }
+        if (wid == 1) {
+            const double x = warp_sum_partials_cg(g.normpart, G);
+            if (lane == 0) s_nrm = x;
+        }
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "CPQR_WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra CPQR_WAIT_%=;\n}" ::"r"(smem_addr(&s_mb)),
+            "r"((uint32_t)(kk & 1))
+            : "memory");
+        __syncthreads();
+        stamp(6);
+        const double alpha = vsm[kk];
+        const double xnorm = sqrt(s_nrm);
+        stamp(11);
+        double tau, beta, scal;
+        if (xnorm == 0.0) {
+            tau = 0.0;
+            beta = alpha;
+            scal = 0.0;
+        } else {
+            beta = -copysign(dlapy2(alpha, xnorm), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        // v = a * scal below kk and 1 at kk: the GEMV uses a (zero at rows <= kk)
+        // and adds Y[kk, j] after scaling its dot: W_j = scal * Y[kk+1:, j]^T a + Y[kk, j]
+        if (b == 0 && threadIdx.x == 0) {
+            g.tau[kk] = tau;
+            g.beta[kk] = beta;
+        }
+        if (threadIdx.x == 0 && cs >= c0 && cs < c1) g.Rcol[cs * k + kk] = beta;
+        if (threadIdx.x == 0) s_nflag = 0;
+        __syncthreads();  // everyone has read alpha
+        if (threadIdx.x == 0) vsm[kk] = 0.0;
+        stamp(12);
+        for (int64_t jj = threadIdx.x; jj < nown; jj += kTThreads) sykk[jj] = __ldg(g.Y + (c0 + jj) * ldy + kk);
+        __syncthreads();
+        stamp(13);
+        if (threadIdx.x < nrow) {  // V[r, kk] of the owned rows (global: other CTAs' row kk, form_q)
+            const double vr = rr < kk ? 0.0 : rr == kk ? 1.0 : vsm[rr] * scal;
+            vown[threadIdx.x * k + kk] = vr;
+            g.V[kk * m + rr] = vr;
+        }
+        stamp(7);
+        stamp(2);
+
+        // ---- GEMV over the owned columns: units (column, 2048-row segment),
+        // two per warp at a time, walked backwards on odd steps ----
+        {
+            const int64_t U = nown * nsegT;
+            const bool rev = kk & 1;
+            const bool full = m == mpad;
+            for (int64_t li = wid; li < U; li += 2 * kTWarps) {
+                const bool h2 = li + kTWarps < U;
+                const int64_t ua = rev ? U - 1 - li : li;
+                const int64_t ub = h2 ? (rev ? U - 1 - (li + kTWarps) : li + kTWarps) : ua;
+                const int64_t ja = ua / nsegT, sa = ua % nsegT, jb = ub / nsegT, sb = ub % nsegT;
+                const bool aa = spos[ja] > kk, ab = h2 && spos[jb] > kk;
+                const double* pa = g.Y + (c0 + ja) * ldy;
+                const double* pb = g.Y + (c0 + jb) * ldy;
+                const uint64_t pola = sa < g.pin_segs ? pol_keep : pol_stream;
+                const uint64_t polb = sb < g.pin_segs ? pol_keep : pol_stream;
+                double s1 = 0.0, s2 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll 1
+                for (int qtr = 0; qtr < 4; ++qtr) {
+                    const int64_t ba = sa * kSegT + qtr * (kSegT / 4) + lane;
+                    const int64_t bb = sb * kSegT + qtr * (kSegT / 4) + lane;
+                    double ya[kSegTLoads], yb[kSegTLoads];
+#pragma unroll
+                    for (int u = 0; u < kSegTLoads; ++u) {
+                        if (full) {
+                            ya[u] = aa ? ld_pol(pa + ba + 32 * u, pola) : 0.0;
+                            yb[u] = ab ? ld_pol(pb + bb + 32 * u, polb) : 0.0;
+                        } else {
+                            ya[u] = aa ? ld_pol(pa + tmin<int64_t>(ba + 32 * u, m - 1), pola) : 0.0;
+                            yb[u] = ab ? ld_pol(pb + tmin<int64_t>(bb + 32 * u, m - 1), polb) : 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kSegTLoads; u += 2) {
+                        s1 = fma(ya[u], vsm[ba + 32 * u], s1);
+                        s2 = fma(yb[u], vsm[bb + 32 * u], s2);
+                        t1 = fma(ya[u + 1], vsm[ba + 32 * u + 32], t1);
+                        t2 = fma(yb[u + 1], vsm[bb + 32 * u + 32], t2);
+                    }
+                }
+                const double wa = warp_sum(s1 + t1), wb = warp_sum(s2 + t2);
+                if (lane == 0) {
+                    part[ja * nsegT + sa] = wa;
+                    if (h2) part[jb * nsegT + sb] = wb;
+                }
+            }
+        }
+        // z_q = V[:, q]^T v = V[kk, q] + scal * (fixed-order sum of the z~ partials)
+        for (int64_t q = wid; q < kk; q += kTWarps) {
+            const double x = warp_sum_partials_cg(g.zpart + q * G, G);
+            if (lane == 0) zsh[q] = fma(scal, x, vrow[q]);
+        }
+        __syncthreads();
+        stamp(3);
+
+        // ---- F column, row kk of R, norm downdates (one warp per column) ----
+        for (int64_t jj = wid; jj < nown; jj += kTWarps) {
+            if (spos[jj] <= kk) continue;
+            const int64_t j = c0 + jj;
+            double wj = 0.0;
+            for (int sg = 0; sg < nsegT; ++sg) wj += part[jj * nsegT + sg];  // fixed order
+            wj = fma(scal, wj, sykk[jj]);
+            double fz = 0.0, fv = 0.0;
+            for (int64_t q = lane; q < kk; q += 32) {
+                const double fq = fown[jj * k + q];
+                fz = fma(fq, zsh[q], fz);
+                fv = fma(fq, vrow[q], fv);
+            }
+            fz = warp_sum(fz);
+            fv = warp_sum(fv);
+            if (lane == 0) {
+                const double f = (wj - fz) * tau;
+                fown[jj * k + kk] = f;
+                g.F[kk * n + j] = f;
+                const double rk = (sykk[jj] - fv) - f;  // V[kk, kk] = 1
+                g.Rcol[j * k + kk] = rk;
+                const double vn1 = svn1[jj];
+                if (kk < m - 1 && vn1 != 0.0) {
+                    double temp = fabs(rk) / vn1;
+                    temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+                    const double ratio = vn1 / svn2[jj];
+                    const double temp2 = temp * ratio * ratio;
+                    if (temp2 <= tol3z) flagged[atomicAdd(&s_nflag, 1)] = jj;
+                    else svn1[jj] = vn1 * sqrt(temp);
+                }
+            }
+        }
+        __syncthreads();
+        // exact norms of the flagged columns below row kk (LAPACK's recompute)
+        const int nflag = s_nflag;
+        for (int fi = wid; fi < nflag; fi += kTWarps) {
+            const int64_t jj = flagged[fi], j = c0 + jj;
+            const double* y = g.Y + j * ldy;
+            double s = 0.0;
+            for (int64_t r = kk + 1 + lane; r < m; r += 32) {
+                double v = y[r];
+                for (int64_t q = 0; q < kk; ++q) v = fma(-__ldcg(g.V + q * m + r), fown[jj * k + q], v);
+                v = fma(-vsm[r] * scal, fown[jj * k + kk], v);
+                s = fma(v, v, s);
+            }
+            s = warp_sum(s);
+            if (lane == 0) {
+                svn1[jj] = sqrt(s);
+                svn2[jj] = sqrt(s);
+            }
+        }
+        __syncthreads();
+        stamp(4);
+        local_argmax(kk + 1, kk + 1);
+        stamp(14);
+        grid_bar_count(g.bar, (unsigned)(++nbar * G));
+        stamp(5);
+    }
+
+    if (tl)
+        for (int i = 0; i < 16; ++i) g.tlog[i] += s_tacc[i];
+    // the pinned segments back to normal eviction priority
+    if (g.pin_segs > 0) {
+        const int64_t rows_pin = tmin<int64_t>(m, (int64_t)g.pin_segs * kSegT);
+        const int64_t lines = ceil_div_d(rows_pin * 8, 128);
+        for (int64_t i = threadIdx.x; i < nown * lines; i += kTThreads) {
+            const double* ln = g.Y + (c0 + i / lines) * ldy + (i % lines) * 16;
+            asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(ln) : "memory");
+        }
+    }
+    // ---- outputs: perm, Rtop, numerical rank ----
+    for (int64_t jj = threadIdx.x; jj < nown; jj += kTThreads) {
+        const int64_t j = c0 + jj, p = spos[jj];
+        g.perm[p] = (int32_t)j;
+        for (int64_t q = 0; q < k; ++q) g.Rtop[q * n + p] = (p >= q) ? g.Rcol[j * k + q] : 0.0;
+    }
+    if (b == 0 && threadIdx.x == 0) {
+        const double lead = fabs(g.beta[0]);
+        int32_t nr = 0;
+        if (lead != 0.0)
+            for (int64_t q = 0; q < k; ++q) nr += fabs(g.beta[q]) > g.rank_tol * lead ? 1 : 0;
+        *g.numerical_rank = nr;
+    }
+}
+
+size_t tall_smem_bytes(int64_t m, int64_t k, int64_t G) {
+    const int64_t mpad = ceil_div(m, (int64_t)kSegT) * kSegT;
+    const int64_t rmax = ceil_div(m, G);
+    return (size_t)(mpad + kMaxOwn * (mpad / kSegT) + 3 * k + 3 * kMaxOwn + kMaxOwn * k + rmax * k) *
+               sizeof(double) +
+           (size_t)kMaxOwn * sizeof(int64_t);
+}
+
+template <class W>
+void carve_tall(W& ws, int64_t m, int64_t n, int64_t k, int64_t G, TallArgs& a) {
+    a.F = ws.template take<double>(n * k);
+    a.Rcol = ws.template take<double>(n * k);
+    a.V = ws.template take<double>(m * k);
+    a.tau = ws.template take<double>(k);
+    a.beta = ws.template take<double>(k);
+    a.a = ws.template take<double>(m + 2);  // a[m] stays zero (bulk copies round up)
+    a.normpart = ws.template take<double>(G);
+    a.zpart = ws.template take<double>(G * k);
+    a.red = ws.template take<double>(k + 1);
+    a.piv = ws.template take<int64_t>(4);
+    a.flag_list = ws.template take<int64_t>(n);
+    a.amax = ws.template take<ArgMax>(G);
+    a.bar = ws.template take<unsigned>(4);
+}
+
 int64_t* g_cpqr_tlog = nullptr;  // debug: per-phase timing of the cooperative kernel
 
 }  // namespace
@@ -1012,7 +1586,10 @@ extern "C" size_t ids_cpqr_workspace_bytes(int64_t rows, int64_t cols, int64_t k
     CountCarve c;
     CpqrArgs a{};
     carve_cpqr(c, rows, cols, k, kMaxG, a);
-    return c.off + 256;
+    CountCarve c2;
+    TallArgs t{};
+    carve_tall(c2, rows, cols, k, kMaxG, t);
+    return tmax(c.off, c2.off) + 256;
 }
 
 extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, int64_t ldy,
@@ -1083,6 +1660,52 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
             ids_count_launch();
             if (Q) {
                 form_q_kernel<<<(unsigned)k, kThreads, 0, st>>>(ca.Vout, ca.tauout, rows, k, Q);
+                IDS_LAUNCH_CHECK();
+            }
+            return IDS_OK;
+        }
+    }
+    if (rows > 1024 && k <= kTallMaxK && !getenv("IDS_CPQR_SEGMENT_UNITS")) {
+        // tall sketch: column-owning CTAs, v in shared memory
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int G = (int)tmin<int64_t>(tmin<int64_t>(sms, kMaxG), cols);
+        const size_t smem = tall_smem_bytes(rows, k, G);
+        if (ceil_div(cols, (int64_t)G) <= kMaxOwn && ceil_div(rows, (int64_t)G) <= kTThreads &&
+            smem <= 200 * 1024) {
+            TallArgs t{};
+            t.Y = Y;
+            t.m = rows;
+            t.n = cols;
+            t.ldy = ldy;
+            t.k = k;
+            t.colnorm2 = colnorm2;
+            t.rank_tol = rank_tol;
+            t.perm = perm;
+            t.Rtop = Rtop;
+            t.numerical_rank = numerical_rank;
+            t.tlog = g_cpqr_tlog;
+            // the leading 2 x 2048 rows of every column stay in L2 across the k
+            // passes (64 MB at C5; larger pins measured slower)
+            t.pin_segs = 2;
+            if (const char* e = getenv("IDS_CPQR_PIN")) t.pin_segs = atoi(e);  // experiments
+            WsCarve ws(workspace, ws_bytes);
+            carve_tall(ws, rows, cols, k, kMaxG, t);
+            if (!ws.ok()) {
+                ids_set_last_error("cpqr: workspace too small");
+                return IDS_EWORKSPACE;
+            }
+            IDS_CUDA_TRY(cudaMemsetAsync(t.bar, 0, 4 * sizeof(unsigned), st));
+            IDS_CUDA_TRY(cudaMemsetAsync(t.a + rows, 0, 2 * sizeof(double), st));
+            IDS_CUDA_TRY(cudaFuncSetAttribute(cpqr_tall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem));
+            void* args[] = {&t};
+            IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cpqr_tall_kernel, dim3(G), dim3(kTThreads),
+                                                     args, smem, st));
+            ids_count_launch();
+            if (Q) {
+                form_q_kernel<<<(unsigned)k, kThreads, 0, st>>>(t.V, t.tau, rows, k, Q);
                 IDS_LAUNCH_CHECK();
             }
             return IDS_OK;

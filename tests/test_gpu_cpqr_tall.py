@@ -57,3 +57,24 @@ def test_tall_cpqr_deficient_and_zero():
     assert np.array_equal(p1[:3], want.perm[:3])
     p1, r1, nr1 = _cpqr(np.zeros((2000, 30)), 4)
     assert nr1 == 0 and not np.any(r1)
+
+
+@pytest.mark.parametrize("m,n,k", [(5001, 777, 13), (2049, 9000, 7), (16384, 300, 1), (3000, 20, 20)])
+def test_column_owner_kernel_vs_segment_units_and_dgeqp3(m, n, k, monkeypatch):
+    """The column-owning tall CPQR (v in shared memory, two grid barriers per
+    step, L2-pinned leading segments) and the segment-unit kernel agree with
+    LAPACK's pivots (odd m: the bulk copy of the residual rounds up)."""
+    from paper_1901_10559_b200.linalg import device_cpqr
+
+    rng = np.random.default_rng(m + n + k)
+    base = rng.standard_normal((m, min(n, 12)))
+    y = base @ rng.standard_normal((min(n, 12), n)) + 1e-3 * rng.standard_normal((m, n))
+    yt = torch.from_numpy(np.ascontiguousarray(y.T)).cuda()
+    a = device_cpqr(yt, m, n, k)
+    monkeypatch.setenv("IDS_CPQR_SEGMENT_UNITS", "1")
+    b = device_cpqr(yt, m, n, k)
+    want = oracle.cpqr(y, k)
+    assert np.array_equal(a.perm[:k].cpu().numpy(), want.perm[:k])
+    assert np.array_equal(b.perm[:k].cpu().numpy(), want.perm[:k])
+    ra, rb = a.rtop.cpu().numpy(), b.rtop.cpu().numpy()
+    assert np.abs(ra - rb).max() <= 1e-11 * np.abs(rb).max()

@@ -11,6 +11,8 @@ lib = _native.load()
 lib.ids_debug_cpqr_timing.argtypes = [ctypes.c_void_p]
 NAMES = ["pivot col", "sync norm", "gemv", "sync gemv", "F/R columns",
          "recompute", "argmax", "sync step", "hh+z", "z-reduce"]
+TALL = ["S1 z loop", "barrier A", "V rows", "gemv", "F/R/downdate", "barrier B", "norm+a loads",
+        "hh", "S1 pivot", "S1 y/f loads", "S1 resid+sum", "alpha", "scale", "sykk", "argmax"]
 
 
 def near_dup(m, n, base, pert, seed):
@@ -24,27 +26,31 @@ def near_dup(m, n, base, pert, seed):
 
 CLUSTER = ["pivot select", "pivot col", "householder", "gemv+z", "F/R/downdate",
            "recompute", "argmax", "cluster sync"]
-for name, m, n, k, base, pert in (("C2", 100, 2000, 20, 20, 1e-2), ("C1", 40, 1000, 10, 10, 1e-2),
-                                  ("C4", 4096, 1000, 10, 10, 1e-3),
-                                  ("C5", 16384, 2000, 20, 20, 1e-4),
-                                  ("C3", 200, 10000, 20, 20, 1e-2)):
-    y = near_dup(m, n, base, pert, 1)
-    for _ in range(3):
-        device_cpqr(y, m, n, k)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(10):
-        device_cpqr(y, m, n, k)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 10
-    buf = torch.zeros(16, dtype=torch.int64, device="cuda")
-    lib.ids_debug_cpqr_timing(buf.data_ptr())
-    device_cpqr(y, m, n, k)
-    torch.cuda.synchronize()
-    lib.ids_debug_cpqr_timing(None)
-    t = buf.cpu().numpy()
-    print(f"{name}: {m}x{n} k={k}: {ms * 1e3:.1f} us per call; flagged {t[15]}")
-    for i, nm in enumerate(CLUSTER if m <= 1024 and name in ("C2", "C1") else NAMES):
-        print(f"   {nm:14s} {t[i] / 1e3:9.1f} us  ({t[i] / 1e3 / k:6.2f}/step)")
+if __name__ != "__main__":
+    pass
+else:
+  for name, m, n, k, base, pert in (("C2", 100, 2000, 20, 20, 1e-2), ("C1", 40, 1000, 10, 10, 1e-2),
+                                    ("C4", 4096, 1000, 10, 10, 1e-3),
+                                    ("C5", 16384, 2000, 20, 20, 1e-4),
+                                    ("C3", 200, 10000, 20, 20, 1e-2)):
+      y = near_dup(m, n, base, pert, 1)
+      for _ in range(3):
+          device_cpqr(y, m, n, k)
+      torch.cuda.synchronize()
+      e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+      e0.record()
+      for _ in range(10):
+          device_cpqr(y, m, n, k)
+      e1.record()
+      torch.cuda.synchronize()
+      ms = e0.elapsed_time(e1) / 10
+      buf = torch.zeros(16, dtype=torch.int64, device="cuda")
+      lib.ids_debug_cpqr_timing(buf.data_ptr())
+      device_cpqr(y, m, n, k)
+      torch.cuda.synchronize()
+      lib.ids_debug_cpqr_timing(None)
+      t = buf.cpu().numpy()
+      print(f"{name}: {m}x{n} k={k}: {ms * 1e3:.1f} us per call; flagged {t[15]}")
+      names = CLUSTER if m <= 1024 and name in ("C2", "C1") else (TALL if m > 1024 else NAMES)
+      for i, nm in enumerate(names):
+          print(f"   {nm:14s} {t[i] / 1e3:9.1f} us  ({t[i] / 1e3 / k:6.2f}/step)")
