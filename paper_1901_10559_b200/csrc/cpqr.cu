@@ -1036,6 +1036,7 @@ struct TallArgs {
     unsigned* bar;
     int64_t* tlog;
     int pin_segs;  // leading 2048-row segments of each column kept in L2 (evict_last)
+    int tmem;      // resident units in tensor memory
 };
 
 __device__ __forceinline__ double block_sum_t(double v, double* red) {
@@ -1180,6 +1181,39 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)
 
 __device__ __forceinline__ int64_t ceil_div_d(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// 16 doubles of this thread's TMEM lane (32 consecutive 32-bit columns)
+__device__ __forceinline__ void tm_st_x32(uint32_t ta, const double* v) {
+    uint32_t r[32];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        r[2 * i] = (uint32_t)__double2loint(v[i]);
+        r[2 * i + 1] = (uint32_t)__double2hiint(v[i]);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(ta),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+        "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+        "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tm_ld_x32(uint32_t ta, double* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(ta)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+
 // Y loads with an L2 eviction policy: the pinned segments of every column
 // (read again by each of the k GEMV passes) evict_last, the rest evict_first
 __device__ __forceinline__ double ld_pol(const double* p, uint64_t pol) {
@@ -1220,6 +1254,22 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
     const double tol3z = sqrt(DBL_EPSILON);
     int64_t* flagged = g.flag_list + c0;
     unsigned nbar = 0;
+    // resident units: warp w keeps (column w / Sres, segment pin + w % Sres),
+    // one of the non-pinned segments, in its quarter of TMEM (128 columns x
+    // 32 lanes = 2048 doubles)
+    const int64_t pin = tmin<int64_t>(g.pin_segs, nsegT);
+    const int64_t Sres = nsegT - pin;
+    const int nres = g.tmem ? (int)tmin<int64_t>(kTWarps, Sres > 0 ? nown * Sres : 0) : 0;
+    __shared__ uint32_t s_tm;
+    if (g.tmem && wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&s_tm))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm_base = g.tmem ? s_tm : 0u;
     uint64_t pol_keep, pol_stream;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
@@ -1409,22 +1459,66 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
         stamp(7);
         stamp(2);
 
-        // ---- GEMV over the owned columns: units (column, 2048-row segment),
-        // two per warp at a time, walked backwards on odd steps ----
+        // ---- GEMV over the owned columns: units (column, 2048-row segment).
+        // Warp w's resident unit (one non-pinned segment) lives in TENSOR MEMORY
+        // after the first pass; the other units stream from L2 (pinned
+        // segments) or DRAM, two per warp at a time, walked backwards on odd
+        // steps ----
         {
-            const int64_t U = nown * nsegT;
+            if (wid < nres) {  // this warp's resident unit
+                const int64_t jr = (int64_t)wid / Sres, sr = pin + (int64_t)wid % Sres;
+                const uint32_t ta = tm_base + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)((wid >> 2) * 128);
+                const bool act = spos[jr] > kk;
+                const double* pr = g.Y + (c0 + jr) * ldy;
+                double s1 = 0.0, t1 = 0.0;
+#pragma unroll 1
+                for (int qtr = 0; qtr < 4; ++qtr) {
+                    const int64_t br = sr * kSegT + qtr * (kSegT / 4) + lane;
+                    double yr[kSegTLoads];
+                    if (kk == 0) {  // first pass: from memory, kept in TMEM
+#pragma unroll
+                        for (int u = 0; u < kSegTLoads; ++u)
+                            yr[u] = __ldg(pr + tmin<int64_t>(br + 32 * u, m - 1));
+                        tm_st_x32(ta + 32 * qtr, yr);
+                    } else {
+                        tm_ld_x32(ta + 32 * qtr, yr);
+                    }
+                    if (act) {
+#pragma unroll
+                        for (int u = 0; u < kSegTLoads; u += 2) {
+                            s1 = fma(yr[u], vsm[br + 32 * u], s1);
+                            t1 = fma(yr[u + 1], vsm[br + 32 * u + 32], t1);
+                        }
+                    }
+                }
+                if (kk == 0) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                const double wr = warp_sum(s1 + t1);
+                if (lane == 0 && act) part[jr * nsegT + sr] = wr;
+            }
+            const int64_t U = nown * nsegT - nres;  // streamed units
+            const int64_t npin = nown * pin;
+            auto unit_of = [&](int64_t li, int64_t& j, int64_t& sg) {
+                if (li < npin) {
+                    j = li / pin;
+                    sg = li % pin;
+                } else {
+                    const int64_t e = nres + (li - npin);
+                    j = e / Sres;
+                    sg = pin + e % Sres;
+                }
+            };
             const bool rev = kk & 1;
             const bool full = m == mpad;
             for (int64_t li = wid; li < U; li += 2 * kTWarps) {
                 const bool h2 = li + kTWarps < U;
-                const int64_t ua = rev ? U - 1 - li : li;
-                const int64_t ub = h2 ? (rev ? U - 1 - (li + kTWarps) : li + kTWarps) : ua;
-                const int64_t ja = ua / nsegT, sa = ua % nsegT, jb = ub / nsegT, sb = ub % nsegT;
+                int64_t ja, sa, jb, sb;
+                unit_of(rev ? U - 1 - li : li, ja, sa);
+                unit_of(h2 ? (rev ? U - 1 - (li + kTWarps) : li + kTWarps) : (rev ? U - 1 - li : li), jb, sb);
                 const bool aa = spos[ja] > kk, ab = h2 && spos[jb] > kk;
                 const double* pa = g.Y + (c0 + ja) * ldy;
                 const double* pb = g.Y + (c0 + jb) * ldy;
-                const uint64_t pola = sa < g.pin_segs ? pol_keep : pol_stream;
-                const uint64_t polb = sb < g.pin_segs ? pol_keep : pol_stream;
+                const uint64_t pola = sa < pin ? pol_keep : pol_stream;
+                const uint64_t polb = sb < pin ? pol_keep : pol_stream;
                 double s1 = 0.0, s2 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll 1
                 for (int qtr = 0; qtr < 4; ++qtr) {
@@ -1525,6 +1619,12 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
 
     if (tl)
         for (int i = 0; i < 16; ++i) g.tlog[i] += s_tacc[i];
+    if (g.tmem) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (wid == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base) : "memory");
+    }
     // the pinned segments back to normal eviction priority
     if (g.pin_segs > 0) {
         const int64_t rows_pin = tmin<int64_t>(m, (int64_t)g.pin_segs * kSegT);
@@ -1689,7 +1789,9 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
             // the leading 2 x 2048 rows of every column stay in L2 across the k
             // passes (64 MB at C5; larger pins measured slower)
             t.pin_segs = 2;
+            t.tmem = 1;
             if (const char* e = getenv("IDS_CPQR_PIN")) t.pin_segs = atoi(e);  // experiments
+            if (const char* e = getenv("IDS_CPQR_TMEM")) t.tmem = atoi(e);
             WsCarve ws(workspace, ws_bytes);
             carve_tall(ws, rows, cols, k, kMaxG, t);
             if (!ws.ok()) {
