@@ -474,7 +474,10 @@ class TensorWorkload:
         self.bytes_local = self.N * self.I * (self.c1 - self.c0) * 8
         self.bytes_total = self.N * self.I * self.R * 8
         self.flops_local = (self.N + 1) * (self.c1 - self.c0) * 2.5 * self.L * np.log2(self.L)
-        self.kernel_name = "tensorsketch_kernel"
+        from paper_1901_10559_b200.tensorsketch import uses_split_kernel
+
+        self.kernel_name = ("ts_split_kernel" if uses_split_kernel(self.N, self.L)
+                            else "tensorsketch_kernel")
         self.graph = None
 
         class _X:

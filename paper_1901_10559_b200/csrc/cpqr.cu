@@ -1020,6 +1020,7 @@ constexpr int kSegT = 2048;   // GEMV unit: rows of one owned column
 constexpr int kSegTLoads = kSegT / 32 / 4;  // loads per lane per quarter unit (16)
 constexpr int kMaxOwn = 64;   // owned columns per CTA
 constexpr int kTallMaxK = 256;
+constexpr int kMaxSegT = 16;  // v segments (rows <= 16 x 2048)
 
 struct TallArgs {
     const double* Y;
@@ -1247,7 +1248,8 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
     __shared__ int s_nflag;
     __shared__ int64_t s_piv[3];
     __shared__ double s_nrm;
-    __shared__ __align__(8) uint64_t s_mb;
+    __shared__ __align__(8) uint64_t s_mb[kMaxSegT];  // one per v segment
+    __shared__ double s_scal, s_tau, s_beta;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t c0 = n * b / G, c1 = n * (b + 1) / G, nown = c1 - c0;
     const int64_t r0 = m * b / G, r1 = m * (b + 1) / G, nrow = r1 - r0;
@@ -1305,7 +1307,8 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
     // ---- prologue: zero v (its padding stays zero), owned columns' norms ----
     for (int64_t r = threadIdx.x; r < mpad; r += kTThreads) vsm[r] = 0.0;
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_mb)) : "memory");
+        for (int sg = 0; sg < nsegT; ++sg)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_mb[sg])) : "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     for (int64_t jj = wid; jj < nown; jj += kTWarps) {
@@ -1374,7 +1377,10 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
             for (int64_t q = 0; q < kk; ++q) s4[q & 3] = fma(vr[q], fpiv[q], s4[q & 3]);
             av = yrr - ((s4[0] + s4[1]) + (s4[2] + s4[3]));
         }
-        if (threadIdx.x < nrow) g.a[rr] = av;
+        if (threadIdx.x < nrow) {
+            g.a[rr] = rr == kk ? 0.0 : av;  // v's row kk enters the GEMV as Y[kk, j]
+            if (rr == kk) g.red[0] = av;      // alpha
+        }
         const double ac = rr > kk ? av : 0.0;  // rows below kk enter the norm and z~
         const double ss = block_sum_t(ac * ac, red);
         if (threadIdx.x == 0) g.normpart[b] = ss;
@@ -1397,67 +1403,57 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
         grid_bar_count(g.bar, (unsigned)(++nbar * G));
         stamp(1);
 
-        // ---- S2: a[] into shared memory by one bulk copy, ||a[kk+1:]|| (fixed-
-        // order sum of the partials), Householder, v = a * scal ----
+        // ---- S2: a[] into shared memory by one bulk copy per 2048-row segment
+        // (each GEMV unit waits only for its own segment), ||a[kk+1:]|| (fixed-
+        // order sum of the partials) and the Householder scalars ----
         if (threadIdx.x == 0) {
-            const uint32_t bytes = (uint32_t)(((m + 1) / 2) * 16);  // a[m] is a zero pad
             asm volatile("fence.proxy.async;" ::: "memory");
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&s_mb)),
-                         "r"(bytes)
-                         : "memory");
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    smem_addr(vsm)),
-                "l"(g.a), "r"(bytes), "r"(smem_addr(&s_mb))
-                : "memory");
+            for (int sg = 0; sg < nsegT; ++sg) {
+                const int64_t lo = (int64_t)sg * kSegT, hi = tmin<int64_t>(m, lo + kSegT);
+                const uint32_t bytes = (uint32_t)(((hi - lo + 1) / 2) * 16);  // a[m] is a zero pad
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                 smem_addr(&s_mb[sg])),
+                             "r"(bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(vsm + lo)),
+                    "l"(g.a + lo), "r"(bytes), "r"(smem_addr(&s_mb[sg]))
+                    : "memory");
+            }
         }
         if (wid == 1) {
             const double x = warp_sum_partials_cg(g.normpart, G);
-            if (lane == 0) s_nrm = x;
+            if (lane == 0) {
+                const double alpha = __ldcg(g.red);
+                const double xnorm = sqrt(x);
+                double tau, beta, scal;
+                if (xnorm == 0.0) {
+                    tau = 0.0;
+                    beta = alpha;
+                    scal = 0.0;
+                } else {
+                    beta = -copysign(dlapy2(alpha, xnorm), alpha);
+                    tau = (beta - alpha) / beta;
+                    scal = 1.0 / (alpha - beta);
+                }
+                s_scal = scal;
+                s_tau = tau;
+                s_beta = beta;
+            }
         }
-        asm volatile(
-            "{\n\t.reg .pred p;\n"
-            "CPQR_WAIT_%=:\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-            "@!p bra CPQR_WAIT_%=;\n}" ::"r"(smem_addr(&s_mb)),
-            "r"((uint32_t)(kk & 1))
-            : "memory");
-        __syncthreads();
-        stamp(6);
-        const double alpha = vsm[kk];
-        const double xnorm = sqrt(s_nrm);
-        stamp(11);
-        double tau, beta, scal;
-        if (xnorm == 0.0) {
-            tau = 0.0;
-            beta = alpha;
-            scal = 0.0;
-        } else {
-            beta = -copysign(dlapy2(alpha, xnorm), alpha);
-            tau = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
-        }
-        // v = a * scal below kk and 1 at kk: the GEMV uses a (zero at rows <= kk)
-        // and adds Y[kk, j] after scaling its dot: W_j = scal * Y[kk+1:, j]^T a + Y[kk, j]
-        if (b == 0 && threadIdx.x == 0) {
-            g.tau[kk] = tau;
-            g.beta[kk] = beta;
-        }
-        if (threadIdx.x == 0 && cs >= c0 && cs < c1) g.Rcol[cs * k + kk] = beta;
         if (threadIdx.x == 0) s_nflag = 0;
-        __syncthreads();  // everyone has read alpha
-        if (threadIdx.x == 0) vsm[kk] = 0.0;
-        stamp(12);
         for (int64_t jj = threadIdx.x; jj < nown; jj += kTThreads) sykk[jj] = __ldg(g.Y + (c0 + jj) * ldy + kk);
-        __syncthreads();
-        stamp(13);
-        if (threadIdx.x < nrow) {  // V[r, kk] of the owned rows (global: other CTAs' row kk, form_q)
-            const double vr = rr < kk ? 0.0 : rr == kk ? 1.0 : vsm[rr] * scal;
-            vown[threadIdx.x * k + kk] = vr;
-            g.V[kk * m + rr] = vr;
-        }
-        stamp(7);
         stamp(2);
+        auto wait_seg = [&](int64_t sg) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n"
+                "CPQR_WAIT_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra CPQR_WAIT_%=;\n}" ::"r"(smem_addr(&s_mb[sg])),
+                "r"((uint32_t)(kk & 1))
+                : "memory");
+        };
 
         // ---- GEMV over the owned columns: units (column, 2048-row segment).
         // Warp w's resident unit (one non-pinned segment) lives in TENSOR MEMORY
@@ -1483,6 +1479,7 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
                     } else {
                         tm_ld_x32(ta + 32 * qtr, yr);
                     }
+                    if (qtr == 0) wait_seg(sr);
                     if (act) {
 #pragma unroll
                         for (int u = 0; u < kSegTLoads; u += 2) {
@@ -1535,6 +1532,10 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
                             yb[u] = ab ? ld_pol(pb + tmin<int64_t>(bb + 32 * u, m - 1), polb) : 0.0;
                         }
                     }
+                    if (qtr == 0) {
+                        wait_seg(sa);
+                        wait_seg(sb);
+                    }
 #pragma unroll
                     for (int u = 0; u < kSegTLoads; u += 2) {
                         s1 = fma(ya[u], vsm[ba + 32 * u], s1);
@@ -1550,6 +1551,18 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
                 }
             }
         }
+        __syncthreads();  // s_scal / s_tau / s_beta
+        const double scal = s_scal, tau = s_tau, beta = s_beta;
+        if (threadIdx.x < nrow) {  // V[r, kk] of the owned rows (global: other CTAs' row kk, form_q)
+            const double vr = rr < kk ? 0.0 : rr == kk ? 1.0 : vsm[rr] * scal;
+            vown[threadIdx.x * k + kk] = vr;
+            g.V[kk * m + rr] = vr;
+        }
+        if (b == 0 && threadIdx.x == 0) {
+            g.tau[kk] = tau;
+            g.beta[kk] = beta;
+        }
+        if (threadIdx.x == 0 && cs >= c0 && cs < c1) g.Rcol[cs * k + kk] = beta;
         // z_q = V[:, q]^T v = V[kk, q] + scal * (fixed-order sum of the z~ partials)
         for (int64_t q = wid; q < kk; q += kTWarps) {
             const double x = warp_sum_partials_cg(g.zpart + q * G, G);
@@ -1773,7 +1786,7 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
         const int G = (int)tmin<int64_t>(tmin<int64_t>(sms, kMaxG), cols);
         const size_t smem = tall_smem_bytes(rows, k, G);
         if (ceil_div(cols, (int64_t)G) <= kMaxOwn && ceil_div(rows, (int64_t)G) <= kTThreads &&
-            smem <= 200 * 1024) {
+            ceil_div(rows, (int64_t)kSegT) <= kMaxSegT && smem <= 200 * 1024) {
             TallArgs t{};
             t.Y = Y;
             t.m = rows;
