@@ -1121,10 +1121,10 @@ static_assert(sizeof(ArgMax) == 32, "ArgMax is read as two 16-byte words");
 __device__ ArgMax reduce_partials_warp_cg(const ArgMax* part, int64_t G) {
     const int lane = threadIdx.x & 31;
     ArgMax best{-1.0, INT64_MAX, -1, -1};
-    for (int64_t i0 = 0; i0 < G; i0 += 128) {
-        ArgMax o[4];
+    for (int64_t i0 = 0; i0 < G; i0 += 160) {  // one batch of loads for G <= 160
+        ArgMax o[5];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 5; ++u) {
             const int64_t i = i0 + lane + 32 * u;
             if (i < G) {
                 const double2* w = reinterpret_cast<const double2*>(part + i);
@@ -1136,7 +1136,7 @@ __device__ ArgMax reduce_partials_warp_cg(const ArgMax* part, int64_t G) {
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 5; ++u) {
             if (better(o[u].val, o[u].pos, best.val, best.pos)) {
                 best.val = o[u].val;
                 best.pos = o[u].pos;
