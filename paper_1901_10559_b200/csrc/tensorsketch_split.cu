@@ -664,27 +664,62 @@ struct PlanOut {
 // one block scan of the per-slot (later rows, has-group) counts.  Returns the
 // chunk's later-row total; writes codes and groups when it is <= cap.
 __device__ int plan_chunk(const int32_t* __restrict__ bucket, const int8_t* __restrict__ sign, int i0,
-                          int i1, int N2, int cap, int32_t* cnt, int32_t* rank, int32_t* s_part,
+                          int i1, int N2, int cap, int32_t* cnt, int32_t* rank, uint16_t* wc, int32_t* s_part,
                           uint32_t* __restrict__ code, uint2* __restrict__ gc, int32_t* ngroups) {
-    const int T = blockDim.x, t = threadIdx.x;
-    for (int s = t; s < N2; s += T) cnt[s] = 0;
-    __syncthreads();
-    if (t < 32) {
-        const int lane = t;
-        const unsigned lt = (1u << lane) - 1u;
-        for (int base = i0; base < i1; base += 32) {
-            const int i = base + lane;
-            const bool ok = i < i1;
-            const int slot = ok ? bucket[i] & (N2 - 1) : 0;
-            const int key = ok ? slot : -1 - lane;
-            const unsigned m = __match_any_sync(0xffffffffu, key);
-            const int bc = ok ? cnt[slot] : 0;
-            __syncwarp();
-            if (ok && (m >> lane) == 1u) cnt[slot] = bc + __popc(m);  // highest lane of its group
-            __syncwarp();
-            if (ok) rank[i - i0] = bc + __popc(m & lt);
+    // The rows' (slot, b >= N2, sign) are staged in shared memory first
+    // (rank[] holds slot | hi << 13 | neg << 14, the rank joins at << 15).
+    // Every warp walks its own eighth of the rows in order (32 at a time,
+    // __match_any_sync resolves equal slots) against its own 16-bit slot
+    // counters; the per-warp counts are then turned into bases by a prefix
+    // over the warps, so rank = base[warp][slot] + rank inside the warp's part.
+    const int T = blockDim.x, t = threadIdx.x, w = t >> 5, lane = t & 31, NW = T >> 5;
+    const int len = i1 - i0;
+    for (int q0 = 0; q0 < len; q0 += 8 * T) {  // eight loads of each array in flight
+        int32_t bb[8];
+        int8_t sg[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * T + t;
+            bb[u] = q < len ? __ldg(bucket + i0 + q) : 0;
+            sg[u] = q < len ? __ldg(sign + i0 + q) : (int8_t)1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * T + t;
+            if (q < len) rank[q] = (bb[u] & (N2 - 1)) | (bb[u] >= N2 ? 1 << 13 : 0) | (sg[u] < 0 ? 1 << 14 : 0);
         }
     }
+    for (int q = t; q < NW * N2 / 8; q += T) reinterpret_cast<uint4*>(wc)[q] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int sub = (len + NW - 1) / NW;
+    const int wa = w * sub, wb = min(len, wa + sub);
+    uint16_t* mine = wc + w * N2;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = wa; base < wb; base += 32) {
+        const int q = base + lane;
+        const bool ok = q < wb;
+        const int e = ok ? rank[q] : 0;
+        const int slot = e & (N2 - 1);
+        const int key = ok ? slot : -1 - lane;
+        const unsigned m = __match_any_sync(0xffffffffu, key);
+        const int bc = ok ? mine[slot] : 0;
+        __syncwarp();
+        if (ok && (m >> lane) == 1u) mine[slot] = (uint16_t)(bc + __popc(m));  // highest lane of its group
+        __syncwarp();
+        if (ok) rank[q] = e | ((bc + __popc(m & lt)) << 15);
+    }
+    __syncthreads();
+    for (int sl = t; sl < N2; sl += T) {  // per-warp counts -> bases; totals
+        int run = 0;
+        for (int v = 0; v < NW; ++v) {
+            const int c = wc[v * N2 + sl];
+            wc[v * N2 + sl] = (uint16_t)run;
+            run += c;
+        }
+        cnt[sl] = run;
+    }
+    __syncthreads();
+    for (int q = t; q < len; q += T) rank[q] += (int)wc[(q / sub) * N2 + (rank[q] & (N2 - 1))] << 15;
     __syncthreads();
     // exclusive scan of packed (count - 1, count >= 2): low 16 bits later
     // rows, high 16 bits groups (both < 2^16 for the chunk sizes used)
@@ -728,13 +763,13 @@ __device__ int plan_chunk(const int32_t* __restrict__ bucket, const int8_t* __re
     }
     if (t == 0) *ngroups = total >> 16;
     __syncthreads();
-    for (int i = i0 + t; i < i1; i += T) {
-        const int b = bucket[i];
-        const int slot = b & (N2 - 1);
-        const int rk = rank[i - i0];
+    for (int q = t; q < len; q += T) {
+        const int e = rank[q];
+        const int slot = e & (N2 - 1);
+        const int rk = e >> 15;
         const uint32_t tp = rk == 0 ? kFirst : (uint32_t)((cnt[slot] & 0xFFFF) + rk - 1);
-        const uint32_t neg = sign[i] < 0 ? 1u : 0u, hi = b >= N2 ? 1u : 0u;
-        code[i] = split_idx(slot) | (neg << kSignShift) | ((neg ^ hi) << (kSignShift + 1)) | (tp << kTailShift);
+        const uint32_t neg = (e >> 14) & 1, hi = (e >> 13) & 1;
+        code[i0 + q] = split_idx(slot) | (neg << kSignShift) | ((neg ^ hi) << (kSignShift + 1)) | (tp << kTailShift);
     }
     __syncthreads();
     return total & 0xFFFF;
@@ -748,14 +783,15 @@ __global__ void ts_split_plan_single(const int32_t* __restrict__ bucket, const i
     __shared__ int32_t s_part[32];
     int32_t* cnt = sm;
     int32_t* rank = sm + N2;
-    const int tot = plan_chunk(bucket, sign, 0, dim, N2, cap, cnt, rank, s_part, out.code, out.groups,
+    uint16_t* wc = reinterpret_cast<uint16_t*>(sm + N2 + ((max(dim, cs) + 3) & ~3));
+    const int tot = plan_chunk(bucket, sign, 0, dim, N2, cap, cnt, rank, wc, s_part, out.code, out.groups,
                                out.ngroups);
     if (tot <= cap) {
         if (threadIdx.x == 0) out.hdr[0] = dim;
         return;
     }
     for (int c = 0; c * cs < dim; ++c)
-        plan_chunk(bucket, sign, c * cs, min(dim, (c + 1) * cs), N2, cs, cnt, rank, s_part, out.code,
+        plan_chunk(bucket, sign, c * cs, min(dim, (c + 1) * cs), N2, cs, cnt, rank, wc, s_part, out.code,
                    out.groups + (int64_t)c * (cs / 2), out.ngroups + c);
     if (threadIdx.x == 0) out.hdr[0] = cs;
 }
@@ -766,7 +802,8 @@ __global__ void ts_split_plan_chunks(const int32_t* __restrict__ bucket, const i
     extern __shared__ int32_t sm[];
     __shared__ int32_t s_part[32];
     const int c = blockIdx.x;
-    plan_chunk(bucket, sign, c * cs, min(dim, (c + 1) * cs), N2, cs, sm, sm + N2, s_part, out.code,
+    plan_chunk(bucket, sign, c * cs, min(dim, (c + 1) * cs), N2, cs, sm, sm + N2,
+               reinterpret_cast<uint16_t*>(sm + N2 + cs), s_part, out.code,
                out.groups + (int64_t)c * (cs / 2), out.ngroups + c);
     if (c == 0 && threadIdx.x == 0) out.hdr[0] = cs;
 }
@@ -865,11 +902,12 @@ extern "C" int ids_ts_split_plan(const int32_t* bucket, const int8_t* sign, int6
                 reinterpret_cast<uint2*>(base + split_groups_off(dim)),
                 reinterpret_cast<int32_t*>(base + split_ngroups_off(dim, out_dim))};
     if (dim <= kSingleMax) {
-        const size_t sm = (size_t)(N2 + tmax<int64_t>(dim, cs)) * sizeof(int32_t);
+        const int64_t rows = (tmax<int64_t>(dim, cs) + 3) & ~int64_t(3);
+        const size_t sm = (size_t)(N2 + rows) * sizeof(int32_t) + 8 * (size_t)N2 * sizeof(uint16_t);
         IDS_CUDA_TRY(cudaFuncSetAttribute(ts_split_plan_single, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         ts_split_plan_single<<<1, 256, sm, st>>>(bucket, sign, (int)dim, N2, cs, split_tail_cap(out_dim), out);
     } else {
-        const size_t sm = (size_t)(N2 + cs) * sizeof(int32_t);
+        const size_t sm = (size_t)(N2 + cs) * sizeof(int32_t) + 8 * (size_t)N2 * sizeof(uint16_t) + 16;
         IDS_CUDA_TRY(cudaFuncSetAttribute(ts_split_plan_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         ts_split_plan_chunks<<<(unsigned)ceil_div(dim, cs), 256, sm, st>>>(bucket, sign, (int)dim, N2, cs, out);
     }
