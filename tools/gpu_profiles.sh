@@ -27,7 +27,8 @@ full cs_rowmajor cs_rowmajor --workload C2
 full cs_coltile cs_coltile --workload C2 --fortran
 full cs_csr_stream cs_csr_stream --workload C3
 full fy_phaseb fy_phaseb_c3 --workload C3
-full tensorsketch_kernel tensorsketch_c4 --workload C4
-full tensorsketch_kernel tensorsketch_c5 --workload C5
-full "cpqr_kernel" cpqr_c5 --workload C5
+full ts_split_kernel ts_split_c4 --workload C4
+full ts_split_kernel ts_split_c5 --workload C5
+full cpqr_tall_kernel cpqr_tall_c5 --workload C5
+full cpqr_tall_kernel cpqr_tall_c4 --workload C4
 echo profiles done

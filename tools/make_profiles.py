@@ -34,6 +34,7 @@ METRICS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "lts__t_sectors_srcunit_tex_op_red.sum",
     "lts__t_sectors_srcunit_tex_op_red_lookup_hit.sum",
+    "lts__t_sector_hit_rate.pct", "smsp__issue_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -91,9 +92,17 @@ for rep, name, title, key in (
         ("pf_full_cs_coltile.ncu-rep", "cs_coltile", "cs_coltile_kernel, C2 in F order", None),
         ("pf_full_cs_csr_stream.ncu-rep", "cs_csr_stream", "cs_csr_stream_kernel, C3", "C3"),
         ("pf_full_fy_phaseb_c3.ncu-rep", "fy_phaseb_c3", "fy_phaseb_kernel, C3 hash (I = 1e7)", None),
-        ("pf_full_tensorsketch_c4.ncu-rep", "tensorsketch_c4", "tensorsketch_kernel<8>, C4", "C4"),
-        ("pf_full_tensorsketch_c5.ncu-rep", "tensorsketch_c5", "tensorsketch_kernel<16>, C5", "C5"),
-        ("pf_full_cpqr_c5.ncu-rep", "cpqr_c5", "cpqr_kernel, C5 sketch 16384 x 2000, k = 20", None)):
+        ("pf_full_tensorsketch_c4.ncu-rep", "tensorsketch_c4", "tensorsketch_kernel<8>, C4", None),
+        ("pf_full_tensorsketch_c5.ncu-rep", "tensorsketch_c5", "tensorsketch_kernel<16>, C5", None),
+        ("pf_full_cpqr_c5.ncu-rep", "cpqr_c5", "cpqr_kernel, C5 sketch 16384 x 2000, k = 20", None),
+        ("pf_full_ts_split_c4.ncu-rep", "ts_split_c4", "ts_split_kernel<1024> (split-spectrum TensorSketch), C4",
+         "C4"),
+        ("pf_full_ts_split_c5.ncu-rep", "ts_split_c5", "ts_split_kernel<4096> (split-spectrum TensorSketch), C5",
+         "C5"),
+        ("pf_full_cpqr_tall_c5.ncu-rep", "cpqr_tall_c5",
+         "cpqr_tall_kernel (column-owning CPQR), C5 sketch 16384 x 2000, k = 20", None),
+        ("pf_full_cpqr_tall_c4.ncu-rep", "cpqr_tall_c4",
+         "cpqr_tall_kernel (column-owning CPQR), C4 sketch 4096 x 1000, k = 10", None)):
     p = os.path.join(OUT, rep)
     if os.path.exists(p):
         full(p, os.path.join(PROF, f"{rnd}_{name}_ncu_full.txt"), title)
