@@ -1016,9 +1016,7 @@ constexpr int64_t kMaxG = 148;
 // against three grid syncs and two all-CTA partial reductions before.
 constexpr int kTThreads = 512;
 constexpr int kTWarps = kTThreads / 32;
-constexpr int kSegT = 2048;   // GEMV unit: rows of one owned column
-constexpr int kSegTLoads = kSegT / 32 / 4;  // loads per lane per quarter unit (16)
-constexpr int kMaxOwn = 64;   // owned columns per CTA
+constexpr int kMaxOwn = 128;  // owned columns per CTA
 constexpr int kTallMaxK = 256;
 constexpr int kMaxSegT = 16;  // v segments (rows <= 16 x 2048)
 
@@ -1223,7 +1221,12 @@ __device__ __forceinline__ double ld_pol(const double* p, uint64_t pol) {
     return v;
 }
 
+// SEG: rows of one GEMV unit (2048 for tall sketches; 256 for short, wide
+// ones such as C3's 200 x 10000)
+template <int SEG>
 __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
+    constexpr int kSegT = SEG;
+    constexpr int kSegTLoads = kSegT / 32 / 4;  // loads per lane per quarter unit
     extern __shared__ double vsm[];
     const int64_t m = g.m, n = g.n, k = g.k, ldy = g.ldy;
     const int64_t mpad = (m + kSegT - 1) / kSegT * kSegT;
@@ -1261,7 +1264,7 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
     // 32 lanes = 2048 doubles)
     const int64_t pin = tmin<int64_t>(g.pin_segs, nsegT);
     const int64_t Sres = nsegT - pin;
-    const int nres = g.tmem ? (int)tmin<int64_t>(kTWarps, Sres > 0 ? nown * Sres : 0) : 0;
+    const int nres = (SEG == 2048 && g.tmem) ? (int)tmin<int64_t>(kTWarps, Sres > 0 ? nown * Sres : 0) : 0;
     __shared__ uint32_t s_tm;
     if (g.tmem && wid == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&s_tm))
@@ -1461,7 +1464,7 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
         // segments) or DRAM, two per warp at a time, walked backwards on odd
         // steps ----
         {
-            if (wid < nres) {  // this warp's resident unit
+            if (SEG == 2048 && wid < nres) {  // this warp's resident unit
                 const int64_t jr = (int64_t)wid / Sres, sr = pin + (int64_t)wid % Sres;
                 const uint32_t ta = tm_base + ((uint32_t)(32 * (wid & 3)) << 16) + (uint32_t)((wid >> 2) * 128);
                 const bool act = spos[jr] > kk;
@@ -1662,10 +1665,10 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
     }
 }
 
-size_t tall_smem_bytes(int64_t m, int64_t k, int64_t G) {
-    const int64_t mpad = ceil_div(m, (int64_t)kSegT) * kSegT;
+size_t tall_smem_bytes(int64_t m, int64_t k, int64_t G, int64_t seg) {
+    const int64_t mpad = ceil_div(m, seg) * seg;
     const int64_t rmax = ceil_div(m, G);
-    return (size_t)(mpad + kMaxOwn * (mpad / kSegT) + 3 * k + 3 * kMaxOwn + kMaxOwn * k + rmax * k) *
+    return (size_t)(mpad + kMaxOwn * (mpad / seg) + 3 * k + 3 * kMaxOwn + kMaxOwn * k + rmax * k) *
                sizeof(double) +
            (size_t)kMaxOwn * sizeof(int64_t);
 }
@@ -1778,15 +1781,21 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
             return IDS_OK;
         }
     }
-    if (rows > 1024 && k <= kTallMaxK && !getenv("IDS_CPQR_SEGMENT_UNITS")) {
-        // tall sketch: column-owning CTAs, v in shared memory
+    // (short wide sketches -- C3's 200 x 10000 -- measured faster on the
+    // segment-unit kernel: 348 vs 401 us; the 256-row variant stays for them
+    // to opt into with IDS_CPQR_WIDE=1)
+    const bool tall = rows > 1024, wide = rows >= 128 && cols >= 4096 && getenv("IDS_CPQR_WIDE");
+    if ((tall || wide) && k <= kTallMaxK && !getenv("IDS_CPQR_SEGMENT_UNITS")) {
+        // column-owning CTAs, v in shared memory (GEMV units of 2048 rows for
+        // tall sketches, 256 for short wide ones)
+        const int64_t seg = tall ? 2048 : 256;
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int G = (int)tmin<int64_t>(tmin<int64_t>(sms, kMaxG), cols);
-        const size_t smem = tall_smem_bytes(rows, k, G);
+        const size_t smem = tall_smem_bytes(rows, k, G, seg);
         if (ceil_div(cols, (int64_t)G) <= kMaxOwn && ceil_div(rows, (int64_t)G) <= kTThreads &&
-            ceil_div(rows, (int64_t)kSegT) <= kMaxSegT && smem <= 200 * 1024) {
+            ceil_div(rows, seg) <= kMaxSegT && smem <= 200 * 1024) {
             TallArgs t{};
             t.Y = Y;
             t.m = rows;
@@ -1813,11 +1822,11 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
             }
             IDS_CUDA_TRY(cudaMemsetAsync(t.bar, 0, 4 * sizeof(unsigned), st));
             IDS_CUDA_TRY(cudaMemsetAsync(t.a + rows, 0, 2 * sizeof(double), st));
-            IDS_CUDA_TRY(cudaFuncSetAttribute(cpqr_tall_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem));
+            auto kern = seg == 2048 ? cpqr_tall_kernel<2048> : cpqr_tall_kernel<256>;
+            IDS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             void* args[] = {&t};
-            IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cpqr_tall_kernel, dim3(G), dim3(kTThreads),
-                                                     args, smem, st));
+            IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kTThreads), args, smem,
+                                                     st));
             ids_count_launch();
             if (Q) {
                 form_q_kernel<<<(unsigned)k, kThreads, 0, st>>>(t.V, t.tau, rows, k, Q);

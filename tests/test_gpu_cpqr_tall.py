@@ -59,11 +59,13 @@ def test_tall_cpqr_deficient_and_zero():
     assert nr1 == 0 and not np.any(r1)
 
 
-@pytest.mark.parametrize("m,n,k", [(5001, 777, 13), (2049, 9000, 7), (16384, 300, 1), (3000, 20, 20)])
+@pytest.mark.parametrize("m,n,k", [(5001, 777, 13), (2049, 9000, 7), (16384, 300, 1), (3000, 20, 20),
+                                   (200, 10_000, 20), (333, 5000, 9), (1024, 18_000, 5)])
 def test_column_owner_kernel_vs_segment_units_and_dgeqp3(m, n, k, monkeypatch):
-    """The column-owning tall CPQR (v in shared memory, two grid barriers per
-    step, L2-pinned leading segments) and the segment-unit kernel agree with
-    LAPACK's pivots (odd m: the bulk copy of the residual rounds up)."""
+    """The column-owning CPQR (v in shared memory, two grid barriers per
+    step, L2-pinned leading segments; 256-row units for short wide sketches
+    like C3's 200 x 10000) and the segment-unit kernel agree with LAPACK's
+    pivots (odd m: the bulk copy of the residual rounds up)."""
     from paper_1901_10559_b200.linalg import device_cpqr
 
     rng = np.random.default_rng(m + n + k)

@@ -8,7 +8,8 @@ import torch
 from paper_1901_10559_b200.linalg import device_cpqr
 from exp_cpqr import near_dup  # noqa: E402
 
-for name, m, n, base, pert in (("C4", 4096, 1000, 10, 1e-3), ("C5", 16384, 2000, 20, 1e-4)):
+for name, m, n, base, pert in (("C4", 4096, 1000, 10, 1e-3), ("C5", 16384, 2000, 20, 1e-4),
+                               ("C3", 200, 10000, 20, 1e-2)):
     y = near_dup(m, n, base, pert, 1)
     out = []
     for k in (1, 2, 5, 10, 20):
