@@ -652,6 +652,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H / 16, (H >= 4096 ?
 // double index of real slot j (packed complex point j >> 1) in the padded buffer
 __device__ __forceinline__ uint32_t split_idx(int j) { return (uint32_t)(2 * spad(j >> 1) + (j & 1)); }
 
+#ifdef IDS_PLAN_TIMING
+__device__ long long g_plan_t[8];
+#endif
+
 struct PlanOut {
     int32_t* hdr;
     uint32_t* code;
@@ -674,6 +678,12 @@ __device__ int plan_chunk(const int32_t* __restrict__ bucket, const int8_t* __re
     // over the warps, so rank = base[warp][slot] + rank inside the warp's part.
     const int T = blockDim.x, t = threadIdx.x, w = t >> 5, lane = t & 31, NW = T >> 5;
     const int len = i1 - i0;
+#ifdef IDS_PLAN_TIMING
+    long long tp0 = clock64();
+#define PSTAMP(k) do { if (t == 0) { long long tn = clock64(); g_plan_t[k] += tn - tp0; tp0 = tn; } } while (0)
+#else
+#define PSTAMP(k) do {} while (0)
+#endif
     for (int q0 = 0; q0 < len; q0 += 8 * T) {  // eight loads of each array in flight
         int32_t bb[8];
         int8_t sg[8];
@@ -691,6 +701,7 @@ __device__ int plan_chunk(const int32_t* __restrict__ bucket, const int8_t* __re
     }
     for (int q = t; q < NW * N2 / 8; q += T) reinterpret_cast<uint4*>(wc)[q] = make_uint4(0, 0, 0, 0);
     __syncthreads();
+    PSTAMP(0);
     const int sub = (len + NW - 1) / NW;
     const int wa = w * sub, wb = min(len, wa + sub);
     uint16_t* mine = wc + w * N2;
@@ -709,60 +720,72 @@ __device__ int plan_chunk(const int32_t* __restrict__ bucket, const int8_t* __re
         if (ok) rank[q] = e | ((bc + __popc(m & lt)) << 15);
     }
     __syncthreads();
-    for (int sl = t; sl < N2; sl += T) {  // per-warp counts -> bases; totals
-        int run = 0;
+    PSTAMP(1);
+    for (int g8 = t; g8 < N2 / 8; g8 += T) {  // per-warp counts -> bases; totals (8 slots a thread)
+        int run[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int v = 0; v < NW; ++v) {
-            const int c = wc[v * N2 + sl];
-            wc[v * N2 + sl] = (uint16_t)run;
-            run += c;
+            uint4* cell = reinterpret_cast<uint4*>(wc + v * N2) + g8;
+            const uint4 c = *cell;
+            const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+            uint32_t ow[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                ow[h] = (uint32_t)run[2 * h] | ((uint32_t)run[2 * h + 1] << 16);
+                run[2 * h] += (int)(cw[h] & 0xFFFFu);
+                run[2 * h + 1] += (int)(cw[h] >> 16);
+            }
+            *cell = make_uint4(ow[0], ow[1], ow[2], ow[3]);
         }
-        cnt[sl] = run;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) cnt[8 * g8 + h] = run[h];
     }
     __syncthreads();
+    PSTAMP(2);
     for (int q = t; q < len; q += T) rank[q] += (int)wc[(q / sub) * N2 + (rank[q] & (N2 - 1))] << 15;
     __syncthreads();
+    PSTAMP(3);
     // exclusive scan of packed (count - 1, count >= 2): low 16 bits later
-    // rows, high 16 bits groups (both < 2^16 for the chunk sizes used)
-    const int per = N2 / T;
-    int sum = 0;
-    for (int q = 0; q < per; ++q) {
-        const int x = cnt[t * per + q];
-        sum += x >= 2 ? (x - 1) | (1 << 16) : 0;
-    }
-    int inc = sum;
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, inc, o);
-        if ((t & 31) >= o) inc += y;
-    }
-    if ((t & 31) == 31) s_part[t >> 5] = inc;
+    // rows, high 16 bits groups (both < 2^16 for the chunk sizes used).
+    // Warp w scans its 1/NW of the slots 32 at a time (lane = slot: no bank
+    // conflicts); pass 1 sums, the warp totals are prefixed, pass 2 writes.
+    const int span = N2 / NW, s0w = w * span;
+    auto packed = [&](int x) { return x >= 2 ? (x - 1) | (1 << 16) : 0; };
+    int wsum = 0;
+    for (int c0 = 0; c0 < span; c0 += 32) wsum += __reduce_add_sync(0xffffffffu, packed(cnt[s0w + c0 + lane]));
+    if (lane == 0) s_part[w] = wsum;
     __syncthreads();
     if (t < 32) {
-        const int nw = T >> 5;
-        int v = t < nw ? s_part[t] : 0;
+        int v = t < NW ? s_part[t] : 0;
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, v, o);
             if (t >= o) v += y;
         }
-        if (t < nw) s_part[t] = v;  // inclusive warp totals
+        if (t < NW) s_part[t] = v;  // inclusive warp totals
     }
     __syncthreads();
-    const int total = s_part[(T >> 5) - 1];
+    const int total = s_part[NW - 1];
     if ((total & 0xFFFF) > cap) {
         __syncthreads();  // everyone has read s_part before the next use
         return total & 0xFFFF;
     }
-    int run = inc - sum + ((t >> 5) ? s_part[(t >> 5) - 1] : 0);
-    for (int q = 0; q < per; ++q) {
-        const int s = t * per + q;
-        const int x = cnt[s];
-        cnt[s] = run;
-        if (x >= 2) {
-            gc[run >> 16] = make_uint2(split_idx(s) | ((uint32_t)(run & 0xFFFF) << 16), (uint32_t)(x - 1));
-            run += (x - 1) | (1 << 16);
+    int carry = w ? s_part[w - 1] : 0;
+    for (int c0 = 0; c0 < span; c0 += 32) {
+        const int sl = s0w + c0 + lane;
+        const int x = cnt[sl];
+        const int pv = packed(x);
+        int inc = pv;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
         }
+        const int run = carry + inc - pv;
+        cnt[sl] = run;
+        if (x >= 2) gc[run >> 16] = make_uint2(split_idx(sl) | ((uint32_t)(run & 0xFFFF) << 16), (uint32_t)(x - 1));
+        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
     if (t == 0) *ngroups = total >> 16;
     __syncthreads();
+    PSTAMP(4);
     for (int q = t; q < len; q += T) {
         const int e = rank[q];
         const int slot = e & (N2 - 1);
@@ -772,7 +795,9 @@ __device__ int plan_chunk(const int32_t* __restrict__ bucket, const int8_t* __re
         code[i0 + q] = split_idx(slot) | (neg << kSignShift) | ((neg ^ hi) << (kSignShift + 1)) | (tp << kTailShift);
     }
     __syncthreads();
+    PSTAMP(5);
     return total & 0xFFFF;
+#undef PSTAMP
 }
 
 // One CTA: the whole column as one chunk if its later rows fit `cap`, else
@@ -955,3 +980,14 @@ extern "C" int ids_tensorsketch_split_f64(int n_modes, const double* const* fact
         default: return launch_split<4096>(a, st);
     }
 }
+
+#ifdef IDS_PLAN_TIMING  // experiments: clock64 per plan phase (thread 0), summed
+extern "C" void ids_debug_plan_timing(long long* host8, int reset) {
+    if (reset) {
+        long long z[8] = {0};
+        cudaMemcpyToSymbol(g_plan_t, z, sizeof(z));
+    } else {
+        cudaMemcpyFromSymbol(host8, g_plan_t, 8 * sizeof(long long));
+    }
+}
+#endif
