@@ -1036,6 +1036,7 @@ struct TallArgs {
     int64_t* tlog;
     int pin_segs;  // leading 2048-row segments of each column kept in L2 (evict_last)
     int tmem;      // resident units in tensor memory
+    float pin_frac;  // fraction of segment pin_segs also kept (evict_last)
 };
 
 __device__ __forceinline__ double block_sum_t(double v, double* red) {
@@ -1275,9 +1276,14 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tm_base = g.tmem ? s_tm : 0u;
-    uint64_t pol_keep, pol_stream;
+    uint64_t pol_keep, pol_stream, pol_half;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    // the next segment: a fraction of its lines evict_last, the rest evict_first
+    const float pin_frac = g.pin_frac;
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;"
+                 : "=l"(pol_half)
+                 : "f"(pin_frac));
 
     auto local_argmax = [&](int64_t pmin, int64_t pnext) {  // warp 0 (nown <= 64)
         if (wid != 0) return;
@@ -1517,8 +1523,8 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
                 const bool aa = spos[ja] > kk, ab = h2 && spos[jb] > kk;
                 const double* pa = g.Y + (c0 + ja) * ldy;
                 const double* pb = g.Y + (c0 + jb) * ldy;
-                const uint64_t pola = sa < pin ? pol_keep : pol_stream;
-                const uint64_t polb = sb < pin ? pol_keep : pol_stream;
+                const uint64_t pola = sa < pin ? pol_keep : (sa == pin && pin_frac > 0.f ? pol_half : pol_stream);
+                const uint64_t polb = sb < pin ? pol_keep : (sb == pin && pin_frac > 0.f ? pol_half : pol_stream);
                 double s1 = 0.0, s2 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll 1
                 for (int qtr = 0; qtr < 4; ++qtr) {
@@ -1643,7 +1649,7 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
     }
     // the pinned segments back to normal eviction priority
     if (g.pin_segs > 0) {
-        const int64_t rows_pin = tmin<int64_t>(m, (int64_t)g.pin_segs * kSegT);
+        const int64_t rows_pin = tmin<int64_t>(m, (int64_t)(g.pin_segs + (g.pin_frac > 0.f ? 1 : 0)) * kSegT);
         const int64_t lines = ceil_div_d(rows_pin * 8, 128);
         for (int64_t i = threadIdx.x; i < nown * lines; i += kTThreads) {
             const double* ln = g.Y + (c0 + i / lines) * ldy + (i % lines) * 16;
@@ -1814,6 +1820,8 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
             t.tmem = 1;
             if (const char* e = getenv("IDS_CPQR_PIN")) t.pin_segs = atoi(e);  // experiments
             if (const char* e = getenv("IDS_CPQR_TMEM")) t.tmem = atoi(e);
+            t.pin_frac = 0.75f;  // C5: 872 vs 895 us at 0 (3 of 4 lines of the third segment, ~88 MB)
+            if (const char* e = getenv("IDS_CPQR_PIN_FRAC")) t.pin_frac = (float)atof(e);
             WsCarve ws(workspace, ws_bytes);
             carve_tall(ws, rows, cols, k, kMaxG, t);
             if (!ws.ok()) {
