@@ -452,28 +452,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H / 16, (H >= 4096 ?
                 __syncthreads();
                 stamp(9);
                 // later rows, one slot per group, in row order (4 groups at a
-                // time; the first three rows of every group loaded up front)
+                // time; the first four rows of every group loaded up front --
+                // longer groups are rare: P(len > 4) ~ 1% at C5)
 #pragma unroll
                 for (int q0 = 0; q0 < kGroupsReg; q0 += 4) {
                     double gs[4], go[4];
-                    double x[4][3];
+                    double x[4][4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint2 d = gd[q0 + q];
                         const int st0 = (int)(d.x >> 16), len = (int)d.y;
 #pragma unroll
-                        for (int e = 0; e < 3; ++e) x[q][e] = e < len ? tail[st0 + e] : 0.0;
+                        for (int e = 0; e < 4; ++e) x[q][e] = e < len ? tail[st0 + e] : 0.0;
                         go[q] = dbuf[d.x & kIdxMask];
                     }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint2 d = gd[q0 + q];
-                        const int st0 = (int)(d.x >> 16), len = (int)d.y;
+                        const int len = (int)d.y;
                         double acc = x[q][0];
                         if (len > 1) acc += x[q][1];
                         if (len > 2) acc += x[q][2];
-                        for (int e = 3; e < len; ++e) acc += tail[st0 + e];
+                        if (len > 3) acc += x[q][3];
                         gs[q] = acc;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint2 d = gd[q0 + q];
+                        const int st0 = (int)(d.x >> 16), len = (int)d.y;
+                        if (len > 4)
+                            for (int e = 4; e < len; ++e) gs[q] += tail[st0 + e];
                     }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) dbuf[gd[q0 + q].x & kIdxMask] = go[q] + gs[q];
