@@ -1016,7 +1016,7 @@ constexpr int64_t kMaxG = 148;
 // against three grid syncs and two all-CTA partial reductions before.
 constexpr int kTThreads = 512;
 constexpr int kTWarps = kTThreads / 32;
-constexpr int kMaxOwn = 128;  // owned columns per CTA
+constexpr int kMaxOwn = 64;  // owned columns per CTA
 constexpr int kTallMaxK = 256;
 constexpr int kMaxSegT = 16;  // v segments (rows <= 16 x 2048)
 
