@@ -1214,6 +1214,14 @@ __device__ __forceinline__ void tm_ld_x32(uint32_t ta, double* v) {
     for (int i = 0; i < 16; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
 }
 
+__device__ __forceinline__ double2 ld_pol2(const double* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
 // Y loads with an L2 eviction policy: the pinned segments of every column
 // (read again by each of the k GEMV passes) evict_last, the rest evict_first
 __device__ __forceinline__ double ld_pol(const double* p, uint64_t pol) {
@@ -1415,9 +1423,10 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
         // ---- S2: a[] into shared memory by one bulk copy per 2048-row segment
         // (each GEMV unit waits only for its own segment), ||a[kk+1:]|| (fixed-
         // order sum of the partials) and the Householder scalars ----
-        if (threadIdx.x == 0) {
+        if (wid == 0 && lane < nsegT) {  // one lane per segment issues its copy
             asm volatile("fence.proxy.async;" ::: "memory");
-            for (int sg = 0; sg < nsegT; ++sg) {
+            {
+                const int sg = lane;
                 const int64_t lo = (int64_t)sg * kSegT, hi = tmin<int64_t>(m, lo + kSegT);
                 const uint32_t bytes = (uint32_t)(((hi - lo + 1) / 2) * 16);  // a[m] is a zero pad
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -1515,6 +1524,8 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
             };
             const bool rev = kk & 1;
             const bool full = m == mpad;
+            // whole segments, even ldy and a 16-byte aligned Y: 16-byte loads
+            const bool vec16 = full && (ldy & 1) == 0 && (reinterpret_cast<uintptr_t>(g.Y) & 15) == 0;
             for (int64_t li = wid; li < U; li += 2 * kTWarps) {
                 const bool h2 = li + kTWarps < U;
                 int64_t ja, sa, jb, sb;
@@ -1527,7 +1538,31 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
                 const uint64_t polb = sb < pin ? pol_keep : (sb == pin && pin_frac > 0.f ? pol_half : pol_stream);
                 double s1 = 0.0, s2 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll 1
-                for (int qtr = 0; qtr < 4; ++qtr) {
+                for (int qtr = 0; qtr < 4 && vec16; ++qtr) {  // 16-byte loads: rows 2 lane + 64 u
+                    const int64_t ba = sa * kSegT + qtr * (kSegT / 4) + 2 * lane;
+                    const int64_t bb = sb * kSegT + qtr * (kSegT / 4) + 2 * lane;
+                    double2 ya[kSegTLoads / 2], yb[kSegTLoads / 2];
+#pragma unroll
+                    for (int u = 0; u < kSegTLoads / 2; ++u) {
+                        ya[u] = aa ? ld_pol2(pa + ba + 64 * u, pola) : make_double2(0.0, 0.0);
+                        yb[u] = ab ? ld_pol2(pb + bb + 64 * u, polb) : make_double2(0.0, 0.0);
+                    }
+                    if (qtr == 0) {
+                        wait_seg(sa);
+                        wait_seg(sb);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kSegTLoads / 2; ++u) {
+                        const double2 va = *reinterpret_cast<const double2*>(vsm + ba + 64 * u);
+                        const double2 vb = *reinterpret_cast<const double2*>(vsm + bb + 64 * u);
+                        s1 = fma(ya[u].x, va.x, s1);
+                        t1 = fma(ya[u].y, va.y, t1);
+                        s2 = fma(yb[u].x, vb.x, s2);
+                        t2 = fma(yb[u].y, vb.y, t2);
+                    }
+                }
+#pragma unroll 1
+                for (int qtr = 0; qtr < 4 && !vec16; ++qtr) {
                     const int64_t ba = sa * kSegT + qtr * (kSegT / 4) + lane;
                     const int64_t bb = sb * kSegT + qtr * (kSegT / 4) + lane;
                     double ya[kSegTLoads], yb[kSegTLoads];
