@@ -409,7 +409,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H / 16, (H >= 4096 ?
                 double v[kRows];
                 uint32_t k[kRows];
             } A, B;
+            // 16-byte loads (rows 2 (t + u T) + {0, 1}) when the column and the
+            // plan codes are 8 / 16-byte aligned at even rows
+            const bool vec = ((reinterpret_cast<uintptr_t>(col) & 15) | (reinterpret_cast<uintptr_t>(code) & 7)) == 0;
             auto ld = [&](RowSet& S, int r0, int cend) {
+                if (vec && (r0 & 1) == 0) {
+#pragma unroll
+                    for (int u = 0; u < kRows / 2; ++u) {
+                        const int i = r0 + 2 * (u * T + t);
+                        if (i + 1 < cend) {
+                            const double2 v2 = __ldg(reinterpret_cast<const double2*>(col + i));
+                            const uint2 k2 = __ldg(reinterpret_cast<const uint2*>(code + i));
+                            S.v[2 * u] = v2.x;
+                            S.v[2 * u + 1] = v2.y;
+                            S.k[2 * u] = k2.x;
+                            S.k[2 * u + 1] = k2.y;
+                        } else {
+                            S.v[2 * u] = i < cend ? __ldg(col + i) : 0.0;
+                            S.k[2 * u] = i < cend ? __ldg(code + i) : (kFirst << kTailShift) | kPadIdx;
+                            S.v[2 * u + 1] = 0.0;
+                            S.k[2 * u + 1] = (kFirst << kTailShift) | kPadIdx;
+                        }
+                    }
+                    return;
+                }
 #pragma unroll
                 for (int u = 0; u < kRows; ++u) {
                     const int i = r0 + u * T + t;
