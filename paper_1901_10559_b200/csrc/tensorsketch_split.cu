@@ -21,18 +21,22 @@
 // inverse: each CTA transforms its half (E or O), and one exchange of H/2
 // points per CTA through distributed shared memory combines
 //   z[m] = E[m] + W_{N2}^{-m} O[m],   z[m + H] = E[m] - W_{N2}^{-m} O[m].
-// Half-size transforms let two CTAs share an SM (75 KB of shared memory and
+// Half-size transforms let two CTAs share an SM (106 KB of shared memory and
 // 128 KB of TMEM each at C5), so one CTA's scatter overlaps the other's FFT.
 //
-// CountSketch order.  A per-mode plan (ids_ts_split_plan) gives every row
-// its folded slot, sign, and its rank among the earlier rows of the same
-// slot inside its chunk of H rows.  Each thread loads 16 rows of a chunk
-// (coalesced), then the chunk is added rank by rank with one barrier per
-// rank: every slot sums its rows in increasing row order, run-to-run
-// identical.  (The fold adds the rows of buckets b and b + N2 in row order,
-// so the sums differ from the reference's per-bucket ones in rounding only:
-// Y agrees to ~1e-15 relative; the FFTs differ from pocketfft at that level
-// anyway.)
+// CountSketch order.  A per-mode plan (ids_ts_split_plan) cuts the rows into
+// one chunk (the whole column) when the later rows of its slots fit the tail
+// buffer, else into 16 T-row chunks, and gives every row its slot's buffer
+// index, its signs in the two halves and -- unless it is the first row of
+// its slot in the chunk -- its position in the chunk's tail buffer; per
+// chunk, the tail groups (slots with later rows).  Rows are loaded coalesced
+// in rounds of 8 T (two rounds in flight); first rows store (chunk 0) or add
+// into their slots -- distinct slots, no conflicts -- later rows park in the
+// tail buffer, and after one barrier one thread per group adds them in row
+// order.  Run-to-run identical.  (The fold adds the rows of buckets b and
+// b + N2 in row order, so the sums differ from the reference's per-bucket
+// ones in rounding only: Y agrees to ~1e-15 relative; the FFTs differ from
+// pocketfft at that level anyway.)
 //
 // Twiddles: one table lookup per thread and stage (coarse x fine tables of
 // W_L in shared memory); the per-point factors are products of that base
@@ -118,39 +122,6 @@ __device__ __forceinline__ void twiddle16(double2* v, double2 w1) {
 }
 
 // ---- tensor memory --------------------------------------------------------
-__device__ __forceinline__ void tm_st16(uint32_t ta, const double2* v) {  // 4 complex
-    uint32_t r[16];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        r[4 * i + 0] = (uint32_t)__double2loint(v[i].x);
-        r[4 * i + 1] = (uint32_t)__double2hiint(v[i].x);
-        r[4 * i + 2] = (uint32_t)__double2loint(v[i].y);
-        r[4 * i + 3] = (uint32_t)__double2hiint(v[i].y);
-    }
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-        "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(ta),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
-        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
-}
-__device__ __forceinline__ void tm_ld16(uint32_t ta, double2* v) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(ta)
-        : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        v[i].x = __hiloint2double((int)r[4 * i + 1], (int)r[4 * i + 0]);
-        v[i].y = __hiloint2double((int)r[4 * i + 3], (int)r[4 * i + 2]);
-    }
-}
 // one complex per thread (4 columns of its lane): two loads, one wait
 __device__ __forceinline__ void tm_ld2(uint32_t ta, uint32_t tb, double2& a, double2& b) {
     uint32_t r[8];
@@ -919,9 +890,6 @@ int launch_split(const SplitArgs& a0, cudaStream_t st) {
     }
     // persistent grid: every resident CTA pair is one cluster
     int fit = ids_sm_count() * occ / 2;
-    if (const char* e = getenv("IDS_TS_SPLIT_CLUSTERS")) fit = atoi(e);  // experiments
-    if (getenv("IDS_TS_SPLIT_VERBOSE"))
-        fprintf(stderr, "ts_split H=%d regs=%d occ=%d smem=%zu clusters=%d\n", H, fa.numRegs, occ, smem, fit);
     const int64_t ncl = tmin<int64_t>(a.ncols, tmax<int64_t>(fit, 1));
     kern<<<(unsigned)(2 * ncl), T, smem, st>>>(a);
     IDS_LAUNCH_CHECK();
