@@ -1833,7 +1833,8 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int G = (int)tmin<int64_t>(tmin<int64_t>(sms, kMaxG), cols);
+        int G = (int)tmin<int64_t>(tmin<int64_t>(sms, kMaxG), cols);
+        if (const char* e = getenv("IDS_CPQR_G")) G = tmin(G, atoi(e));  // experiments
         const size_t smem = tall_smem_bytes(rows, k, G, seg);
         if (ceil_div(cols, (int64_t)G) <= kMaxOwn && ceil_div(rows, (int64_t)G) <= kTThreads &&
             ceil_div(rows, seg) <= kMaxSegT && smem <= 200 * 1024) {
