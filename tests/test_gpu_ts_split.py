@@ -141,3 +141,21 @@ def test_split_abi_arguments():
     with pytest.raises(ValueError):
         call("ids_tensorsketch_split_f64", n, ctypes.addressof(ptrs), ctypes.addressof(dims),
              ctypes.addressof(lds), 1, ctypes.addressof(plans), 4096, None, y.data_ptr(), None, None)
+
+
+def test_split_without_norms_and_single_term():
+    """colnorm2 = NULL (no norm epilogue) gives the same sketch; one term
+    column runs on one cluster."""
+    rng = np.random.default_rng(17)
+    dims, L = [3000, 2500], 16384
+    for r in (1, 37):
+        fac = _factors(rng, dims, r)
+        w = torch.from_numpy(rng.random(r) + 0.5).cuda()
+        op = ids.TensorSketchOp(dims, L, seed=2)
+        y_n, nrm = op.apply_device(fac, w, norms=True)
+        y = op.apply_device(fac, w)
+        assert torch.equal(y, y_n)
+        assert float(((nrm - (y * y).sum(dim=1)).abs() / nrm).max()) <= 1e-13
+        want = oracle.OracleTensorSketch(dims, L, seed=2).apply([f.cpu().numpy() for f in fac],
+                                                               w.cpu().numpy())
+        assert relerr_fro(y.t().cpu().numpy(), want) <= 1e-12
