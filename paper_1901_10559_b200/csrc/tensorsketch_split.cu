@@ -269,7 +269,7 @@ __device__ __forceinline__ int64_t gtimer() {
 }
 
 template <int H>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H / 16, (H >= 4096 ? 2 : 1))
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H / 16, (H >= 4096 ? 2 : (H == 2048 ? 4 : 8)))
     ts_split_kernel(SplitArgs g) {
     constexpr int T = H / 16, M = 4 * H, R1 = H / 256;
     constexpr int RS = T * kRows;  // rows per load round
