@@ -398,6 +398,239 @@ __global__ void __launch_bounds__(kCtThreads) cs_coltile_kernel(
     }
 }
 
+// ---- column-major tiled kernel, register accumulators ----
+// The same tile pipeline, but every tile's rows are sorted by BUCKET (stable,
+// so each bucket's run is in increasing row order) and each (slot, column)
+// lane owns BPL buckets -- slot x owns x, x + nslots, ... with nslots =
+// ceil(L / BPL) -- whose running sums stay in registers: per tile the lane
+// walks its buckets' runs one after the other.  Per element that is one list
+// load, one tile load, a sign flip on the high word and one DADD; the
+// per-tile time is the longest slot (~kTT * BPL / L rows) instead of the
+// 32-slot layout's (whose L = 100 slots 0..3 own 4 buckets and the rest 3).
+// Order per Y entry: increasing row from +0.0 (or from Y when accumulating),
+// so Y is bit-identical to the 32-slot kernel's and to scipy's.
+constexpr int kRaMaxBuckets = 512;
+
+// One CTA per TT-row tile: lists[tile][q] = 8 * row in tile | sign << 31, grouped
+// by bucket in increasing row order; starts[tile * ss + b] = first q of
+// bucket b (b = 0..L), padded with the tile's total up to ss.
+template <int TT>
+__global__ void __launch_bounds__(kCtThreads) tile_bucket_lists_kernel(
+    const int32_t* __restrict__ codes, int64_t rows, int nb, int ss,
+    int32_t* __restrict__ lists, int32_t* __restrict__ starts) {
+    constexpr int kRpt = TT / kCtThreads, kGroups = TT / 32, kWarps = kCtThreads / 32;
+    constexpr int kPerLane = kRaMaxBuckets / 32;
+    static_assert(TT % kCtThreads == 0 && TT <= 512, "rows per tile");
+    __shared__ int s_cnt[kGroups][kRaMaxBuckets + 1];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t rb = (int64_t)blockIdx.x * TT;
+    const int n = (int)tmin<int64_t>(TT, rows - rb);
+    const uint32_t lt = (1u << lane) - 1u;
+    int b2[kRpt], rank2[kRpt], ent2[kRpt];
+#pragma unroll
+    for (int h = 0; h < kRpt; ++h) {
+        const int g = warp + kWarps * h, r = 32 * g + lane;
+        const int32_t e = r < n ? codes[rb + r] : INT_MIN;
+        const int b = e == INT_MIN ? nb : (int)dec_row(e);
+        ent2[h] = (e < 0 ? (int)0x80000000u : 0) | (r << 3);  // byte offset of the row
+        const uint32_t peers = __match_any_sync(0xffffffffu, b);
+        const int rank = __popc(peers & lt);
+        for (int x = lane; x <= nb; x += 32) s_cnt[g][x] = 0;
+        __syncwarp();
+        if (rank == 0) s_cnt[g][b] = __popc(peers);
+        b2[h] = b;
+        rank2[h] = rank;
+    }
+    __syncthreads();
+    if (warp == 0) {  // lane owns buckets kPerLane lane .. kPerLane (lane + 1) - 1
+        int sum = 0;
+        for (int j = 0; j < kPerLane; ++j) {
+            const int x = kPerLane * lane + j;
+            if (x < nb)
+                for (int g = 0; g < kGroups; ++g) sum += s_cnt[g][x];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        int run = incl - sum;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        int32_t* st = starts + blockIdx.x * (int64_t)ss;
+        for (int j = 0; j < kPerLane; ++j) {
+            const int x = kPerLane * lane + j;
+            if (x < nb) {
+                st[x] = run;
+                for (int g = 0; g < kGroups; ++g) {
+                    const int cg = s_cnt[g][x];
+                    s_cnt[g][x] = run;
+                    run += cg;
+                }
+            }
+        }
+        for (int x = nb + lane; x < ss; x += 32) st[x] = total;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < kRpt; ++h) {
+        const int g = warp + kWarps * h;
+        if (b2[h] < nb) lists[rb + s_cnt[g][b2[h]] + rank2[h]] = ent2[h];
+    }
+}
+
+template <int TT>
+__host__ __device__ __forceinline__ size_t coltile_ra_stage_bytes(int ss) {
+    return (size_t)kCt * (TT + 2) * sizeof(double) + TT * sizeof(int32_t) + (size_t)ss * sizeof(int32_t);
+}
+
+__device__ __forceinline__ uint32_t cs_smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Needs 16-byte aligned columns (A and ld even).  Warp-specialised: the last
+// warp is the producer -- per tile, one bulk copy per column (one lane each)
+// plus the list and the slot starts, against the stage's `full` mbarrier --
+// and every consumer warp walks its slots and releases the stage on its
+// `empty` mbarrier, so warps drift up to S tiles apart instead of meeting at
+// a CTA barrier per tile, and no consumer ever issues copies.
+template <int BPL, int TT, int S>
+__global__ void __launch_bounds__(512 + 32, 2) cs_coltile_ra_kernel(
+    const double* __restrict__ A, int64_t ld, int64_t rows, int64_t cols,
+    const int32_t* __restrict__ lists, const int32_t* __restrict__ starts, int64_t L, int nslots,
+    int ss, int ngroups, double* __restrict__ out, int init_from_out) {
+    constexpr int TTp = TT + 2;
+    extern __shared__ __align__(16) char ra_stages[];
+    __shared__ __align__(8) uint64_t s_full[S], s_empty[S];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int ncw = (int)(blockDim.x >> 5) - 1;  // consumer warps; warp ncw produces
+    const int group = blockIdx.x;
+    const int64_t c0 = cols * group / ngroups;
+    const int nc = (int)(cols * (group + 1) / ngroups - c0);
+    const int64_t ntl = (rows + TT - 1) / TT;
+    const size_t stage_bytes = coltile_ra_stage_bytes<TT>(ss);
+    auto stage_tile = [&](int s) { return reinterpret_cast<double*>(ra_stages + s * stage_bytes); };
+    auto stage_list = [&](int s) {
+        return reinterpret_cast<int32_t*>(ra_stages + s * stage_bytes + (size_t)kCt * TTp * sizeof(double));
+    };
+    auto stage_starts = [&](int s) { return stage_list(s) + TT; };
+    auto wait = [&](uint64_t* mb, uint32_t parity) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "RA_WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra RA_WAIT_%=;\n}" ::"r"(cs_smem_addr(mb)),
+            "r"(parity)
+            : "memory");
+    };
+    if (t == 0) {
+        for (int s = 0; s < S; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cs_smem_addr(&s_full[s])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cs_smem_addr(&s_empty[s])), "r"(ncw)
+                         : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == ncw) {  // ---- producer ----
+        for (int64_t k = 0; k < ntl; ++k) {
+            const int s = (int)(k % S);
+            if (k >= S) wait(&s_empty[s], (uint32_t)((k / S - 1) & 1));
+            const int64_t rb = k * TT;
+            const int n = (int)tmin<int64_t>(TT, rows - rb);
+            double* dst = stage_tile(s);
+            const uint32_t col_bytes = (uint32_t)(n & ~1) * 8u;
+            if ((n & 1) && lane < nc)  // odd last tile: its last row by plain loads
+                dst[lane * TTp + n - 1] = A[(c0 + lane) * ld + rb + n - 1];
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                 cs_smem_addr(&s_full[s])),
+                             "r"(nc * col_bytes + TT * 4u + (uint32_t)ss * 4u)
+                             : "memory");
+            __syncwarp();
+            const void* src = nullptr;
+            void* d = nullptr;
+            uint32_t bytes = 0;
+            if (lane < nc) {
+                src = A + (c0 + lane) * ld + rb;
+                d = dst + lane * TTp;
+                bytes = col_bytes;
+            } else if (lane == kCt) {
+                src = lists + rb;
+                d = stage_list(s);
+                bytes = TT * 4u;
+            } else if (lane == kCt + 1) {
+                src = starts + k * ss;
+                d = stage_starts(s);
+                bytes = (uint32_t)ss * 4u;
+            }
+            if (bytes)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        cs_smem_addr(d)),
+                    "l"(src), "r"(bytes), "r"(cs_smem_addr(&s_full[s]))
+                    : "memory");
+        }
+        return;
+    }
+
+    // ---- consumers ----
+    const int slot = t / kCt, c = t % kCt;
+    const bool active = c < nc && slot < nslots;
+    double acc[BPL];
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        const int64_t b = slot + (int64_t)j * nslots;
+        acc[j] = (init_from_out && active && b < L) ? out[(c0 + c) * L + b] : 0.0;
+    }
+    for (int64_t k = 0; k < ntl; ++k) {
+        const int s = (int)(k % S);
+        wait(&s_full[s], (uint32_t)((k / S) & 1));
+        const double* tl = stage_tile(s) + c * TTp;
+        const int32_t* lst = stage_list(s);
+        const int32_t* sts = stage_starts(s);
+        if (active) {
+            auto sgn = [](int32_t e, double v) {  // v with the entry's sign applied
+                return __hiloint2double(__double2hiint(v) ^ (e & (int)0x80000000u), __double2loint(v));
+            };
+#pragma unroll
+            for (int j = 0; j < BPL; ++j) {
+                const int b = slot + j * nslots;
+                if (b < L) {
+                    int q = sts[b];
+                    const int q1 = sts[b + 1];
+                    const char* tb = reinterpret_cast<const char*>(tl);
+                    auto at = [&](int32_t e) { return *reinterpret_cast<const double*>(tb + (e & 0xFF8)); };
+                    for (; q + 3 < q1; q += 4) {
+                        const int32_t e0 = lst[q], e1 = lst[q + 1], e2 = lst[q + 2], e3 = lst[q + 3];
+                        const double v0 = at(e0), v1 = at(e1), v2 = at(e2), v3 = at(e3);
+                        acc[j] += sgn(e0, v0);
+                        acc[j] += sgn(e1, v1);
+                        acc[j] += sgn(e2, v2);
+                        acc[j] += sgn(e3, v3);
+                    }
+                    for (; q < q1; ++q) {
+                        const int32_t e0 = lst[q];
+                        acc[j] += sgn(e0, at(e0));
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0)  // this warp is done with the stage
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cs_smem_addr(&s_empty[s])) : "memory");
+    }
+    if (active) {
+#pragma unroll
+        for (int j = 0; j < BPL; ++j) {
+            const int64_t b = slot + (int64_t)j * nslots;
+            if (b < L) out[(c0 + c) * L + b] = acc[j];
+        }
+    }
+}
+
 // Y[e] = (accumulate ? Y[e] : 0) + sum_s part[s][e], s in order.
 __global__ void seg_reduce_kernel(const double* __restrict__ part, int nseg, int64_t n,
                                   int64_t seg_stride, double* __restrict__ Y, int accumulate) {
@@ -490,10 +723,59 @@ struct ColTilePlan {
     int ngroups, nseg;
     int64_t ntiles;
     size_t smem;
+    // register-accumulator variant (cs_coltile_ra_kernel): BPL buckets per slot
+    int bpl, nslots, ss, threads, ngroups_ra, tt;
+    int64_t ntiles_ra;
+    size_t smem_ra;
+    int64_t starts_stride;  // int32 per tile in the starts array
 };
 
-// The tiled kernel needs L x kCt accumulators beside the tile pipeline, and
-// packs buckets into 21 bits of a list entry.
+// rows per tile and pipeline stages of the register variant (IDS_COLTILE_TT
+// = 256 selects 256-row tiles in 6 stages, the default 512 x 3)
+int coltile_ra_tt() {
+    static const int tt = [] {
+        const char* e = getenv("IDS_COLTILE_TT");
+        return (e && atoi(e) == 256) ? 256 : 512;
+    }();
+    return tt;
+}
+
+template <int BPL, int TT, int S>
+int coltile_ra_occupancy(int threads, size_t smem) {
+    static int cached[1024 / 32 + 1] = {};
+    int& c = cached[threads / 32];
+    if (!c) {
+        // every ss this kernel takes (<= kRaMaxBuckets + 4) fits the attribute
+        const size_t smax = S * coltile_ra_stage_bytes<TT>(kRaMaxBuckets + 4);
+        IDS_CUDA_TRY(cudaFuncSetAttribute(cs_coltile_ra_kernel<BPL, TT, S>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cs_coltile_ra_kernel<BPL, TT, S>,
+                                                          threads + 32, smem) != cudaSuccess || occ < 1)
+            occ = 1;
+        c = occ;
+    }
+    return c;
+}
+
+int coltile_ra_occ(int bpl, int tt, int threads, size_t smem) {
+    if (tt == 256) switch (bpl) {
+            case 2: return coltile_ra_occupancy<2, 256, 6>(threads, smem);
+            case 4: return coltile_ra_occupancy<4, 256, 6>(threads, smem);
+            default: return coltile_ra_occupancy<8, 256, 6>(threads, smem);
+        }
+    switch (bpl) {
+        case 2: return coltile_ra_occupancy<2, 512, 3>(threads, smem);
+        case 4: return coltile_ra_occupancy<4, 512, 3>(threads, smem);
+        default: return coltile_ra_occupancy<8, 512, 3>(threads, smem);
+    }
+}
+
+// The tiled kernels need kCt columns of a tile per stage; the 32-slot one
+// also L x kCt accumulators, and both pack buckets into 21 bits of a list
+// entry.  The register variant takes over when L <= 512 (at most 64 slots of
+// up to 8 buckets, <= 512 threads) and no row segments are needed; set
+// IDS_COLTILE_RA=0 to keep the 32-slot kernel.
 ColTilePlan plan_coltile(int64_t rows, int64_t cols, int64_t L, int flags) {
     ColTilePlan p{};
     p.smem = coltile_smem(L);
@@ -505,6 +787,23 @@ ColTilePlan plan_coltile(int64_t rows, int64_t cols, int64_t L, int flags) {
     p.nseg = 1;
     if (!(flags & IDS_FLAG_ORDERED) && p.ngroups < wave)
         p.nseg = (int)tmax<int64_t>(1, tmin<int64_t>(ceil_div(wave, p.ngroups), p.ntiles / 4));
+    p.starts_stride = kStartsStride;
+    static const int ra_env = [] {
+        const char* e = getenv("IDS_COLTILE_RA");
+        return e ? atoi(e) : 1;
+    }();
+    if (ra_env && p.nseg == 1 && L <= 512) {
+        p.bpl = L <= 128 ? 2 : (L <= 256 ? 4 : 8);
+        p.nslots = (int)ceil_div(L, p.bpl);
+        p.threads = (int)ceil_div((int64_t)p.nslots * kCt, 32) * 32;
+        p.ss = (int)ceil_div(L + 1, 4) * 4;  // bucket starts per tile
+        p.tt = coltile_ra_tt();
+        p.ntiles_ra = ceil_div(rows, p.tt);
+        p.smem_ra = p.tt == 256 ? 6 * coltile_ra_stage_bytes<256>(p.ss) : 3 * coltile_ra_stage_bytes<512>(p.ss);
+        const int64_t cap = (int64_t)ids_sm_count() * coltile_ra_occ(p.bpl, p.tt, p.threads, p.smem_ra);
+        p.ngroups_ra = (int)tmax<int64_t>(ceil_div(cols, kCt), tmin<int64_t>(cols, cap));
+        p.starts_stride = tmax<int64_t>(kStartsStride, p.ss);
+    }
     return p;
 }
 
@@ -519,10 +818,11 @@ extern "C" size_t ids_countsketch_dense_workspace_bytes(int64_t rows, int64_t co
     WsCount c;
     if (layout == IDS_COL_MAJOR && plan_coltile(rows, cols, out_dim, 0).use) {
         const ColTilePlan q = plan_coltile(rows, cols, out_dim, 0);
+        const ColTilePlan qo = plan_coltile(rows, cols, out_dim, IDS_FLAG_ORDERED);
         c.take<double>((size_t)tmax(nseg, q.nseg) * out_dim * cols);
         c.take<int32_t>((size_t)rows);
         c.take<int32_t>((size_t)q.ntiles * kTT);
-        c.take<int32_t>((size_t)q.ntiles * kStartsStride);
+        c.take<int32_t>((size_t)ceil_div(rows, 256) * tmax(q.starts_stride, qo.starts_stride));
         return c.off + 256;
     }
     c.take<double>((size_t)nseg * out_dim * cols);
@@ -551,7 +851,7 @@ extern "C" int ids_countsketch_dense_f64(const double* A, int64_t rows, int64_t 
             double* part = q.nseg > 1 ? ws.take<double>((size_t)q.nseg * out_dim * cols) : nullptr;
             int32_t* codes = ws.take<int32_t>((size_t)rows);
             int32_t* lists = ws.take<int32_t>((size_t)q.ntiles * kTT);
-            int32_t* starts = ws.take<int32_t>((size_t)q.ntiles * kStartsStride);
+            int32_t* starts = ws.take<int32_t>((size_t)ceil_div(rows, 256) * q.starts_stride);
             if (!ws.ok()) {
                 ids_set_last_error("dense countsketch: workspace too small");
                 return IDS_EWORKSPACE;
@@ -560,20 +860,45 @@ extern "C" int ids_countsketch_dense_f64(const double* A, int64_t rows, int64_t 
             const unsigned gc = (unsigned)tmin<int64_t>(ceil_div(rows, 256), 148 * 8);
             row_codes_kernel<<<gc, 256, 0, st>>>(bucket, sign, row0, rows, codes);
             IDS_LAUNCH_CHECK();
-            tile_slot_lists_kernel<<<(unsigned)q.ntiles, kCtThreads, 0, st>>>(codes, rows, lists,
-                                                                              starts);
-            IDS_LAUNCH_CHECK();
             const int vec16 = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (ld % 2 == 0);
             double* out = q.nseg > 1 ? part : Y;
             const int init = (q.nseg == 1 && accumulate) ? 1 : 0;
-            const unsigned grid = (unsigned)((int64_t)q.ngroups * q.nseg);
-            IDS_CUDA_TRY(cudaFuncSetAttribute(cs_coltile_kernel,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)q.smem));
-            cs_coltile_kernel<<<grid, kCtThreads, q.smem, st>>>(A, ld, rows, cols, lists, starts,
-                                                                out_dim, q.ngroups, q.nseg, vec16,
-                                                                out, seg_stride, init);
-            IDS_LAUNCH_CHECK();
+            if (q.bpl && vec16) {
+                if (q.tt == 256)
+                    tile_bucket_lists_kernel<256><<<(unsigned)q.ntiles_ra, kCtThreads, 0, st>>>(
+                        codes, rows, (int)out_dim, q.ss, lists, starts);
+                else
+                    tile_bucket_lists_kernel<512><<<(unsigned)q.ntiles_ra, kCtThreads, 0, st>>>(
+                        codes, rows, (int)out_dim, q.ss, lists, starts);
+                IDS_LAUNCH_CHECK();
+                const unsigned grid = (unsigned)q.ngroups_ra;
+#define IDS_RA_LAUNCH(B, TT, S)                                                              \
+    cs_coltile_ra_kernel<B, TT, S><<<grid, q.threads + 32, q.smem_ra, st>>>(                      \
+        A, ld, rows, cols, lists, starts, out_dim, q.nslots, q.ss, q.ngroups_ra, out, init)
+                if (q.tt == 256) {
+                    if (q.bpl == 2) IDS_RA_LAUNCH(2, 256, 6);
+                    else if (q.bpl == 4) IDS_RA_LAUNCH(4, 256, 6);
+                    else IDS_RA_LAUNCH(8, 256, 6);
+                } else {
+                    if (q.bpl == 2) IDS_RA_LAUNCH(2, 512, 3);
+                    else if (q.bpl == 4) IDS_RA_LAUNCH(4, 512, 3);
+                    else IDS_RA_LAUNCH(8, 512, 3);
+                }
+#undef IDS_RA_LAUNCH
+                IDS_LAUNCH_CHECK();
+            } else {
+                tile_slot_lists_kernel<<<(unsigned)q.ntiles, kCtThreads, 0, st>>>(codes, rows, lists,
+                                                                                  starts);
+                IDS_LAUNCH_CHECK();
+                const unsigned grid = (unsigned)((int64_t)q.ngroups * q.nseg);
+                IDS_CUDA_TRY(cudaFuncSetAttribute(cs_coltile_kernel,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)q.smem));
+                cs_coltile_kernel<<<grid, kCtThreads, q.smem, st>>>(A, ld, rows, cols, lists, starts,
+                                                                    out_dim, q.ngroups, q.nseg, vec16,
+                                                                    out, seg_stride, init);
+                IDS_LAUNCH_CHECK();
+            }
             if (q.nseg > 1) {
                 const unsigned g = (unsigned)tmin<int64_t>(ceil_div(seg_stride, 256), 148 * 8);
                 seg_reduce_kernel<<<g, 256, 0, st>>>(part, q.nseg, seg_stride, seg_stride, Y,

@@ -32,7 +32,8 @@ def _fortran_dev(a, pad_rows=0):
 @pytest.mark.parametrize("rows,cols,L", [
     (512, 8, 37), (513, 8, 37), (1, 3, 1), (1000, 5, 128), (3000, 333, 100),
     (5001, 17, 1000), (2049, 300, 7), (4096, 64, 33), (10240, 20, 128), (2112, 9, 97),
-    (1538, 8, 64), (20480, 600, 100)])
+    (1538, 8, 64), (20480, 600, 100), (3000, 40, 200), (2500, 30, 129), (4000, 25, 300),
+    (6000, 11, 512), (1024, 301, 257), (700, 2, 2)])
 @pytest.mark.parametrize("pad", [0, 1])
 def test_fortran_ordered_bit_exact(rows, cols, L, pad):
     rng = np.random.default_rng(rows * 7 + cols + L)
@@ -61,6 +62,22 @@ def test_fortran_segmented_and_shards():
         op.sketch_into(dense_operand(_fortran_dev(a[r0:r1])), y, row0=r0, accumulate=True,
                        flags=IDS_FLAG_ORDERED)
     assert relerr_fro(y.t().cpu().numpy(), want) <= 1e-13
+
+
+@pytest.mark.parametrize("L", [100, 300])
+def test_fortran_ordered_shards_accumulate_bit_exact(L):
+    """Ordered row shards accumulated into one Y continue each entry's sum in
+    increasing row order, so the result is the one-shot sum bit for bit."""
+    rng = np.random.default_rng(L)
+    rows, cols = 30_000, 21
+    a = rng.standard_normal((rows, cols))
+    op = ids.CountSketchOp(rows, L, seed=3, surjective=True)
+    want = oracle.cs_apply(op.bucket, op.sign, L, a)
+    y = torch.zeros((cols, L), dtype=torch.float64, device="cuda")
+    for r0, r1 in [(0, 511), (511, 1537), (1537, 20_000), (20_000, 30_000)]:
+        op.sketch_into(dense_operand(_fortran_dev(a[r0:r1])), y, row0=r0, accumulate=True,
+                       flags=IDS_FLAG_ORDERED)
+    assert np.array_equal(y.t().cpu().numpy(), want)
 
 
 def test_fortran_large_sketch_dim_falls_back():
