@@ -479,9 +479,10 @@ __global__ void __launch_bounds__(kCtThreads) tile_bucket_lists_kernel(
     }
 }
 
-template <int TT>
+// stage = CT columns of a 512-row tile (padded stride) + its list + its starts
+template <int CT>
 __host__ __device__ __forceinline__ size_t coltile_ra_stage_bytes(int ss) {
-    return (size_t)kCt * (TT + 2) * sizeof(double) + TT * sizeof(int32_t) + (size_t)ss * sizeof(int32_t);
+    return (size_t)CT * kTTp * sizeof(double) + kTT * sizeof(int32_t) + (size_t)ss * sizeof(int32_t);
 }
 
 __device__ __forceinline__ uint32_t cs_smem_addr(const void* p) {
@@ -490,16 +491,18 @@ __device__ __forceinline__ uint32_t cs_smem_addr(const void* p) {
 
 // Needs 16-byte aligned columns (A and ld even).  Warp-specialised: the last
 // warp is the producer -- per tile, one bulk copy per column (one lane each)
-// plus the list and the slot starts, against the stage's `full` mbarrier --
-// and every consumer warp walks its slots and releases the stage on its
-// `empty` mbarrier, so warps drift up to S tiles apart instead of meeting at
-// a CTA barrier per tile, and no consumer ever issues copies.
-template <int BPL, int TT, int S>
-__global__ void __launch_bounds__(512 + 32, 2) cs_coltile_ra_kernel(
+// plus the list and the bucket starts, against the stage's `full` mbarrier --
+// and every consumer warp walks its buckets and releases the stage on its
+// `empty` mbarrier, so warps drift up to kCtStages tiles apart instead of
+// meeting at a CTA barrier per tile, and no consumer issues copies.  The CTA
+// owns up to CT = 8 * CPL columns; lane (slot, c) adds into columns c, c + 8,
+// .. (CPL of them), so one list entry's decode serves CPL columns.
+template <int BPL, int CPL>
+__global__ void __launch_bounds__(512 + 32, CPL == 1 ? 2 : 1) cs_coltile_ra_kernel(
     const double* __restrict__ A, int64_t ld, int64_t rows, int64_t cols,
     const int32_t* __restrict__ lists, const int32_t* __restrict__ starts, int64_t L, int nslots,
     int ss, int ngroups, double* __restrict__ out, int init_from_out) {
-    constexpr int TTp = TT + 2;
+    constexpr int S = kCtStages, CT = kCt * CPL;
     extern __shared__ __align__(16) char ra_stages[];
     __shared__ __align__(8) uint64_t s_full[S], s_empty[S];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -507,13 +510,13 @@ __global__ void __launch_bounds__(512 + 32, 2) cs_coltile_ra_kernel(
     const int group = blockIdx.x;
     const int64_t c0 = cols * group / ngroups;
     const int nc = (int)(cols * (group + 1) / ngroups - c0);
-    const int64_t ntl = (rows + TT - 1) / TT;
-    const size_t stage_bytes = coltile_ra_stage_bytes<TT>(ss);
+    const int64_t ntl = (rows + kTT - 1) / kTT;
+    const size_t stage_bytes = coltile_ra_stage_bytes<CT>(ss);
     auto stage_tile = [&](int s) { return reinterpret_cast<double*>(ra_stages + s * stage_bytes); };
     auto stage_list = [&](int s) {
-        return reinterpret_cast<int32_t*>(ra_stages + s * stage_bytes + (size_t)kCt * TTp * sizeof(double));
+        return reinterpret_cast<int32_t*>(ra_stages + s * stage_bytes + (size_t)CT * kTTp * sizeof(double));
     };
-    auto stage_starts = [&](int s) { return stage_list(s) + TT; };
+    auto stage_starts = [&](int s) { return stage_list(s) + kTT; };
     auto wait = [&](uint64_t* mb, uint32_t parity) {
         asm volatile(
             "{\n\t.reg .pred p;\n"
@@ -537,17 +540,17 @@ __global__ void __launch_bounds__(512 + 32, 2) cs_coltile_ra_kernel(
         for (int64_t k = 0; k < ntl; ++k) {
             const int s = (int)(k % S);
             if (k >= S) wait(&s_empty[s], (uint32_t)((k / S - 1) & 1));
-            const int64_t rb = k * TT;
-            const int n = (int)tmin<int64_t>(TT, rows - rb);
+            const int64_t rb = k * kTT;
+            const int n = (int)tmin<int64_t>(kTT, rows - rb);
             double* dst = stage_tile(s);
             const uint32_t col_bytes = (uint32_t)(n & ~1) * 8u;
             if ((n & 1) && lane < nc)  // odd last tile: its last row by plain loads
-                dst[lane * TTp + n - 1] = A[(c0 + lane) * ld + rb + n - 1];
+                dst[lane * kTTp + n - 1] = A[(c0 + lane) * ld + rb + n - 1];
             __syncwarp();
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                                  cs_smem_addr(&s_full[s])),
-                             "r"(nc * col_bytes + TT * 4u + (uint32_t)ss * 4u)
+                             "r"(nc * col_bytes + kTT * 4u + (uint32_t)ss * 4u)
                              : "memory");
             __syncwarp();
             const void* src = nullptr;
@@ -555,13 +558,13 @@ __global__ void __launch_bounds__(512 + 32, 2) cs_coltile_ra_kernel(
             uint32_t bytes = 0;
             if (lane < nc) {
                 src = A + (c0 + lane) * ld + rb;
-                d = dst + lane * TTp;
+                d = dst + lane * kTTp;
                 bytes = col_bytes;
-            } else if (lane == kCt) {
+            } else if (lane == CT) {
                 src = lists + rb;
                 d = stage_list(s);
-                bytes = TT * 4u;
-            } else if (lane == kCt + 1) {
+                bytes = kTT * 4u;
+            } else if (lane == CT + 1) {
                 src = starts + k * ss;
                 d = stage_starts(s);
                 bytes = (uint32_t)ss * 4u;
@@ -579,41 +582,84 @@ __global__ void __launch_bounds__(512 + 32, 2) cs_coltile_ra_kernel(
     // ---- consumers ----
     const int slot = t / kCt, c = t % kCt;
     const bool active = c < nc && slot < nslots;
-    double acc[BPL];
+    // columns c + 8 p past nc read stale shared memory into sums never written
+    double acc[BPL][CPL];
 #pragma unroll
-    for (int j = 0; j < BPL; ++j) {
-        const int64_t b = slot + (int64_t)j * nslots;
-        acc[j] = (init_from_out && active && b < L) ? out[(c0 + c) * L + b] : 0.0;
-    }
+    for (int j = 0; j < BPL; ++j)
+#pragma unroll
+        for (int p = 0; p < CPL; ++p) {
+            const int64_t b = slot + (int64_t)j * nslots;
+            const int cc = c + kCt * p;
+            acc[j][p] = (init_from_out && active && cc < nc && b < L) ? out[(c0 + cc) * L + b] : 0.0;
+        }
+    auto sgn = [](int32_t e, double v) {  // v with the entry's sign applied
+        return __hiloint2double(__double2hiint(v) ^ (e & (int)0x80000000u), __double2loint(v));
+    };
     for (int64_t k = 0; k < ntl; ++k) {
         const int s = (int)(k % S);
         wait(&s_full[s], (uint32_t)((k / S) & 1));
-        const double* tl = stage_tile(s) + c * TTp;
+        const char* tb = reinterpret_cast<const char*>(stage_tile(s) + c * kTTp);
         const int32_t* lst = stage_list(s);
         const int32_t* sts = stage_starts(s);
+        // value of column c + 8 p at the entry's row
+        auto at = [&](int32_t e, int p) {
+            return *reinterpret_cast<const double*>(tb + (e & 0xFF8) + p * (kCt * kTTp * 8));
+        };
         if (active) {
-            auto sgn = [](int32_t e, double v) {  // v with the entry's sign applied
-                return __hiloint2double(__double2hiint(v) ^ (e & (int)0x80000000u), __double2loint(v));
-            };
+            if constexpr (BPL <= 2) {
+                // the runs walked side by side: BPL x CPL independent add
+                // chains per lane, as many steps as the longest run
+                int q[BPL], q1[BPL];
 #pragma unroll
-            for (int j = 0; j < BPL; ++j) {
-                const int b = slot + j * nslots;
-                if (b < L) {
-                    int q = sts[b];
-                    const int q1 = sts[b + 1];
-                    const char* tb = reinterpret_cast<const char*>(tl);
-                    auto at = [&](int32_t e) { return *reinterpret_cast<const double*>(tb + (e & 0xFF8)); };
-                    for (; q + 3 < q1; q += 4) {
-                        const int32_t e0 = lst[q], e1 = lst[q + 1], e2 = lst[q + 2], e3 = lst[q + 3];
-                        const double v0 = at(e0), v1 = at(e1), v2 = at(e2), v3 = at(e3);
-                        acc[j] += sgn(e0, v0);
-                        acc[j] += sgn(e1, v1);
-                        acc[j] += sgn(e2, v2);
-                        acc[j] += sgn(e3, v3);
+                for (int j = 0; j < BPL; ++j) {
+                    const int b = slot + j * nslots;
+                    q[j] = b < L ? sts[b] : 0;
+                    q1[j] = b < L ? sts[b + 1] : 0;
+                }
+                int steps = 0;
+#pragma unroll
+                for (int j = 0; j < BPL; ++j) steps = max(steps, q1[j] - q[j]);
+                for (int i = 0; i < steps; ++i) {
+                    int32_t e[BPL];
+                    double v[BPL][CPL];
+#pragma unroll
+                    for (int j = 0; j < BPL; ++j) {
+                        e[j] = lst[min(q[j] + i, max(q1[j] - 1, 0))];
+#pragma unroll
+                        for (int p = 0; p < CPL; ++p) v[j][p] = at(e[j], p);
                     }
-                    for (; q < q1; ++q) {
-                        const int32_t e0 = lst[q];
-                        acc[j] += sgn(e0, at(e0));
+#pragma unroll
+                    for (int j = 0; j < BPL; ++j)
+                        if (q[j] + i < q1[j])
+#pragma unroll
+                            for (int p = 0; p < CPL; ++p) acc[j][p] += sgn(e[j], v[j][p]);
+                }
+            } else {  // one run after the other
+#pragma unroll
+                for (int j = 0; j < BPL; ++j) {
+                    const int b = slot + j * nslots;
+                    if (b < L) {
+                        int q = sts[b];
+                        const int q1 = sts[b + 1];
+                        for (; q + 1 < q1; q += 2) {
+                            const int32_t e0 = lst[q], e1 = lst[q + 1];
+                            double v0[CPL], v1[CPL];
+#pragma unroll
+                            for (int p = 0; p < CPL; ++p) {
+                                v0[p] = at(e0, p);
+                                v1[p] = at(e1, p);
+                            }
+#pragma unroll
+                            for (int p = 0; p < CPL; ++p) {
+                                acc[j][p] += sgn(e0, v0[p]);
+                                acc[j][p] += sgn(e1, v1[p]);
+                            }
+                        }
+                        if (q < q1) {
+                            const int32_t e0 = lst[q];
+#pragma unroll
+                            for (int p = 0; p < CPL; ++p) acc[j][p] += sgn(e0, at(e0, p));
+                        }
                     }
                 }
             }
@@ -624,10 +670,13 @@ __global__ void __launch_bounds__(512 + 32, 2) cs_coltile_ra_kernel(
     }
     if (active) {
 #pragma unroll
-        for (int j = 0; j < BPL; ++j) {
-            const int64_t b = slot + (int64_t)j * nslots;
-            if (b < L) out[(c0 + c) * L + b] = acc[j];
-        }
+        for (int j = 0; j < BPL; ++j)
+#pragma unroll
+            for (int p = 0; p < CPL; ++p) {
+                const int64_t b = slot + (int64_t)j * nslots;
+                const int cc = c + kCt * p;
+                if (b < L && cc < nc) out[(c0 + cc) * L + b] = acc[j][p];
+            }
     }
 }
 
@@ -724,33 +773,32 @@ struct ColTilePlan {
     int64_t ntiles;
     size_t smem;
     // register-accumulator variant (cs_coltile_ra_kernel): BPL buckets per slot
-    int bpl, nslots, ss, threads, ngroups_ra, tt;
-    int64_t ntiles_ra;
+    int bpl, cpl, nslots, ss, threads, ngroups_ra;
     size_t smem_ra;
     int64_t starts_stride;  // int32 per tile in the starts array
 };
 
-// rows per tile and pipeline stages of the register variant (IDS_COLTILE_TT
-// = 256 selects 256-row tiles in 6 stages, the default 512 x 3)
-int coltile_ra_tt() {
-    static const int tt = [] {
-        const char* e = getenv("IDS_COLTILE_TT");
-        return (e && atoi(e) == 256) ? 256 : 512;
+// columns per lane of the register variant: 1 (8-column CTAs, two per SM) or
+// 2 (16-column CTAs, one per SM); IDS_COLTILE_CPL overrides the default
+int coltile_ra_cpl() {
+    static const int cpl = [] {
+        const char* e = getenv("IDS_COLTILE_CPL");
+        return (e && atoi(e) == 1) ? 1 : (e && atoi(e) == 2 ? 2 : 2);
     }();
-    return tt;
+    return cpl;
 }
 
-template <int BPL, int TT, int S>
+template <int BPL, int CPL>
 int coltile_ra_occupancy(int threads, size_t smem) {
     static int cached[1024 / 32 + 1] = {};
     int& c = cached[threads / 32];
     if (!c) {
         // every ss this kernel takes (<= kRaMaxBuckets + 4) fits the attribute
-        const size_t smax = S * coltile_ra_stage_bytes<TT>(kRaMaxBuckets + 4);
-        IDS_CUDA_TRY(cudaFuncSetAttribute(cs_coltile_ra_kernel<BPL, TT, S>,
+        const size_t smax = kCtStages * coltile_ra_stage_bytes<kCt * CPL>(kRaMaxBuckets + 4);
+        IDS_CUDA_TRY(cudaFuncSetAttribute(cs_coltile_ra_kernel<BPL, CPL>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
         int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cs_coltile_ra_kernel<BPL, TT, S>,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cs_coltile_ra_kernel<BPL, CPL>,
                                                           threads + 32, smem) != cudaSuccess || occ < 1)
             occ = 1;
         c = occ;
@@ -758,16 +806,16 @@ int coltile_ra_occupancy(int threads, size_t smem) {
     return c;
 }
 
-int coltile_ra_occ(int bpl, int tt, int threads, size_t smem) {
-    if (tt == 256) switch (bpl) {
-            case 2: return coltile_ra_occupancy<2, 256, 6>(threads, smem);
-            case 4: return coltile_ra_occupancy<4, 256, 6>(threads, smem);
-            default: return coltile_ra_occupancy<8, 256, 6>(threads, smem);
+int coltile_ra_occ(int bpl, int cpl, int threads, size_t smem) {
+    if (cpl == 2) switch (bpl) {
+            case 2: return coltile_ra_occupancy<2, 2>(threads, smem);
+            case 4: return coltile_ra_occupancy<4, 2>(threads, smem);
+            default: return coltile_ra_occupancy<8, 2>(threads, smem);
         }
     switch (bpl) {
-        case 2: return coltile_ra_occupancy<2, 512, 3>(threads, smem);
-        case 4: return coltile_ra_occupancy<4, 512, 3>(threads, smem);
-        default: return coltile_ra_occupancy<8, 512, 3>(threads, smem);
+        case 2: return coltile_ra_occupancy<2, 1>(threads, smem);
+        case 4: return coltile_ra_occupancy<4, 1>(threads, smem);
+        default: return coltile_ra_occupancy<8, 1>(threads, smem);
     }
 }
 
@@ -797,11 +845,11 @@ ColTilePlan plan_coltile(int64_t rows, int64_t cols, int64_t L, int flags) {
         p.nslots = (int)ceil_div(L, p.bpl);
         p.threads = (int)ceil_div((int64_t)p.nslots * kCt, 32) * 32;
         p.ss = (int)ceil_div(L + 1, 4) * 4;  // bucket starts per tile
-        p.tt = coltile_ra_tt();
-        p.ntiles_ra = ceil_div(rows, p.tt);
-        p.smem_ra = p.tt == 256 ? 6 * coltile_ra_stage_bytes<256>(p.ss) : 3 * coltile_ra_stage_bytes<512>(p.ss);
-        const int64_t cap = (int64_t)ids_sm_count() * coltile_ra_occ(p.bpl, p.tt, p.threads, p.smem_ra);
-        p.ngroups_ra = (int)tmax<int64_t>(ceil_div(cols, kCt), tmin<int64_t>(cols, cap));
+        p.cpl = coltile_ra_cpl();
+        p.smem_ra = kCtStages * (p.cpl == 2 ? coltile_ra_stage_bytes<2 * kCt>(p.ss)
+                                            : coltile_ra_stage_bytes<kCt>(p.ss));
+        const int64_t cap = (int64_t)ids_sm_count() * coltile_ra_occ(p.bpl, p.cpl, p.threads, p.smem_ra);
+        p.ngroups_ra = (int)tmax<int64_t>(ceil_div(cols, (int64_t)kCt * p.cpl), tmin<int64_t>(cols, cap));
         p.starts_stride = tmax<int64_t>(kStartsStride, p.ss);
     }
     return p;
@@ -822,7 +870,7 @@ extern "C" size_t ids_countsketch_dense_workspace_bytes(int64_t rows, int64_t co
         c.take<double>((size_t)tmax(nseg, q.nseg) * out_dim * cols);
         c.take<int32_t>((size_t)rows);
         c.take<int32_t>((size_t)q.ntiles * kTT);
-        c.take<int32_t>((size_t)ceil_div(rows, 256) * tmax(q.starts_stride, qo.starts_stride));
+        c.take<int32_t>((size_t)q.ntiles * tmax(q.starts_stride, qo.starts_stride));
         return c.off + 256;
     }
     c.take<double>((size_t)nseg * out_dim * cols);
@@ -851,7 +899,7 @@ extern "C" int ids_countsketch_dense_f64(const double* A, int64_t rows, int64_t 
             double* part = q.nseg > 1 ? ws.take<double>((size_t)q.nseg * out_dim * cols) : nullptr;
             int32_t* codes = ws.take<int32_t>((size_t)rows);
             int32_t* lists = ws.take<int32_t>((size_t)q.ntiles * kTT);
-            int32_t* starts = ws.take<int32_t>((size_t)ceil_div(rows, 256) * q.starts_stride);
+            int32_t* starts = ws.take<int32_t>((size_t)q.ntiles * q.starts_stride);
             if (!ws.ok()) {
                 ids_set_last_error("dense countsketch: workspace too small");
                 return IDS_EWORKSPACE;
@@ -864,25 +912,21 @@ extern "C" int ids_countsketch_dense_f64(const double* A, int64_t rows, int64_t 
             double* out = q.nseg > 1 ? part : Y;
             const int init = (q.nseg == 1 && accumulate) ? 1 : 0;
             if (q.bpl && vec16) {
-                if (q.tt == 256)
-                    tile_bucket_lists_kernel<256><<<(unsigned)q.ntiles_ra, kCtThreads, 0, st>>>(
-                        codes, rows, (int)out_dim, q.ss, lists, starts);
-                else
-                    tile_bucket_lists_kernel<512><<<(unsigned)q.ntiles_ra, kCtThreads, 0, st>>>(
-                        codes, rows, (int)out_dim, q.ss, lists, starts);
+                tile_bucket_lists_kernel<kTT><<<(unsigned)q.ntiles, kCtThreads, 0, st>>>(
+                    codes, rows, (int)out_dim, q.ss, lists, starts);
                 IDS_LAUNCH_CHECK();
                 const unsigned grid = (unsigned)q.ngroups_ra;
-#define IDS_RA_LAUNCH(B, TT, S)                                                              \
-    cs_coltile_ra_kernel<B, TT, S><<<grid, q.threads + 32, q.smem_ra, st>>>(                      \
+#define IDS_RA_LAUNCH(B, C)                                                                  \
+    cs_coltile_ra_kernel<B, C><<<grid, q.threads + 32, q.smem_ra, st>>>(                     \
         A, ld, rows, cols, lists, starts, out_dim, q.nslots, q.ss, q.ngroups_ra, out, init)
-                if (q.tt == 256) {
-                    if (q.bpl == 2) IDS_RA_LAUNCH(2, 256, 6);
-                    else if (q.bpl == 4) IDS_RA_LAUNCH(4, 256, 6);
-                    else IDS_RA_LAUNCH(8, 256, 6);
+                if (q.cpl == 2) {
+                    if (q.bpl == 2) IDS_RA_LAUNCH(2, 2);
+                    else if (q.bpl == 4) IDS_RA_LAUNCH(4, 2);
+                    else IDS_RA_LAUNCH(8, 2);
                 } else {
-                    if (q.bpl == 2) IDS_RA_LAUNCH(2, 512, 3);
-                    else if (q.bpl == 4) IDS_RA_LAUNCH(4, 512, 3);
-                    else IDS_RA_LAUNCH(8, 512, 3);
+                    if (q.bpl == 2) IDS_RA_LAUNCH(2, 1);
+                    else if (q.bpl == 4) IDS_RA_LAUNCH(4, 1);
+                    else IDS_RA_LAUNCH(8, 1);
                 }
 #undef IDS_RA_LAUNCH
                 IDS_LAUNCH_CHECK();

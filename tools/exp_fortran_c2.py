@@ -10,7 +10,7 @@ opnd = dense_operand(G.dense_config("C2", layout="F"))
 op = ids.CountSketchOp(1_000_000, 100, seed=1, surjective=True)
 op.bucket_index()
 y = torch.empty((2000, 100), dtype=torch.float64, device="cuda")
-for rep in range(3):
+for rep in range(5):
     for _ in range(2):
         op.sketch_into(opnd, y, flags=1)
     torch.cuda.synchronize()

@@ -24,7 +24,7 @@ full() {  # $1 kernel regex, $2 report name, $3.. prof_config args
       -o gpurun_out/pf_full_$name python tools/prof_config.py "$@" > gpurun_out/pf_ncu_full_$name.log 2>&1
 }
 full cs_rowmajor cs_rowmajor --workload C2
-full cs_coltile cs_coltile --workload C2 --fortran
+full cs_coltile_ra cs_coltile_ra --workload C2 --fortran
 full cs_csr_stream cs_csr_stream --workload C3
 full fy_phaseb fy_phaseb_c3 --workload C3
 full ts_split_kernel ts_split_c4 --workload C4

@@ -89,7 +89,9 @@ for cfg, what in (("C2", "C2 countsketch_id, dense 1e6 x 2000, K=20, L=100"),
 traffic = {}
 for rep, name, title, key in (
         ("pf_full_cs_rowmajor.ncu-rep", "cs_rowmajor", "cs_rowmajor_kernel, C2 sketch (C order)", "C2"),
-        ("pf_full_cs_coltile.ncu-rep", "cs_coltile", "cs_coltile_kernel, C2 in F order", None),
+        ("pf_full_cs_coltile.ncu-rep", "cs_coltile", "cs_coltile_kernel (32-slot), C2 in F order", None),
+        ("pf_full_cs_coltile_ra.ncu-rep", "cs_coltile_ra",
+         "cs_coltile_ra_kernel<2,512,3> (bucket-sorted tiles, register accumulators), C2 in F order", None),
         ("pf_full_cs_csr_stream.ncu-rep", "cs_csr_stream", "cs_csr_stream_kernel, C3", "C3"),
         ("pf_full_fy_phaseb_c3.ncu-rep", "fy_phaseb_c3", "fy_phaseb_kernel, C3 hash (I = 1e7)", None),
         ("pf_full_tensorsketch_c4.ncu-rep", "tensorsketch_c4", "tensorsketch_kernel<8>, C4", None),
