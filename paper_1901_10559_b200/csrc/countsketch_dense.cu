@@ -9,10 +9,12 @@
 // so Y is bit-identical to the reference when each bucket is one segment.
 //
 // Col-major A (Fortran order, what the reference's as_dense produces):
-// column-stream kernel.  One warp owns NC columns and a row segment; lanes
-// read 32 consecutive rows (coalesced) and scatter into a per-warp L x NC
-// shared-memory accumulator.  Lanes that hit the same bucket are ordered by
-// row with __match_any_sync ranks, so the sum order is again increasing row.
+// tiled kernels over 512-row tiles whose rows a pre-pass sorts by bucket
+// (cs_coltile_ra_kernel: producer warp + bulk copies, register running sums;
+// cs_coltile_kernel: 32 slots with shared-memory sums for L > 512), and a
+// column-stream fallback (one warp per NC columns and a row segment, lanes
+// ordered per bucket with __match_any_sync ranks).  Every path adds each Y
+// entry's terms in increasing row order.
 //
 // Both paths are HBM-streaming kernels (algorithmic traffic = bytes of A);
 // tensor cores have nothing to do here.
