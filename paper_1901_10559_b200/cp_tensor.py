@@ -172,6 +172,8 @@ class CpTensor:
 
     def select(self, cols, weights):
         """CP tensor built from the given term indices and new weights."""
+        if all(isinstance(f, np.ndarray) for f in self.factors):
+            return self._select_dense(cols, weights)
         sel = []
         for f in self.factors:
             if _is_cuda(f):
@@ -181,6 +183,29 @@ class CpTensor:
             else:
                 sel.append(f[:, cols])
         return CpTensor(weights, sel)
+
+    def _select_dense(self, cols, weights):
+        """select() for dense host factors without re-validating them: the
+        chosen columns are already unit to 1e-12 (this tensor's own
+        normalization), so CpTensor(weights, sel) would keep them bit for bit
+        and only move negative weights' signs into mode 0 -- which is all
+        this does."""
+        cols = np.asarray(cols, dtype=np.int64)
+        weights = np.asarray(weights, dtype=np.float64).copy()
+        if weights.shape != (cols.size,):
+            raise ValueError(f"weights must have length {cols.size}")
+        if not np.isfinite(weights).all():
+            raise ValueError("weights must be finite")
+        sel = [np.asfortranarray(f[:, cols]) for f in self.factors]
+        negative = weights < 0.0
+        if negative.any():
+            sel[0] = sel[0] * np.where(negative, -1.0, 1.0)
+            weights = np.abs(weights)
+        out = object.__new__(CpTensor)
+        out.weights = weights
+        out.factors = sel
+        out.zero_columns = np.zeros(0, dtype=np.int64)
+        return out
 
     def to_dense(self, max_entries=_MAX_DENSE_ENTRIES):
         """Materialize the full tensor (testing and small problems only)."""
@@ -258,8 +283,69 @@ def tensorsketch_device(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RA
 def tensorsketch_id(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL):
     """Rank reduction via a TensorSketch of the flattened rank-1 terms
     (cp_tensor.py:266-276)."""
+    res = _host_graph_call(x, rank, sketch_dim, seed, rank_tol)
+    if res is not None:
+        return res
     d, _ = tensorsketch_device(x, rank, sketch_dim, seed, rank_tol)
     return _assemble(x, d.to_host("tensorsketch"), "tensorsketch")
+
+
+# Repeated tensorsketch_id calls on host tensors of one shape (trials,
+# serving) replay a captured TensorIdGraph over persistent device copies of
+# the factors: the second call with a given (mode dims, R, rank, L, rank_tol)
+# captures it, later calls copy the factors and weights in (async DMA when
+# the host memory is pinned), replay, and read (j, P) back in one copy.  The
+# kernels and their order are the eager path's, so results are identical.
+# One shape is kept; factors above HOST_GRAPH_MAX_BYTES always go eager.
+HOST_GRAPHS = True
+HOST_GRAPH_MAX_BYTES = 1 << 30
+_host_graph = {"key": None, "seen": None, "graph": None, "bufs": None, "w": None}
+
+
+def _host_graph_call(x, rank, sketch_dim, seed, rank_tol):
+    import torch
+
+    from . import _device
+    from .matrix_id import DeviceId
+
+    if not HOST_GRAPHS or not all(isinstance(f, np.ndarray) for f in x.factors):
+        return None
+    if sum(f.nbytes for f in x.factors) > HOST_GRAPH_MAX_BYTES:
+        return None
+    L = check_tensor_id_args(x, rank, sketch_dim, "tensorsketch")
+    from ._native import query
+
+    if not query("ids_tensorsketch_fused_ok", len(x.mode_dims), L):
+        return None  # the long-sketch (spectral) route is not captured
+    key = (tuple(x.mode_dims), int(x.rank), int(rank), int(L), float(rank_tol),
+           _device.device().index)
+    st = _host_graph
+    if st["key"] != key:
+        if st["seen"] != key:  # first sighting: the eager path this time
+            st["seen"] = key
+            return None
+        st.update(key=None, graph=None, bufs=None, w=None)
+        bufs = [_device.empty((int(x.rank), d), torch.float64) for d in x.mode_dims]
+        w = _device.empty(int(x.rank), torch.float64)
+        _host_graph_fill(x, bufs, w)
+        g = TensorIdGraph([b.t() for b in bufs], w, rank, L, rank_tol, host_weights=x.weights)
+        st.update(key=key, graph=g, bufs=bufs, w=w)
+    else:
+        _host_graph_fill(x, st["bufs"], st["w"])
+    g = st["graph"]
+    g.host_out.copy_(g.device(seed), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    d = DeviceId.unpack(g.host_out.numpy(), int(rank), int(x.rank), "tensorsketch")
+    return _assemble(x, d, "tensorsketch")
+
+
+def _host_graph_fill(x, bufs, w):
+    import torch
+
+    for f, b in zip(x.factors, bufs):
+        t = torch.from_numpy(f.T)  # F-order I_n x R -> contiguous (R, I_n)
+        b.copy_(t, non_blocking=t.is_pinned())
+    w.copy_(torch.from_numpy(np.ascontiguousarray(x.weights, dtype=np.float64)))
 
 
 class TensorIdGraph:

@@ -37,7 +37,11 @@ def factor_to_device(f):
     arr = np.asarray(f, dtype=np.float64)
     if arr.ndim != 2:
         raise ValueError("factor must be 2-D")
-    return torch.from_numpy(np.ascontiguousarray(arr.T)).to(_device.device())
+    t = torch.from_numpy(np.ascontiguousarray(arr.T))
+    # page-locked host memory (e.g. a view of a pinned buffer): an async DMA
+    # ordered on the current stream; the caller's array outlives the call,
+    # which ends with a synchronizing device->host read
+    return t.to(_device.device(), non_blocking=t.is_pinned())
 
 
 SCATTER_MIN_DIM = 4096  # mode length from which the fused kernel uses a scatter plan

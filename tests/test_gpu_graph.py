@@ -87,3 +87,50 @@ def test_device_cp_tensor_matches_host():
 def test_tensor_id_graph_rejects_host_inputs():
     with pytest.raises(ValueError):
         ids.TensorIdGraph([np.ones((5, 3))] * 2, np.ones(3), 2, 8)
+
+
+def _eager(x, k, L, seed):
+    from paper_1901_10559_b200 import cp_tensor
+
+    cp_tensor.HOST_GRAPHS = False
+    try:
+        return ids.tensorsketch_id(x, k, L, seed=seed)
+    finally:
+        cp_tensor.HOST_GRAPHS = True
+
+
+def _same(a, b):
+    assert np.array_equal(a.cols, b.cols)
+    assert np.array_equal(a.coeffs, b.coeffs)
+    assert np.array_equal(a.new_weights, b.new_weights)
+    assert a.numerical_rank == b.numerical_rank and a.rank_deficient == b.rank_deficient
+    assert all(np.array_equal(p, q) for p, q in zip(a.reduced.factors, b.reduced.factors))
+    assert np.array_equal(a.reduced.weights, b.reduced.weights)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_tensor_repeat_calls_replay_graph(pinned):
+    """tensorsketch_id on host factors: the second call of a shape captures
+    a graph over device copies of the factors, later calls refill them and
+    replay; every result equals the eager path's, also when shapes alternate
+    and when the factor values change between calls."""
+    from paper_1901_10559_b200 import cp_tensor
+
+    rng = np.random.default_rng(4)
+
+    def tensor(dims, R, scale=1.0):
+        fs = []
+        for d in dims:
+            f = torch.from_numpy(rng.standard_normal((R, d)) * scale)
+            f = f / f.norm(dim=1, keepdim=True)
+            fs.append((f.pin_memory() if pinned else f).numpy().T)
+        return ids.CpTensor(rng.random(R) + 0.1, fs)
+
+    xa, xb = tensor((300, 200, 90), 400), tensor((5000, 64), 300)
+    for x, k, L, seed in [(xa, 10, 4096, 1), (xa, 10, 4096, 2), (xa, 10, 4096, 3),
+                          (xb, 7, 1024, 4), (xb, 7, 1024, 5), (xa, 10, 4096, 6),
+                          (xa, 10, 4096, 7)]:
+        _same(ids.tensorsketch_id(x, k, L, seed=seed), _eager(x, k, L, seed))
+    assert cp_tensor._host_graph["graph"] is not None
+    xc = tensor((300, 200, 90), 400, scale=3.0)  # same shape, new values
+    _same(ids.tensorsketch_id(xc, 10, 4096, seed=8), _eager(xc, 10, 4096, 8))

@@ -114,3 +114,27 @@ def test_sparse_sketch_mode_validation():
     assert ids.set_sparse_sketch_mode(prev) == "stream"
     with pytest.raises(ValueError):
         ids.set_sparse_sketch_mode("fast")
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_cptensor_select_matches_full_constructor(seed):
+    """select() on dense factors skips re-validation; the result must equal
+    CpTensor(weights, the selected columns) bit for bit (zero columns, signs
+    moved into mode 0, -0.0 and 0 weights, repeated columns)."""
+    rng = np.random.default_rng(seed)
+    facs = [np.asfortranarray(rng.standard_normal((50 + 7 * n, 40))) for n in range(3)]
+    facs[1][:, 3] = 0.0
+    x = CpTensor(rng.standard_normal(40), facs)
+    cols = np.concatenate([[3, 3], rng.choice(40, 10, replace=False)])
+    w = rng.standard_normal(cols.size)
+    w[2], w[4] = 0.0, -0.0
+    for ww in (w, np.abs(w)):
+        got = x.select(cols, ww)
+        want = CpTensor(ww, [f[:, cols] for f in x.factors])
+        assert all(np.array_equal(a, b) for a, b in zip(got.factors, want.factors))
+        assert np.array_equal(got.weights, want.weights)
+        assert np.array_equal(np.signbit(got.weights), np.signbit(want.weights))
+        assert np.array_equal(got.zero_columns, want.zero_columns)
+        assert all(f.flags.f_contiguous for f in got.factors)
+    with pytest.raises(ValueError):
+        x.select(cols, np.full(cols.size, np.nan))
