@@ -299,7 +299,7 @@ def tensorsketch_id(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_T
 # One shape is kept; factors above HOST_GRAPH_MAX_BYTES always go eager.
 HOST_GRAPHS = True
 HOST_GRAPH_MAX_BYTES = 1 << 30
-_host_graph = {"key": None, "seen": None, "graph": None, "bufs": None, "w": None}
+_host_graph = {"key": None, "seen": None, "graph": None, "bufs": None, "w": None, "stream": None}
 
 
 def _host_graph_call(x, rank, sketch_dim, seed, rank_tol):
@@ -328,12 +328,18 @@ def _host_graph_call(x, rank, sketch_dim, seed, rank_tol):
         bufs = [_device.empty((int(x.rank), d), torch.float64) for d in x.mode_dims]
         w = _device.empty(int(x.rank), torch.float64)
         _host_graph_fill(x, bufs, w)
-        g = TensorIdGraph([b.t() for b in bufs], w, rank, L, rank_tol, host_weights=x.weights)
-        st.update(key=key, graph=g, bufs=bufs, w=w)
+        g = TensorIdGraph([b.t() for b in bufs], w, rank, L, rank_tol, host_weights=x.weights,
+                          split=True)
+        st.update(key=key, graph=g, bufs=bufs, w=w, stream=torch.cuda.Stream())
+        g.host_out.copy_(g.device(seed), non_blocking=True)
     else:
-        _host_graph_fill(x, st["bufs"], st["w"])
-    g = st["graph"]
-    g.host_out.copy_(g.device(seed), non_blocking=True)
+        # the factor copies on a side stream, under the hash-draw replay
+        g, side, main = st["graph"], st["stream"], torch.cuda.current_stream()
+        side.wait_stream(main)  # buffers free, seeds and weights ordered
+        with torch.cuda.stream(side):
+            _host_graph_fill(x, st["bufs"], st["w"])
+        g.host_out.copy_(g.device(seed, before_compute=lambda: main.wait_stream(side)),
+                         non_blocking=True)
     torch.cuda.current_stream().synchronize()
     d = DeviceId.unpack(g.host_out.numpy(), int(rank), int(x.rank), "tensorsketch")
     return _assemble(x, d, "tensorsketch")
@@ -369,7 +375,7 @@ class TensorIdGraph:
     formed in numpy, bit-identical to the reference)."""
 
     def __init__(self, factors, weights, rank, sketch_dim=None, rank_tol=DEFAULT_RANK_TOL,
-                 host_weights=None):
+                 host_weights=None, split=False):
         import torch
 
         from . import _device
@@ -399,29 +405,46 @@ class TensorIdGraph:
         self.seed_dev = _device.empty((n, 4), torch.int64)
         self.seed_host.numpy()[:] = TensorSketchOp.mode_seed_states(n, 0)
         self.seed_dev.copy_(self.seed_host)
-        self._body()  # eager run: lazy initialization outside the capture
+        self._compute(self._draw())  # eager run: lazy initialization outside the capture
         torch.cuda.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
         lib = _device.lib()
         n0 = lib.ids_launch_count()
+        # split=True: two graphs, the hash draws (which do not read the
+        # factors) and the rest, so that a caller can refill the factors on
+        # another stream while the draws replay (see _host_graph_call)
+        self.graph = torch.cuda.CUDAGraph()
+        self.graph_compute = torch.cuda.CUDAGraph() if split else None
         with torch.cuda.graph(self.graph, capture_error_mode="relaxed"):
-            self.out = self._body()
+            self._op = self._draw()
+            if not split:
+                self.out = self._compute(self._op)
+        if split:
+            with torch.cuda.graph(self.graph_compute, capture_error_mode="relaxed"):
+                self.out = self._compute(self._op)
         self.launches = int(lib.ids_launch_count() - n0)  # library kernels per replay
         self.host_out = torch.empty(self.out.shape, dtype=self.out.dtype, pin_memory=True)
 
-    def _body(self):
-        op = TensorSketchOp(self.mode_dims, self.L, _seed_dev=self.seed_dev)
+    def _draw(self):
+        return TensorSketchOp(self.mode_dims, self.L, _seed_dev=self.seed_dev)
+
+    def _compute(self, op):
         y, nrm = op.apply_device(self.factors, self.weights, norms=True)
         return device_matrix_id(y, self.L, self.R, self.k, self.rank_tol, colnorm2=nrm).packed()
 
-    def device(self, seed):
+    def device(self, seed, before_compute=None):
         """Replay for `seed`; the packed (cols, numerical rank, deficient, P)
-        device vector (valid until the next replay)."""
+        device vector (valid until the next replay).  before_compute (split
+        graphs only): called between the two replays, e.g. to make the
+        current stream wait for factor copies issued on another stream."""
         import torch
 
         self.seed_host.numpy()[:] = TensorSketchOp.mode_seed_states(len(self.mode_dims), seed)
         self.seed_dev.copy_(self.seed_host, non_blocking=True)
         self.graph.replay()
+        if self.graph_compute is not None:
+            if before_compute is not None:
+                before_compute()
+            self.graph_compute.replay()
         return self.out
 
     def trials(self, seeds):
@@ -443,6 +466,8 @@ class TensorIdGraph:
         for t in range(len(seeds)):
             self.seed_dev.copy_(st_dev[t])
             self.graph.replay()
+            if self.graph_compute is not None:
+                self.graph_compute.replay()
             outs.append(self.out.clone())
         host = _device.to_host(torch.stack(outs))
         res = []

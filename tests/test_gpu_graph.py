@@ -134,3 +134,19 @@ def test_host_tensor_repeat_calls_replay_graph(pinned):
     assert cp_tensor._host_graph["graph"] is not None
     xc = tensor((300, 200, 90), 400, scale=3.0)  # same shape, new values
     _same(ids.tensorsketch_id(xc, 10, 4096, seed=8), _eager(xc, 10, 4096, 8))
+
+
+def test_split_graph_matches_single_graph():
+    """TensorIdGraph(split=True) (draw and compute graphs) gives the single
+    graph's results, through __call__ and trials()."""
+    w, facs = G.cp_config("C4")
+    cfg = G.CONFIGS["C4"]
+    a = ids.TensorIdGraph(facs, w, cfg["k"], cfg["L"])
+    b = ids.TensorIdGraph(facs, w, cfg["k"], cfg["L"], split=True)
+    for seed in (5, 6):
+        (da, na), (db, nb) = a(seed), b(seed)
+        assert np.array_equal(da.cols, db.cols) and np.array_equal(da.coeffs, db.coeffs)
+        assert np.array_equal(na, nb)
+    for (da, na), (db, nb) in zip(a.trials([1, 2, 3]), b.trials([1, 2, 3])):
+        assert np.array_equal(da.cols, db.cols) and np.array_equal(da.coeffs, db.coeffs)
+        assert np.array_equal(na, nb)
