@@ -182,6 +182,37 @@ def _raise_if_nonfinite(flag, operand):
         raise ValueError("a contains non-finite entries")
 
 
+class _Shape:
+    """Shape-only stand-in for check_matrix_id_args on host inputs."""
+
+    def __init__(self, a):
+        self.shape = tuple(a.shape) if sp.issparse(a) else tuple(np.shape(a))
+
+
+def _host_input(a):
+    """numpy / scipy / CPU-tensor A, 2-D and non-empty, that still has to be
+    uploaded (anything else takes the plain path and its error order)."""
+    if isinstance(a, (DenseOperand, SparseOperand)):
+        return False
+    if isinstance(a, torch.Tensor) and a.device.type == "cuda":
+        return False
+    try:
+        shape = _Shape(a).shape
+    except Exception:
+        return False
+    return len(shape) == 2 and shape[0] >= 1 and shape[1] >= 1
+
+
+_UPLOAD_SIDE = {}
+
+
+def _upload_side_stream():
+    dev = _device.device()
+    if dev.index not in _UPLOAD_SIDE:
+        _UPLOAD_SIDE[dev.index] = torch.cuda.Stream(device=dev)
+    return _UPLOAD_SIDE[dev.index]
+
+
 def countsketch_device(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_TOL,
                        surjective=True, flags=IDS_FLAG_ORDERED, check_finite=True,
                        defer_check=False):
@@ -189,9 +220,21 @@ def countsketch_device(a, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RAN
     defer_check=True leaves the non-finite flag of the sketch on the device
     (DeviceId.nonfinite, DeviceId.operand) for the caller to read with the
     result -- no host synchronization before the ID is enqueued."""
-    operand = a if isinstance(a, (DenseOperand, SparseOperand)) else matrix_operand(a)
-    sketch_dim = check_matrix_id_args(operand, rank, sketch_dim, "countsketch")
-    op = CountSketchOp(operand.rows, sketch_dim, seed=seed, surjective=surjective)
+    if _host_input(a):
+        # host A: the hash is drawn on a side stream while A is uploaded (it
+        # does not read A), then joined back into the current stream
+        sketch_dim = check_matrix_id_args(_Shape(a), rank, sketch_dim, "countsketch")
+        main, side = torch.cuda.current_stream(), _upload_side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            op = CountSketchOp(_Shape(a).shape[0], sketch_dim, seed=seed, surjective=surjective)
+        operand = matrix_operand(a)
+        main.wait_stream(side)
+        op.record_stream(main)
+    else:
+        operand = a if isinstance(a, (DenseOperand, SparseOperand)) else matrix_operand(a)
+        sketch_dim = check_matrix_id_args(operand, rank, sketch_dim, "countsketch")
+        op = CountSketchOp(operand.rows, sketch_dim, seed=seed, surjective=surjective)
     nonfinite = _device.zeros(1, torch.int32) if check_finite else None
     y = op.apply_device(operand, flags=flags, nonfinite=nonfinite)
     if check_finite and not defer_check:
