@@ -1851,8 +1851,12 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
             t.numerical_rank = numerical_rank;
             t.tlog = g_cpqr_tlog;
             // the leading 2 x 2048 rows of every column stay in L2 across the k
-            // passes (64 MB at C5; larger pins measured slower)
-            t.pin_segs = 2;
+            // passes (64 MB at C5; larger pins measured slower) -- unless every
+            // CTA's units fit in TMEM (one per warp): then none is pinned and
+            // all of them stay resident (C4, 4096 x 1000: 152 -> 127 us)
+            const bool all_resident =
+                seg == 2048 && ceil_div(cols, (int64_t)G) * ceil_div(rows, seg) <= kTThreads / 32;
+            t.pin_segs = all_resident ? 0 : 2;
             t.tmem = 1;
             if (const char* e = getenv("IDS_CPQR_PIN")) t.pin_segs = atoi(e);  // experiments
             if (const char* e = getenv("IDS_CPQR_TMEM")) t.tmem = atoi(e);
