@@ -1,0 +1,78 @@
+"""C2 trials: what the background hash draws cost the sketch stream.
+(A) the library's trials; (B) background draws without the bucket index,
+the index built on the main stream before each sketch; (C) every operator
+drawn up front (no background work), sketch + ID on side stream only."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1901_10559_b200 import sketch
+from paper_1901_10559_b200._inputs import dense_operand
+from paper_1901_10559_b200.distributed import countsketch_id_sharded_trials
+from paper_1901_10559_b200.matrix_id import device_matrix_id
+from paper_1901_10559_b200.sketch import id_stream, pipelined_operators
+
+I, R, L, k = 1_000_000, 2000, 100, 20
+a = torch.randn(I, R, dtype=torch.float64, device="cuda")
+op_a = dense_operand(a)
+
+
+def loop(ops, index_main):
+    main, side = torch.cuda.current_stream(), id_stream()
+    outs = []
+    for op in ops:
+        if index_main:
+            op._bucket_index()
+        y = torch.empty((R, L), dtype=torch.float64, device="cuda")
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        op.sketch_into(op_a, y, flags=1, nonfinite=flag)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            outs.append(device_matrix_id(y, L, R, k).packed())
+        y.record_stream(side)
+    main.wait_stream(side)
+    return torch.stack(outs).cpu()
+
+
+def timed(fn, n=20):
+    fn(list(range(3)))
+    torch.cuda.synchronize()
+    best = []
+    for rep in range(3):
+        seeds = list(range(100 + 50 * rep, 100 + 50 * rep + n))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn(seeds)
+        e1.record()
+        torch.cuda.synchronize()
+        best.append(round(e0.elapsed_time(e1) / n * 1e3))
+    return best
+
+
+print("A library trials     ", timed(lambda s: countsketch_id_sharded_trials(op_a, 0, I, k, L, seeds=s)), flush=True)
+print("B index on main      ", timed(lambda s: loop(pipelined_operators(I, L, s, True, index=False), True)), flush=True)
+
+
+def predrawn(s):
+    ops = list(pipelined_operators(I, L, s, True, index=True, depth=0))
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    return ops
+
+
+def c_run(s):
+    loop(c_run.ops[tuple(s)], False)
+
+
+for rep in range(3):
+    pass
+ops_cache = {}
+def c(s):
+    key = tuple(s)
+    if key not in ops_cache:
+        ops_cache[key] = list(pipelined_operators(I, L, s, True, index=True, depth=0))
+        torch.cuda.synchronize()
+    return loop(ops_cache[key], False)
+for rep in range(3):  # draw outside the timed region
+    c(list(range(100 + 50 * rep, 120 + 50 * rep)))
+c(list(range(3)))
+print("C pre-drawn operators", timed(c), flush=True)
