@@ -52,19 +52,6 @@ print("A library trials     ", timed(lambda s: countsketch_id_sharded_trials(op_
 print("B index on main      ", timed(lambda s: loop(pipelined_operators(I, L, s, True, index=False), True)), flush=True)
 
 
-def predrawn(s):
-    ops = list(pipelined_operators(I, L, s, True, index=True, depth=0))
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    return ops
-
-
-def c_run(s):
-    loop(c_run.ops[tuple(s)], False)
-
-
-for rep in range(3):
-    pass
 ops_cache = {}
 def c(s):
     key = tuple(s)
