@@ -10,6 +10,7 @@ numpy's own evaluation bit for bit (the reference test
 test_cp_tensor.py:193-203 demands array_equal).
 """
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -300,6 +301,7 @@ def tensorsketch_id(x, rank, sketch_dim=None, seed=None, rank_tol=DEFAULT_RANK_T
 HOST_GRAPHS = True
 HOST_GRAPH_MAX_BYTES = 1 << 30
 _host_graph = {"key": None, "seen": None, "graph": None, "bufs": None, "w": None, "stream": None}
+_host_graph_lock = threading.Lock()
 
 
 def _host_graph_call(x, rank, sketch_dim, seed, rank_tol):
@@ -319,29 +321,41 @@ def _host_graph_call(x, rank, sketch_dim, seed, rank_tol):
         return None  # the long-sketch (spectral) route is not captured
     key = (tuple(x.mode_dims), int(x.rank), int(rank), int(L), float(rank_tol),
            _device.device().index)
-    st = _host_graph
-    if st["key"] != key:
-        if st["seen"] != key:  # first sighting: the eager path this time
-            st["seen"] = key
-            return None
-        st.update(key=None, graph=None, bufs=None, w=None)
-        bufs = [_device.empty((int(x.rank), d), torch.float64) for d in x.mode_dims]
-        w = _device.empty(int(x.rank), torch.float64)
-        _host_graph_fill(x, bufs, w)
-        g = TensorIdGraph([b.t() for b in bufs], w, rank, L, rank_tol, host_weights=x.weights,
-                          split=True)
-        st.update(key=key, graph=g, bufs=bufs, w=w, stream=torch.cuda.Stream())
-        g.host_out.copy_(g.device(seed), non_blocking=True)
-    else:
-        # the factor copies on a side stream, under the hash-draw replay
-        g, side, main = st["graph"], st["stream"], torch.cuda.current_stream()
-        side.wait_stream(main)  # buffers free, seeds and weights ordered
-        with torch.cuda.stream(side):
-            _host_graph_fill(x, st["bufs"], st["w"])
-        g.host_out.copy_(g.device(seed, before_compute=lambda: main.wait_stream(side)),
-                         non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    d = DeviceId.unpack(g.host_out.numpy(), int(rank), int(x.rank), "tensorsketch")
+    # one caller at a time owns the cached graph and its buffers; concurrent
+    # callers (other threads) take the eager path, which shares nothing
+    if not _host_graph_lock.acquire(blocking=False):
+        return None
+    try:
+        st = _host_graph
+        if st["key"] != key:
+            if st["seen"] != key:  # first sighting: the eager path this time
+                st["seen"] = key
+                return None
+            st.update(key=None, graph=None, bufs=None, w=None, stream=None)
+            try:
+                bufs = [_device.empty((int(x.rank), d), torch.float64) for d in x.mode_dims]
+                w = _device.empty(int(x.rank), torch.float64)
+                _host_graph_fill(x, bufs, w)
+                g = TensorIdGraph([b.t() for b in bufs], w, rank, L, rank_tol,
+                                  host_weights=x.weights, split=True)
+            except Exception:  # capture not possible here (e.g. memory): stay eager
+                st["seen"] = ("no graph",) + key
+                torch.cuda.synchronize()
+                return None
+            st.update(key=key, graph=g, bufs=bufs, w=w, stream=torch.cuda.Stream())
+            g.host_out.copy_(g.device(seed), non_blocking=True)
+        else:
+            # the factor copies on a side stream, under the hash-draw replay
+            g, side, main = st["graph"], st["stream"], torch.cuda.current_stream()
+            side.wait_stream(main)  # buffers free, seeds and weights ordered
+            with torch.cuda.stream(side):
+                _host_graph_fill(x, st["bufs"], st["w"])
+            g.host_out.copy_(g.device(seed, before_compute=lambda: main.wait_stream(side)),
+                             non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        d = DeviceId.unpack(g.host_out.numpy(), int(rank), int(x.rank), "tensorsketch")
+    finally:
+        _host_graph_lock.release()
     return _assemble(x, d, "tensorsketch")
 
 

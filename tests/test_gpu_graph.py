@@ -150,3 +150,34 @@ def test_split_graph_matches_single_graph():
     for (da, na), (db, nb) in zip(a.trials([1, 2, 3]), b.trials([1, 2, 3])):
         assert np.array_equal(da.cols, db.cols) and np.array_equal(da.coeffs, db.coeffs)
         assert np.array_equal(na, nb)
+
+
+def test_host_tensor_graph_concurrent_threads():
+    """Calls from several threads: one owns the cached graph at a time, the
+    others run eagerly; every result equals the eager path's."""
+    import threading
+
+    rng = np.random.default_rng(9)
+    facs = []
+    for d in (300, 200, 90):
+        f = rng.standard_normal((d, 400))
+        facs.append(np.asfortranarray(f / np.linalg.norm(f, axis=0)))
+    x = ids.CpTensor(rng.random(400) + 0.1, facs)
+    want = {s: _eager(x, 10, 4096, s) for s in range(8)}
+    got, errs = {}, []
+
+    def work(seeds):
+        try:
+            for s in seeds:
+                got[s] = ids.tensorsketch_id(x, 10, 4096, seed=s)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=([s, s + 4],)) for s in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+    for s in range(8):
+        _same(got[s], want[s])
