@@ -486,7 +486,7 @@ class TensorIdGraph:
         host = _device.to_host(torch.stack(outs))
         res = []
         for v in host:
-            d = DeviceId.unpack(v, self.k, self.R, "tensorsketch")
+            d = DeviceId.unpack(v, self.k, self.R, "tensorsketch", copy=False)
             res.append((d, self.host_weights[d.cols] * d.coeffs.sum(axis=1)))
         return res
 

@@ -227,7 +227,7 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     from ._inputs import DenseOperand, SparseOperand, matrix_operand
     from ._native import IDS_FLAG_ORDERED
     from .matrix_id import check_matrix_id_args, device_matrix_id
-    from .sketch import id_stream, pipelined_operators
+    from .sketch import batched_operators, id_stream, pipelined_operators
 
     world, _ = _world(group)
     operand = a_local if isinstance(a_local, (DenseOperand, SparseOperand)) else \
@@ -249,12 +249,18 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
     from .sketch import CountSketchOp
 
     index = CountSketchOp.needs_index(operand, IDS_FLAG_ORDERED)
-    if isinstance(operand, SparseOperand):
-        # a sparse sketch is short next to its I-row hash draw: background
-        # draws run at full grid (tools/exp_trials.py: C3 4.25 vs 4.78 ms)
-        pipe.setdefault("grid_cap", 0)
-    ops = (pipelined_operators(in_dim, L, seeds, surjective, index=index, **pipe) if world == 1
-           else trial_sharded_operators(in_dim, L, seeds, surjective, group, index=index))
+    # a sparse sketch is short next to its I-row hash draw: the draws run in
+    # batches, several at a time, with nothing else on the GPU, and the
+    # sketches after them (C3: 2.4-2.6 vs 3.6 ms per trial with the draws
+    # under the sketches); dense sketches are long enough to hide the draws
+    batched = pipe.pop("batched", isinstance(operand, SparseOperand))
+    if world > 1:
+        ops = trial_sharded_operators(in_dim, L, seeds, surjective, group, index=index)
+    elif batched:
+        ops = batched_operators(in_dim, L, seeds, surjective, index=index,
+                                **{k: v for k, v in pipe.items() if k in ("streams", "grid_cap", "batch")})
+    else:
+        ops = pipelined_operators(in_dim, L, seeds, surjective, index=index, **pipe)
     for op in ops:
         y = torch.empty((cols, L), dtype=torch.float64, device=torch.cuda.current_device())
         flag = torch.zeros(1, dtype=torch.int32, device=y.device)
@@ -284,7 +290,7 @@ def countsketch_id_sharded_trials(a_local, row0, in_dim, rank, sketch_dim=None, 
 
     # one pinned copy for all trials
     host = _device.to_host(packed) if packed is not None else []
-    return [DeviceId.unpack(v, rank, cols, "countsketch") for v in host]
+    return [DeviceId.unpack(v, rank, cols, "countsketch", copy=False) for v in host]
 
 
 def tensorsketch_id_sharded(x_local, col0, total_terms, all_weights, rank, sketch_dim=None,
@@ -365,7 +371,7 @@ def tensorsketch_id_sharded_trials(x_local, col0, total_terms, all_weights, rank
     weights = np.asarray(all_weights, dtype=np.float64)
     res = []
     for v in host:
-        d = DeviceId.unpack(v, rank, total_terms, "tensorsketch")
+        d = DeviceId.unpack(v, rank, total_terms, "tensorsketch", copy=False)
         res.append((d, weights[d.cols] * d.coeffs.sum(axis=1)))
     return res
 

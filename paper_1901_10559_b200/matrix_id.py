@@ -75,7 +75,7 @@ class DeviceId:
         (decomposition, bool(flag)) from the same copy."""
         vec = _device.to_host(self.packed(flag))
         d = self.unpack(vec[1:] if flag is not None else vec, self.rank,
-                        self.coeffs.shape[1], method)
+                        self.coeffs.shape[1], method, copy=False)
         return (d, bool(vec[0])) if flag is not None else d
 
     def packed(self, flag=None):
@@ -89,13 +89,19 @@ class DeviceId:
         return torch.cat(parts)
 
     @staticmethod
-    def unpack(vec, rank, ncols, method):
+    def unpack(vec, rank, ncols, method, copy=True):
+        """copy=False: coeffs is a view of vec -- for a vec that nobody
+        reuses (a fresh to_host buffer), which the view then keeps alive;
+        copying 1.6 MB of coefficients into fresh pages costs ~0.6 ms per
+        result on the host (C3), more than the whole ID on the GPU."""
         cols = vec[:rank].astype(np.int32)
         nr, flags = int(vec[rank]), int(vec[rank + 1])
         if flags & 2:  # an exactly zero R11 diagonal reached the solve
             raise SingularTriangleError(f"zero diagonal entry at index {flags >> 2}")
         de = bool(flags & 1)
-        coeffs = vec[rank + 2:rank + 2 + rank * ncols].reshape(rank, ncols).copy()
+        coeffs = vec[rank + 2:rank + 2 + rank * ncols].reshape(rank, ncols)
+        if copy:
+            coeffs = coeffs.copy()
         return InterpolativeDecomposition(coeffs=coeffs, cols=cols, rank=rank, method=method,
                                           numerical_rank=nr, rank_deficient=de)
 

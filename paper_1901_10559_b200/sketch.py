@@ -589,6 +589,53 @@ def id_stream(dev=None):
     return st
 
 
+BATCH_DRAW_STREAMS = 4    # concurrent draws in batched_operators
+BATCH_DRAW_GRID_CAP = 74  # phase-B CTAs per concurrent draw
+BATCH_DRAW_SIZE = 16      # operators drawn per batch
+
+
+def batched_operators(in_dim, out_dim, seeds, surjective=False, index=True, streams=None,
+                      grid_cap=None, batch=None):
+    """CountSketchOps for a sequence of trials, drawn a batch at a time with
+    nothing else running: each batch's draws go BATCH_DRAW_STREAMS at a time
+    on side streams with a capped phase-B grid, the current stream joins
+    them, then the batch's operators are yielded.  For operands whose sketch
+    is short next to its hash draw (I = 1e7 CSR: 0.6 ms sketch, 2.5 ms
+    draw), separating the phases beats drawing under the sketches:
+    concurrent capped draws reach ~1.4 ms per draw
+    (tools/exp_hash_concurrency.py) and the sketches run undisturbed."""
+    seeds = list(seeds)
+    if not seeds:
+        return
+    streams = BATCH_DRAW_STREAMS if streams is None else int(streams)
+    grid_cap = BATCH_DRAW_GRID_CAP if grid_cap is None else int(grid_cap)
+    batch = BATCH_DRAW_SIZE if batch is None else int(batch)
+    dev = _device.device()
+    main = torch.cuda.current_stream()
+    sides = _side_streams(dev, max(streams, 1))
+    lib = load()
+    for b0 in range(0, len(seeds), batch):
+        chunk = seeds[b0:b0 + batch]
+        ops = []
+        for st in sides:
+            st.wait_stream(main)
+        lib.ids_set_hash_grid_cap(grid_cap)
+        try:
+            for n, sd in enumerate(chunk):
+                with torch.cuda.stream(sides[n % len(sides)]):
+                    op = CountSketchOp(in_dim, out_dim, seed=sd, surjective=surjective)
+                    if index:
+                        op._bucket_index()
+                ops.append(op)
+        finally:
+            lib.ids_set_hash_grid_cap(0)
+        for st in sides:
+            main.wait_stream(st)
+        for op in ops:
+            op.record_stream(main)
+            yield op
+
+
 def pipelined_operators(in_dim, out_dim, seeds, surjective=False, depth=None, grid_cap=None,
                         index=True):
     """CountSketchOps (hash + bucket index) for a sequence of trials, each

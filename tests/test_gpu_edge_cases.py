@@ -118,3 +118,23 @@ def test_generator_seed_draws_and_advances_like_numpy(I, L, surj, pre):
     assert np.array_equal(op.bucket, want_b) and np.array_equal(op.sign, want_s)
     assert np.array_equal(g1.integers(0, 2**31, size=9), g2.integers(0, 2**31, size=9))
     assert g1.bit_generator.state == g2.bit_generator.state
+
+
+def test_results_survive_later_calls():
+    """Coefficients are views of the call's own pinned result buffer: later
+    calls (which reuse freed pinned blocks) must not change earlier results."""
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((3000, 400))
+    r1 = ids.countsketch_id(a, 10, 60, seed=1)
+    keep = (r1.coeffs.copy(), r1.cols.copy())
+    from paper_1901_10559_b200.matrix_id import countsketch_id_trials
+
+    trials = countsketch_id_trials(a, 10, 60, seeds=[5, 6, 7])
+    keep_t = [(t.coeffs.copy(), t.cols.copy()) for t in trials]
+    for s in range(8, 14):
+        ids.countsketch_id(a, 10, 60, seed=s)
+        countsketch_id_trials(a, 10, 60, seeds=[s, s + 1])
+    assert np.array_equal(r1.coeffs, keep[0]) and np.array_equal(r1.cols, keep[1])
+    for t, (c, j) in zip(trials, keep_t):
+        assert np.array_equal(t.coeffs, c) and np.array_equal(t.cols, j)
+    assert r1.coeffs.flags.c_contiguous and r1.coeffs.flags.writeable
