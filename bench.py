@@ -785,8 +785,10 @@ def main():
             "data": "synthetic (seeded, paper_1901_10559_b200.generators)",
             "config": head["config"], "id_seconds": head["id_seconds"],
             "trials": ("K trials (seeds) of the same input queued back to back, one host sync "
-                       "at the end (matrices); hash draws pipelined on side streams (N = 1) or "
-                       "split over the ranks and broadcast (N > 1)"),
+                       "at the end (matrices); N = 1: dense inputs draw each hash on a side "
+                       "stream under the previous sketch, sparse inputs draw them in batches "
+                       "(4 concurrent) ahead of the sketches; N > 1: draws split over the "
+                       "ranks and broadcast"),
             "phases_ms": head["phases_ms"], "roofline": head["roofline"],
             "cpu_baseline": head["cpu_baseline"], "parity": head["parity"], "e2e": head["e2e"],
             "gpu_launches": head["gpu_launches"], "clocks": head.get("clocks"),
