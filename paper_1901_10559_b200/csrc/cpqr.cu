@@ -1706,6 +1706,349 @@ __global__ void __launch_bounds__(kTThreads, 1) cpqr_tall_kernel(TallArgs g) {
     }
 }
 
+// ---- short, wide sketches: column slices resident in shared memory ---------
+// For m <= 1024 rows and many columns (C3: 200 x 10000).  CTA b owns a
+// contiguous block of columns for the whole factorization and copies its
+// slice of Y into shared memory once; it also keeps the rows of F, R and V it
+// needs there, so the GEMV, the F / R columns, the downdates and the norm
+// recomputes never touch global memory.  A step needs ONE grid barrier: each
+// CTA publishes its argmax candidate TOGETHER with that column's residual
+// a = Y[:, c] - V F[c, :]^T (computed by the owner from shared memory), so
+// after the barrier every CTA agrees on the pivot, reads its residual from
+// L2 and builds the Householder vector itself.  The arithmetic (operation
+// order included) is that of cpqr_kernel's short-sketch path, so both give
+// identical factors.
+struct WideArgs {
+    const double* Y;
+    int64_t m, n, ldy, k;
+    const double* colnorm2;
+    double rank_tol;
+    int32_t* perm;
+    double* Rtop;
+    int32_t* numerical_rank;
+    double *V, *tau, *beta;  // global copies for form_q_kernel and the rank count
+    ArgMax* amax;            // [2][G] candidates, by step parity
+    double* apub;            // [2][G][m] candidate residuals, by step parity
+    unsigned* bar;           // monotonic arrival counter (zero at launch)
+    int64_t nc_max;          // owned columns per CTA (max)
+    int64_t* tlog;
+};
+
+constexpr int64_t kWideMinCols = 256;
+
+size_t wide_smem_bytes(int64_t m, int64_t k, int64_t nc) {
+    // Ys (nc m), Vs (k m), Fs and Rs (nc k each), v and a (m each), z and
+    // V[kk, :] (k each), vn1 / vn2 (nc each); pos (nc int64), flagged (nc int32)
+    return (size_t)(nc * m + k * m + 2 * nc * (k | 1) + 2 * m + 2 * k + 2 * nc) * sizeof(double) +
+           (size_t)nc * sizeof(int64_t) + (size_t)nc * sizeof(int32_t) + 64;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) cpqr_wide_kernel(WideArgs g) {
+    extern __shared__ double wsm[];
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    const int64_t m = g.m, n = g.n, k = g.k, ldy = g.ldy;
+    const int64_t c0 = n * b / G, c1 = n * (b + 1) / G, nc = c1 - c0;
+    const int64_t ncm = g.nc_max;
+    double* Ys = wsm;                 // ncm x m, column jl at Ys + jl m
+    double* Vs = Ys + ncm * m;        // k x m: V[:, q] at Vs + q m
+    const int64_t kp = k | 1;         // odd row stride: thread-per-column loops conflict-free
+    double* Fs = Vs + k * m;          // F[q, c0 + jl] at Fs + jl kp + q
+    double* Rs = Fs + ncm * kp;       // R[q, c0 + jl] at Rs + jl kp + q
+    double* vsm = Rs + ncm * kp;      // v (m)
+    double* asm_ = vsm + m;           // pivot residual a (m)
+    double* zsh = asm_ + m;           // z (k)
+    double* vrow = zsh + k;           // V[kk, :kk] (k)
+    double* vn1 = vrow + k;           // ncm
+    double* vn2 = vn1 + ncm;          // ncm
+    int64_t* pos = reinterpret_cast<int64_t*>(vn2 + ncm);   // ncm
+    int32_t* flagged = reinterpret_cast<int32_t*>(pos + ncm);  // ncm
+    __shared__ int s_nflag;
+    __shared__ double s_red0;
+    __shared__ double red[kWarps];
+    __shared__ ArgMax warp_best[kWarps];
+    __shared__ int64_t s_piv[4];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const double tol3z = sqrt(DBL_EPSILON);
+
+    // ---- prologue: the slice into shared memory (cp.async, all in flight) ----
+    {
+        const uint32_t ys = (uint32_t)__cvta_generic_to_shared(Ys);
+        const int64_t tot = nc * m;
+        for (int64_t e = threadIdx.x; e < tot; e += kThreads) {
+            const int64_t jl = e / m, r = e - jl * m;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(ys + (uint32_t)(8 * e)),
+                         "l"(g.Y + (c0 + jl) * ldy + r)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    }
+    for (int64_t r = threadIdx.x; r < m; r += kThreads) vsm[r] = 0.0;
+    __syncthreads();
+    for (int64_t jl = wid; jl < nc; jl += kWarps) {
+        const double s = g.colnorm2 ? g.colnorm2[c0 + jl] : warp_sum(lane_dot(Ys + jl * m, Ys + jl * m, 0, m));
+        if (lane == 0) {
+            vn1[jl] = sqrt(s);
+            vn2[jl] = sqrt(s);
+            pos[jl] = c0 + jl;
+        }
+    }
+    __syncthreads();
+
+    // local argmax over owned columns with pos >= step; publishes the
+    // candidate and its residual (rows >= step, `step` terms of V F^T) into
+    // buffer step & 1
+    auto publish = [&](int64_t step) {
+        ArgMax best{-1.0, INT64_MAX, -1, -1};
+        for (int64_t jl = threadIdx.x; jl < nc; jl += kThreads) {
+            const int64_t pj = pos[jl];
+            if (pj == step) best.col_at_next = c0 + jl;
+            if (pj >= step && better(vn1[jl], pj, best.val, best.pos)) {
+                best.val = vn1[jl];
+                best.pos = pj;
+                best.col = c0 + jl;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            ArgMax ot;
+            ot.val = __shfl_xor_sync(0xffffffffu, best.val, o);
+            ot.pos = __shfl_xor_sync(0xffffffffu, best.pos, o);
+            ot.col = __shfl_xor_sync(0xffffffffu, best.col, o);
+            ot.col_at_next = __shfl_xor_sync(0xffffffffu, best.col_at_next, o);
+            if (better(ot.val, ot.pos, best.val, best.pos)) {
+                best.val = ot.val;
+                best.pos = ot.pos;
+                best.col = ot.col;
+            }
+            if (ot.col_at_next >= 0) best.col_at_next = ot.col_at_next;
+        }
+        if (lane == 0) warp_best[wid] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ArgMax r = warp_best[0];
+            for (int i = 1; i < kWarps; ++i) {
+                const ArgMax o = warp_best[i];
+                if (better(o.val, o.pos, r.val, r.pos)) {
+                    r.val = o.val;
+                    r.pos = o.pos;
+                    r.col = o.col;
+                }
+                if (o.col_at_next >= 0) r.col_at_next = o.col_at_next;
+            }
+            g.amax[(step & 1) * G + b] = r;
+            // the column whose residual is published: the candidate, else (no
+            // finite norm left here) the column at position `step`, if owned
+            s_piv[3] = r.col >= 0 ? r.col : r.col_at_next;
+        }
+        __syncthreads();
+        const int64_t pc = s_piv[3];
+        if (pc >= 0 && step < k) {
+            const int64_t jl = pc - c0;
+            double* out = g.apub + ((step & 1) * G + b) * m;
+            for (int64_t r = step + threadIdx.x; r < m; r += kThreads)
+                out[r] = sub_dot(Ys[jl * m + r], Vs + r, m, Fs + jl * kp, 1, step);
+        }
+    };
+
+    const bool tl = g.tlog && b == 0 && threadIdx.x == 0;
+    int64_t tprev = tl ? gtimer() : 0;
+    auto stamp = [&](int phase) {
+        if (tl) {
+            const int64_t t = gtimer();
+            g.tlog[phase] += t - tprev;
+            tprev = t;
+        }
+    };
+    publish(0);
+    grid_bar_count(g.bar, (unsigned)G);
+    stamp(0);
+
+    for (int64_t kk = 0; kk < k; ++kk) {
+        // ---- pivot: reduce the candidates, fetch the winner's residual ----
+        const ArgMax* cand = g.amax + (kk & 1) * G;
+        if (wid == 0) {
+            const ArgMax r = reduce_partials_warp_cg(cand, G);
+            if (lane == 0) {
+                s_piv[0] = r.col;
+                s_piv[1] = r.pos;
+                s_piv[2] = r.col_at_next;
+            }
+        }
+        __syncthreads();
+        int64_t cs = s_piv[0], ps = s_piv[1];
+        const int64_t ck = s_piv[2];
+        if (cs < 0) {  // every remaining norm is NaN (non-finite input): keep position kk
+            cs = ck;
+            ps = kk;
+        }
+        if (threadIdx.x == 0) {
+            if (ck >= c0 && ck < c1 && ck != cs) pos[ck - c0] = ps;
+            if (cs >= c0 && cs < c1) pos[cs - c0] = kk;
+        }
+        int64_t ob = cs * G / n;  // owner CTA of column cs
+        while (ob + 1 < G && n * (ob + 1) / G <= cs) ++ob;
+        while (ob > 0 && n * ob / G > cs) --ob;
+        const double* ain = g.apub + ((kk & 1) * G + ob) * m;
+        double ss = 0.0;
+        for (int64_t r = kk + threadIdx.x; r < m; r += kThreads) {
+            const double v = __ldcg(ain + r);
+            asm_[r] = v;
+            if (r > kk) ss = fma(v, v, ss);
+        }
+        ss = block_sum(ss, red);
+        stamp(1);
+
+        // ---- Householder vector (every CTA), z = V^T v, V[kk, :kk] ----
+        const double alpha = asm_[kk];
+        const double xnorm = sqrt(ss);
+        double tau, beta, scal;
+        if (xnorm == 0.0) {
+            tau = 0.0;
+            beta = alpha;
+            scal = 0.0;
+        } else {
+            beta = -copysign(dlapy2(alpha, xnorm), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        for (int64_t r = threadIdx.x; r < m; r += kThreads) {
+            const double v = r < kk ? 0.0 : (r == kk) ? 1.0 : asm_[r] * scal;
+            vsm[r] = v;
+            Vs[kk * m + r] = v;
+            if (b == 0) g.V[kk * m + r] = v;
+        }
+        if (b == 0 && threadIdx.x == 0) {
+            g.tau[kk] = tau;
+            g.beta[kk] = beta;
+        }
+        if (threadIdx.x == 0 && cs >= c0 && cs < c1) Rs[(cs - c0) * kp + kk] = beta;
+        __syncthreads();
+        for (int64_t q = wid; q < kk; q += kWarps) {
+            const double sz = warp_sum(lane_dot(Vs + q * m, vsm, kk, m));
+            if (lane == 0) {
+                zsh[q] = sz;
+                vrow[q] = Vs[q * m + kk];
+            }
+        }
+        if (threadIdx.x == 0) s_nflag = 0;
+        stamp(2);
+        // ---- GEMV W_j = Y[:, j]^T v over the owned columns: one warp per
+        // column, four columns per warp side by side (rows lane + 32 t,
+        // clamped to m - 1 where v is zero; two chains per column) ----
+        {
+            const int nl = (int)((m + 31) / 32);
+            for (int64_t jb = 4 * wid; jb < nc; jb += 4 * kWarps) {
+                const double* y[4];
+                bool on[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    on[c] = jb + c < nc && pos[jb + c] > kk;
+                    y[c] = Ys + (on[c] ? jb + c : jb) * m;
+                }
+                double s1[4] = {0.0, 0.0, 0.0, 0.0}, t1[4] = {0.0, 0.0, 0.0, 0.0};
+                for (int t = 0; t < nl; t += 2) {
+                    const int64_t ra = lane + 32 * t, rb = ra + 32;
+                    const int64_t ca = tmin(ra, m - 1), cb = tmin(rb, m - 1);
+                    const double va = ra < m ? vsm[ra] : 0.0, vb = rb < m ? vsm[rb] : 0.0;
+                    const bool two = t + 1 < nl;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        s1[c] = fma(y[c][ca], va, s1[c]);
+                        if (two) t1[c] = fma(y[c][cb], vb, t1[c]);
+                    }
+                }
+                double w[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) w[c] = s1[c] + t1[c];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+                }
+                if (lane < 4 && on[lane]) {
+                    double wl = w[0];
+#pragma unroll
+                    for (int c = 1; c < 4; ++c) wl = lane == c ? w[c] : wl;
+                    Fs[(jb + lane) * kp + kk] = wl;  // W_j, turned into F[kk, j] below
+                }
+            }
+        }
+        __syncthreads();
+        stamp(3);
+        // ---- F column, row kk of R, norm downdate (one thread per column) ----
+        for (int64_t jl = threadIdx.x; jl < nc; jl += kThreads) {
+            if (pos[jl] <= kk) continue;
+            const double wj = 0.0 + Fs[jl * kp + kk];
+            double f = sub_dot(wj, Fs + jl * kp, 1, zsh, 1, kk);
+            double rk = sub_dot(Ys[jl * m + kk], Fs + jl * kp, 1, vrow, 1, kk);
+            f *= tau;
+            Fs[jl * kp + kk] = f;
+            rk -= f;  // V[kk, kk] = 1
+            Rs[jl * kp + kk] = rk;
+            const double v1 = vn1[jl];
+            if (kk < m - 1 && v1 != 0.0) {
+                double temp = fabs(rk) / v1;
+                temp = fmax(0.0, (1.0 + temp) * (1.0 - temp));
+                const double ratio = v1 / vn2[jl];
+                const double temp2 = temp * ratio * ratio;
+                if (temp2 <= tol3z) flagged[atomicAdd(&s_nflag, 1)] = (int32_t)jl;
+                else vn1[jl] = v1 * sqrt(temp);
+            }
+        }
+        __syncthreads();
+        stamp(4);
+        // exact norms of the flagged columns below row kk (LAPACK's recompute)
+        const int nflag = s_nflag;
+        if (g.tlog && threadIdx.x == 0) atomicAdd((unsigned long long*)&g.tlog[15], (unsigned long long)nflag);
+        for (int fi = wid; fi < nflag; fi += kWarps) {
+            const int64_t jl = flagged[fi];
+            const double* y = Ys + jl * m;
+            double s = 0.0;
+            for (int64_t r = kk + 1 + lane; r < m; r += 32) {
+                double v = sub_dot(y[r], Vs + r, m, Fs + jl * kp, 1, kk);
+                v = fma(-vsm[r], Fs[jl * kp + kk], v);
+                s = fma(v, v, s);
+            }
+            s = warp_sum(s);
+            if (lane == 0) {
+                vn1[jl] = sqrt(s);
+                vn2[jl] = sqrt(s);
+            }
+        }
+        __syncthreads();
+        stamp(5);
+        if (kk + 1 < k) {
+            publish(kk + 1);
+            stamp(6);
+            grid_bar_count(g.bar, (unsigned)(G * (kk + 2)));
+            stamp(7);
+        }
+    }
+
+    // ---- outputs: perm, Rtop, numerical rank ----
+    for (int64_t jl = threadIdx.x; jl < nc; jl += kThreads) {
+        const int64_t p = pos[jl];
+        g.perm[p] = (int32_t)(c0 + jl);
+        for (int64_t q = 0; q < k; ++q) g.Rtop[q * n + p] = (p >= q) ? Rs[jl * kp + q] : 0.0;
+    }
+    if (b == 0 && threadIdx.x == 0) {
+        const double lead = fabs(g.beta[0]);
+        int32_t nr = 0;
+        if (lead != 0.0)
+            for (int64_t q = 0; q < k; ++q) nr += fabs(g.beta[q]) > g.rank_tol * lead ? 1 : 0;
+        *g.numerical_rank = nr;
+    }
+}
+
+template <class W>
+void carve_wide(W& ws, int64_t m, int64_t k, int64_t G, WideArgs& a) {
+    a.V = ws.template take<double>(m * k);
+    a.tau = ws.template take<double>(k);
+    a.beta = ws.template take<double>(k);
+    a.amax = ws.template take<ArgMax>(2 * G);
+    a.apub = ws.template take<double>(2 * G * m);
+    a.bar = ws.template take<unsigned>(4);
+}
+
 size_t tall_smem_bytes(int64_t m, int64_t k, int64_t G, int64_t seg) {
     const int64_t mpad = ceil_div(m, seg) * seg;
     const int64_t rmax = ceil_div(m, G);
@@ -1746,7 +2089,10 @@ extern "C" size_t ids_cpqr_workspace_bytes(int64_t rows, int64_t cols, int64_t k
     CountCarve c2;
     TallArgs t{};
     carve_tall(c2, rows, cols, k, kMaxG, t);
-    return tmax(c.off, c2.off) + 256;
+    CountCarve c3;
+    WideArgs w{};
+    carve_wide(c3, rows, k, kMaxG, w);
+    return tmax(tmax(c.off, c2.off), c3.off) + 256;
 }
 
 extern "C" int ids_cpqr_trunc_f64(const double* Y, int64_t rows, int64_t cols, int64_t ldy,
@@ -1822,9 +2168,56 @@ extern "C" int ids_cpqr_trunc_norms_f64(const double* Y, int64_t rows, int64_t c
             return IDS_OK;
         }
     }
-    // (short wide sketches -- C3's 200 x 10000 -- measured faster on the
-    // segment-unit kernel: 348 vs 401 us; the 256-row variant stays for them
-    // to opt into with IDS_CPQR_WIDE=1)
+    if (rows <= 1024 && !getenv("IDS_CPQR_NO_WIDE")) {
+        // short sketch too large for one cluster (C3's 200 x 10000): column
+        // slices resident in shared memory on every SM, one grid barrier per
+        // step (C3: 219 us vs 349 on the segment-unit kernel; the cluster
+        // kernel above stays faster where it fits: C2 167 vs 172 us)
+        int dev = 0, sms = 148, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        const int64_t G = tmin<int64_t>(tmin<int64_t>(sms, kMaxG), cols);
+        const int64_t ncm = ceil_div(cols, G);
+        const size_t smem = wide_smem_bytes(rows, k, ncm);
+        if (cols >= kWideMinCols && smem <= (size_t)optin - 1024) {
+            WideArgs w{};
+            w.Y = Y;
+            w.m = rows;
+            w.n = cols;
+            w.ldy = ldy;
+            w.k = k;
+            w.colnorm2 = colnorm2;
+            w.rank_tol = rank_tol;
+            w.perm = perm;
+            w.Rtop = Rtop;
+            w.numerical_rank = numerical_rank;
+            w.nc_max = ncm;
+            w.tlog = g_cpqr_tlog;
+            WsCarve ws(workspace, ws_bytes);
+            carve_wide(ws, rows, k, kMaxG, w);
+            if (!ws.ok()) {
+                ids_set_last_error("cpqr: workspace too small");
+                return IDS_EWORKSPACE;
+            }
+            IDS_CUDA_TRY(cudaMemsetAsync(w.bar, 0, 4 * sizeof(unsigned), st));
+            IDS_CUDA_TRY(cudaFuncSetAttribute(cpqr_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem));
+            void* args[] = {&w};
+            IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cpqr_wide_kernel, dim3((unsigned)G),
+                                                     dim3(kThreads), args, smem, st));
+            ids_count_launch();
+            if (Q) {
+                form_q_kernel<<<(unsigned)k, kThreads, 0, st>>>(w.V, w.tau, rows, k, Q);
+                IDS_LAUNCH_CHECK();
+            }
+            return IDS_OK;
+        }
+    }
+    // (short wide sketches beyond the shared-memory kernels: the segment-unit
+    // kernel measured faster than the 256-row column-owning variant at C3's
+    // shape, 348 vs 401 us; that variant stays for them to opt into with
+    // IDS_CPQR_WIDE=1)
     const bool tall = rows > 1024, wide = rows >= 128 && cols >= 4096 && getenv("IDS_CPQR_WIDE");
     if ((tall || wide) && k <= kTallMaxK && !getenv("IDS_CPQR_SEGMENT_UNITS")) {
         // column-owning CTAs, v in shared memory (GEMV units of 2048 rows for

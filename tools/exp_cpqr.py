@@ -24,6 +24,8 @@ def near_dup(m, n, base, pert, seed):
     return y.t().contiguous()  # (n, m) == col-major m x n
 
 
+WIDE = ["prologue", "pivot+a", "hh+z", "gemv", "F/R/downdate", "recompute", "publish",
+        "barrier"]
 CLUSTER = ["pivot select", "pivot col", "householder", "gemv+z", "F/R/downdate",
            "recompute", "argmax", "cluster sync"]
 if __name__ != "__main__":
@@ -34,23 +36,30 @@ else:
                                     ("C5", 16384, 2000, 20, 20, 1e-4),
                                     ("C3", 200, 10000, 20, 20, 1e-2)):
       y = near_dup(m, n, base, pert, 1)
-      for _ in range(3):
-          device_cpqr(y, m, n, k)
-      torch.cuda.synchronize()
-      e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-      e0.record()
-      for _ in range(10):
-          device_cpqr(y, m, n, k)
-      e1.record()
-      torch.cuda.synchronize()
-      ms = e0.elapsed_time(e1) / 10
-      buf = torch.zeros(16, dtype=torch.int64, device="cuda")
-      lib.ids_debug_cpqr_timing(buf.data_ptr())
-      device_cpqr(y, m, n, k)
-      torch.cuda.synchronize()
-      lib.ids_debug_cpqr_timing(None)
-      t = buf.cpu().numpy()
-      print(f"{name}: {m}x{n} k={k}: {ms * 1e3:.1f} us per call; flagged {t[15]}")
-      names = CLUSTER if m <= 1024 and name in ("C2", "C1") else (TALL if m > 1024 else NAMES)
-      for i, nm in enumerate(names):
-          print(f"   {nm:14s} {t[i] / 1e3:9.1f} us  ({t[i] / 1e3 / k:6.2f}/step)")
+      for variant in ("", "old"):
+        if variant == "old":
+            if m > 1024:
+                continue
+            os.environ["IDS_CPQR_NO_WIDE"] = "1"
+        else:
+            os.environ.pop("IDS_CPQR_NO_WIDE", None)
+        for _ in range(3):
+            device_cpqr(y, m, n, k)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            device_cpqr(y, m, n, k)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        buf = torch.zeros(16, dtype=torch.int64, device="cuda")
+        lib.ids_debug_cpqr_timing(buf.data_ptr())
+        device_cpqr(y, m, n, k)
+        torch.cuda.synchronize()
+        lib.ids_debug_cpqr_timing(None)
+        t = buf.cpu().numpy()
+        print(f"{name}{variant}: {m}x{n} k={k}: {ms * 1e3:.1f} us per call; flagged {t[15]}")
+        names = TALL if m > 1024 else (WIDE if not variant else (CLUSTER if name in ("C2", "C1") else NAMES))
+        for i, nm in enumerate(names):
+            print(f"   {nm:14s} {t[i] / 1e3:9.1f} us  ({t[i] / 1e3 / k:6.2f}/step)")
