@@ -85,6 +85,15 @@ int ids_countsketch_hash_dev(const uint64_t* seed_dev, int64_t in_dim, int64_t o
  * different streams (independent trials) run side by side.  Process-wide;
  * read when a draw is enqueued. */
 void ids_set_hash_grid_cap(int ctas);
+/* Staging of the surjective draw: the Fisher-Yates chain is resolved in up to
+ * `stages` band groups (1..3, default 3) and the swaps of a finished group are
+ * applied on an internal side stream beside the rest of the chain; the
+ * caller's stream waits for the last application before the call's later
+ * work.  Draws shorter than `min_in_dim` rows (0 = keep the default, 2^21),
+ * draws under a grid cap (ids_set_hash_grid_cap) and draws on a capturing
+ * stream are not staged.  The hash is bit-identical
+ * for every setting.  Process-wide; read when a draw is enqueued. */
+void ids_set_hash_stages(int stages, int64_t min_in_dim);
 
 /* ---------------------------------------------------------------------------
  * Bucket index: the rows of each bucket in increasing row order, i.e. the CSR

@@ -100,6 +100,7 @@ SIGNATURES = {
         _c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p]
     ),
     "ids_set_hash_grid_cap": (None, [_c_int]),
+    "ids_set_hash_stages": (None, [_c_int, _c_i64]),
     "ids_mm_info": (_c_int, [ctypes.c_char_p, _c_p, _c_p, _c_p, _c_p]),
     "ids_mm_read": (_c_int, [ctypes.c_char_p, _c_int, _c_p, _c_p, _c_p, _c_i64, _c_p]),
     "ids_dcpqr_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_i64]),

@@ -23,6 +23,8 @@
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -687,7 +689,8 @@ constexpr int kPbThreads = 128;
 __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
     const uint32_t* __restrict__ g, int64_t nbuf, int64_t n, int32_t* __restrict__ jout,
     FyState* st, FyChunk* __restrict__ ch, int64_t* __restrict__ starts, int64_t max_chunks,
-    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max, int custom_bar, double e2_min_draws) {
+    int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max,
+    int custom_bar, double e2_min_draws, int k_first, int k_last, int is_first, int is_last) {
     cg::grid_group grid = cg::this_grid();
     auto gsync = [&]() {
         if (custom_bar) ids_grid_bar(&st->bar_count, gridDim.x);
@@ -713,15 +716,22 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         if (blockIdx.x == 0 && threadIdx.x == 0) *consumed = 0;
         return;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        st->pos = 0;
-        st->i = n - 1;
-        st->done = 0;
+    // A launch covers bands k_first .. k_last of the chain (the staged draw
+    // splits it so that finished bands' swaps are applied beside the rest of
+    // the chain); st carries the exact (pos, i) from one launch to the next.
+    if (is_first) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            st->pos = 0;
+            st->i = n - 1;
+            st->done = 0;
+        }
+        gsync();
     }
-    gsync();
     stamp(0);
     int top = 0;
     while ((2LL << top) <= n - 1) ++top;
+    if (k_first < top) top = k_first;
+    if (k_last > kmin) kmin = k_last;
     for (int k = top; k >= kmin; --k) {
         const int64_t lo_band = 1LL << k;
         const int64_t i0 = tmin<int64_t>(2 * lo_band - 1, n - 1);
@@ -773,6 +783,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         gsync();
     }
     stamp(9000);
+    if (!is_last) return;
     if (lead_warp) {
         const WalkOut r = st->i < 16384 ? warp_walk1(g, st->pos, nbuf, st->i, 0, jout)
                                         : warp_walk(g, st->pos, nbuf, st->i, 0, jout, 0, nullptr, 0);
@@ -796,9 +807,17 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
 //   final[i]   = incoming(i) if j[i] == i;
 //              = incoming(min{s in S_{j[i]} : s > i}) if that exists,
 //              = slots[j[i]] otherwise;     final[0] = incoming(0).
-__global__ void fy_count_kernel(const int32_t* __restrict__ j, int64_t n, int32_t* first,
-                                int32_t* gcount) {
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; s < n;
+//
+// Staged form: the swaps of [s_lo, s_hi) can be applied as soon as the chain
+// has passed s_lo, while it is still resolving the lower swaps: final[i] for
+// i >= s_lo depends on swaps > i only.  A later stage [s_lo', s_lo) groups
+// only its own swaps; the earlier stages' swaps into p are all above it, so
+// the smallest of them, the value first[p] held before this stage's count
+// (`first_prev`), stands in for their whole list.
+__global__ void fy_count_kernel(const int32_t* __restrict__ j, int64_t s_lo, int64_t n,
+                                int32_t* first, int32_t* gcount) {
+    if (s_lo < 1) s_lo = 1;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + s_lo; s < n;
          s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t p = j[s];
         if (p < s) {
@@ -808,10 +827,11 @@ __global__ void fy_count_kernel(const int32_t* __restrict__ j, int64_t n, int32_
     }
 }
 
-__global__ void fy_scatter_kernel(const int32_t* __restrict__ j, int64_t n,
+__global__ void fy_scatter_kernel(const int32_t* __restrict__ j, int64_t s_lo, int64_t n,
                                   const int32_t* __restrict__ goff, int32_t* cursor,
                                   int32_t* members) {
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; s < n;
+    if (s_lo < 1) s_lo = 1;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + s_lo; s < n;
          s += (int64_t)gridDim.x * blockDim.x) {
         const int32_t p = j[s];
         if (p < s) members[goff[p] + atomicAdd(&cursor[p], 1)] = (int32_t)s;
@@ -832,12 +852,13 @@ __device__ __forceinline__ int32_t incoming(int32_t s, const int32_t* __restrict
     return slot_value(s, L, tail);
 }
 
-__global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_t L,
+__global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t i_lo, int64_t n, int64_t L,
                                 const int32_t* __restrict__ tail,
                                 const int32_t* __restrict__ first,
+                                const int32_t* __restrict__ first_prev,
                                 const int32_t* __restrict__ goff,
                                 const int32_t* __restrict__ members, int32_t* bucket) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + i_lo; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t out;
         if (i == 0) {
@@ -852,6 +873,7 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_
                     const int32_t m = members[k];
                     if (m > i && m < best) best = m;
                 }
+                if (best == kNone && first_prev) best = first_prev[p];
                 out = best == kNone ? slot_value(p, L, tail) : incoming(best, first, L, tail);
             }
         }
@@ -859,7 +881,44 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t n, int64_
     }
 }
 
-int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel
+int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel (single stage)
+int g_fy_stages = 3;           // band groups of the staged draw (1 = chain, then every swap)
+int64_t g_fy_stage_min = 1 << 21;  // shorter draws are not staged (no gain measured at 1e6)
+int g_fy_side_per_sm = 2;      // CTAs per SM of the applications that run beside the chain
+int g_fy_split[2] = {2, 2};    // bands per stage (stage 1, stage 2)
+
+// Side streams for the staged swap application: a small per-device pool
+// handed out round robin, so concurrent draws (trial batches) do not queue
+// their applications behind one another.
+struct SidePipe {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t done = nullptr;
+};
+constexpr int kPipes = 8, kPipeDevs = 16;
+SidePipe g_pipes[kPipeDevs][kPipes];
+unsigned g_pipe_next[kPipeDevs];
+std::mutex g_pipe_mu;
+
+SidePipe* side_pipe() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kPipeDevs) return nullptr;
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    SidePipe* sp = &g_pipes[dev][g_pipe_next[dev]++ % kPipes];
+    if (!sp->stream) {
+        cudaStream_t s;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        bool ok = cudaEventCreateWithFlags(&sp->done, cudaEventDisableTiming) == cudaSuccess;
+        for (int t = 0; t < 3; ++t)
+            ok = ok && cudaEventCreateWithFlags(&sp->ev[t], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        sp->stream = s;
+    }
+    return sp;
+}
 int g_fy_grid_cap = 0;         // >0: cap on the phase-B grid (CTAs)
 double g_fy_e2_min = 65536.0;  // bands with fewer draws skip the second epoch (swept 0..1e30)
 int g_fy_custom_bar = 1;       // 1: nanosleep grid barrier (measured ~10% faster than cg grid.sync)
@@ -908,7 +967,7 @@ HashPlan make_plan(int64_t I, int64_t L, int surj) {
 template <class W>
 void carve(W& ws, const HashPlan& p, int64_t** blk_cnt, int64_t** blk_off, int64_t** scal,
            void** scan_tmp, int32_t** tail, uint32_t** draws, int32_t** jarr, int32_t** first,
-           int32_t** gcount, int32_t** goff, int32_t** members, FyState** fst, FyChunk** chunks,
+           int32_t** first_prev, int32_t** gcount, int32_t** goff, int32_t** members, FyState** fst, FyChunk** chunks,
            int64_t** starts) {
     *blk_cnt = ws.template take<int64_t>(p.nblk);
     *blk_off = ws.template take<int64_t>(p.nblk);
@@ -920,6 +979,7 @@ void carve(W& ws, const HashPlan& p, int64_t** blk_cnt, int64_t** blk_off, int64
         *draws = ws.template take<uint32_t>(p.nbuf);
         *jarr = ws.template take<int32_t>(p.I + 1);
         *first = ws.template take<int32_t>(p.I + 1);
+        *first_prev = ws.template take<int32_t>(p.I + 1);
         *gcount = ws.template take<int32_t>(p.I + 1);
         *goff = ws.template take<int32_t>(p.I + 1);
         *members = ws.template take<int32_t>(p.I + 1);
@@ -946,12 +1006,12 @@ extern "C" size_t ids_hash_workspace_bytes(int64_t in_dim, int64_t out_dim, int 
     NullCarve nc;
     int64_t *a, *b, *c;
     void* d;
-    int32_t *e, *g, *h, *i2, *j2, *k2;
+    int32_t *e, *g, *h, *hp, *i2, *j2, *k2;
     uint32_t* f;
     FyState* fs;
     FyChunk* fc;
     int64_t* sts;
-    carve(nc, p, &a, &b, &c, &d, &e, &f, &g, &h, &i2, &j2, &k2, &fs, &fc, &sts);
+    carve(nc, p, &a, &b, &c, &d, &e, &f, &g, &h, &hp, &i2, &j2, &k2, &fs, &fc, &sts);
     return nc.off + 256;
 }
 
@@ -998,19 +1058,22 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
     WsCarve ws(workspace, ws_bytes);
     int64_t *blk_cnt, *blk_off, *scal;
     void* scan_tmp;
-    int32_t *tail = nullptr, *jarr = nullptr, *first = nullptr, *gcount = nullptr,
+    int32_t *tail = nullptr, *jarr = nullptr, *first = nullptr, *first_prev = nullptr,
+            *gcount = nullptr,
             *goff = nullptr, *members = nullptr;
     uint32_t* draws = nullptr;
     FyState* fst = nullptr;
     FyChunk* chunks = nullptr;
     int64_t* starts = nullptr;
-    carve(ws, p, &blk_cnt, &blk_off, &scal, &scan_tmp, &tail, &draws, &jarr, &first, &gcount,
+    carve(ws, p, &blk_cnt, &blk_off, &scal, &scan_tmp, &tail, &draws, &jarr, &first, &first_prev,
+          &gcount,
           &goff, &members, &fst, &chunks, &starts);
     if (!ws.ok()) {
         ids_set_last_error("hash: workspace too small");
         return IDS_EWORKSPACE;
     }
     int64_t* d = draws_out ? draws_out : scal;
+    cudaEvent_t join = nullptr;  // set when swaps were applied on a side stream
     IDS_CUDA_TRY(cudaMemsetAsync(d, 0, 4 * sizeof(int64_t), st));
     Seed sd{state_hi, state_lo, inc_hi, inc_lo, seed_dev};
     const uint32_t L = (uint32_t)out_dim;
@@ -1047,48 +1110,102 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
         const unsigned gb = (unsigned)ceil_div(p.nbuf, (int64_t)kGenThreads * kChunk);
         raw_draws_kernel<<<gb, kGenThreads, 0, st>>>(sd, d, 1, p.nbuf, draws);
         IDS_LAUNCH_CHECK();
-        {
-            int dev = 0, sms = 148, per_sm = 1;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fy_phaseb_kernel, kPbThreads, 0);
-            int G = tmax(1, sms * tmin(per_sm, 2));
-            if (g_fy_grid_cap > 0) G = tmin(G, g_fy_grid_cap);
-            const uint32_t* dr = draws;
-            int64_t nbuf = p.nbuf, nI = I, mc = p.max_chunks;
-            int kmin = kMinBand;
-            int64_t* sts = starts + 1;
-            int64_t* cons = d + 1;
-            int64_t* stat = d + 3;
-            int64_t* tlog = g_fy_tlog;
-            int cbar = g_fy_custom_bar;
-            if (cbar) IDS_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(FyState), st));
-            double tmul = g_fy_tmul;
-            double e2min = g_fy_e2_min;
-            int64_t tmax = g_fy_tmax;
-            void* args[] = {&dr, &nbuf, &nI, &jarr, &fst, &chunks, &sts, &mc, &kmin, &cons, &stat,
-                            &tlog, &tmul, &tmax, &cbar, &e2min};
-            IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fy_phaseb_kernel, dim3(G),
-                                                     dim3(kPbThreads), args, 0, st));
-            ids_count_launch();
+        // Stage plan: the chain is launched band group by band group; the
+        // swaps of a finished group are applied on a side stream beside the
+        // rest of the chain (only the last group's application stays on the
+        // critical path).  Captured streams, short draws and draws with a
+        // capped grid (the caller runs other draws or a sketch beside this
+        // one, which already fill the chain's idle SMs: staging measured
+        // 2.33-2.48 vs 2.12 ms per C3 trial) take one stage.
+        int top = 0;
+        while ((2LL << top) <= I - 1) ++top;
+        int nst = 1;
+        SidePipe* pipe = nullptr;
+        if (I > 1 && g_fy_stages > 1 && g_fy_grid_cap == 0 && I >= g_fy_stage_min && top - 6 > kMinBand && !g_fy_tlog) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            IDS_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+            if (cs == cudaStreamCaptureStatusNone) pipe = side_pipe();
+            if (pipe) nst = g_fy_stages > 3 ? 3 : g_fy_stages;
         }
+        // stage t covers bands k_first[t] .. k_last[t]; its swaps are [s_lo[t], s_hi[t])
+        int k_first[3] = {top, 0, 0}, k_last[3] = {0, 0, 0};
+        int64_t s_lo[3] = {0, 0, 0}, s_hi[3] = {I, 0, 0};
+        if (nst >= 2) {
+            k_last[0] = top - g_fy_split[0] + 1;
+            k_first[1] = k_last[0] - 1;
+        }
+        if (nst == 3) {
+            k_last[1] = k_first[1] - g_fy_split[1] + 1;
+            k_first[2] = k_last[1] - 1;
+        }
+        for (int t = 0; t + 1 < nst; ++t) {
+            s_lo[t] = 1LL << k_last[t];
+            s_hi[t + 1] = s_lo[t];
+        }
+        cudaStream_t ap = pipe ? pipe->stream : st;  // where the swaps are applied
         if (I > 1) {
             fill_i32_kernel<<<1024, 256, 0, st>>>(first, I, kNone);
             IDS_LAUNCH_CHECK();
-            IDS_CUDA_TRY(cudaMemsetAsync(gcount, 0, sizeof(int32_t) * (I + 1), st));
-            const unsigned grid = (unsigned)tmin<int64_t>(ceil_div(I, 256), 148 * 16);
-            fy_count_kernel<<<grid, 256, 0, st>>>(jarr, I, first, gcount);
+        }
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fy_phaseb_kernel, kPbThreads, 0);
+        int G = tmax(1, sms * tmin(per_sm, 2));
+        if (g_fy_grid_cap > 0) G = tmin(G, g_fy_grid_cap);
+        if (g_fy_custom_bar) IDS_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(FyState), st));
+        for (int t = 0; t < nst; ++t) {
+            {
+                const uint32_t* dr = draws;
+                int64_t nbuf = p.nbuf, nI = I, mc = p.max_chunks;
+                int kmin = kMinBand;
+                int64_t* sts = starts + 1;
+                int64_t* cons = d + 1;
+                int64_t* stat = d + 3;
+                int64_t* tlog = g_fy_tlog;
+                int cbar = g_fy_custom_bar;
+                double tmul = g_fy_tmul;
+                double e2min = g_fy_e2_min;
+                int64_t tmax = g_fy_tmax;
+                int kf = k_first[t], kl = k_last[t], isf = t == 0, isl = t == nst - 1;
+                void* args[] = {&dr,   &nbuf, &nI,   &jarr, &fst,  &chunks, &sts, &mc,  &kmin, &cons,
+                                &stat, &tlog, &tmul, &tmax, &cbar, &e2min,  &kf,  &kl,  &isf,  &isl};
+                IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fy_phaseb_kernel, dim3(G),
+                                                         dim3(kPbThreads), args, 0, st));
+                ids_count_launch();
+            }
+            if (I <= 1) break;
+            if (pipe) {
+                IDS_CUDA_TRY(cudaEventRecord(pipe->ev[t], st));
+                IDS_CUDA_TRY(cudaStreamWaitEvent(ap, pipe->ev[t], 0));
+            }
+            const int64_t lo = s_lo[t], hi = s_hi[t];  // targets of these swaps lie in [0, hi)
+            const unsigned agrid = (unsigned)tmin<int64_t>(
+                ceil_div(hi - lo, 256), (int64_t)sms * (t + 1 < nst ? g_fy_side_per_sm : 16));
+            const int32_t* prev = nullptr;
+            if (t > 0) {  // what the earlier stages left in first[0, hi)
+                IDS_CUDA_TRY(cudaMemcpyAsync(first_prev, first, sizeof(int32_t) * hi,
+                                             cudaMemcpyDeviceToDevice, ap));
+                prev = first_prev;
+            }
+            IDS_CUDA_TRY(cudaMemsetAsync(gcount, 0, sizeof(int32_t) * (hi + 1), ap));
+            fy_count_kernel<<<agrid, 256, 0, ap>>>(jarr, lo, hi, first, gcount);
             IDS_LAUNCH_CHECK();
             size_t sb = p.scan2_bytes;
             IDS_CUDA_TRY(
-                cub::DeviceScan::ExclusiveSum(scan_tmp, sb, gcount, goff, (int)(I + 1), st));
-            IDS_CUDA_TRY(cudaMemsetAsync(gcount, 0, sizeof(int32_t) * (I + 1), st));
-            fy_scatter_kernel<<<grid, 256, 0, st>>>(jarr, I, goff, gcount, members);
+                cub::DeviceScan::ExclusiveSum(scan_tmp, sb, gcount, goff, (int)(hi + 1), ap));
+            IDS_CUDA_TRY(cudaMemsetAsync(gcount, 0, sizeof(int32_t) * (hi + 1), ap));
+            fy_scatter_kernel<<<agrid, 256, 0, ap>>>(jarr, lo, hi, goff, gcount, members);
             IDS_LAUNCH_CHECK();
-            fy_final_kernel<<<grid, 256, 0, st>>>(jarr, I, out_dim, tail, first, goff,
+            fy_final_kernel<<<agrid, 256, 0, ap>>>(jarr, lo, hi, out_dim, tail, first, prev, goff,
                                                    members, bucket);
             IDS_LAUNCH_CHECK();
-        } else {
+        }
+        if (pipe && I > 1) {  // the caller's stream continues after the last application
+            IDS_CUDA_TRY(cudaEventRecord(pipe->done, ap));
+            join = pipe->done;
+        }
+        if (I <= 1) {
             fill_i32_kernel<<<1, 32, 0, st>>>(bucket, 1, 0);
             IDS_LAUNCH_CHECK();
         }
@@ -1103,6 +1220,7 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
         set_i64_kernel<<<1, 1, 0, st>>>(d + 2, in_dim);
         IDS_LAUNCH_CHECK();
     }
+    if (join) IDS_CUDA_TRY(cudaStreamWaitEvent(st, join, 0));
     return IDS_OK;
 }
 
@@ -1123,3 +1241,16 @@ extern "C" void ids_debug_phaseb_timing(int64_t* buf) { g_fy_tlog = buf; }
 // Cap the phase-B grid at `ctas` CTAs (0 = whole GPU); lets several hash
 // streams share the GPU.
 extern "C" void ids_set_hash_grid_cap(int ctas) { g_fy_grid_cap = ctas > 0 ? ctas : 0; }
+
+extern "C" void ids_debug_fy_side(int per_sm, int b0, int b1) {
+    g_fy_side_per_sm = per_sm > 0 ? per_sm : 2;
+    g_fy_split[0] = b0 > 0 ? b0 : 2;
+    g_fy_split[1] = b1 > 0 ? b1 : 2;
+}
+
+// Band groups of the staged surjective draw (1..3; 1 = unstaged) and the
+// smallest in_dim that is staged (0 keeps the default).
+extern "C" void ids_set_hash_stages(int stages, int64_t min_in_dim) {
+    g_fy_stages = stages < 1 ? 1 : stages > 3 ? 3 : stages;
+    if (min_in_dim > 0) g_fy_stage_min = min_in_dim;
+}

@@ -105,6 +105,52 @@ def test_hash_band_boundaries_vs_oracle(I):
         assert np.array_equal(op.sign, o.sign), (I, L, seed)
 
 
+@pytest.mark.parametrize("stages", [1, 2, 3])
+@pytest.mark.parametrize("I", [524288, 524289, 700_001, 1048575, 1048576, 2_500_000])
+def test_hash_staged_draw_vs_oracle(I, stages):
+    # the chain resolved in band groups, finished groups' swaps applied on a
+    # side stream beside the rest (ids_set_hash_stages): same hash, same draws
+    from paper_1901_10559_b200 import _native
+
+    lib = _native.load()
+    lib.ids_set_hash_stages(stages, 1 << 19)
+    try:
+        for L, seed in [(1, 1), (100, 2), (I // 3, 3)]:
+            op = ids.CountSketchOp(I, L, seed=seed, surjective=True)
+            o = oracle.OracleCountSketch(I, L, seed, True)
+            assert op.draws == tuple(int(v) for v in o.draws), (I, L, seed)
+            assert np.array_equal(op.bucket, o.bucket), (I, L, seed)
+            assert np.array_equal(op.sign, o.sign), (I, L, seed)
+    finally:
+        lib.ids_set_hash_stages(3, 1 << 21)
+
+
+def test_hash_staged_concurrent_draws_share_side_streams():
+    # more concurrent staged draws than side pipes (8): every draw keeps its
+    # own workspace, the shared side streams only order the applications
+    from paper_1901_10559_b200 import _native
+
+    lib = _native.load()
+    I, L = 600_000, 50
+    lib.ids_set_hash_stages(3, 1 << 19)
+    try:
+        streams = [torch.cuda.Stream() for _ in range(10)]
+        ops = []
+        for n, st in enumerate(streams):
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                ops.append(ids.CountSketchOp(I, L, seed=40 + n, surjective=True))
+        for st in streams:
+            torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        for n, op in enumerate(ops):
+            o = oracle.OracleCountSketch(I, L, 40 + n, True)
+            assert np.array_equal(op.bucket, o.bucket), n
+            assert np.array_equal(op.sign, o.sign), n
+    finally:
+        lib.ids_set_hash_stages(3, 1 << 21)
+
+
 def test_surjective_covers_all_buckets():
     op = ids.CountSketchOp(1000, 10, seed=1, surjective=True)
     assert np.unique(op.bucket).size == 10
