@@ -548,46 +548,49 @@ __device__ void chunk_work(const uint32_t* __restrict__ g, int64_t nbuf, int64_t
     int64_t hi = tmin<int64_t>((int64_t)floor(gi) + half, i0);
     if (c == 0) s = hi = i0;
     const int64_t pos0 = pos + c * T;
-    FyChunk out;
-    out.w = -1;
-    out.a = 0;
-    out.ne = 0;
-    out.s = 0;
+    int64_t o_s = 0;
+    int32_t o_w = -1, o_a = 0, o_ne = 0;
+    int32_t myf = 0x7fffffff;  // lane f holds flat f of the sorted list (never <= d when unused)
     if (s - T > lo_band && hi >= s && pos0 + T <= nbuf) {
         const int64_t w = hi - s;
         const WalkOut r = warp_walk(g, pos0, pos0 + T, s, s - T - 1, nullptr, w, ev, kEvMax);
         __syncwarp();
-        out.s = s;
-        out.w = (int32_t)w;
-        out.a = (int32_t)(s - r.i);
+        o_s = s;
+        o_w = (int32_t)w;
+        o_a = (int32_t)(s - r.i);
         // gap g is taken by every trajectory whose current offset is >= g: the
-        // smallest such start d* solves d* = g + #{flats <= d*}
+        // smallest such start d* solves d* = g + #{flats <= d*}; the count is
+        // one ballot over the lanes' flats
         int nf = 0;
         const bool over = r.nev > kEvMax;
         if (!over) {
             for (int e = 0; e < r.nev; ++e) {
                 const int gap = ev[e];
-                int d = gap;
+                int d = gap, cnt;
                 for (;;) {
-                    int cnt = 0;
-                    for (int f = 0; f < nf; ++f) cnt += out.ev[f] <= d ? 1 : 0;
+                    cnt = __popc(__ballot_sync(0xffffffffu, myf <= d));
                     if (gap + cnt == d) break;
                     d = gap + cnt;
                 }
                 if (d > w) continue;  // no trajectory of the window reaches it
-                int at = nf++;
-                while (at > 0 && out.ev[at - 1] > d) {
-                    out.ev[at] = out.ev[at - 1];
-                    --at;
-                }
-                out.ev[at] = d;
+                // sorted insert at position cnt: later flats move up one lane
+                const int32_t up = __shfl_up_sync(0xffffffffu, myf, 1);
+                if (ln > cnt) myf = up;
+                else if (ln == cnt) myf = d;
+                ++nf;
             }
         }
-        out.ne = over ? -1 : nf;
-        for (int e = nf; e < kEvMax; ++e) out.ev[e] = 0x7fffffff;  // never <= d
+        o_ne = over ? -1 : nf;
+        if (over) myf = 0x7fffffff;
         __syncwarp();
     }
-    if (ln == 0) ch[c] = out;
+    if (ln == 0) {
+        ch[c].s = o_s;
+        ch[c].w = o_w;
+        ch[c].a = o_a;
+        ch[c].ne = o_ne;
+    }
+    if (ln < kEvMax) ch[c].ev[ln] = myf;
 }
 
 // One block (warp 0 walks, the block stages summaries in shared memory):
@@ -611,6 +614,7 @@ __device__ void stitch_block(FyState* st, const FyChunk* __restrict__ ch, int64_
                              int64_t T, int64_t* __restrict__ starts, FyChunk* sm2) {
     __shared__ int64_t s_S, s_done;
     __shared__ int s_ok;
+    __shared__ int32_t s_cs[kStitchBatch], s_k[kStitchBatch], s_cw[kStitchBatch];
     const int64_t pos0 = st->pos;
     if (threadIdx.x == 0) {
         s_S = st->i;
@@ -634,33 +638,56 @@ __device__ void stitch_block(FyState* st, const FyChunk* __restrict__ ch, int64_
         __syncthreads();
         if (!s_ok) break;
         if (threadIdx.x < 32) {  // warp 0: lane e holds flat e; one ballot per chunk
+            // The serial chain per chunk is start -> offset -> ballot -> popc ->
+            // next start.  Everything else is taken off it: starts are kept
+            // relative to the batch's first window (32-bit), the per-chunk
+            // constants are prepared by the lanes in parallel, a chunk that
+            // cannot be resolved is recorded (not branched on) and the walk
+            // of the batch simply runs on, and the exact starts are written
+            // 32 at a time.
             const int ln = threadIdx.x;
-            int64_t S = s_S;
-            int l = 0;
-            // chunk l's fields are loaded before chunk l-1 is resolved
-            int64_t cs = sm[0].s;
-            int cw = sm[0].w, cne = sm[0].ne, ca = sm[0].a;
-            int32_t cf = (ln < kEvMax && ln < cne) ? sm[0].ev[ln] : 0x7fffffff;
-            for (; l < cnt; ++l) {
+            const int64_t base = sm[0].s;
+            for (int l = ln; l < cnt; l += 32) {
+                const int32_t c32 = (int32_t)(sm[l].s - base);
+                s_cs[l] = c32;
+                s_k[l] = c32 - sm[l].a;
+                s_cw[l] = (sm[l].w < 0 || sm[l].ne < 0) ? -1 : sm[l].w;
+            }
+            __syncwarp();
+            const int64_t S0 = s_S;
+            // a start outside +-2^30 of the first window fails chunk 0 anyway
+            const int64_t rel = S0 - base;
+            int32_t S = rel > (1 << 30) ? (1 << 30) : rel < -(1 << 30) ? -(1 << 30) : (int32_t)rel;
+            int bad = cnt;
+            int32_t Sbad = 0, keep = 0;
+            int32_t cs = s_cs[0], ck = s_k[0], cw = s_cw[0];
+            int32_t cf = ln < kEvMax ? sm[0].ev[ln] : 0x7fffffff;
+#pragma unroll 4
+            for (int l = 0; l < cnt; ++l) {
                 const int nl = l + 1 < cnt ? l + 1 : l;
-                const int64_t ns = sm[nl].s;
-                const int nw = sm[nl].w, nne = sm[nl].ne, na = sm[nl].a;
-                const int32_t nf = (ln < kEvMax && ln < nne) ? sm[nl].ev[ln] : 0x7fffffff;
-                const int64_t d = S - cs;
-                if (cw < 0 || cne < 0 || d < 0 || d > cw) break;
+                const int32_t ncs = s_cs[nl], nk = s_k[nl], nw = s_cw[nl];
+                const int32_t nf = ln < kEvMax ? sm[nl].ev[ln] : 0x7fffffff;
+                const int32_t d = S - cs;
+                if ((d < 0 || d > cw) && l < bad) {
+                    bad = l;
+                    Sbad = S;
+                }
                 const int nflat = __popc(__ballot_sync(0xffffffffu, cf <= d));
-                if (ln == 0) starts[c0 + l] = S;
-                S = cs - ca + (d - nflat);
-                cs = ns;
+                if (ln == (l & 31)) keep = S;
+                S = ck + d - nflat;
+                if ((l & 31) == 31 || l == cnt - 1) {
+                    const int l0 = l & ~31;
+                    if (l0 + ln <= l && l0 + ln < bad) starts[c0 + l0 + ln] = base + keep;
+                }
+                cs = ncs;
+                ck = nk;
                 cw = nw;
-                cne = nne;
-                ca = na;
                 cf = nf;
             }
             if (ln == 0) {
-                if (l < cnt) s_ok = 0;
-                s_S = S;
-                s_done += l;
+                if (bad < cnt) s_ok = 0;
+                s_S = bad < cnt ? (bad == 0 ? S0 : base + Sbad) : base + S;
+                s_done += bad;
             }
         }
         __syncthreads();  // this buffer is refilled two batches on
