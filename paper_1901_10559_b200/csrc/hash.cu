@@ -767,6 +767,10 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         const double draws1 = (double)(2 * lo_band) * log((double)(i0 + 1) / (double)lo_band);
         const int64_t rem_i = (int64_t)(3.0 * sqrt(draws1) + 16.0) + T1 + 64;
         const int64_t T2 = tmax<int64_t>(256, T1 / 8);
+        // Both epochs are stitched first; their exact re-runs (which only
+        // write j) then run on every other warp while the lead warp walks
+        // the band's tail.
+        int64_t done_e[2] = {0, 0};
         for (int e = 0; e < 2; ++e) {
             const int64_t T = e == 0 ? T1 : T2;
             const int64_t nch = tmin<int64_t>(e == 0 ? (int64_t)(draws1 / (double)T1) + 2
@@ -781,29 +785,33 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
             stamp(100 * k + 10 * e + 1);
             gsync();
             stamp(100 * k + 10 * e + 2);
-            if (blockIdx.x == 0) stitch_block(st, ch, nch, T, starts, sm);
+            if (blockIdx.x == 0) stitch_block(st, ch, nch, T, starts + e * (max_chunks + 1), sm);
             stamp(100 * k + 10 * e + 3);
             gsync();
             stamp(100 * k + 10 * e + 4);
-            const int64_t done = st->done;
-            for (int64_t c = gw; c < done; c += nw) {
-                const int64_t p0 = starts[-1] + c * T;
-                warp_walk(g, p0, p0 + T, starts[c], lo_band, jout, 0, nullptr, 0);
-            }
-            // the next epoch's chunk stage only reads st and writes ch; the
-            // stitch that rewrites `starts` is behind the next grid barrier
+            done_e[e] = st->done;  // the next stitch (behind a grid barrier) rewrites it
         }
-        stamp(100 * k + 5);
-        gsync();  // exact re-runs may still write j; st is final for the walk
         stamp(100 * k + 6);
         if (lead_warp) {
             const WalkOut r = lo_band < 16384
                                   ? warp_walk1(g, st->pos, nbuf, st->i, lo_band - 1, jout)
                                   : warp_walk(g, st->pos, nbuf, st->i, lo_band - 1, jout, 0, nullptr, 0);
+            // every lane holds r: st is read by all of them above
+            __syncwarp();
             if (threadIdx.x == 0) {
                 if (r.i > lo_band - 1) *status = IDS_ERETRY;
                 st->i = r.i;
                 st->pos = r.pos;
+            }
+        } else {
+            const int64_t wk = nw > 1 ? nw - 1 : 1;
+            for (int e = 0; e < 2; ++e) {
+                const int64_t T = e == 0 ? T1 : T2;
+                const int64_t* se = starts + e * (max_chunks + 1);
+                for (int64_t c = gw - 1; c < done_e[e]; c += wk) {
+                    const int64_t p0 = se[-1] + c * T;
+                    warp_walk(g, p0, p0 + T, se[c], lo_band, jout, 0, nullptr, 0);
+                }
             }
         }
         stamp(100 * k + 7);
@@ -1012,7 +1020,7 @@ void carve(W& ws, const HashPlan& p, int64_t** blk_cnt, int64_t** blk_off, int64
         *members = ws.template take<int32_t>(p.I + 1);
         *fst = ws.template take<FyState>(1);
         *chunks = ws.template take<FyChunk>(p.max_chunks);
-        *starts = ws.template take<int64_t>(p.max_chunks + 1);
+        *starts = ws.template take<int64_t>(2 * (p.max_chunks + 1));  // one list per epoch
     }
 }
 
