@@ -442,6 +442,158 @@ __device__ WalkOut warp_walk(const uint32_t* __restrict__ g, int64_t pos, int64_
     return WalkOut{i, tmin<int64_t>(pos, limit), nev};
 }
 
+// warp_walk for a walk that stays inside one band (cmask = 2 * lo_band - 1,
+// lo_band - 1 <= i_stop, i <= cmask): the mask is a constant, and a lane whose
+// eight draws are all definite needs no second pass -- its accepts are the
+// classification's, so its j[] stores and near-miss gaps follow from the
+// exact start by bit counts.  Only the first ambiguous lane walks its draws
+// one by one.  The prefix sum of the lanes' accept counts (<= 8 each) is four
+// bit-sliced ballots instead of five dependent shuffles.
+__device__ WalkOut band_walk(const uint32_t* __restrict__ g, int64_t pos, int64_t limit,
+                             int64_t i64, int64_t i_stop64, int32_t* __restrict__ jout,
+                             int64_t w64, int32_t* __restrict__ ev, int evmax, uint32_t cmask) {
+    const int ln = threadIdx.x & 31;
+    const uint32_t ltm = (1u << ln) - 1u;
+    int32_t i = (int32_t)i64;
+    const int32_t i_stop = (int32_t)i_stop64;
+    const int32_t w = (int32_t)tmin<int64_t>(w64, 0x7fffffff);
+    int nev = 0;
+    uint32_t xn[kWalkAhead][8];
+    {
+        const int64_t rem = limit - pos;
+#pragma unroll
+        for (int d = 0; d < kWalkAhead; ++d)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int o = 256 * d + 8 * ln + q;
+                xn[d][q] = o < rem ? __ldg(g + pos + o) : 0u;
+            }
+    }
+    while (i > i_stop && pos < limit) {
+        const int64_t rem = limit - pos;
+        const int nval = rem < 256 ? (int)rem : 256;  // valid draws in this window
+        int32_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            v[q] = (int32_t)(xn[0][q] & cmask);
+#pragma unroll
+            for (int d = 0; d + 1 < kWalkAhead; ++d) xn[d][q] = xn[d + 1][q];
+            const int o = 256 * kWalkAhead + 8 * ln + q;
+            xn[kWalkAhead - 1][q] = o < rem ? __ldg(g + pos + o) : 0u;
+        }
+        int b = 0;
+        int32_t ib = i;
+        bool stop = false;
+        int64_t pos_final = 0;
+        while (b < 32) {
+            // -- speculative classification of this lane's draws
+            int a = 0;
+            uint32_t accm = 0;
+            bool amb = false;
+            if (ln >= b) {
+                const int32_t umax = 8 * (ln - b);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (!amb) {
+                        const int32_t hi = ib - a, lo = hi - umax;
+                        if (8 * ln + q >= nval || lo <= i_stop) {
+                            amb = true;
+                        } else if (v[q] <= lo) {
+                            ++a;
+                            accm |= 1u << q;
+                        } else if (v[q] <= hi) {
+                            amb = true;
+                        }
+                    }
+                }
+            }
+            const uint32_t ambb = __ballot_sync(0xffffffffu, amb);
+            const int ls = ambb ? __ffs(ambb) - 1 : 32;
+            const int cnt = (ln >= b && ln < ls) ? a : 0;
+            const uint32_t c0 = __ballot_sync(0xffffffffu, cnt & 1);
+            const uint32_t c1 = __ballot_sync(0xffffffffu, cnt & 2);
+            const uint32_t c2 = __ballot_sync(0xffffffffu, cnt & 4);
+            const uint32_t c3 = __ballot_sync(0xffffffffu, cnt & 8);
+            const int excl = __popc(c0 & ltm) + 2 * __popc(c1 & ltm) + 4 * __popc(c2 & ltm) +
+                             8 * __popc(c3 & ltm);
+            const int total = __popc(c0) + 2 * __popc(c1) + 4 * __popc(c2) + 8 * __popc(c3);
+            int32_t ii = ib - excl;
+            int endq = 8;
+            int ne = 0;
+            int32_t gaps[8];  // gaps[q] (statically indexed): near miss at draw q, or 0
+            if (ln >= b && ln < ls) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int32_t iq = ii - __popc(accm & ((1u << q) - 1u));
+                    gaps[q] = 0;
+                    if ((accm >> q) & 1u) {
+                        if (jout) jout[iq] = v[q];
+                    } else if (v[q] - iq <= w) {
+                        gaps[q] = v[q] - iq;
+                        ++ne;
+                    }
+                }
+                ii -= a;
+            } else if (ln == ls) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    gaps[q] = 0;
+                    if (endq == 8) {
+                        if (8 * ln + q >= nval || ii <= i_stop) {
+                            endq = q;
+                        } else if (v[q] <= ii) {
+                            if (jout) jout[ii] = v[q];
+                            --ii;
+                        } else if (v[q] - ii <= w) {
+                            gaps[q] = v[q] - ii;
+                            ++ne;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) gaps[q] = 0;
+            }
+            if (w > 0 && __ballot_sync(0xffffffffu, ne > 0)) {
+                int einc = ne;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, einc, o);
+                    if (ln >= o) einc += y;
+                }
+                int at = nev + einc - ne;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (gaps[q] != 0) {
+                        if (at < evmax) ev[at] = gaps[q];
+                        ++at;
+                    }
+                }
+                nev += __shfl_sync(0xffffffffu, einc, 31);
+            }
+            if (ls == 32) {
+                ib -= total;
+                break;
+            }
+            ib = __shfl_sync(0xffffffffu, ii, ls);
+            const int eq = __shfl_sync(0xffffffffu, endq, ls);
+            b = ls + 1;
+            if (eq < 8) {
+                stop = true;
+                pos_final = pos + 8 * ls + eq;
+                break;
+            }
+        }
+        i = ib;
+        if (stop) {
+            pos = pos_final;
+            break;
+        }
+        pos += 256;
+    }
+    return WalkOut{i, tmin<int64_t>(pos, limit), nev};
+}
+
 // Small-i variant of warp_walk: one draw per lane (32-draw windows, read 1024
 // draws ahead), so the uncertainty of a lane's i is at most 31 -- better when
 // i is small and wide windows would be mostly ambiguous.
@@ -553,7 +705,8 @@ __device__ void chunk_work(const uint32_t* __restrict__ g, int64_t nbuf, int64_t
     int32_t myf = 0x7fffffff;  // lane f holds flat f of the sorted list (never <= d when unused)
     if (s - T > lo_band && hi >= s && pos0 + T <= nbuf) {
         const int64_t w = hi - s;
-        const WalkOut r = warp_walk(g, pos0, pos0 + T, s, s - T - 1, nullptr, w, ev, kEvMax);
+        const WalkOut r = band_walk(g, pos0, pos0 + T, s, s - T - 1, nullptr, w, ev, kEvMax,
+                                    (uint32_t)(2 * lo_band - 1));
         __syncwarp();
         o_s = s;
         o_w = (int32_t)w;
@@ -795,7 +948,8 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         if (lead_warp) {
             const WalkOut r = lo_band < 16384
                                   ? warp_walk1(g, st->pos, nbuf, st->i, lo_band - 1, jout)
-                                  : warp_walk(g, st->pos, nbuf, st->i, lo_band - 1, jout, 0, nullptr, 0);
+                                  : band_walk(g, st->pos, nbuf, st->i, lo_band - 1, jout, 0, nullptr, 0,
+                                              (uint32_t)(2 * lo_band - 1));
             // every lane holds r: st is read by all of them above
             __syncwarp();
             if (threadIdx.x == 0) {
@@ -810,7 +964,8 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
                 const int64_t* se = starts + e * (max_chunks + 1);
                 for (int64_t c = gw - 1; c < done_e[e]; c += wk) {
                     const int64_t p0 = se[-1] + c * T;
-                    warp_walk(g, p0, p0 + T, se[c], lo_band, jout, 0, nullptr, 0);
+                    band_walk(g, p0, p0 + T, se[c], lo_band, jout, 0, nullptr, 0,
+                              (uint32_t)(2 * lo_band - 1));
                 }
             }
         }
@@ -919,6 +1074,7 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t i_lo, int
 int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel (single stage)
 int g_fy_stages = 3;           // band groups of the staged draw (1 = chain, then every swap)
 int64_t g_fy_stage_min = 1 << 21;  // shorter draws are not staged (no gain measured at 1e6)
+int g_fy_per_sm = 2;           // chain CTAs per SM (x 4 warps)
 int g_fy_side_per_sm = 2;      // CTAs per SM of the applications that run beside the chain
 int g_fy_split[2] = {2, 2};    // bands per stage (stage 1, stage 2)
 
@@ -1186,7 +1342,7 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fy_phaseb_kernel, kPbThreads, 0);
-        int G = tmax(1, sms * tmin(per_sm, 2));
+        int G = tmax(1, sms * tmin(per_sm, g_fy_per_sm));
         if (g_fy_grid_cap > 0) G = tmin(G, g_fy_grid_cap);
         if (g_fy_custom_bar) IDS_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(FyState), st));
         for (int t = 0; t < nst; ++t) {
@@ -1276,6 +1432,8 @@ extern "C" void ids_debug_phaseb_timing(int64_t* buf) { g_fy_tlog = buf; }
 // Cap the phase-B grid at `ctas` CTAs (0 = whole GPU); lets several hash
 // streams share the GPU.
 extern "C" void ids_set_hash_grid_cap(int ctas) { g_fy_grid_cap = ctas > 0 ? ctas : 0; }
+
+extern "C" void ids_debug_fy_per_sm(int v) { g_fy_per_sm = v > 0 ? v : 2; }
 
 extern "C" void ids_debug_fy_side(int per_sm, int b0, int b1) {
     g_fy_side_per_sm = per_sm > 0 ? per_sm : 2;
