@@ -870,7 +870,8 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
     const uint32_t* __restrict__ g, int64_t nbuf, int64_t n, int32_t* __restrict__ jout,
     FyState* st, FyChunk* __restrict__ ch, int64_t* __restrict__ starts, int64_t max_chunks,
     int kmin, int64_t* consumed, int64_t* status, int64_t* tlog, double tmul, int64_t t1max,
-    int custom_bar, double e2_min_draws, int k_first, int k_last, int is_first, int is_last) {
+    int custom_bar, double e2_min_draws, int k_first, int k_last, int is_first, int is_last,
+    int64_t walk1_below) {
     cg::grid_group grid = cg::this_grid();
     auto gsync = [&]() {
         if (custom_bar) ids_grid_bar(&st->bar_count, gridDim.x);
@@ -946,7 +947,7 @@ __global__ void __launch_bounds__(kPbThreads) fy_phaseb_kernel(
         }
         stamp(100 * k + 6);
         if (lead_warp) {
-            const WalkOut r = lo_band < 16384
+            const WalkOut r = lo_band < walk1_below
                                   ? warp_walk1(g, st->pos, nbuf, st->i, lo_band - 1, jout)
                                   : band_walk(g, st->pos, nbuf, st->i, lo_band - 1, jout, 0, nullptr, 0,
                                               (uint32_t)(2 * lo_band - 1));
@@ -1074,9 +1075,11 @@ __global__ void fy_final_kernel(const int32_t* __restrict__ j, int64_t i_lo, int
 int64_t* g_fy_tlog = nullptr;  // debug: stage timestamps of the phase-B kernel (single stage)
 int g_fy_stages = 3;           // band groups of the staged draw (1 = chain, then every swap)
 int64_t g_fy_stage_min = 1 << 21;  // shorter draws are not staged (no gain measured at 1e6)
+int g_fy_kmin = 12;            // bands below 2^kmin are walked exactly by one warp
+int64_t g_fy_walk1_below = 16384;  // band tails below this use the one-draw-per-lane walk
 int g_fy_per_sm = 2;           // chain CTAs per SM (x 4 warps)
-int g_fy_side_per_sm = 2;      // CTAs per SM of the applications that run beside the chain
-int g_fy_split[2] = {2, 2};    // bands per stage (stage 1, stage 2)
+int g_fy_side_per_sm = 4;      // CTAs per SM of the applications that run beside the chain
+int g_fy_split[2] = {3, 3};    // bands per stage (stage 1, stage 2)
 
 // Side streams for the staged swap application: a small per-device pool
 // handed out round robin, so concurrent draws (trial batches) do not queue
@@ -1340,8 +1343,23 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
         }
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fy_phaseb_kernel, kPbThreads, 0);
+        {  // launch geometry, queried once per device
+            static int c_sms[kPipeDevs], c_per_sm[kPipeDevs];
+            static std::mutex mu;
+            std::lock_guard<std::mutex> lk(mu);
+            if (dev >= 0 && dev < kPipeDevs && c_sms[dev] > 0) {
+                sms = c_sms[dev];
+                per_sm = c_per_sm[dev];
+            } else {
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fy_phaseb_kernel,
+                                                              kPbThreads, 0);
+                if (dev >= 0 && dev < kPipeDevs) {
+                    c_sms[dev] = sms;
+                    c_per_sm[dev] = per_sm;
+                }
+            }
+        }
         int G = tmax(1, sms * tmin(per_sm, g_fy_per_sm));
         if (g_fy_grid_cap > 0) G = tmin(G, g_fy_grid_cap);
         if (g_fy_custom_bar) IDS_CUDA_TRY(cudaMemsetAsync(fst, 0, sizeof(FyState), st));
@@ -1349,7 +1367,8 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
             {
                 const uint32_t* dr = draws;
                 int64_t nbuf = p.nbuf, nI = I, mc = p.max_chunks;
-                int kmin = kMinBand;
+                int kmin = g_fy_kmin;
+                int64_t wb = g_fy_walk1_below;
                 int64_t* sts = starts + 1;
                 int64_t* cons = d + 1;
                 int64_t* stat = d + 3;
@@ -1360,7 +1379,7 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
                 int64_t tmax = g_fy_tmax;
                 int kf = k_first[t], kl = k_last[t], isf = t == 0, isl = t == nst - 1;
                 void* args[] = {&dr,   &nbuf, &nI,   &jarr, &fst,  &chunks, &sts, &mc,  &kmin, &cons,
-                                &stat, &tlog, &tmul, &tmax, &cbar, &e2min,  &kf,  &kl,  &isf,  &isl};
+                                &stat, &tlog, &tmul, &tmax, &cbar, &e2min,  &kf,  &kl,  &isf,  &isl, &wb};
                 IDS_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fy_phaseb_kernel, dim3(G),
                                                          dim3(kPbThreads), args, 0, st));
                 ids_count_launch();
@@ -1435,10 +1454,15 @@ extern "C" void ids_set_hash_grid_cap(int ctas) { g_fy_grid_cap = ctas > 0 ? cta
 
 extern "C" void ids_debug_fy_per_sm(int v) { g_fy_per_sm = v > 0 ? v : 2; }
 
+extern "C" void ids_debug_fy_small(int kmin, int64_t walk1_below) {
+    g_fy_kmin = kmin >= 9 && kmin <= kMinBand ? kmin : kMinBand;
+    g_fy_walk1_below = walk1_below > 0 ? walk1_below : 16384;
+}
+
 extern "C" void ids_debug_fy_side(int per_sm, int b0, int b1) {
-    g_fy_side_per_sm = per_sm > 0 ? per_sm : 2;
-    g_fy_split[0] = b0 > 0 ? b0 : 2;
-    g_fy_split[1] = b1 > 0 ? b1 : 2;
+    g_fy_side_per_sm = per_sm > 0 ? per_sm : 4;
+    g_fy_split[0] = b0 > 0 ? b0 : 3;
+    g_fy_split[1] = b1 > 0 ? b1 : 3;
 }
 
 // Band groups of the staged surjective draw (1..3; 1 = unstaged) and the
