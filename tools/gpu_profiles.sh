@@ -26,7 +26,8 @@ full() {  # $1 kernel regex, $2 report name, $3.. prof_config args
 full cs_rowmajor cs_rowmajor --workload C2
 full cs_coltile_ra cs_coltile_ra --workload C2 --fortran
 full cs_csr_stream cs_csr_stream --workload C3
-full fy_phaseb fy_phaseb_c3 --workload C3
+IDS_HASH_STAGES=1 full fy_phaseb fy_phaseb_c3 --workload C3
+full cpqr_wide_kernel cpqr_wide_c3 --workload C3
 full ts_split_kernel ts_split_c4 --workload C4
 full ts_split_kernel ts_split_c5 --workload C5
 full cpqr_tall_kernel cpqr_tall_c5 --workload C5

@@ -93,7 +93,10 @@ for rep, name, title, key in (
         ("pf_full_cs_coltile_ra.ncu-rep", "cs_coltile_ra",
          "cs_coltile_ra_kernel<2,512,3> (bucket-sorted tiles, register accumulators), C2 in F order", None),
         ("pf_full_cs_csr_stream.ncu-rep", "cs_csr_stream", "cs_csr_stream_kernel, C3", "C3"),
-        ("pf_full_fy_phaseb_c3.ncu-rep", "fy_phaseb_c3", "fy_phaseb_kernel, C3 hash (I = 1e7)", None),
+        ("pf_full_fy_phaseb_c3.ncu-rep", "fy_phaseb_c3",
+         "fy_phaseb_kernel, C3 hash (I = 1e7), the whole chain in one launch (ids_set_hash_stages(1))", None),
+        ("pf_full_cpqr_wide_c3.ncu-rep", "cpqr_wide_c3",
+         "cpqr_wide_kernel (column slices in shared memory), C3 sketch 200 x 10000, k = 20", None),
         ("pf_full_tensorsketch_c4.ncu-rep", "tensorsketch_c4", "tensorsketch_kernel<8>, C4", None),
         ("pf_full_tensorsketch_c5.ncu-rep", "tensorsketch_c5", "tensorsketch_kernel<16>, C5", None),
         ("pf_full_cpqr_c5.ncu-rep", "cpqr_c5", "cpqr_kernel, C5 sketch 16384 x 2000, k = 20", None),

@@ -23,6 +23,10 @@ p.add_argument("--steps", type=int, default=1)
 p.add_argument("--fortran", action="store_true", help="C2 in column-major layout")
 args = p.parse_args()
 torch.cuda.set_device(0)
+if os.environ.get("IDS_HASH_STAGES"):  # 1: the whole hash chain in one launch (for a kernel capture)
+    from paper_1901_10559_b200 import _native
+
+    _native.load().ids_set_hash_stages(int(os.environ["IDS_HASH_STAGES"]), 0)
 cfg = G.CONFIGS[args.workload]
 if cfg["kind"] in ("dense", "csr"):
     from paper_1901_10559_b200.matrix_id import countsketch_device
