@@ -1098,21 +1098,32 @@ SidePipe* side_pipe() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kPipeDevs) return nullptr;
     std::lock_guard<std::mutex> lk(g_pipe_mu);
-    SidePipe* sp = &g_pipes[dev][g_pipe_next[dev]++ % kPipes];
-    if (!sp->stream) {
-        cudaStream_t s;
-        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-        bool ok = cudaEventCreateWithFlags(&sp->done, cudaEventDisableTiming) == cudaSuccess;
-        for (int t = 0; t < 3; ++t)
-            ok = ok && cudaEventCreateWithFlags(&sp->ev[t], cudaEventDisableTiming) == cudaSuccess;
-        if (!ok) {
-            cudaGetLastError();
-            return nullptr;
+    // all of a device's pipes are made by its first staged draw (a stream
+    // costs ~0.3 ms to create: not something to meet again on later calls)
+    if (!g_pipes[dev][kPipes - 1].stream) {
+        for (int k = 0; k < kPipes; ++k) {
+            SidePipe* sp = &g_pipes[dev][k];
+            if (sp->stream) continue;
+            cudaStream_t s;
+            if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+            bool ok = cudaEventCreateWithFlags(&sp->done, cudaEventDisableTiming) == cudaSuccess;
+            for (int t = 0; t < 3; ++t)
+                ok = ok &&
+                     cudaEventCreateWithFlags(&sp->ev[t], cudaEventDisableTiming) == cudaSuccess;
+            if (!ok) {
+                cudaGetLastError();
+                cudaStreamDestroy(s);
+                return nullptr;
+            }
+            sp->stream = s;
         }
-        sp->stream = s;
     }
-    return sp;
+    return &g_pipes[dev][g_pipe_next[dev]++ % kPipes];
 }
+
 int g_fy_grid_cap = 0;         // >0: cap on the phase-B grid (CTAs)
 double g_fy_e2_min = 65536.0;  // bands with fewer draws skip the second epoch (swept 0..1e30)
 int g_fy_custom_bar = 1;       // 1: nanosleep grid barrier (measured ~10% faster than cg grid.sync)
