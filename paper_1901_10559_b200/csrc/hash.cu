@@ -1085,6 +1085,7 @@ int g_fy_split[2] = {3, 3};    // bands per stage (stage 1, stage 2)
 // handed out round robin, so concurrent draws (trial batches) do not queue
 // their applications behind one another.
 struct SidePipe {
+    std::mutex mu;  // held while one draw enqueues on the pipe (its events are re-recorded per draw)
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t done = nullptr;
@@ -1279,6 +1280,7 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
     }
     int64_t* d = draws_out ? draws_out : scal;
     cudaEvent_t join = nullptr;  // set when swaps were applied on a side stream
+    std::unique_lock<std::mutex> pipe_lock;  // that stream's pipe, held until the join is enqueued
     IDS_CUDA_TRY(cudaMemsetAsync(d, 0, 4 * sizeof(int64_t), st));
     Seed sd{state_hi, state_lo, inc_hi, inc_lo, seed_dev};
     const uint32_t L = (uint32_t)out_dim;
@@ -1330,7 +1332,10 @@ static int countsketch_hash(uint64_t state_hi, uint64_t state_lo, uint64_t inc_h
             cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
             IDS_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
             if (cs == cudaStreamCaptureStatusNone) pipe = side_pipe();
-            if (pipe) nst = g_fy_stages > 3 ? 3 : g_fy_stages;
+            if (pipe) {
+                nst = g_fy_stages > 3 ? 3 : g_fy_stages;
+                pipe_lock = std::unique_lock<std::mutex>(pipe->mu);
+            }
         }
         // stage t covers bands k_first[t] .. k_last[t]; its swaps are [s_lo[t], s_hi[t])
         int k_first[3] = {top, 0, 0}, k_last[3] = {0, 0, 0};

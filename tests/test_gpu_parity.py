@@ -151,6 +151,43 @@ def test_hash_staged_concurrent_draws_share_side_streams():
         lib.ids_set_hash_stages(3, 1 << 21)
 
 
+def test_hash_staged_draws_from_host_threads():
+    # host threads drawing at once: each draw holds its side pipe while it
+    # enqueues, so another thread cannot re-record the pipe's events under it
+    import threading
+
+    from paper_1901_10559_b200 import _native
+
+    lib = _native.load()
+    I, L = 560_000, 33
+    lib.ids_set_hash_stages(3, 1 << 19)
+    out, errs = {}, []
+
+    def work(t):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                for r in range(3):
+                    op = ids.CountSketchOp(I, L, seed=1000 + 10 * t + r, surjective=True)
+                    out[(t, r)] = (op.bucket.copy(), op.sign.copy())
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    try:
+        ths = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+    finally:
+        lib.ids_set_hash_stages(3, 1 << 21)
+    assert not errs, errs
+    for (t, r), (b, sg) in out.items():
+        o = oracle.OracleCountSketch(I, L, 1000 + 10 * t + r, True)
+        assert np.array_equal(b, o.bucket), (t, r)
+        assert np.array_equal(sg, o.sign), (t, r)
+
+
 def test_surjective_covers_all_buckets():
     op = ids.CountSketchOp(1000, 10, seed=1, surjective=True)
     assert np.unique(op.bucket).size == 10
