@@ -14,12 +14,20 @@
 //     LCG to its chunk with the 2^k tables (pcg_tables.h) and generates
 //     sequentially; Lemire rejections are stream-compacted with a block scan;
 //   * phase B's accept/reject chain is inherently sequential in i; it is
-//     resolved by one CTA that classifies 1024 draws per round (definite
-//     accept / reject / ambiguous) and only settles ambiguous lanes one at a
-//     time, then by one warp once i < 65536;
+//     resolved band by band (i in [2^k, 2^(k+1)): one mask) by a persistent
+//     cooperative kernel: every warp summarises a chunk of draws as a function
+//     of its unknown starting i (lowest start simulated, near misses folded
+//     into "flats"), one warp stitches the summaries in order, the chunks are
+//     re-run from their now exact starts to write j[], and one warp walks what
+//     is left of the band (and everything below 2^12) exactly;
 //   * the Fisher-Yates swaps themselves are applied in parallel: the value
 //     that lands at position i is found by chasing "first later swap that
-//     targeted this position" links (see fy_final_kernel), O(I) work.
+//     targeted this position" links (see fy_final_kernel), O(I) work;
+//   * large draws are staged: the chain runs in three band groups and the
+//     swaps of a finished group are applied on a side stream beside the rest
+//     of the chain (final[i] depends on swaps above i only).  The signs are
+//     drawn last, from the stream position the chain ends at, so no row's
+//     sign -- and no part of the sketch -- can start before the chain ends.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
