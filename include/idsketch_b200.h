@@ -381,6 +381,25 @@ int ids_mm_info(const char* path, int64_t* rows, int64_t* cols, int64_t* entries
 int ids_mm_read(const char* path, int nthreads, int64_t* row, int64_t* col, double* val,
                 int64_t capacity, int64_t* count);
 
+/* ---------------------------------------------------------------------------
+ * TensorSketch for transforms beyond the fused kernels (sketch.py:170-186 step
+ * by step; any out_dim, any number of modes).  The caller sketches each mode's
+ * factor matrix with the CountSketch kernels (y: nb x out_dim row-major, one
+ * row per rank-1 term) and calls ids_ts_spectral_mode_f64 once per mode: the
+ * rows are zero-padded to M = ids_ts_spectral_len(n_modes, out_dim) (out_dim
+ * itself when it is a power of two, else the power of two >= n_modes *
+ * (out_dim - 1) + 1), transformed by a hand-written batched Stockham FFT
+ * (radix-4 passes through global memory) and multiplied into `spec` (nb x M
+ * complex, interleaved re/im; first != 0 stores instead).  `work` holds
+ * 2 * nb * M complex.  ids_ts_spectral_finish_f64 inverse-transforms spec
+ * (destroyed; work: nb * M complex), folds the result modulo out_dim and
+ * scales row b by weights[b] (NULL: 1) into out (nb x out_dim row-major). */
+int64_t ids_ts_spectral_len(int n_modes, int64_t out_dim);
+int ids_ts_spectral_mode_f64(const double* y, int64_t nb, int64_t out_dim, int64_t M, double* spec,
+                             double* work, int first, void* stream);
+int ids_ts_spectral_finish_f64(double* spec, int64_t nb, int64_t out_dim, int64_t M,
+                               const double* weights, double* work, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

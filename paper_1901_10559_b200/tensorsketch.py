@@ -150,24 +150,40 @@ def _identity_op(L):
     return op
 
 
+SPECTRAL_WORK_BYTES = 3 << 29  # spectrum + FFT ping-pong buffers of one batch of terms (1.5 GB)
+
+
 def _tensorsketch_spectral(op, factors, w, ncols, L):
-    """Transforms longer than the fused kernel holds in shared memory
-    (sketch.py:170-186 step by step): each mode's CountSketch S_n A_n with the
-    dense or CSC kernel (bit-exact, scipy's order), then length-L rfft / irfft
-    through cuFFT with the spectra multiplied left to right, weights applied
-    after the inverse -- the reference's own sequence of operations."""
+    """Transforms longer than the fused kernels hold in shared memory, or
+    more modes than they take (sketch.py:170-186 step by step): each mode's
+    CountSketch S_n A_n with the dense or CSC kernel (bit-exact, scipy's
+    order), then ids_ts_spectral_mode_f64 / ids_ts_spectral_finish_f64 -- a
+    hand-written batched Stockham FFT through global memory, spectra
+    multiplied left to right, the inverse folded modulo L, weights applied
+    last (the reference's own sequence of operations; no library FFT).  The
+    terms are processed in batches sized to SPECTRAL_WORK_BYTES."""
     from ._inputs import dense_operand, sparse_operand
     from ._native import IDS_FLAG_ORDERED
 
-    spec = None
+    n = len(factors)
+    M = int(query("ids_ts_spectral_len", n, L))
+    ys = []
     for mode, f in zip(op.mode_ops, factors):
         if sp.issparse(f):  # CSC sketch straight from the sparse arrays
             y = mode.apply_device(sparse_operand(sp.csc_array(f, dtype=np.float64)))
         else:  # (R, I_n) == col-major I_n x R
             y = mode.apply_device(dense_operand(factor_to_device(f).t()), flags=IDS_FLAG_ORDERED)
-        s = torch.fft.rfft(y, n=L, dim=1)
-        spec = s if spec is None else spec.mul_(s)
-    y = torch.fft.irfft(spec, n=L, dim=1).contiguous()
-    if w is not None:
-        y.mul_(w[:, None])
-    return y
+        ys.append(y.contiguous())  # (R, L) row-major
+    out = _device.empty((ncols, L), torch.float64)
+    nb_max = max(1, min(ncols, SPECTRAL_WORK_BYTES // (3 * 16 * M)))
+    spec = _device.empty(nb_max * M * 2, torch.float64)
+    work = _device.empty(nb_max * M * 4, torch.float64)
+    for c0 in range(0, ncols, nb_max):
+        nb = min(nb_max, ncols - c0)
+        for m, y in enumerate(ys):
+            call("ids_ts_spectral_mode_f64", _device.ptr(y[c0:c0 + nb]), nb, L, M,
+                 _device.ptr(spec), _device.ptr(work), int(m == 0), _device.stream_ptr())
+        call("ids_ts_spectral_finish_f64", _device.ptr(spec), nb, L, M,
+             _device.ptr(w[c0:c0 + nb]) if w is not None else None, _device.ptr(work),
+             _device.ptr(out[c0:c0 + nb]), _device.stream_ptr())
+    return out

@@ -192,11 +192,11 @@ def test_reduced_preserves_sparsity_pattern():
 
 
 @pytest.mark.parametrize("dims,L", [([30, 20, 10, 8], 5000), ([12, 11], 32768), ([9, 9, 9], 16385),
-                                    ([2] * 9, 16)])
+                                    ([2] * 9, 16), ([40, 30], 65536), ([7, 6, 5], 100_003)])
 def test_long_transforms_beyond_the_fused_kernel(dims, L):
     """Sketch lengths whose transform exceeds the fused kernel's shared memory
-    (and more than 8 modes) take the per-mode CountSketch + cuFFT route; same
-    result as pocketfft."""
+    (and more than 8 modes) take the per-mode CountSketch + global-memory
+    Stockham FFT route (ids_ts_spectral_*); same result as pocketfft."""
     from paper_1901_10559_b200._native import query
 
     assert not query("ids_tensorsketch_fused_ok", len(dims), L)
@@ -207,6 +207,24 @@ def test_long_transforms_beyond_the_fused_kernel(dims, L):
     want = oracle.OracleTensorSketch(dims, L, seed=9).apply(factors, lam)
     assert relerr_fro(op.apply(factors, lam), want) <= 1e-12
     assert query("ids_tensorsketch_fused_ok", 4, 16384) and query("ids_tensorsketch_fused_ok", 3, 3000)
+
+
+def test_long_transform_batches_and_weights(monkeypatch):
+    # the spectral route in several batches of terms (small work budget),
+    # with and without weights, sparse and dense factors
+    from paper_1901_10559_b200 import tensorsketch as T
+
+    dims, L, R = [50, 40, 30], 20_000, 23
+    M = 65536
+    monkeypatch.setattr(T, "SPECTRAL_WORK_BYTES", 3 * 16 * M * 5)  # five terms per batch
+    rng = np.random.default_rng(3)
+    factors = [rng.standard_normal((d, R)) for d in dims]
+    factors[1] = sp.csc_array(factors[1] * (rng.random((dims[1], R)) < 0.3))
+    lam = rng.random(R) + 0.5
+    op = ids.TensorSketchOp(dims, L, seed=2)
+    orc = oracle.OracleTensorSketch(dims, L, seed=2)
+    assert relerr_fro(op.apply(factors, lam), orc.apply(factors, lam)) <= 1e-12
+    assert relerr_fro(op.apply(factors), orc.apply(factors)) <= 1e-12
 
 
 # ---- scatter plans (contiguous factor-column reads) vs the gather path ----
