@@ -391,12 +391,16 @@ int ids_mm_read(const char* path, int nthreads, int64_t* row, int64_t* col, doub
  * (out_dim - 1) + 1), transformed by a hand-written batched Stockham FFT
  * (radix-4 passes through global memory) and multiplied into `spec` (nb x M
  * complex, interleaved re/im; first != 0 stores instead).  `work` holds
- * 2 * nb * M complex.  ids_ts_spectral_finish_f64 inverse-transforms spec
+ * 2 * nb * M complex.  ids_ts_spectral_pair_f64 takes two modes at once: their
+ * real rows ride one complex transform (ya + i yb) and are separated in the
+ * frequency domain before their product enters spec.  ids_ts_spectral_finish_f64 inverse-transforms spec
  * (destroyed; work: nb * M complex), folds the result modulo out_dim and
  * scales row b by weights[b] (NULL: 1) into out (nb x out_dim row-major). */
 int64_t ids_ts_spectral_len(int n_modes, int64_t out_dim);
 int ids_ts_spectral_mode_f64(const double* y, int64_t nb, int64_t out_dim, int64_t M, double* spec,
                              double* work, int first, void* stream);
+int ids_ts_spectral_pair_f64(const double* ya, const double* yb, int64_t nb, int64_t out_dim,
+                             int64_t M, double* spec, double* work, int first, void* stream);
 int ids_ts_spectral_finish_f64(double* spec, int64_t nb, int64_t out_dim, int64_t M,
                                const double* weights, double* work, double* out, void* stream);
 

@@ -78,6 +78,9 @@ SIGNATURES = {
     "ids_tensorsketch_split_ok": (_c_int, [_c_int, _c_i64]),
     "ids_ts_spectral_len": (_c_i64, [_c_int, _c_i64]),
     "ids_ts_spectral_mode_f64": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_int, _c_p]),
+    "ids_ts_spectral_pair_f64": (
+        _c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_int, _c_p]
+    ),
     "ids_ts_spectral_finish_f64": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p]),
     "ids_ts_split_plan_bytes": (_c_sz, [_c_i64, _c_i64]),
     "ids_ts_split_plan": (_c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_p, _c_sz, _c_p]),

@@ -33,6 +33,36 @@ sp_pad_kernel(const double* __restrict__ y, int64_t nb, int64_t L, int64_t M,
     }
 }
 
+// Two real rows in one complex transform: z = ya + i yb.
+__global__ void __launch_bounds__(kSpThreads)
+sp_pad2_kernel(const double* __restrict__ ya, const double* __restrict__ yb, int64_t nb, int64_t L,
+               int64_t M, double2* __restrict__ z) {
+    const int64_t tot = nb * M;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / M, t = i - b * M;
+        z[i] = t < L ? make_double2(ya[b * L + t], yb[b * L + t]) : make_double2(0.0, 0.0);
+    }
+}
+
+// Z = FFT(ya + i yb): FFT(ya)[k] = (Z[k] + conj Z[M-k]) / 2 and
+// FFT(yb)[k] = (Z[k] - conj Z[M-k]) / (2i); their product enters the spectrum.
+__global__ void __launch_bounds__(kSpThreads)
+sp_mul2_kernel(double2* __restrict__ spec, const double2* __restrict__ z, int64_t nb, int64_t M,
+               int first) {
+    const int64_t tot = nb * M;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / M, k = i - b * M;
+        const double2 zk = z[i], zm = conj2(z[b * M + ((M - k) & (M - 1))]);
+        const double2 fa = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y + zm.y));
+        const double2 df = csub(zk, zm);
+        const double2 fb = make_double2(0.5 * df.y, -0.5 * df.x);  // df / (2i)
+        const double2 pr = cmul(fa, fb);
+        spec[i] = first ? pr : cmul(spec[i], pr);
+    }
+}
+
 __device__ __forceinline__ double2 twiddle(int64_t p, int64_t n, int sign) {
     double sn, cs;
     sincospi(2.0 * (double)p / (double)n, &sn, &cs);
@@ -162,6 +192,26 @@ extern "C" int ids_ts_spectral_mode_f64(const double* y, int64_t nb, int64_t out
     if (int rc = fft_passes(a, b, nb, M, -1, st, &z)) return rc;
     sp_mul_kernel<<<grid_for(nb * M), kSpThreads, 0, st>>>(reinterpret_cast<double2*>(spec), z,
                                                           nb * M, first);
+    IDS_LAUNCH_CHECK();
+    return IDS_OK;
+}
+
+extern "C" int ids_ts_spectral_pair_f64(const double* ya, const double* yb, int64_t nb,
+                                        int64_t out_dim, int64_t M, double* spec, double* work,
+                                        int first, void* stream) {
+    if (!ya || !yb || !spec || !work || nb < 1 || out_dim < 1 || M < out_dim || !pow2(M)) {
+        ids_set_last_error("ts spectral pair: bad arguments");
+        return IDS_EINVAL;
+    }
+    cudaStream_t st = as_stream(stream);
+    double2* a = reinterpret_cast<double2*>(work);
+    double2* b = a + nb * M;
+    sp_pad2_kernel<<<grid_for(nb * M), kSpThreads, 0, st>>>(ya, yb, nb, out_dim, M, a);
+    IDS_LAUNCH_CHECK();
+    const double2* z = nullptr;
+    if (int rc = fft_passes(a, b, nb, M, -1, st, &z)) return rc;
+    sp_mul2_kernel<<<grid_for(nb * M), kSpThreads, 0, st>>>(reinterpret_cast<double2*>(spec), z, nb,
+                                                           M, first);
     IDS_LAUNCH_CHECK();
     return IDS_OK;
 }

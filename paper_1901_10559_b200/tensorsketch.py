@@ -158,8 +158,8 @@ def _tensorsketch_spectral(op, factors, w, ncols, L):
     more modes than they take (sketch.py:170-186 step by step): each mode's
     CountSketch S_n A_n with the dense or CSC kernel (bit-exact, scipy's
     order), then ids_ts_spectral_mode_f64 / ids_ts_spectral_finish_f64 -- a
-    hand-written batched Stockham FFT through global memory, spectra
-    multiplied left to right, the inverse folded modulo L, weights applied
+    hand-written batched Stockham FFT through global memory (two modes'
+    real rows per complex transform), spectra multiplied left to right, the inverse folded modulo L, weights applied
     last (the reference's own sequence of operations; no library FFT).  The
     terms are processed in batches sized to SPECTRAL_WORK_BYTES."""
     from ._inputs import dense_operand, sparse_operand
@@ -180,9 +180,13 @@ def _tensorsketch_spectral(op, factors, w, ncols, L):
     work = _device.empty(nb_max * M * 4, torch.float64)
     for c0 in range(0, ncols, nb_max):
         nb = min(nb_max, ncols - c0)
-        for m, y in enumerate(ys):
-            call("ids_ts_spectral_mode_f64", _device.ptr(y[c0:c0 + nb]), nb, L, M,
-                 _device.ptr(spec), _device.ptr(work), int(m == 0), _device.stream_ptr())
+        for m in range(0, n - 1, 2):  # two modes per complex transform
+            call("ids_ts_spectral_pair_f64", _device.ptr(ys[m][c0:c0 + nb]),
+                 _device.ptr(ys[m + 1][c0:c0 + nb]), nb, L, M, _device.ptr(spec),
+                 _device.ptr(work), int(m == 0), _device.stream_ptr())
+        if n % 2:
+            call("ids_ts_spectral_mode_f64", _device.ptr(ys[-1][c0:c0 + nb]), nb, L, M,
+                 _device.ptr(spec), _device.ptr(work), int(n == 1), _device.stream_ptr())
         call("ids_ts_spectral_finish_f64", _device.ptr(spec), nb, L, M,
              _device.ptr(w[c0:c0 + nb]) if w is not None else None, _device.ptr(work),
              _device.ptr(out[c0:c0 + nb]), _device.stream_ptr())
