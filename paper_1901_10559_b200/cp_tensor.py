@@ -368,6 +368,18 @@ def _host_graph_fill(x, bufs, w):
     w.copy_(torch.from_numpy(np.ascontiguousarray(x.weights, dtype=np.float64)))
 
 
+_TRIAL_SIDE = {}
+
+
+def _trial_side_stream(device):
+    import torch
+
+    st = _TRIAL_SIDE.get(device)
+    if st is None:
+        st = _TRIAL_SIDE[device] = torch.cuda.Stream(device=device)
+    return st
+
+
 class TensorIdGraph:
     """tensorsketch_id of one device-resident CP tensor, captured once as a
     CUDA graph and replayed per seed (B200 extension; the reference has no
@@ -386,10 +398,15 @@ class TensorIdGraph:
     contiguous tensor) -- normalized CP factors, as CpTensor stores them;
     weights: CUDA float64 (R,); host_weights: the same weights on the host
     (new_weights = weights[cols] * coeffs.sum(axis=1), cp_tensor.py:216, is
-    formed in numpy, bit-identical to the reference)."""
+    formed in numpy, bit-identical to the reference).
+
+    trials() of three or more seeds run on two split twins of the graph
+    (pipeline_trials=True): the next trial's draw graph replays on a side
+    stream beside the current trial's compute graph (C4 0.36 -> 0.32 ms per
+    trial, C5 1.99 -> 1.93)."""
 
     def __init__(self, factors, weights, rank, sketch_dim=None, rank_tol=DEFAULT_RANK_TOL,
-                 host_weights=None, split=False):
+                 host_weights=None, split=False, pipeline_trials=True):
         import torch
 
         from . import _device
@@ -412,6 +429,7 @@ class TensorIdGraph:
         _X.total_entries = int(np.prod(self.mode_dims))
         self.L = check_tensor_id_args(_X, rank, sketch_dim, "tensorsketch")
         self.k, self.rank_tol = int(rank), float(rank_tol)
+        self.pipeline_trials, self._twin_graphs = bool(pipeline_trials), None
         self.host_weights = (np.asarray(host_weights, dtype=np.float64) if host_weights is not None
                              else weights.detach().cpu().numpy())
         n = len(self.mode_dims)
@@ -437,6 +455,16 @@ class TensorIdGraph:
                 self.out = self._compute(self._op)
         self.launches = int(lib.ids_launch_count() - n0)  # library kernels per replay
         self.host_out = torch.empty(self.out.shape, dtype=self.out.dtype, pin_memory=True)
+
+    PIPELINE_MIN_TRIALS = 3
+
+    def _twins(self):
+        if self._twin_graphs is None:
+            mk = lambda: TensorIdGraph(self.factors, self.weights, self.k, self.L, self.rank_tol,
+                                       host_weights=self.host_weights, split=True,
+                                       pipeline_trials=False)
+            self._twin_graphs = (mk(), mk())
+        return self._twin_graphs
 
     def _draw(self):
         return TensorSketchOp(self.mode_dims, self.L, _seed_dev=self.seed_dev)
@@ -477,12 +505,49 @@ class TensorIdGraph:
         st = torch.from_numpy(np.stack([TensorSketchOp.mode_seed_states(n, s) for s in seeds]))
         st_dev = st.pin_memory().to(self.seed_dev.device, non_blocking=True)
         outs = []
-        for t in range(len(seeds)):
-            self.seed_dev.copy_(st_dev[t])
-            self.graph.replay()
-            if self.graph_compute is not None:
-                self.graph_compute.replay()
-            outs.append(self.out.clone())
+        if len(seeds) >= TensorIdGraph.PIPELINE_MIN_TRIALS and self.pipeline_trials:
+            # Two split twins of this graph (their own hash / plan / sketch
+            # buffers) take the trials in turn: the next trial's draw graph
+            # (hash draws, bucket indexes, scatter plans: short serial
+            # kernels that leave the GPU idle) replays on a side stream
+            # beside the current trial's compute graph.
+            a, b = self._twins()
+            main = torch.cuda.current_stream()
+            side = _trial_side_stream(main.device)
+            side.wait_stream(main)
+            drawn = [None, None]
+            computed = [None, None]
+
+            def draw(t):
+                g = (a, b)[t & 1]
+                with torch.cuda.stream(side):
+                    if computed[t & 1] is not None:  # the twin's last compute read its buffers
+                        side.wait_event(computed[t & 1])
+                    g.seed_dev.copy_(st_dev[t])
+                    g.graph.replay()
+                    ev = torch.cuda.Event()
+                    ev.record()
+                drawn[t & 1] = ev
+
+            draw(0)
+            for t in range(len(seeds)):
+                if t + 1 < len(seeds):
+                    draw(t + 1)
+                g = (a, b)[t & 1]
+                main.wait_event(drawn[t & 1])
+                g.graph_compute.replay()
+                outs.append(g.out.clone())
+                ev = torch.cuda.Event()
+                ev.record()
+                computed[t & 1] = ev
+            st_dev.record_stream(side)
+        else:
+            for t in range(len(seeds)):
+                self.seed_dev.copy_(st_dev[t])
+                self.graph.replay()
+                if self.graph_compute is not None:
+                    self.graph_compute.replay()
+                outs.append(self.out.clone())
         host = _device.to_host(torch.stack(outs))
         res = []
         for v in host:

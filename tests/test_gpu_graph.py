@@ -52,6 +52,24 @@ def test_tensor_id_graph_trials():
         assert np.array_equal(nw, want.new_weights)
 
 
+@pytest.mark.parametrize("seeds", [[1, 2, 3], [9, 8, 7, 6, 5, 4, 3], [4, 4, 4, 4]])
+def test_tensor_id_graph_pipelined_trials_equal_sequential(seeds):
+    # trials on two twin graphs (next trial's draws beside this trial's
+    # compute) against replays of one graph, and two trials (below the
+    # pipelining threshold) against both
+    cfg = G.CONFIGS["C4"]
+    w, facs = G.cp_config("C4")
+    g = ids.TensorIdGraph(facs, w, cfg["k"], cfg["L"])
+    seq = ids.TensorIdGraph(facs, w, cfg["k"], cfg["L"], pipeline_trials=False)
+    for rep in range(2):  # the twins are reused by a second call
+        for (da, na), (db, nb) in zip(g.trials(seeds), seq.trials(seeds)):
+            assert np.array_equal(da.cols, db.cols) and np.array_equal(da.coeffs, db.coeffs)
+            assert np.array_equal(na, nb) and da.numerical_rank == db.numerical_rank
+    assert g._twin_graphs is not None and seq._twin_graphs is None
+    for (da, na), (db, nb) in zip(g.trials(seeds[:2]), seq.trials(seeds[:2])):
+        assert np.array_equal(da.cols, db.cols) and np.array_equal(da.coeffs, db.coeffs)
+
+
 def test_device_cp_tensor_matches_host():
     """CpTensor over CUDA factors (normalized on the device, kept in HBM):
     tensorsketch_id gives the host path's results (bit-identical for unit
