@@ -774,7 +774,7 @@ def main():
             if name == args.workload:
                 continue
             wls[name] = make_workload(ctx, name)
-            secondary[name] = results[name] = measure(ctx, wls[name], 6, 3, args, headline=False)
+            secondary[name] = results[name] = measure(ctx, wls[name], 20, 5, args, headline=False)
     cpu_legs(ctx, wls, results, args)
     del wls
     torch.cuda.empty_cache()
